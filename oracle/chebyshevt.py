@@ -1,0 +1,225 @@
+"""ORACLE -- plain, slow, obviously-correct CPU fp64 implementation of the truncated low-rank
+ChebyshevT solve (arxiv 2008.10275).  TEST INFRASTRUCTURE ONLY.
+
+Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s cpu_baseline / `--impl reference`
+legs may import, call or execute anything under `oracle/`.  The product path
+(`paper_2008_10275_b200`) never does; it shares no code, header, table or helper with
+this file.  Inputs come from `synth/` (input construction only).
+
+Citations: "P:n" = /root/reference/PAPER.md line n; "S:n" = SPEC.md line n;
+readings S1..S19 = SURVEY.md §8(c) / DESIGN.md "Readings".
+
+What is computed:
+  operator (`equation_intro_mat1`):
+      L(S) = A0 S + A1 S Dmu + rho_f A2 S Dnu + rho_f Jrho S + Jmu S Dmu + lambda_s Jlam S
+  written as six terms  sum_t c_t A_t S diag(e_t)  with
+      (c_t, e_t) = (1, 1), (1, d_mu), (rho_f, d_nu), (rho_f, 1), (1, d_mu), (lambda_s, 1).
+  Chebyshev semi-iteration for a spectrum in [d - c, d + c] (P:547-569 names c, d; the
+  algorithm text is in the cited [WeiBR20_ZAMM, Alg. 3], absent from the paper: reading S1):
+      X_{k+1} = T( w_{k+1} [X_k + gamma (B - L(X_k))] + (1 - w_{k+1}) X_{k-1} ),
+      gamma = 1/d, w_1 = 1, w_2 = 1/(1 - c^2/(2 d^2)), w_{k+1} = 1/(1 - w_k c^2/(4 d^2)).
+  truncation T ("truncation operator T(.)", htucker):
+      Householder QR of the left factor, SVD of the small core, keep
+      r' = min(R, #{sigma_i > tau sigma_1}) (reading S5), U' = Q P_r, V' = Y_r Sigma_r.
+  The concatenation is the LITERAL six-term one (8r + r_B columns); the GPU path groups
+  terms by right diagonal -- both give the same X_{k+1} in exact arithmetic.
+
+Every pin of this file is in tests/test_oracle_pins.py (closed forms, Kronecker solves,
+brute-force SVD, paper examples).  The cap-bound truncated trajectory itself has no
+closed form: "parity unpinned" beyond GPU-vs-oracle.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+import scipy.sparse as sp
+
+
+# --------------------------------------------------------------------------------------------
+# operator  (D's P:38-40)
+# --------------------------------------------------------------------------------------------
+def csr_matrices(M: int, row_ptr, col_idx, vals: Sequence[np.ndarray]) -> List[sp.csr_matrix]:
+    """The six M x M matrices A0, A1, A2, J_rho, J_mu, J_lambda (J is M x M, S11)."""
+    return [sp.csr_matrix((np.asarray(v, dtype=np.float64), col_idx, row_ptr), shape=(M, M))
+            for v in vals]
+
+
+def term_list(mats, rho_f: float, lambda_s: float, d_mu, d_nu):
+    """[(c_t, A_t, e_t)] of P:30-36: A0 S, A1 S Dmu, rho_f A2 S Dnu, rho_f Jrho S, Jmu S Dmu, lambda_s Jlam S."""
+    n = len(d_mu)
+    one = np.ones(n)
+    d_mu = np.asarray(d_mu, dtype=np.float64)
+    d_nu = np.asarray(d_nu, dtype=np.float64)
+    return [
+        (1.0, mats[0], one),
+        (1.0, mats[1], d_mu),
+        (rho_f, mats[2], d_nu),
+        (rho_f, mats[3], one),
+        (1.0, mats[4], d_mu),
+        (lambda_s, mats[5], one),
+    ]
+
+
+def apply_dense(terms, S: np.ndarray) -> np.ndarray:
+    """L(S) for a dense M x n S, term by term: sum_t c_t (A_t S) diag(e_t)."""
+    Y = np.zeros_like(S, dtype=np.float64)
+    for c, A, e in terms:
+        Y += c * (A @ S) * e[None, :]
+    return Y
+
+
+def apply_lowrank(terms, U: np.ndarray, V: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+    """L(U V^T) in factored form: A S D = (A U)(D V)^T for each term.
+
+    Returns (U_L, V_L) with U_L = [A_0 U | ... | A_5 U], V_L = [c_0 e_0*V | ... | c_5 e_5*V].
+    """
+    Us = [A @ U for (_, A, _) in terms]
+    Vs = [c * (e[:, None] * V) for (c, _, e) in terms]
+    return np.hstack(Us), np.hstack(Vs)
+
+
+def kron_operator(terms) -> sp.csr_matrix:
+    """Vector notation: vec(L(S)) = (sum_t c_t diag(e_t) (x) A_t) vec(S),
+    vec = column stacking; block-diagonal with blocks A(mu_j, nu_j)."""
+    acc = None
+    for c, A, e in terms:
+        k = sp.kron(sp.diags(c * e), A, format="csr")
+        acc = k if acc is None else acc + k
+    return acc.tocsr()
+
+
+def vec(S: np.ndarray) -> np.ndarray:
+    """Column stacking."""
+    return np.asarray(S).reshape(-1, order="F")
+
+
+def unvec(s: np.ndarray, M: int) -> np.ndarray:
+    """Inverse of vec."""
+    return np.asarray(s).reshape(M, -1, order="F")
+
+
+# --------------------------------------------------------------------------------------------
+# truncation operator T (readings S5, S12, S13)
+# --------------------------------------------------------------------------------------------
+def truncate(U: np.ndarray, V: np.ndarray, tau: float, R: int):
+    """T_{tau,R}(U V^T): Householder QR of U (LAPACK geqrf via numpy), SVD of the core C = R_u V^T.
+
+    Returns (U', V', sigma) where sigma is the full singular-value vector of the core and
+    U' V'^T is the best rank-r' approximation, r' = min(R, #{sigma_i > tau sigma_1}); r' = 0
+    if sigma_1 = 0 or the factor is empty.
+    """
+    M, n = U.shape[0], V.shape[0]
+    if U.shape[1] == 0:
+        return np.zeros((M, 0)), np.zeros((n, 0)), np.zeros(0)
+    Q, Ru = np.linalg.qr(U, mode="reduced")
+    C = Ru @ V.T
+    P, s, Yt = np.linalg.svd(C, full_matrices=False)
+    if s[0] == 0.0:
+        return np.zeros((M, 0)), np.zeros((n, 0)), s
+    r = int(min(R, np.count_nonzero(s > tau * s[0])))
+    return Q @ P[:, :r], Yt[:r].T * s[:r][None, :], s
+
+
+def frobenius_lowrank(U: np.ndarray, V: np.ndarray) -> float:
+    """||U V^T||_F without densifying: ||R_u V^T||_F with U = Q R_u (Householder)."""
+    if U.shape[1] == 0:
+        return 0.0
+    _, Ru = np.linalg.qr(U, mode="reduced")
+    return float(np.linalg.norm(Ru @ V.T))
+
+
+# --------------------------------------------------------------------------------------------
+# Chebyshev coefficients (reading S1/S2/S18)
+# --------------------------------------------------------------------------------------------
+def chebyshev_cd(lam_min: float, lam_max: float) -> Tuple[float, float]:
+    """Interval [d - c, d + c] = [lam_min, lam_max] (reading S2): d centre, c half-width."""
+    return 0.5 * (lam_max - lam_min), 0.5 * (lam_max + lam_min)
+
+
+def omegas(lam_min: float, lam_max: float, N: int) -> np.ndarray:
+    """w_1..w_N of the three-term recurrence: w_1 = 1, w_2 = 1/(1 - c^2/(2d^2)),
+    w_{k+1} = 1/(1 - w_k c^2/(4 d^2))."""
+    c, d = chebyshev_cd(lam_min, lam_max)
+    w = np.empty(N)
+    for k in range(N):
+        if k == 0:
+            w[k] = 1.0
+        elif k == 1:
+            w[k] = 1.0 / (1.0 - c * c / (2.0 * d * d))
+        else:
+            w[k] = 1.0 / (1.0 - w[k - 1] * c * c / (4.0 * d * d))
+    return w
+
+
+# --------------------------------------------------------------------------------------------
+# ChebyshevT-S2 (reading S1, S4, S6, S7, S8)
+# --------------------------------------------------------------------------------------------
+@dataclasses.dataclass
+class Result:
+    U: np.ndarray
+    V: np.ndarray
+    ranks: List[int]
+    sigmas: List[np.ndarray]
+    iterates: List[Tuple[np.ndarray, np.ndarray]]   # X_1..X_N as factors (if recorded)
+    rel_residual: float
+
+
+def chebyshevt_step(terms, BU, BV, Uk, Vk, Ukm1, Vkm1, omega: float, gamma: float, tau: float, R: int):
+    """One update X_{k+1} = T( w [X_k + gamma (B - L(X_k))] + (1 - w) X_{k-1} ) via the literal
+    six-term concatenation  U = [B_U | U_k | A_0U_k ... A_5U_k | U_{k-1}],
+    V = [w gamma B_V | w V_k | -w gamma c_t e_t*V_k ... | (1-w) V_{k-1}]  (empty blocks dropped)."""
+    Ublocks = [BU]
+    Vblocks = [omega * gamma * BV]
+    if Uk.shape[1] > 0:
+        UL, VL = apply_lowrank(terms, Uk, Vk)
+        Ublocks += [Uk, UL]
+        Vblocks += [omega * Vk, -omega * gamma * VL]
+    if Ukm1.shape[1] > 0:
+        Ublocks.append(Ukm1)
+        Vblocks.append((1.0 - omega) * Vkm1)
+    return truncate(np.hstack(Ublocks), np.hstack(Vblocks), tau, R)
+
+
+def residual(terms, BU, BV, U, V) -> float:
+    """Honest relative residual ||B - L(U V^T)||_F / ||B||_F, untruncated (reading S14)."""
+    nb = frobenius_lowrank(BU, BV)
+    if nb == 0.0:
+        return 0.0
+    if U.shape[1] == 0:
+        return 1.0
+    UL, VL = apply_lowrank(terms, U, V)
+    return frobenius_lowrank(np.hstack([BU, UL]), np.hstack([BV, -VL])) / nb
+
+
+def chebyshevt(terms, BU, BV, lam_min: float, lam_max: float, tau: float, R: int, N: int,
+               record_iterates: bool = True, final_residual: bool = True,
+               restart_every: Optional[int] = None) -> Result:
+    """N updates X_1..X_N from X_0 = X_{-1} = 0 (readings S6, S7).  Optional restart (S8,
+    P:546 'restarted once after 6 iterations'): the w sequence restarts with X_{-1} := X_k."""
+    M, n = BU.shape[0], BV.shape[0]
+    c, d = chebyshev_cd(lam_min, lam_max)
+    gamma = 1.0 / d
+    w_all = omegas(lam_min, lam_max, N)
+    Uk, Vk = np.zeros((M, 0)), np.zeros((n, 0))
+    Ukm1, Vkm1 = np.zeros((M, 0)), np.zeros((n, 0))
+    ranks, sigmas, iterates = [], [], []
+    j = 0
+    for k in range(N):
+        if restart_every and k > 0 and k % restart_every == 0:
+            j = 0
+            Ukm1, Vkm1 = Uk, Vk
+        Un, Vn, s = chebyshevt_step(terms, BU, BV, Uk, Vk, Ukm1, Vkm1, w_all[j], gamma, tau, R)
+        j += 1
+        Ukm1, Vkm1, Uk, Vk = Uk, Vk, Un, Vn
+        ranks.append(Un.shape[1])
+        sigmas.append(s)
+        if record_iterates:
+            iterates.append((Un, Vn))
+    rho = residual(terms, BU, BV, Uk, Vk) if final_residual else float("nan")
+    return Result(Uk, Vk, ranks, sigmas, iterates, rho)
+
+
+def dense_product(U: np.ndarray, V: np.ndarray) -> np.ndarray:
+    return U @ V.T

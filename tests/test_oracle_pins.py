@@ -1,0 +1,398 @@
+"""Pins of the CPU oracle against things other than itself (SURVEY.md §8(c) pins P1-P9).
+
+Each test cites what fixes the expected value: a closed form, a textbook/library routine,
+brute force, or a number printed in the paper.  No expected value comes from the CUDA path.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+from numpy.polynomial import chebyshev as npcheb
+
+from oracle import chebyshevt as orc
+from synth import generator as gen
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ------------------------------------------------------------------------------------------
+# helpers (input construction only)
+# ------------------------------------------------------------------------------------------
+def diagonal_problem(M=40, n=6, rB=2, seed=5, lo=1.0):
+    rng = np.random.default_rng(seed)
+    a = [lo + rng.random(M) * 3.0] + [rng.random(M) for _ in range(5)]
+    mats = [sp.diags(x).tocsr() for x in a]
+    d_mu = 0.5 + rng.random(n) * 1.5
+    d_nu = 0.5 + rng.random(n) * 1.5
+    rho, lam = 1.0, 2.0
+    terms = orc.term_list(mats, rho, lam, d_mu, d_nu)
+    # eigenvalue lambda_ij of the diagonal operator, written out from P:30-36 entry by entry
+    Lam = (a[0][:, None] + d_mu[None, :] * a[1][:, None] + rho * d_nu[None, :] * a[2][:, None]
+           + rho * a[3][:, None] + d_mu[None, :] * a[4][:, None] + lam * a[5][:, None])
+    BU = rng.standard_normal((M, rB))
+    BV = rng.standard_normal((n, rB))
+    return terms, Lam, BU, BV
+
+
+def cheb_T(k, x):
+    """T_k(x) via numpy's Chebyshev-series evaluation (library routine)."""
+    coef = np.zeros(k + 1)
+    coef[k] = 1.0
+    return npcheb.chebval(x, coef)
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    prob = gen.make_problem("tiny")
+    d_mu, d_nu, BU, BV = prob.subset(0)
+    mats = orc.csr_matrices(prob.op.M, prob.op.row_ptr, prob.op.col_idx, prob.op.vals)
+    terms = orc.term_list(mats, prob.op.rho_f, prob.op.lambda_s, d_mu, d_nu)
+    return prob, terms, BU, BV
+
+
+def block_solve(terms, B):
+    """Exact S* by per-column sparse solves of the block-diagonal system."""
+    M, n = B.shape
+    S = np.zeros_like(B)
+    for j in range(n):
+        Aj = None
+        for c, A, e in terms:
+            Aj = c * e[j] * A if Aj is None else Aj + c * e[j] * A
+        S[:, j] = spla.spsolve(Aj.tocsc(), B[:, j])
+    return S
+
+
+# ------------------------------------------------------------------------------------------
+# P1: exact Chebyshev error polynomial on diagonal operators
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("N", [1, 2, 5, 12])
+def test_P1_diagonal_closed_form(N):
+    terms, Lam, BU, BV = diagonal_problem()
+    lmin, lmax = Lam.min(), Lam.max()
+    res = orc.chebyshevt(terms, BU, BV, lmin, lmax, tau=0.0, R=BV.shape[0], N=N)
+    X = orc.dense_product(res.U, res.V)
+    B = BU @ BV.T
+    S_star = B / Lam
+    c, d = 0.5 * (lmax - lmin), 0.5 * (lmax + lmin)
+    pN = cheb_T(N, (d - Lam) / c) / cheb_T(N, d / c)       # error polynomial
+    X_exact = (1.0 - pN) * S_star
+    assert np.linalg.norm(X - X_exact) <= 1e-13 * np.linalg.norm(X_exact)
+
+
+def test_P1_richardson_c0_closed_form():
+    """c = 0 (lam_min = lam_max = d): Richardson with gamma = 1/d, error (1 - lambda/d)^N."""
+    terms, Lam, BU, BV = diagonal_problem(lo=3.0)
+    d = float(Lam.max())
+    N = 7
+    res = orc.chebyshevt(terms, BU, BV, d, d, tau=0.0, R=BV.shape[0], N=N)
+    S_star = (BU @ BV.T) / Lam
+    X_exact = (1.0 - (1.0 - Lam / d) ** N) * S_star
+    X = orc.dense_product(res.U, res.V)
+    assert np.linalg.norm(X - X_exact) <= 1e-13 * np.linalg.norm(X_exact)
+
+
+# ------------------------------------------------------------------------------------------
+# P2 / P4: Chebyshev bound and dense Kronecker solve on Tiny
+# ------------------------------------------------------------------------------------------
+def test_P4_kronecker_solution_matches_column_solves(tiny):
+    prob, terms, BU, BV = tiny
+    B = BU @ BV.T
+    K = orc.kron_operator(terms)
+    s = spla.spsolve(K.tocsc(), orc.vec(B))
+    S_kron = orc.unvec(s, prob.op.M)
+    S_cols = block_solve(terms, B)
+    assert np.linalg.norm(S_kron - S_cols) <= 1e-12 * np.linalg.norm(S_cols)
+
+
+def test_P2_chebyshev_bound_untruncated(tiny):
+    prob, terms, BU, BV = tiny
+    n = BV.shape[0]
+    N = 30
+    res = orc.chebyshevt(terms, BU, BV, prob.lam_min, prob.lam_max, tau=0.0, R=n, N=N)
+    S_star = block_solve(terms, BU @ BV.T)
+    c, d = 0.5 * (prob.lam_max - prob.lam_min), 0.5 * (prob.lam_max + prob.lam_min)
+    bound = np.linalg.norm(S_star) / cheb_T(N, d / c)
+    err = np.linalg.norm(orc.dense_product(res.U, res.V) - S_star)
+    assert err <= bound * (1 + 1e-6) + 1e-13 * np.linalg.norm(S_star)
+    assert err >= 1e-3 * bound   # it really is a Chebyshev rate, not an exact solve
+
+
+def test_P4_converged_solution_untruncated(tiny):
+    prob, terms, BU, BV = tiny
+    n = BV.shape[0]
+    N = 70
+    res = orc.chebyshevt(terms, BU, BV, prob.lam_min, prob.lam_max, tau=1e-15, R=n, N=N,
+                         record_iterates=False)
+    S_star = block_solve(terms, BU @ BV.T)
+    err = np.linalg.norm(orc.dense_product(res.U, res.V) - S_star) / np.linalg.norm(S_star)
+    assert err <= 1e-11
+    assert res.rel_residual <= 1e-11
+
+
+def test_P4_truncated_solution_near_best_rank(tiny):
+    """BJ's Tiny settings (R = 10, tau = 1e-10, N = 30): error close to the best rank-10 error of S*."""
+    prob, terms, BU, BV = tiny
+    cfg = prob.cfg
+    res = orc.chebyshevt(terms, BU, BV, prob.lam_min, prob.lam_max, tau=cfg.tol, R=cfg.rank_cap,
+                         N=cfg.n_iter, record_iterates=False)
+    S_star = block_solve(terms, BU @ BV.T)
+    s = np.linalg.svd(S_star, compute_uv=False)
+    best = np.sqrt(np.sum(s[cfg.rank_cap:] ** 2))
+    err = np.linalg.norm(orc.dense_product(res.U, res.V) - S_star)
+    assert best <= err <= 1.5 * best
+    assert res.U.shape[1] == cfg.rank_cap
+
+
+# ------------------------------------------------------------------------------------------
+# P3: identity operator, c = 0, d = 1
+# ------------------------------------------------------------------------------------------
+def test_P3_identity_operator_one_step():
+    M, n = 30, 5
+    rng = np.random.default_rng(3)
+    I = sp.identity(M, format="csr")
+    Z = sp.csr_matrix((M, M))
+    terms = orc.term_list([I, Z, Z, Z, Z, Z], 1.0, 2.0, rng.random(n), rng.random(n))
+    BU, BV = rng.standard_normal((M, 2)), rng.standard_normal((n, 2))
+    res = orc.chebyshevt(terms, BU, BV, 1.0, 1.0, tau=0.0, R=n, N=4)
+    B = BU @ BV.T
+    for U, V in res.iterates:
+        assert np.linalg.norm(U @ V.T - B) <= 1e-14 * np.linalg.norm(B)
+    assert res.rel_residual <= 1e-14
+
+
+# ------------------------------------------------------------------------------------------
+# P5: truncation vs brute-force dense SVD
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("R,tau", [(1, 0.0), (3, 0.0), (5, 1e-3), (12, 1e-10), (20, 0.0)])
+def test_P5_truncation_is_best_rank_approx(R, tau):
+    rng = np.random.default_rng(11)
+    M, n, w = 200, 30, 12
+    U = rng.standard_normal((M, w)) * np.logspace(0, -6, w)[None, :]
+    V = rng.standard_normal((n, w))
+    X = U @ V.T
+    Ut, Vt, s = orc.truncate(U, V, tau, R)
+    Pd, sd, Qd = np.linalg.svd(X, full_matrices=False)       # brute force on the dense product
+    r = min(R, w, int(np.sum(sd > tau * sd[0])))   # rank(X) <= w
+    assert Ut.shape[1] == r
+    Xr = (Pd[:, :r] * sd[:r]) @ Qd[:r]
+    assert np.linalg.norm(Ut @ Vt.T - Xr) <= 1e-12 * np.linalg.norm(X)
+    assert np.allclose(s[:min(w, n)], sd[:min(w, n)], rtol=0, atol=1e-12 * sd[0])
+    # error equals the tail singular-value norm
+    assert abs(np.linalg.norm(X - Ut @ Vt.T) - np.sqrt(np.sum(sd[r:] ** 2))) <= 1e-11 * sd[0]
+    # U' has orthonormal columns (reading S12)
+    assert np.linalg.norm(Ut.T @ Ut - np.eye(r)) <= 1e-13
+
+
+def test_P5_truncation_edge_cases():
+    rng = np.random.default_rng(2)
+    M, n = 50, 8
+    # zero factor -> rank 0
+    Ut, Vt, _ = orc.truncate(np.zeros((M, 3)), rng.standard_normal((n, 3)), 0.0, 5)
+    assert Ut.shape == (M, 0) and Vt.shape == (n, 0)
+    # empty factor
+    Ut, Vt, s = orc.truncate(np.zeros((M, 0)), np.zeros((n, 0)), 0.0, 5)
+    assert Ut.shape[1] == 0 and s.size == 0
+    # rank-1 is kept exactly
+    a, b = rng.standard_normal((M, 1)), rng.standard_normal((n, 1))
+    Ut, Vt, _ = orc.truncate(a, b, 1e-12, 1)
+    assert np.linalg.norm(Ut @ Vt.T - a @ b.T) <= 1e-14 * np.linalg.norm(a @ b.T)
+    # exactly rank-deficient concatenation (duplicated column blocks, the k = 2 situation)
+    U = rng.standard_normal((M, 4))
+    Ud = np.hstack([U, U, U[:, :2]])
+    Vd = rng.standard_normal((n, 10))
+    Ut, Vt, s = orc.truncate(Ud, Vd, 1e-12, 10)
+    assert Ut.shape[1] == 4
+    assert np.linalg.norm(Ut @ Vt.T - Ud @ Vd.T) <= 1e-13 * np.linalg.norm(Ud @ Vd.T)
+
+
+# ------------------------------------------------------------------------------------------
+# P6: operator -- factored vs Kronecker vector notation vs dense
+# ------------------------------------------------------------------------------------------
+def test_P6_operator_factored_vs_kronecker(tiny):
+    prob, terms, BU, BV = tiny
+    rng = np.random.default_rng(7)
+    U, V = rng.standard_normal((prob.op.M, 4)), rng.standard_normal((BV.shape[0], 4))
+    UL, VL = orc.apply_lowrank(terms, U, V)
+    K = orc.kron_operator(terms)
+    LX_kron = orc.unvec(K @ orc.vec(U @ V.T), prob.op.M)
+    LX_dense = orc.apply_dense(terms, U @ V.T)
+    ref = np.linalg.norm(LX_kron)
+    assert np.linalg.norm(UL @ VL.T - LX_kron) <= 1e-13 * ref
+    assert np.linalg.norm(LX_dense - LX_kron) <= 1e-13 * ref
+
+
+def test_P6_kronecker_is_block_diagonal(tiny):
+    """vec(L(S)) = diago(A(mu_j, nu_j)) vec(S) with A(mu,nu) = A0 + mu A1 + rho nu A2 + rho Jr + mu Jm + lam Jl."""
+    prob, terms, BU, BV = tiny
+    op = prob.op
+    d_mu, d_nu = prob.mu, prob.nu
+    mats = orc.csr_matrices(op.M, op.row_ptr, op.col_idx, op.vals)
+    blocks = [mats[0] + m * mats[1] + op.rho_f * v * mats[2] + op.rho_f * mats[3] + m * mats[4]
+              + op.lambda_s * mats[5] for m, v in zip(d_mu, d_nu)]
+    K_blocks = sp.block_diag(blocks, format="csr")
+    K = orc.kron_operator(terms)
+    assert abs(K - K_blocks).max() <= 1e-14 * abs(K).max()
+
+
+def test_vec_roundtrip():
+    S = np.arange(12.0).reshape(4, 3)
+    v = orc.vec(S)
+    assert np.array_equal(v[:4], S[:, 0])            # column stacking
+    assert np.array_equal(orc.unvec(v, 4), S)
+
+
+# ------------------------------------------------------------------------------------------
+# P7: omega recursion vs closed form 2 sigma T_k(sigma) / T_{k+1}(sigma)
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("lmin,lmax", [(4.0, 40.0), (0.9, 1.1), (1.0, 100.0)])
+def test_P7_omega_closed_form(lmin, lmax):
+    N = 40
+    w = orc.omegas(lmin, lmax, N)
+    c, d = 0.5 * (lmax - lmin), 0.5 * (lmax + lmin)
+    sig = d / c
+    assert w[0] == 1.0
+    for k in range(1, N):
+        closed = 2.0 * sig * cheb_T(k, sig) / cheb_T(k + 1, sig)
+        assert abs(w[k] - closed) <= 1e-13 * closed
+    # monotone decreasing from w_2 towards the limit 2 / (1 + sqrt(1 - c^2/d^2))
+    assert np.all(np.diff(w[1:]) <= 0) and w[-1] >= 2.0 / (1.0 + np.sqrt(1.0 - (c / d) ** 2)) - 1e-14
+
+
+def test_P7_omega_c0_is_one():
+    assert np.all(orc.omegas(2.0, 2.0, 10) == 1.0)
+
+
+# ------------------------------------------------------------------------------------------
+# P8: structural rank bounds
+# ------------------------------------------------------------------------------------------
+def test_P8_rank_structure(tiny):
+    prob, terms, BU, BV = tiny
+    rng = np.random.default_rng(9)
+    r = 3
+    U, V = rng.standard_normal((prob.op.M, r)), rng.standard_normal((BV.shape[0], r))
+    UL, VL = orc.apply_lowrank(terms, U, V)
+    s = np.linalg.svd(UL @ VL.T, compute_uv=False)
+    # rank(L(X)) <= 3 rank(X): the six terms have only three distinct right diagonals
+    assert s[3 * r] <= 1e-12 * s[0]
+    cfg = prob.cfg
+    res = orc.chebyshevt(terms, BU, BV, prob.lam_min, prob.lam_max, cfg.tol, cfg.rank_cap, 8)
+    rB = BU.shape[1]
+    prev = 0
+    for rk in res.ranks:
+        assert rk <= min(cfg.rank_cap, BV.shape[0], rB + 4 * prev)
+        prev = rk
+    assert res.ranks[0] == rB
+
+
+# ------------------------------------------------------------------------------------------
+# P9: asymptotic contraction on a spectrum in [0.9, 1.1]
+# ------------------------------------------------------------------------------------------
+def test_P9_contraction_rate():
+    M, n = 60, 4
+    rng = np.random.default_rng(4)
+    lam = np.linspace(0.9, 1.1, M)
+    Z = sp.csr_matrix((M, M))
+    terms = orc.term_list([sp.diags(lam).tocsr(), Z, Z, Z, Z, Z], 1.0, 2.0, np.ones(n), np.ones(n))
+    BU, BV = rng.standard_normal((M, 2)), rng.standard_normal((n, 2))
+    S_star = (BU @ BV.T) / lam[:, None]
+    errs = []
+    for N in (4, 8):
+        res = orc.chebyshevt(terms, BU, BV, 0.9, 1.1, tau=0.0, R=n, N=N)
+        errs.append(np.linalg.norm(res.U @ res.V.T - S_star))
+    rate = (errs[1] / errs[0]) ** (1.0 / 4.0)
+    expected = 0.1 / (1.0 + np.sqrt(1.0 - 0.01))              # c / (d + sqrt(d^2 - c^2)) = 0.0501
+    assert abs(expected - 0.0501) < 1e-4
+    assert rate <= expected * 1.05
+
+
+# ------------------------------------------------------------------------------------------
+# residual vs brute force
+# ------------------------------------------------------------------------------------------
+def test_residual_vs_dense(tiny):
+    prob, terms, BU, BV = tiny
+    rng = np.random.default_rng(8)
+    U, V = rng.standard_normal((prob.op.M, 5)) * 1e-2, rng.standard_normal((BV.shape[0], 5))
+    B = BU @ BV.T
+    K = orc.kron_operator(terms)
+    Rd = B - orc.unvec(K @ orc.vec(U @ V.T), prob.op.M)
+    assert abs(orc.residual(terms, BU, BV, U, V) - np.linalg.norm(Rd) / np.linalg.norm(B)) <= 1e-13
+    assert orc.residual(terms, BU, BV, np.zeros((prob.op.M, 0)), np.zeros((BV.shape[0], 0))) == 1.0
+    assert orc.residual(terms, np.zeros((prob.op.M, 0)), np.zeros((BV.shape[0], 0)), U, V) == 0.0
+
+
+def test_restart_resets_omega(tiny):
+    """Reading S8: after a restart the recurrence starts again with w_1 = 1 (one Richardson step)."""
+    prob, terms, BU, BV = tiny
+    res = orc.chebyshevt(terms, BU, BV, prob.lam_min, prob.lam_max, 0.0, 16, 8, restart_every=6)
+    assert len(res.ranks) == 8 and np.isfinite(res.rel_residual)
+    res0 = orc.chebyshevt(terms, BU, BV, prob.lam_min, prob.lam_max, 0.0, 16, 6)
+    np.testing.assert_allclose(res.iterates[5][0] @ res.iterates[5][1].T, res0.U @ res0.V.T, atol=1e-13)
+
+
+# ------------------------------------------------------------------------------------------
+# paper examples: clustering and the column <-> parameter map
+# ------------------------------------------------------------------------------------------
+def test_clustering_example_golden():
+    with open(os.path.join(GOLDEN, "clustering_example.json")) as f:
+        g = json.load(f)
+    m1, m2, K = g["m1"], g["m2"], g["K"]
+    subs = gen.split_subsets(m1 * m2, K)
+    for (s, e), members, med in zip(subs, g["subsets"], g["upper_median"]):
+        got = [[(p % m1) + 1, (p // m1) + 1] for p in range(s, e)]
+        assert got == members
+        assert list(gen.upper_median_index(s, e, m1)) == med
+
+
+def test_column_parameter_map():
+    cfg = gen.config_by_name("small")
+    mu, nu = gen.parameter_grid(cfg)
+    mu_ax = np.linspace(*cfg.mu_range, cfg.m1)
+    nu_ax = np.linspace(*cfg.nu_range, cfg.m2)
+    for p in range(1, cfg.m + 1):                      # 1-based column p
+        assert mu[p - 1] == mu_ax[((p - 1) % cfg.m1)]
+        assert nu[p - 1] == nu_ax[int(np.ceil(p / cfg.m1)) - 1]
+
+
+# ------------------------------------------------------------------------------------------
+# generator sanity (inputs, not the method)
+# ------------------------------------------------------------------------------------------
+def test_generator_structure(tiny):
+    prob, terms, BU, BV = tiny
+    op = prob.op
+    g = op.g
+    assert op.nnz == 25 * (3 * g - 2) ** 2
+    mats = orc.csr_matrices(op.M, op.row_ptr, op.col_idx, op.vals)
+    for A in mats:
+        assert abs(A - A.T).max() == 0.0
+    for A in mats[3:]:
+        assert abs(np.linalg.norm(A.toarray(), 2) - 0.05) < 0.005
+    # bounds enclose every block spectrum
+    for m, v in zip(prob.mu, prob.nu):
+        Aj = (mats[0] + m * mats[1] + op.rho_f * v * mats[2] + op.rho_f * mats[3] + m * mats[4]
+              + op.lambda_s * mats[5]).toarray()
+        ev = np.linalg.eigvalsh(Aj)
+        assert prob.lam_min < ev[0] and ev[-1] < prob.lam_max
+
+
+def test_generator_closed_form_bounds_enclose_small():
+    prob = gen.make_problem("small")
+    op = prob.op
+    from scipy.sparse.linalg import eigsh
+    for m in (prob.mu.min(), prob.mu.max()):
+        for v in (prob.nu.min(), prob.nu.max()):
+            vals = (op.vals[0] + m * (op.vals[1] + op.vals[4]) + op.rho_f * v * op.vals[2]
+                    + op.rho_f * op.vals[3] + op.lambda_s * op.vals[5])
+            A = sp.csr_matrix((vals, op.col_idx, op.row_ptr), shape=(op.M, op.M))
+            hi = eigsh(A, k=1, which="LA", return_eigenvectors=False, tol=1e-8)[0]
+            assert hi < prob.lam_max
+    assert prob.lam_min < 4.0
+
+
+def test_counter_rng_is_pure_function():
+    a = gen.counter_normal(0, 7, np.arange(1000, dtype=np.uint64))
+    b = gen.counter_normal(0, 7, np.arange(500, 1000, dtype=np.uint64))
+    assert np.array_equal(a[500:], b)
+    assert abs(a.mean()) < 0.15 and abs(a.std() - 1.0) < 0.1
