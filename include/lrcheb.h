@@ -1,0 +1,153 @@
+/*
+ * lrcheb.h -- C ABI of the B200-native truncated low-rank ChebyshevT solver ("liblrcheb").
+ *
+ * What is solved (equation `equation_intro_mat1`; the Newton step on one
+ * parameter subset, P:251-256 / reading S3 of DESIGN.md):
+ *
+ *     A0 S + A1 S Dmu + rho_f A2 S Dnu + rho_f Jrho S + Jmu S Dmu + lambda_s Jlam S = B,
+ *
+ * with B = B_U B_V^T of low rank, S = U V^T kept factored,
+ * the six M x M sparse matrices sharing one CSR pattern, Dmu = diag(d_mu),
+ * Dnu = diag(d_nu) the parameters of the subset.  The solver is the truncated
+ * Chebyshev semi-iteration "ChebyshevT" (named P:14; parameters c, d
+ * P:547-569; the iteration itself is DESIGN.md reading S1) with the truncation operator T of
+ * P:544 (best rank-r' approximation, r' = min(cap, #{sigma_i > tol * sigma_1}), reading S5).
+ *
+ * Conventions (all calls):
+ *   - fp64 everywhere; every dense factor is ROW-MAJOR with an explicit leading dimension
+ *     counted in elements (ld >= number of columns).
+ *   - CSR: row_ptr int32[M+1] (row_ptr[0] = 0, non-decreasing, row_ptr[M] = nnz),
+ *     col_idx int32[nnz] with 0 <= col < M, strictly increasing inside a row.
+ *   - `where` says where caller pointers live: LRC_MEM_HOST (pageable or pinned host memory;
+ *     the library copies), LRC_MEM_DEVICE (device memory on ctx's device; inputs are copied
+ *     into ctx-owned memory, outputs are written in place), LRC_MEM_DEVICE_BORROW (set_operator
+ *     only: the library keeps the caller's device pointers; the caller keeps them alive and
+ *     unchanged until the next set_operator or lrc_destroy).
+ *   - Every call returns an lrc_status; nothing throws or exits.  On error the outputs are
+ *     untouched and lrc_last_error(ctx) holds a one-line message.
+ *   - All work is ordered on ctx's stream; calls return after the work completed (host
+ *     synchronous) unless stated otherwise.  One ctx per host thread; no internal locking.
+ *
+ * Limits of this build (checked, LRC_ERR_ARG otherwise): M < 2^31, nnz < 2^31,
+ *   rank_cap <= 128, r_B <= 64, min(n, r_B + 4 rank_cap) <= 128, n <= 1024,
+ *   lrc_apply_dense: ncols <= 256.
+ */
+#ifndef LRCHEB_H
+#define LRCHEB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lrc_ctx lrc_ctx;
+
+typedef enum {
+  LRC_OK = 0,
+  LRC_ERR_ARG = 1,      /* invalid argument (null pointer, bad CSR, bad bounds, over a limit) */
+  LRC_ERR_SHAPE = 2,    /* shapes inconsistent with the operator / parameters already set */
+  LRC_ERR_STATE = 3,    /* call order: solve before set_operator + set_params, etc. */
+  LRC_ERR_NOMEM = 4,    /* device allocation failed */
+  LRC_ERR_CUDA = 5,     /* a CUDA runtime error (message has the CUDA error string) */
+  LRC_ERR_NUMERIC = 6   /* shifted Cholesky failed after all shift escalations */
+} lrc_status;
+
+typedef enum { LRC_MEM_HOST = 0, LRC_MEM_DEVICE = 1, LRC_MEM_DEVICE_BORROW = 2 } lrc_mem;
+
+/* lrc_solve_opts.flags */
+#define LRC_RECORD_ITERATES      1u  /* keep every X_k = U_k V_k^T on the device for lrc_get_iterate */
+#define LRC_SKIP_FINAL_RESIDUAL  2u  /* do not compute info->rel_residual (set to NaN) */
+#define LRC_NO_GRAPH             4u  /* launch the iteration kernels directly instead of a CUDA graph */
+
+/* lrc_apply_lowrank modes */
+#define LRC_APPLY_PLAIN3  0u  /* W = [W0 | W1 | W2], W0 = (A0+rho Jrho+lam Jlam)U, W1 = (A1+Jmu)U, W2 = rho A2 U */
+#define LRC_APPLY_SIX     1u  /* W = [c_0 A0 U | c_1 A1 U | ... | c_5 Jlam U], (c_t) = (1,1,rho,rho,1,lam) */
+#define LRC_APPLY_S2STEP  2u  /* W = [U - gamma W0 | W1 | W2]  (the fused Chebyshev-step epilogue) */
+
+/* Context lifetime.  device: CUDA ordinal; cuda_stream: a cudaStream_t on that device to order
+ * all work on, or NULL for a ctx-owned non-blocking stream. */
+lrc_status  lrc_create(lrc_ctx **out, int device, void *cuda_stream);
+void        lrc_destroy(lrc_ctx *ctx);                 /* NULL-safe; frees everything ctx owns */
+const char *lrc_last_error(const lrc_ctx *ctx);        /* valid until the next call on ctx */
+const char *lrc_version(void);
+
+/* The operator: shared CSR pattern + six value arrays in the order
+ * A0, A1, A2, Jrho, Jmu, Jlambda (zeros stored explicitly where a matrix has no entry),
+ * and the scalars rho_f, lambda_s.  Validates the CSR (LRC_ERR_ARG on a violation) and
+ * detects runs of consecutive rows with identical column lists (node blocks, <= 8 rows)
+ * that the fused SpMM exploits.  Invalidates parameters and workspaces that depend on M. */
+lrc_status lrc_set_operator(lrc_ctx *ctx, int64_t M, int64_t nnz,
+                            const int32_t *row_ptr, const int32_t *col_idx,
+                            const double *const vals[6], double rho_f, double lambda_s,
+                            lrc_mem where);
+
+/* The subset's parameters: d_mu, d_nu of length n (finite). where: HOST or DEVICE. */
+lrc_status lrc_set_params(lrc_ctx *ctx, int64_t n, const double *d_mu, const double *d_nu,
+                          lrc_mem where);
+
+typedef struct {
+  double lambda_min, lambda_max;  /* spectrum bounds [d-c, d+c] (reading S2); 0 < min <= max */
+  double tol;                     /* relative truncation tolerance tau >= 0 (reading S5) */
+  int64_t rank_cap;               /* R, 1 <= R <= min(M, n, 128) */
+  int64_t n_iter;                 /* N >= 1 updates X_1..X_N from X_0 = 0 (readings S6, S7) */
+  int64_t restart_every;          /* 0: no restart; else the omega sequence restarts every k iterations (S8) */
+  uint32_t flags;                 /* LRC_RECORD_ITERATES | LRC_SKIP_FINAL_RESIDUAL | LRC_NO_GRAPH */
+} lrc_solve_opts;
+
+typedef struct {
+  int64_t rank;               /* rank of X_N */
+  double rel_residual;        /* ||B - L(X_N)||_F / ||B||_F (0 if B = 0; NaN if skipped) */
+  double b_norm;              /* ||B||_F */
+  int32_t diverged;           /* 1 if rel_residual > 1 (last iterate still returned) */
+  int32_t shift_escalations;  /* total shift escalations in the Cholesky passes */
+  float ms_iterations;        /* device time of the N iterations (CUDA events) */
+  float ms_total;             /* device time of the whole call */
+  int64_t *rank_history;      /* caller array[n_iter] or NULL: rank of X_1..X_N */
+  double *sigma_history;      /* caller array[n_iter * 128] or NULL: core singular values per
+                                 iteration, descending, zero padded */
+} lrc_solve_info;
+
+/* Solve F(S) = B for the current operator/params.
+ * B_U: M x r_B (ld_bu), B_V: n x r_B (ld_bv); r_B may be 0 (then X = 0, rank 0, residual 0).
+ * Outputs: U_out M x rank_cap (ld_u >= rank_cap), V_out n x rank_cap (ld_v >= rank_cap);
+ * columns >= info->rank are set to 0.  U has orthonormal columns, V = Y Sigma (reading S12).
+ * where: HOST (pointers are host memory; copies are inside the call) or DEVICE.
+ * info may be NULL. */
+lrc_status lrc_solve(lrc_ctx *ctx,
+                     const double *B_U, int64_t ld_bu, const double *B_V, int64_t ld_bv, int64_t r_B,
+                     const lrc_solve_opts *opts,
+                     double *U_out, int64_t ld_u, double *V_out, int64_t ld_v,
+                     lrc_mem where, lrc_solve_info *info);
+
+/* Test / bench hooks (same ctx state; where = HOST or DEVICE for all pointers of the call). */
+
+/* W = L-pieces of U (M x r, ld_u): mode LRC_APPLY_PLAIN3 / LRC_APPLY_S2STEP write M x 3r,
+ * LRC_APPLY_SIX writes M x 6r into W (ld_w).  gamma is used by S2STEP only.  r <= 128. */
+lrc_status lrc_apply_lowrank(lrc_ctx *ctx, const double *U, int64_t ld_u, int64_t r,
+                             double *W, int64_t ld_w, uint32_t mode, double gamma, lrc_mem where);
+
+/* Dense operator application (BASELINE config 5): Y = sum_t c_t A_t S diag(e_t) for a dense
+ * S (M x ncols, ld_s), with e_t in {1, d_mu, d_nu} taken from the params (n == ncols). */
+lrc_status lrc_apply_dense(lrc_ctx *ctx, const double *S, int64_t ld_s, int64_t ncols,
+                           double *Y, int64_t ld_y, lrc_mem where);
+
+/* Truncation operator T_{tol,cap}(U V^T): U M x w (ld_u), V n x w (ld_v), w <= 256.
+ * Writes U_out M x cap (ld cap), V_out n x cap (ld cap), *rank, and sigma (min(n,w) values,
+ * descending) if non-NULL. */
+lrc_status lrc_truncate(lrc_ctx *ctx, const double *U, int64_t ld_u, const double *V, int64_t ld_v,
+                        int64_t w, double tol, int64_t cap,
+                        double *U_out, double *V_out, int64_t *rank, double *sigma, lrc_mem where);
+
+/* Iterate X_k (1 <= k <= n_iter) of the last solve run with LRC_RECORD_ITERATES:
+ * U (M x rank_cap, ld rank_cap), V (n x rank_cap, ld rank_cap), *rank. */
+lrc_status lrc_get_iterate(lrc_ctx *ctx, int64_t k, double *U, double *V, int64_t *rank, lrc_mem where);
+
+/* Device time (ms, CUDA events on ctx's stream) of the last lrc_apply_lowrank / lrc_apply_dense
+ * call's kernel, for the bench's SpMM roofline. */
+float lrc_last_kernel_ms(const lrc_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LRCHEB_H */

@@ -1,0 +1,891 @@
+// liblrcheb C ABI (include/lrcheb.h): context, validation, workspaces, and the ChebyshevT driver.
+//
+// One iteration k (X_k -> X_{k+1}, reading S1) is enqueued as
+//   fork:  [s0] K1 spmm S2STEP(U_k) -> Wcat = [B_U | U_k - g W0 | W1 | W2]        (a1)
+//          [s1] vside: Vcat, Householder QR -> T1 = R_V^T, Q_V                    (a2)
+//   join:  ts GRAM(Ucat, T1) -> reduce -> chol1 -> T2                            (a3)
+//          ts GRAM(Ucat, T2) -> reduce -> chol2 + Jacobi + rank -> Z, V_{k+1}    (a4, a5)
+//          ts STORE(Ucat, Z) -> U_{k+1}                                          (a6)
+// with Ucat = [Wcat | U_{k-1}] never copied (two strided blocks) and all ranks device-resident,
+// so the whole N-iteration loop is captured once into a CUDA graph and replayed.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/lrcheb.h"
+#include "lrc_internal.cuh"
+
+namespace lrc {
+size_t vside_smem_bytes(int n, int wmax, int pmax);
+cudaError_t spmm_prepare();
+cudaError_t ts_prepare();
+cudaError_t small_prepare();
+}  // namespace lrc
+
+using namespace lrc;
+
+static thread_local std::string g_create_err;   // lrc_last_error(NULL): lrc_create failures
+
+namespace {
+
+constexpr size_t kSmemLimit = 232448;   // B200 opt-in dynamic shared memory per CTA
+
+struct Workspace {
+  int64_t M = 0, n = 0;
+  int rb = 0, cap = 0, N = 0, pmax = 0, wmax = 0, capp = 0, grid = 0;
+  bool record = false;
+  int LDW = 0, LDU = 0;
+  double* Wcat = nullptr;
+  double* Ubuf[3] = {nullptr, nullptr, nullptr};
+  double* Vbuf[3] = {nullptr, nullptr, nullptr};
+  double* BV = nullptr;
+  double* omega = nullptr;
+  int* ints = nullptr;        // rk[N+4], p, w, flags, esc
+  double* sigma = nullptr;    // (N+2) x 128
+  double* scal = nullptr;     // 8
+  double* T1 = nullptr; double* QV = nullptr; double* G = nullptr; double* R1 = nullptr;
+  double* T2 = nullptr; double* Z = nullptr;
+  double* partials = nullptr;
+  double* Uh = nullptr; double* Vh = nullptr;   // iterate history
+  double* tmpA = nullptr; size_t tmpA_sz = 0;   // hook scratch
+  double* tmpB = nullptr; size_t tmpB_sz = 0;
+  double* tmpC = nullptr; size_t tmpC_sz = 0;
+};
+
+struct GraphKey {
+  int64_t gen = -1, N = 0; int rb = 0, cap = 0; double gamma = 0, tol = 0; uint32_t flags = 0;
+  bool operator==(const GraphKey& o) const {
+    return gen == o.gen && N == o.N && rb == o.rb && cap == o.cap && gamma == o.gamma &&
+           tol == o.tol && flags == o.flags;
+  }
+};
+
+}  // namespace
+
+struct lrc_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::string err;
+  // operator
+  bool op_set = false, borrowed = false;
+  int64_t M = 0, nnz = 0;
+  int* row_ptr = nullptr; int* col_idx = nullptr; double* vals[6] = {};
+  int* group_ptr = nullptr; int ngroups = 0;
+  double rho = 0, lam = 0;
+  // params
+  bool par_set = false;
+  int64_t n = 0;
+  double* dmu = nullptr; double* dnu = nullptr;
+  Workspace ws;
+  int64_t gen = 0;
+  // graph
+  cudaGraphExec_t gexec = nullptr;
+  GraphKey gkey;
+  // last solve
+  int64_t last_N = 0; bool last_record = false; int last_cap = 0;
+  float last_kernel_ms = 0.f;
+};
+
+namespace {
+
+lrc_status fail(lrc_ctx* c, lrc_status s, const std::string& m) {
+  if (c) c->err = m;
+  return s;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? LRC_ERR_NOMEM : LRC_ERR_CUDA,   \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                    \
+  } while (0)
+
+void dfree(void* p) { if (p) cudaFree(p); }
+
+cudaMemcpyKind kind_in(lrc_mem where) {
+  return where == LRC_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+}
+cudaMemcpyKind kind_out(lrc_mem where) {
+  return where == LRC_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+}
+
+void free_ws(Workspace& w) {
+  dfree(w.Wcat);
+  for (int i = 0; i < 3; ++i) { dfree(w.Ubuf[i]); dfree(w.Vbuf[i]); }
+  dfree(w.BV); dfree(w.omega); dfree(w.ints); dfree(w.sigma); dfree(w.scal);
+  dfree(w.T1); dfree(w.QV); dfree(w.G); dfree(w.R1); dfree(w.T2); dfree(w.Z);
+  dfree(w.partials); dfree(w.Uh); dfree(w.Vh); dfree(w.tmpA); dfree(w.tmpB); dfree(w.tmpC);
+  w = Workspace();
+}
+
+void drop_graph(lrc_ctx* ctx) {
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  ctx->gexec = nullptr;
+  ctx->gkey = GraphKey();
+}
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t count) {
+  return cudaMalloc((void**)p, sizeof(T) * (count ? count : 1));
+}
+
+// Ensure a workspace for (M, n, r_B <= rb, rank cap, N iterations, wmax).
+lrc_status ensure_ws(lrc_ctx* ctx, int rb, int cap, int N, int wmax, bool record) {
+  Workspace& w = ctx->ws;
+  const int p_need = (int)std::min<int64_t>(ctx->n, wmax);
+  const int pmax = ts_pmax_for(p_need < 1 ? 1 : p_need);
+  const int capp = ts_pmax_for(cap);
+  if (w.Wcat && w.M == ctx->M && w.n == ctx->n && w.rb >= rb && w.cap == cap && w.N >= N &&
+      w.wmax >= wmax && w.pmax == pmax && (!record || w.record))
+    return LRC_OK;
+  cudaStreamSynchronize(ctx->stream);
+  drop_graph(ctx);
+  free_ws(w);
+  ++ctx->gen;
+  const size_t M = (size_t)ctx->M, n = (size_t)ctx->n;
+  w.M = ctx->M; w.n = ctx->n; w.rb = rb; w.cap = cap; w.N = N; w.pmax = pmax; w.wmax = wmax;
+  w.capp = capp; w.record = record;
+  w.LDW = rb + 3 * cap; w.LDW += (w.LDW & 1);
+  w.LDU = cap + (cap & 1);
+  w.grid = ts_grid_for((int)ctx->M);
+  CK(dalloc(&w.Wcat, M * w.LDW));
+  for (int i = 0; i < 3; ++i) {
+    CK(dalloc(&w.Ubuf[i], M * w.LDU));
+    CK(dalloc(&w.Vbuf[i], n * cap));
+  }
+  CK(dalloc(&w.BV, n * (rb > 0 ? rb : 1)));
+  CK(dalloc(&w.omega, (size_t)N + 1));
+  CK(dalloc(&w.ints, (size_t)N + 16));
+  CK(dalloc(&w.sigma, ((size_t)N + 4) * kSigmaStride));
+  CK(dalloc(&w.scal, 8));
+  CK(dalloc(&w.T1, (size_t)wmax * pmax));
+  CK(dalloc(&w.QV, n * pmax));
+  CK(dalloc(&w.G, (size_t)pmax * pmax));
+  CK(dalloc(&w.R1, (size_t)pmax * pmax));
+  CK(dalloc(&w.T2, (size_t)wmax * pmax));
+  CK(dalloc(&w.Z, (size_t)wmax * capp));
+  CK(dalloc(&w.partials, (size_t)w.grid * pmax * pmax));
+  if (record) {
+    CK(dalloc(&w.Uh, (size_t)N * M * w.LDU));
+    CK(dalloc(&w.Vh, (size_t)N * n * cap));
+  }
+  CK(cudaMemsetAsync(w.Wcat, 0, sizeof(double) * M * w.LDW, ctx->stream));
+  for (int i = 0; i < 3; ++i) {
+    CK(cudaMemsetAsync(w.Ubuf[i], 0, sizeof(double) * M * w.LDU, ctx->stream));
+    CK(cudaMemsetAsync(w.Vbuf[i], 0, sizeof(double) * n * cap, ctx->stream));
+  }
+  return LRC_OK;
+}
+
+lrc_status ensure_tmp(lrc_ctx* ctx, double** p, size_t* sz, size_t count) {
+  if (*sz >= count && *p) return LRC_OK;
+  cudaStreamSynchronize(ctx->stream);
+  dfree(*p);
+  *p = nullptr; *sz = 0;
+  CK(dalloc(p, count));
+  *sz = count;
+  return LRC_OK;
+}
+
+State make_state(Workspace& w) {
+  State s;
+  s.rk = w.ints;
+  s.p = w.ints + w.N + 4;
+  s.w = w.ints + w.N + 5;
+  s.flags = w.ints + w.N + 6;
+  s.esc = w.ints + w.N + 7;
+  s.sigma = w.sigma;
+  s.scal = w.scal;
+  return s;
+}
+
+SmallBufs make_bufs(Workspace& w) {
+  SmallBufs b{};
+  b.T1 = w.T1; b.QV = w.QV; b.G = w.G; b.R1 = w.R1; b.T2 = w.T2; b.Z = w.Z;
+  b.ldT = w.pmax; b.ldZ = w.capp;
+  return b;
+}
+
+SpmmArgs spmm_base(lrc_ctx* ctx) {
+  SpmmArgs a{};
+  a.M = (int)ctx->M;
+  a.ngroups = ctx->ngroups;
+  a.group_ptr = ctx->group_ptr;
+  a.row_ptr = ctx->row_ptr;
+  a.col_idx = ctx->col_idx;
+  for (int t = 0; t < 6; ++t) a.v[t] = ctx->vals[t];
+  a.rho = ctx->rho;
+  a.lam = ctx->lam;
+  return a;
+}
+
+// Truncation of Ucat V^T given the Vcat descriptor (a2-a6).  rank_slot / sigma_row: where the
+// rank and singular values go; Vout / Uout receive V_{new} (n x cap) and U_{new} (M x cap).
+lrc_status enqueue_truncation(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, const double* omega,
+                              int k, double tol, int cap, int rank_slot, int sigma_row,
+                              double* Uout, int ldu_out, double* Vout, int ldv_out,
+                              cudaStream_t s, bool fork_from_spmm) {
+  Workspace& w = ctx->ws;
+  State st = make_state(w);
+  SmallBufs b = make_bufs(w);
+  if (fork_from_spmm) {
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    CK(launch_vside(vd, (int)ctx->n, ctx->dmu, ctx->dnu, omega, k, st, b, w.wmax, ctx->side));
+    CK(cudaEventRecord(ctx->ev_join, ctx->side));
+    CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
+  } else {
+    CK(launch_vside(vd, (int)ctx->n, ctx->dmu, ctx->dnu, omega, k, st, b, w.wmax, s));
+  }
+  TsArgs ta{};
+  ta.M = (int)ctx->M;
+  ta.u = ud;
+  ta.rk = st.rk;
+  ta.T = w.T1;
+  ta.ldt = w.pmax;
+  ta.d_p = st.p;
+  ta.partials = w.partials;
+  CK(launch_ts(0, ta, w.pmax, w.grid, s));
+  CK(launch_gram_reduce(w.partials, w.grid, w.pmax, w.G, s));
+  CK(launch_chol1(st, b, w.pmax, w.wmax, s));
+  ta.T = w.T2;
+  CK(launch_ts(0, ta, w.pmax, w.grid, s));
+  CK(launch_gram_reduce(w.partials, w.grid, w.pmax, w.G, s));
+  CK(launch_chol2_svd(st, b, w.pmax, w.wmax, (int)ctx->n, tol, cap, rank_slot, sigma_row, Vout,
+                      ldv_out, s));
+  TsArgs tb{};
+  tb.M = (int)ctx->M;
+  tb.u = ud;
+  tb.rk = st.rk;
+  tb.T = w.Z;
+  tb.ldt = w.capp;
+  tb.d_p = st.rk + rank_slot;
+  tb.out = Uout;
+  tb.ldo = ldu_out;
+  CK(launch_ts(1, tb, w.capp, w.grid, s));
+  return LRC_OK;
+}
+
+// ||Ucat Vcat^T||_F^2 -> scal[slot]  (vside QR + one Gram pass; X = Y Q_V^T, ||X|| = ||Y||)
+lrc_status enqueue_norm2(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, int slot, cudaStream_t s) {
+  Workspace& w = ctx->ws;
+  State st = make_state(w);
+  SmallBufs b = make_bufs(w);
+  CK(launch_vside(vd, (int)ctx->n, ctx->dmu, ctx->dnu, nullptr, 0, st, b, w.wmax, s));
+  TsArgs ta{};
+  ta.M = (int)ctx->M;
+  ta.u = ud;
+  ta.rk = st.rk;
+  ta.T = w.T1;
+  ta.ldt = w.pmax;
+  ta.d_p = st.p;
+  ta.partials = w.partials;
+  CK(launch_ts(0, ta, w.pmax, w.grid, s));
+  CK(launch_gram_reduce(w.partials, w.grid, w.pmax, w.G, s));
+  CK(launch_trace(st, w.G, w.pmax, slot, s));
+  return LRC_OK;
+}
+
+VBlock vblock(const double* ptr, int ld, int w_fixed, int w_idx, double scale, int diag, int use_omega) {
+  VBlock v{};
+  v.ptr = ptr; v.ld = ld; v.w_fixed = w_fixed; v.w_idx = w_idx; v.w_mul = 1;
+  v.scale = scale; v.diag = diag; v.use_omega = use_omega;
+  return v;
+}
+
+// One ChebyshevT iteration k: X_k -> X_{k+1}.
+lrc_status enqueue_iteration(lrc_ctx* ctx, int k, int rb, int cap, double gamma, double tol,
+                             bool record) {
+  Workspace& w = ctx->ws;
+  cudaStream_t s = ctx->stream;
+  State st = make_state(w);
+  double* Ucur = w.Ubuf[(k + 1) % 3];
+  double* Uprev = w.Ubuf[k % 3];
+  double* Unext = w.Ubuf[(k + 2) % 3];
+  double* Vcur = w.Vbuf[(k + 1) % 3];
+  double* Vprev = w.Vbuf[k % 3];
+  double* Vnext = w.Vbuf[(k + 2) % 3];
+
+  CK(cudaEventRecord(ctx->ev_fork, s));
+  SpmmArgs a = spmm_base(ctx);
+  a.U = Ucur;
+  a.ldu = w.LDU;
+  a.d_r = st.rk + (k + 1);
+  a.out = w.Wcat;
+  a.ldo = w.LDW;
+  a.out_off = rb;
+  a.gamma = gamma;
+  CK(launch_spmm(SPMM_S2STEP, a, cap, s));
+
+  VDesc vd{};
+  vd.nb = 5;
+  vd.b[0] = vblock(w.BV, rb, rb, -1, gamma, 0, 1);             // w g B_V
+  vd.b[1] = vblock(Vcur, cap, 0, k + 1, 1.0, 0, 1);            // w V_k
+  vd.b[2] = vblock(Vcur, cap, 0, k + 1, -gamma, 1, 1);         // -w g d_mu * V_k
+  vd.b[3] = vblock(Vcur, cap, 0, k + 1, -gamma, 2, 1);         // -w g d_nu * V_k
+  vd.b[4] = vblock(Vprev, cap, 0, k, 1.0, 0, 2);               // (1-w) V_{k-1}
+  UDesc ud{};
+  ud.A = w.Wcat; ud.lda = w.LDW; ud.wa_fixed = rb; ud.wa_mul = 3; ud.wa_idx = k + 1;
+  ud.B = Uprev; ud.ldb = w.LDU; ud.wb_fixed = 0; ud.wb_idx = k;
+  lrc_status r = enqueue_truncation(ctx, ud, vd, w.omega, k, tol, cap, k + 2, k, Unext, w.LDU,
+                                    Vnext, cap, s, true);
+  if (r != LRC_OK) return r;
+  if (record) {
+    CK(cudaMemcpyAsync(w.Uh + (size_t)k * ctx->M * w.LDU, Unext,
+                       sizeof(double) * ctx->M * w.LDU, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(w.Vh + (size_t)k * ctx->n * cap, Vnext, sizeof(double) * ctx->n * cap,
+                       cudaMemcpyDeviceToDevice, s));
+  }
+  return LRC_OK;
+}
+
+std::vector<double> omega_schedule(double lmin, double lmax, int N, int restart) {
+  const double c = 0.5 * (lmax - lmin), d = 0.5 * (lmax + lmin);
+  std::vector<double> om(N > 0 ? N : 1, 1.0);
+  int j = 0;
+  double prev = 1.0;
+  for (int k = 0; k < N; ++k) {
+    if (restart > 0 && k > 0 && k % restart == 0) j = 0;
+    double wk;
+    if (j == 0) wk = 1.0;
+    else if (j == 1) wk = 1.0 / (1.0 - c * c / (2.0 * d * d));
+    else wk = 1.0 / (1.0 - prev * c * c / (4.0 * d * d));
+    om[k] = wk;
+    prev = wk;
+    ++j;
+  }
+  return om;
+}
+
+bool valid_mem(lrc_mem m) { return m == LRC_MEM_HOST || m == LRC_MEM_DEVICE; }
+
+}  // namespace
+
+// =============================================================================================
+// C ABI
+// =============================================================================================
+extern "C" {
+
+const char* lrc_version(void) { return "liblrcheb 0.1 (sm_100a, fp64)"; }
+
+lrc_status lrc_create(lrc_ctx** out, int device, void* cuda_stream) {
+  if (!out) return LRC_ERR_ARG;
+  *out = nullptr;
+  lrc_ctx* ctx = new (std::nothrow) lrc_ctx();
+  if (!ctx) return LRC_ERR_NOMEM;
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) { g_create_err = cudaGetErrorString(e); delete ctx; return LRC_ERR_CUDA; }
+  if (cuda_stream) {
+    ctx->stream = (cudaStream_t)cuda_stream;
+  } else {
+    e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { delete ctx; return LRC_ERR_CUDA; }
+    ctx->own_stream = true;
+  }
+  if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    lrc_destroy(ctx);
+    return LRC_ERR_CUDA;
+  }
+  for (int i = 0; i < 4; ++i)
+    if (cudaEventCreate(&ctx->ev[i]) != cudaSuccess) { lrc_destroy(ctx); return LRC_ERR_CUDA; }
+  cudaError_t pe = spmm_prepare();
+  if (pe == cudaSuccess) pe = ts_prepare();
+  if (pe == cudaSuccess) pe = small_prepare();
+  if (pe != cudaSuccess) {
+    g_create_err = std::string("kernel attribute setup: ") + cudaGetErrorString(pe);
+    lrc_destroy(ctx);
+    return LRC_ERR_CUDA;
+  }
+  *out = ctx;
+  return LRC_OK;
+}
+
+void lrc_destroy(lrc_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  drop_graph(ctx);
+  free_ws(ctx->ws);
+  if (!ctx->borrowed) {
+    dfree(ctx->row_ptr); dfree(ctx->col_idx);
+    for (int t = 0; t < 6; ++t) dfree(ctx->vals[t]);
+  }
+  dfree(ctx->group_ptr); dfree(ctx->dmu); dfree(ctx->dnu);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  for (int i = 0; i < 4; ++i) if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* lrc_last_error(const lrc_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+
+float lrc_last_kernel_ms(const lrc_ctx* ctx) { return ctx ? ctx->last_kernel_ms : 0.f; }
+
+lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t* row_ptr,
+                            const int32_t* col_idx, const double* const vals[6], double rho_f,
+                            double lambda_s, lrc_mem where) {
+  if (!ctx) return LRC_ERR_ARG;
+  ctx->err.clear();
+  if (M < 1 || M >= (int64_t)1 << 31) return fail(ctx, LRC_ERR_ARG, "M must be in [1, 2^31)");
+  if (nnz < 0 || nnz >= (int64_t)1 << 31) return fail(ctx, LRC_ERR_ARG, "nnz must be in [0, 2^31)");
+  if (!row_ptr || (nnz > 0 && !col_idx) || !vals) return fail(ctx, LRC_ERR_ARG, "null pointer");
+  for (int t = 0; t < 6; ++t)
+    if (nnz > 0 && !vals[t]) return fail(ctx, LRC_ERR_ARG, "null value array");
+  if (!std::isfinite(rho_f) || !std::isfinite(lambda_s)) return fail(ctx, LRC_ERR_ARG, "rho_f, lambda_s must be finite");
+  if (where != LRC_MEM_HOST && where != LRC_MEM_DEVICE && where != LRC_MEM_DEVICE_BORROW)
+    return fail(ctx, LRC_ERR_ARG, "bad lrc_mem");
+  CK(cudaSetDevice(ctx->device));
+  // host copies of the pattern for validation + node-block detection
+  std::vector<int32_t> hrp(M + 1), hci(nnz);
+  if (where == LRC_MEM_HOST) {
+    std::memcpy(hrp.data(), row_ptr, sizeof(int32_t) * (M + 1));
+    if (nnz) std::memcpy(hci.data(), col_idx, sizeof(int32_t) * nnz);
+  } else {
+    CK(cudaMemcpy(hrp.data(), row_ptr, sizeof(int32_t) * (M + 1), cudaMemcpyDeviceToHost));
+    if (nnz) CK(cudaMemcpy(hci.data(), col_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost));
+  }
+  if (hrp[0] != 0) return fail(ctx, LRC_ERR_ARG, "row_ptr[0] != 0");
+  if (hrp[M] != nnz) return fail(ctx, LRC_ERR_ARG, "row_ptr[M] != nnz");
+  for (int64_t i = 0; i < M; ++i) {
+    if (hrp[i + 1] < hrp[i]) return fail(ctx, LRC_ERR_ARG, "row_ptr not non-decreasing at row " + std::to_string(i));
+    for (int32_t e = hrp[i]; e < hrp[i + 1]; ++e) {
+      if (hci[e] < 0 || hci[e] >= M) return fail(ctx, LRC_ERR_ARG, "col_idx out of range in row " + std::to_string(i));
+      if (e > hrp[i] && hci[e] <= hci[e - 1])
+        return fail(ctx, LRC_ERR_ARG, "col_idx not strictly increasing in row " + std::to_string(i));
+    }
+  }
+  // node blocks: runs of consecutive rows with identical column lists (<= kGroupMax rows)
+  std::vector<int32_t> groups;
+  groups.reserve(M / 4 + 2);
+  groups.push_back(0);
+  int gsz = 1;
+  for (int64_t i = 1; i < M; ++i) {
+    const int32_t l0 = hrp[i] - hrp[i - 1], l1 = hrp[i + 1] - hrp[i];
+    bool same = (gsz < kGroupMax) && l0 == l1 &&
+                (l1 == 0 || std::memcmp(&hci[hrp[i - 1]], &hci[hrp[i]], sizeof(int32_t) * l1) == 0);
+    if (same) { ++gsz; }
+    else { groups.push_back((int32_t)i); gsz = 1; }
+  }
+  groups.push_back((int32_t)M);
+
+  CK(cudaStreamSynchronize(ctx->stream));
+  drop_graph(ctx);
+  free_ws(ctx->ws);
+  if (!ctx->borrowed) {
+    dfree(ctx->row_ptr); dfree(ctx->col_idx);
+    for (int t = 0; t < 6; ++t) dfree(ctx->vals[t]);
+  }
+  dfree(ctx->group_ptr);
+  ctx->row_ptr = nullptr; ctx->col_idx = nullptr; ctx->group_ptr = nullptr;
+  for (int t = 0; t < 6; ++t) ctx->vals[t] = nullptr;
+  ctx->op_set = false;
+  ctx->par_set = false;   // params depend on nothing here, but workspaces do; keep semantics simple
+  ++ctx->gen;
+
+  if (where == LRC_MEM_DEVICE_BORROW) {
+    ctx->borrowed = true;
+    ctx->row_ptr = const_cast<int*>(row_ptr);
+    ctx->col_idx = const_cast<int*>(col_idx);
+    for (int t = 0; t < 6; ++t) ctx->vals[t] = const_cast<double*>(vals[t]);
+  } else {
+    ctx->borrowed = false;
+    CK(dalloc(&ctx->row_ptr, M + 1));
+    CK(dalloc(&ctx->col_idx, nnz));
+    CK(cudaMemcpy(ctx->row_ptr, hrp.data(), sizeof(int32_t) * (M + 1), cudaMemcpyHostToDevice));
+    if (nnz) CK(cudaMemcpy(ctx->col_idx, hci.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
+    for (int t = 0; t < 6; ++t) {
+      CK(dalloc(&ctx->vals[t], nnz));
+      if (nnz) CK(cudaMemcpy(ctx->vals[t], vals[t], sizeof(double) * nnz, kind_in(where)));
+    }
+  }
+  CK(dalloc(&ctx->group_ptr, groups.size()));
+  CK(cudaMemcpy(ctx->group_ptr, groups.data(), sizeof(int32_t) * groups.size(), cudaMemcpyHostToDevice));
+  ctx->ngroups = (int)groups.size() - 1;
+  ctx->M = M;
+  ctx->nnz = nnz;
+  ctx->rho = rho_f;
+  ctx->lam = lambda_s;
+  ctx->op_set = true;
+  return LRC_OK;
+}
+
+lrc_status lrc_set_params(lrc_ctx* ctx, int64_t n, const double* d_mu, const double* d_nu, lrc_mem where) {
+  if (!ctx) return LRC_ERR_ARG;
+  ctx->err.clear();
+  if (!ctx->op_set) return fail(ctx, LRC_ERR_STATE, "lrc_set_params before lrc_set_operator");
+  if (n < 1 || n > 1024) return fail(ctx, LRC_ERR_ARG, "n must be in [1, 1024]");
+  if (!d_mu || !d_nu) return fail(ctx, LRC_ERR_ARG, "null pointer");
+  if (!valid_mem(where)) return fail(ctx, LRC_ERR_ARG, "bad lrc_mem");
+  CK(cudaSetDevice(ctx->device));
+  std::vector<double> hm(n), hn(n);
+  CK(cudaMemcpy(hm.data(), d_mu, sizeof(double) * n, where == LRC_MEM_HOST ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(hn.data(), d_nu, sizeof(double) * n, where == LRC_MEM_HOST ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < n; ++i)
+    if (!std::isfinite(hm[i]) || !std::isfinite(hn[i])) return fail(ctx, LRC_ERR_ARG, "d_mu / d_nu must be finite");
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (n != ctx->n) {
+    drop_graph(ctx);
+    free_ws(ctx->ws);
+    dfree(ctx->dmu); dfree(ctx->dnu);
+    ctx->dmu = ctx->dnu = nullptr;
+    CK(dalloc(&ctx->dmu, n));
+    CK(dalloc(&ctx->dnu, n));
+  }
+  CK(cudaMemcpy(ctx->dmu, hm.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->dnu, hn.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+  ctx->n = n;
+  ctx->par_set = true;
+  return LRC_OK;
+}
+
+lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const double* B_V, int64_t ld_bv,
+                     int64_t r_B, const lrc_solve_opts* opts, double* U_out, int64_t ld_u,
+                     double* V_out, int64_t ld_v, lrc_mem where, lrc_solve_info* info) {
+  if (!ctx) return LRC_ERR_ARG;
+  ctx->err.clear();
+  if (!ctx->op_set || !ctx->par_set) return fail(ctx, LRC_ERR_STATE, "lrc_solve before lrc_set_operator + lrc_set_params");
+  if (!opts) return fail(ctx, LRC_ERR_ARG, "null opts");
+  if (!valid_mem(where)) return fail(ctx, LRC_ERR_ARG, "bad lrc_mem");
+  const double lmin = opts->lambda_min, lmax = opts->lambda_max;
+  if (!(lmin > 0.0) || !(lmax >= lmin) || !std::isfinite(lmax))
+    return fail(ctx, LRC_ERR_ARG, "need 0 < lambda_min <= lambda_max (d > c >= 0)");
+  if (!(opts->tol >= 0.0) || !std::isfinite(opts->tol)) return fail(ctx, LRC_ERR_ARG, "tol must be finite and >= 0");
+  const int64_t M = ctx->M, n = ctx->n;
+  if (opts->rank_cap < 1 || opts->rank_cap > std::min<int64_t>(std::min(M, n), kMaxRank))
+    return fail(ctx, LRC_ERR_ARG, "rank_cap must be in [1, min(M, n, 128)]");
+  if (opts->n_iter < 1 || opts->n_iter > 100000) return fail(ctx, LRC_ERR_ARG, "n_iter must be in [1, 100000]");
+  if (opts->restart_every < 0) return fail(ctx, LRC_ERR_ARG, "restart_every must be >= 0");
+  if (r_B < 0 || r_B > 64) return fail(ctx, LRC_ERR_ARG, "r_B must be in [0, 64]");
+  if (r_B > 0 && (!B_U || !B_V)) return fail(ctx, LRC_ERR_ARG, "null B_U / B_V");
+  if (r_B > 0 && (ld_bu < r_B || ld_bv < r_B)) return fail(ctx, LRC_ERR_SHAPE, "ld_bu / ld_bv < r_B");
+  const int cap = (int)opts->rank_cap;
+  if (!U_out || !V_out) return fail(ctx, LRC_ERR_ARG, "null output");
+  if (ld_u < cap || ld_v < cap) return fail(ctx, LRC_ERR_SHAPE, "ld_u / ld_v < rank_cap");
+  const int rb = (int)r_B, N = (int)opts->n_iter;
+  const int wmax = std::max(rb + 4 * cap, 3 * cap + rb);
+  if (wmax > kMaxW) return fail(ctx, LRC_ERR_ARG, "r_B + 4 rank_cap must be <= 256");
+  const int p_need = (int)std::min<int64_t>(n, wmax);
+  if (p_need > 112) return fail(ctx, LRC_ERR_ARG, "min(n, r_B + 4 rank_cap) must be <= 112 in this build");
+  if (lrc::vside_smem_bytes((int)n, wmax, ts_pmax_for(p_need)) > kSmemLimit)
+    return fail(ctx, LRC_ERR_ARG, "n x (r_B + 4 rank_cap) too large for the single-CTA V-side QR");
+  const bool record = (opts->flags & LRC_RECORD_ITERATES) != 0;
+  const bool use_graph = (opts->flags & LRC_NO_GRAPH) == 0;
+  CK(cudaSetDevice(ctx->device));
+  lrc_status st = ensure_ws(ctx, std::max(rb, 1), cap, N, wmax, record);
+  if (st != LRC_OK) return st;
+  Workspace& w = ctx->ws;
+  cudaStream_t s = ctx->stream;
+  State sd = make_state(w);
+  const double c_ = 0.5 * (lmax - lmin), d_ = 0.5 * (lmax + lmin);
+  (void)c_;
+  const double gamma = 1.0 / d_;
+
+  CK(cudaEventRecord(ctx->ev[0], s));
+  // inputs: B_U into Wcat[:, :rb], B_V into BV
+  if (rb > 0) {
+    CK(cudaMemcpy2DAsync(w.Wcat, sizeof(double) * w.LDW, B_U, sizeof(double) * ld_bu,
+                         sizeof(double) * rb, M, kind_in(where), s));
+    CK(cudaMemcpy2DAsync(w.BV, sizeof(double) * rb, B_V, sizeof(double) * ld_bv,
+                         sizeof(double) * rb, n, kind_in(where), s));
+  }
+  std::vector<double> om = omega_schedule(lmin, lmax, N, (int)opts->restart_every);
+  CK(cudaMemcpyAsync(w.omega, om.data(), sizeof(double) * N, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(w.ints, 0, sizeof(int) * (w.N + 16), s));
+  CK(cudaMemsetAsync(w.scal, 0, sizeof(double) * 8, s));
+  CK(cudaMemsetAsync(w.sigma, 0, sizeof(double) * (size_t)(N + 4) * kSigmaStride, s));
+
+  if (rb > 0) {
+    // ||B||_F^2 -> scal[0]
+    UDesc ub{};
+    ub.A = w.Wcat; ub.lda = w.LDW; ub.wa_fixed = rb; ub.wa_idx = -1; ub.B = nullptr; ub.wb_idx = -1;
+    VDesc vb{};
+    vb.nb = 1;
+    vb.b[0] = vblock(w.BV, rb, rb, -1, 1.0, 0, 0);
+    st = enqueue_norm2(ctx, ub, vb, 0, s);
+    if (st != LRC_OK) return st;
+
+    CK(cudaEventRecord(ctx->ev[1], s));
+    const uint32_t gflags = opts->flags & (LRC_RECORD_ITERATES);
+    GraphKey key;
+    key.gen = ctx->gen; key.N = N; key.rb = rb; key.cap = cap; key.gamma = gamma; key.tol = opts->tol;
+    key.flags = gflags;
+    if (use_graph) {
+      if (!(ctx->gexec && ctx->gkey == key)) {
+        drop_graph(ctx);
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        lrc_status es = LRC_OK;
+        for (int k = 0; k < N && es == LRC_OK; ++k)
+          es = enqueue_iteration(ctx, k, rb, cap, gamma, opts->tol, record);
+        cudaGraph_t g = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(s, &g);
+        if (es != LRC_OK) { if (g) cudaGraphDestroy(g); return es; }
+        if (ce != cudaSuccess) return fail(ctx, LRC_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+        ce = cudaGraphInstantiate(&ctx->gexec, g, 0);
+        cudaGraphDestroy(g);
+        if (ce != cudaSuccess) { ctx->gexec = nullptr; return fail(ctx, LRC_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce)); }
+        ctx->gkey = key;
+      }
+      CK(cudaGraphLaunch(ctx->gexec, s));
+    } else {
+      for (int k = 0; k < N; ++k) {
+        st = enqueue_iteration(ctx, k, rb, cap, gamma, opts->tol, record);
+        if (st != LRC_OK) return st;
+      }
+    }
+    CK(cudaEventRecord(ctx->ev[2], s));
+    const int slotN = N + 1;   // rk index of X_N
+    double* UN = w.Ubuf[(N + 1) % 3];
+    double* VN = w.Vbuf[(N + 1) % 3];
+    if (!(opts->flags & LRC_SKIP_FINAL_RESIDUAL)) {
+      // residual factors: Ucat = [B_U | W0 | W1 | W2], Vcat = [B_V | -V | -d_mu V | -d_nu V]
+      SpmmArgs a = spmm_base(ctx);
+      a.U = UN; a.ldu = w.LDU; a.d_r = sd.rk + slotN; a.out = w.Wcat; a.ldo = w.LDW; a.out_off = rb;
+      CK(launch_spmm(SPMM_PLAIN3, a, cap, s));
+      UDesc ur{};
+      ur.A = w.Wcat; ur.lda = w.LDW; ur.wa_fixed = rb; ur.wa_mul = 3; ur.wa_idx = slotN; ur.B = nullptr; ur.wb_idx = -1;
+      VDesc vr{};
+      vr.nb = 4;
+      vr.b[0] = vblock(w.BV, rb, rb, -1, 1.0, 0, 0);
+      vr.b[1] = vblock(VN, cap, 0, slotN, -1.0, 0, 0);
+      vr.b[2] = vblock(VN, cap, 0, slotN, -1.0, 1, 0);
+      vr.b[3] = vblock(VN, cap, 0, slotN, -1.0, 2, 0);
+      st = enqueue_norm2(ctx, ur, vr, 1, s);
+      if (st != LRC_OK) return st;
+    }
+    // outputs (zero the columns >= rank)
+    CK(launch_zero_cols(UN, (int)M, w.LDU, sd.rk + slotN, 0, cap, s));
+    CK(launch_zero_cols(VN, (int)n, cap, sd.rk + slotN, 0, cap, s));
+    CK(cudaMemcpy2DAsync(U_out, sizeof(double) * ld_u, UN, sizeof(double) * w.LDU, sizeof(double) * cap, M, kind_out(where), s));
+    CK(cudaMemcpy2DAsync(V_out, sizeof(double) * ld_v, VN, sizeof(double) * cap, sizeof(double) * cap, n, kind_out(where), s));
+  } else {
+    CK(cudaEventRecord(ctx->ev[1], s));
+    CK(cudaEventRecord(ctx->ev[2], s));
+    if (where == LRC_MEM_HOST) {
+      for (int64_t i = 0; i < M; ++i) std::memset(U_out + i * ld_u, 0, sizeof(double) * cap);
+      for (int64_t i = 0; i < n; ++i) std::memset(V_out + i * ld_v, 0, sizeof(double) * cap);
+    } else {
+      CK(cudaMemset2DAsync(U_out, sizeof(double) * ld_u, 0, sizeof(double) * cap, M, s));
+      CK(cudaMemset2DAsync(V_out, sizeof(double) * ld_v, 0, sizeof(double) * cap, n, s));
+    }
+  }
+  CK(cudaEventRecord(ctx->ev[3], s));
+  // results
+  std::vector<int> ints(w.N + 16, 0);
+  std::vector<double> scal(8, 0.0);
+  CK(cudaMemcpyAsync(ints.data(), w.ints, sizeof(int) * (w.N + 16), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(scal.data(), w.scal, sizeof(double) * 8, cudaMemcpyDeviceToHost, s));
+  std::vector<double> sig;
+  if (info && info->sigma_history) {
+    sig.resize((size_t)N * kSigmaStride);
+    CK(cudaMemcpyAsync(sig.data(), w.sigma, sizeof(double) * sig.size(), cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  ctx->last_N = N;
+  ctx->last_record = record;
+  ctx->last_cap = cap;
+  const int flags = ints[w.N + 6];
+  if (info) {
+    float ms_it = 0.f, ms_tot = 0.f;
+    cudaEventElapsedTime(&ms_it, ctx->ev[1], ctx->ev[2]);
+    cudaEventElapsedTime(&ms_tot, ctx->ev[0], ctx->ev[3]);
+    info->rank = rb > 0 ? ints[N + 1] : 0;
+    const double b2 = scal[0];
+    info->b_norm = std::sqrt(b2);
+    if (opts->flags & LRC_SKIP_FINAL_RESIDUAL) info->rel_residual = NAN;
+    else info->rel_residual = (b2 > 0.0) ? std::sqrt(scal[1] / b2) : 0.0;
+    info->diverged = (info->rel_residual > 1.0) ? 1 : 0;
+    info->shift_escalations = ints[w.N + 7];
+    info->ms_iterations = ms_it;
+    info->ms_total = ms_tot;
+    if (info->rank_history)
+      for (int k = 0; k < N; ++k) info->rank_history[k] = rb > 0 ? ints[k + 2] : 0;
+    if (info->sigma_history) std::memcpy(info->sigma_history, sig.data(), sizeof(double) * sig.size());
+  }
+  if (flags & 1) return fail(ctx, LRC_ERR_NUMERIC, "shifted Cholesky failed after all escalations");
+  if (flags & 2) return fail(ctx, LRC_ERR_NUMERIC, "non-finite singular value in the core SVD");
+  return LRC_OK;
+}
+
+lrc_status lrc_apply_lowrank(lrc_ctx* ctx, const double* U, int64_t ld_u, int64_t r, double* W,
+                             int64_t ld_w, uint32_t mode, double gamma, lrc_mem where) {
+  if (!ctx) return LRC_ERR_ARG;
+  ctx->err.clear();
+  if (!ctx->op_set) return fail(ctx, LRC_ERR_STATE, "lrc_apply_lowrank before lrc_set_operator");
+  if (!valid_mem(where)) return fail(ctx, LRC_ERR_ARG, "bad lrc_mem");
+  if (r < 1 || r > kMaxRank) return fail(ctx, LRC_ERR_ARG, "r must be in [1, 128]");
+  if (!U || !W) return fail(ctx, LRC_ERR_ARG, "null pointer");
+  if (mode > LRC_APPLY_S2STEP) return fail(ctx, LRC_ERR_ARG, "bad mode");
+  const int nout = (mode == LRC_APPLY_SIX) ? 6 : 3;
+  if (ld_u < r || ld_w < nout * r) return fail(ctx, LRC_ERR_SHAPE, "leading dimension too small");
+  CK(cudaSetDevice(ctx->device));
+  const int64_t M = ctx->M;
+  cudaStream_t s = ctx->stream;
+  const double* Ud = U;
+  double* Wd = W;
+  int ldu = (int)ld_u, ldw = (int)ld_w;
+  if (where == LRC_MEM_HOST) {
+    lrc_status st = ensure_tmp(ctx, &ctx->ws.tmpA, &ctx->ws.tmpA_sz, (size_t)M * r);
+    if (st != LRC_OK) return st;
+    st = ensure_tmp(ctx, &ctx->ws.tmpB, &ctx->ws.tmpB_sz, (size_t)M * nout * r);
+    if (st != LRC_OK) return st;
+    CK(cudaMemcpy2DAsync(ctx->ws.tmpA, sizeof(double) * r, U, sizeof(double) * ld_u, sizeof(double) * r, M, cudaMemcpyHostToDevice, s));
+    Ud = ctx->ws.tmpA; ldu = (int)r;
+    Wd = ctx->ws.tmpB; ldw = nout * (int)r;
+  }
+  SpmmArgs a = spmm_base(ctx);
+  a.U = Ud; a.ldu = ldu; a.d_r = nullptr; a.r_fixed = (int)r; a.out = Wd; a.ldo = ldw; a.out_off = 0;
+  a.gamma = gamma;
+  CK(cudaEventRecord(ctx->ev[0], s));
+  if (mode == LRC_APPLY_SIX) {
+    for (int t = 0; t < 6; ++t) {
+      a.single_t = t;
+      a.out_off = t * (int)r;
+      CK(launch_spmm(SPMM_SINGLE, a, (int)r, s));
+    }
+  } else {
+    CK(launch_spmm(mode == LRC_APPLY_S2STEP ? SPMM_S2STEP : SPMM_PLAIN3, a, (int)r, s));
+  }
+  CK(cudaEventRecord(ctx->ev[1], s));
+  if (where == LRC_MEM_HOST)
+    CK(cudaMemcpy2DAsync(W, sizeof(double) * ld_w, Wd, sizeof(double) * ldw, sizeof(double) * nout * r, M, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  cudaEventElapsedTime(&ctx->last_kernel_ms, ctx->ev[0], ctx->ev[1]);
+  return LRC_OK;
+}
+
+lrc_status lrc_apply_dense(lrc_ctx* ctx, const double* S, int64_t ld_s, int64_t ncols, double* Y,
+                           int64_t ld_y, lrc_mem where) {
+  if (!ctx) return LRC_ERR_ARG;
+  ctx->err.clear();
+  if (!ctx->op_set || !ctx->par_set) return fail(ctx, LRC_ERR_STATE, "lrc_apply_dense before set_operator + set_params");
+  if (!valid_mem(where)) return fail(ctx, LRC_ERR_ARG, "bad lrc_mem");
+  if (ncols != ctx->n) return fail(ctx, LRC_ERR_SHAPE, "ncols must equal n of lrc_set_params");
+  if (ncols < 1 || ncols > 256) return fail(ctx, LRC_ERR_ARG, "ncols must be in [1, 256]");
+  if (!S || !Y) return fail(ctx, LRC_ERR_ARG, "null pointer");
+  if (ld_s < ncols || ld_y < ncols) return fail(ctx, LRC_ERR_SHAPE, "leading dimension too small");
+  CK(cudaSetDevice(ctx->device));
+  const int64_t M = ctx->M;
+  cudaStream_t s = ctx->stream;
+  const double* Sd = S;
+  double* Yd = Y;
+  int lds = (int)ld_s, ldy = (int)ld_y;
+  if (where == LRC_MEM_HOST) {
+    lrc_status st = ensure_tmp(ctx, &ctx->ws.tmpA, &ctx->ws.tmpA_sz, (size_t)M * ncols);
+    if (st != LRC_OK) return st;
+    st = ensure_tmp(ctx, &ctx->ws.tmpB, &ctx->ws.tmpB_sz, (size_t)M * ncols);
+    if (st != LRC_OK) return st;
+    CK(cudaMemcpy2DAsync(ctx->ws.tmpA, sizeof(double) * ncols, S, sizeof(double) * ld_s, sizeof(double) * ncols, M, cudaMemcpyHostToDevice, s));
+    Sd = ctx->ws.tmpA; lds = (int)ncols;
+    Yd = ctx->ws.tmpB; ldy = (int)ncols;
+  }
+  SpmmArgs a = spmm_base(ctx);
+  a.U = Sd; a.ldu = lds; a.d_r = nullptr; a.r_fixed = (int)ncols; a.out = Yd; a.ldo = ldy;
+  a.dmu = ctx->dmu; a.dnu = ctx->dnu;
+  CK(cudaEventRecord(ctx->ev[0], s));
+  CK(launch_spmm(SPMM_DENSE, a, (int)ncols, s));
+  CK(cudaEventRecord(ctx->ev[1], s));
+  if (where == LRC_MEM_HOST)
+    CK(cudaMemcpy2DAsync(Y, sizeof(double) * ld_y, Yd, sizeof(double) * ldy, sizeof(double) * ncols, M, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  cudaEventElapsedTime(&ctx->last_kernel_ms, ctx->ev[0], ctx->ev[1]);
+  return LRC_OK;
+}
+
+lrc_status lrc_truncate(lrc_ctx* ctx, const double* U, int64_t ld_u, const double* V, int64_t ld_v,
+                        int64_t wdt, double tol, int64_t cap, double* U_out, double* V_out,
+                        int64_t* rank, double* sigma, lrc_mem where) {
+  if (!ctx) return LRC_ERR_ARG;
+  ctx->err.clear();
+  if (!ctx->op_set || !ctx->par_set) return fail(ctx, LRC_ERR_STATE, "lrc_truncate before set_operator + set_params");
+  if (!valid_mem(where)) return fail(ctx, LRC_ERR_ARG, "bad lrc_mem");
+  if (wdt < 1 || wdt > kMaxW) return fail(ctx, LRC_ERR_ARG, "w must be in [1, 256]");
+  if (cap < 1 || cap > std::min<int64_t>(kMaxRank, std::min(ctx->M, ctx->n))) return fail(ctx, LRC_ERR_ARG, "cap must be in [1, min(M, n, 128)]");
+  if (!(tol >= 0.0)) return fail(ctx, LRC_ERR_ARG, "tol must be >= 0");
+  if (!U || !V || !U_out || !V_out || !rank) return fail(ctx, LRC_ERR_ARG, "null pointer");
+  if (ld_u < wdt || ld_v < wdt) return fail(ctx, LRC_ERR_SHAPE, "leading dimension too small");
+  const int64_t M = ctx->M, n = ctx->n;
+  const int w = (int)wdt, capi = (int)cap;
+  const int p_need = (int)std::min<int64_t>(n, w);
+  if (p_need > 112) return fail(ctx, LRC_ERR_ARG, "min(n, w) must be <= 112 in this build");
+  const int wmax = std::max(w, 4 * capi + 1);
+  if (lrc::vside_smem_bytes((int)n, std::max(w, 1), ts_pmax_for(p_need)) > kSmemLimit)
+    return fail(ctx, LRC_ERR_ARG, "n x w too large for the single-CTA V-side QR");
+  CK(cudaSetDevice(ctx->device));
+  lrc_status st = ensure_ws(ctx, std::max(ctx->ws.rb, 1), capi, std::max(ctx->ws.N, 1),
+                            std::max(wmax, ctx->ws.wmax), ctx->ws.record);
+  if (st != LRC_OK) return st;
+  Workspace& ws = ctx->ws;
+  cudaStream_t s = ctx->stream;
+  // inputs
+  st = ensure_tmp(ctx, &ws.tmpA, &ws.tmpA_sz, (size_t)M * w);
+  if (st != LRC_OK) return st;
+  st = ensure_tmp(ctx, &ws.tmpB, &ws.tmpB_sz, (size_t)n * w + (size_t)n * capi);
+  if (st != LRC_OK) return st;
+  st = ensure_tmp(ctx, &ws.tmpC, &ws.tmpC_sz, (size_t)M * capi);
+  if (st != LRC_OK) return st;
+  CK(cudaMemcpy2DAsync(ws.tmpA, sizeof(double) * w, U, sizeof(double) * ld_u, sizeof(double) * w, M, kind_in(where), s));
+  CK(cudaMemcpy2DAsync(ws.tmpB, sizeof(double) * w, V, sizeof(double) * ld_v, sizeof(double) * w, n, kind_in(where), s));
+  State sd = make_state(ws);
+  const int slot = ws.N + 2;
+  CK(cudaMemsetAsync(ws.ints, 0, sizeof(int) * (ws.N + 16), s));
+  CK(cudaMemsetAsync(ws.sigma, 0, sizeof(double) * (size_t)(ws.N + 4) * kSigmaStride, s));
+  UDesc ud{};
+  ud.A = ws.tmpA; ud.lda = w; ud.wa_fixed = w; ud.wa_idx = -1; ud.B = nullptr; ud.wb_idx = -1;
+  VDesc vd{};
+  vd.nb = 1;
+  vd.b[0] = vblock(ws.tmpB, w, w, -1, 1.0, 0, 0);
+  double* Vnew = ws.tmpB + (size_t)n * w;
+  st = enqueue_truncation(ctx, ud, vd, nullptr, 0, tol, capi, slot, ws.N, ws.tmpC, capi, Vnew, capi, s, false);
+  if (st != LRC_OK) return st;
+  CK(launch_zero_cols(ws.tmpC, (int)M, capi, sd.rk + slot, 0, capi, s));
+  CK(cudaMemcpyAsync(U_out, ws.tmpC, sizeof(double) * M * capi, kind_out(where), s));
+  CK(cudaMemcpyAsync(V_out, Vnew, sizeof(double) * n * capi, kind_out(where), s));
+  int hr = 0, flags = 0;
+  CK(cudaMemcpyAsync(&hr, sd.rk + slot, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&flags, sd.flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+  std::vector<double> sg(kSigmaStride);
+  CK(cudaMemcpyAsync(sg.data(), ws.sigma + (size_t)ws.N * kSigmaStride, sizeof(double) * kSigmaStride, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  *rank = hr;
+  if (sigma) std::memcpy(sigma, sg.data(), sizeof(double) * p_need);
+  ctx->last_record = false;   // tmp state overwrote the iterate bookkeeping slots
+  if (flags & 1) return fail(ctx, LRC_ERR_NUMERIC, "shifted Cholesky failed after all escalations");
+  if (flags & 2) return fail(ctx, LRC_ERR_NUMERIC, "non-finite singular value in the core SVD");
+  return LRC_OK;
+}
+
+lrc_status lrc_get_iterate(lrc_ctx* ctx, int64_t k, double* U, double* V, int64_t* rank, lrc_mem where) {
+  if (!ctx) return LRC_ERR_ARG;
+  ctx->err.clear();
+  if (!ctx->last_record || !ctx->ws.Uh) return fail(ctx, LRC_ERR_STATE, "no recorded iterates (solve with LRC_RECORD_ITERATES)");
+  if (k < 1 || k > ctx->last_N) return fail(ctx, LRC_ERR_ARG, "k must be in [1, n_iter]");
+  if (!U || !V || !rank) return fail(ctx, LRC_ERR_ARG, "null pointer");
+  if (!valid_mem(where)) return fail(ctx, LRC_ERR_ARG, "bad lrc_mem");
+  CK(cudaSetDevice(ctx->device));
+  Workspace& w = ctx->ws;
+  cudaStream_t s = ctx->stream;
+  const int cap = ctx->last_cap;
+  const size_t M = (size_t)ctx->M, n = (size_t)ctx->n;
+  int hr = 0;
+  CK(cudaMemcpyAsync(&hr, w.ints + (k + 1), sizeof(int), cudaMemcpyDeviceToHost, s));
+  double* Uk = w.Uh + (size_t)(k - 1) * M * w.LDU;
+  CK(launch_zero_cols(Uk, (int)M, w.LDU, w.ints + (k + 1), 0, cap, s));
+  const double* Vk = w.Vh + (size_t)(k - 1) * n * cap;
+  CK(cudaMemcpy2DAsync(U, sizeof(double) * cap, Uk, sizeof(double) * w.LDU, sizeof(double) * cap, M, kind_out(where), s));
+  CK(cudaMemcpyAsync(V, Vk, sizeof(double) * n * cap, kind_out(where), s));
+  CK(cudaStreamSynchronize(s));
+  *rank = hr;
+  return LRC_OK;
+}
+
+}  // extern "C"

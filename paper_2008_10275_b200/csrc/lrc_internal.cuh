@@ -1,0 +1,122 @@
+// Internal declarations shared by the liblrcheb translation units (kernels + C ABI driver).
+// Product code only: nothing here is shared with oracle/ (DESIGN.md "Independence").
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lrc {
+
+constexpr int kMaxRank = 128;    // rank_cap limit
+constexpr int kMaxP = 128;       // max Gram width p = min(n, w)
+constexpr int kMaxW = 256;       // max concatenation width w = r_B + 4 r
+constexpr int kGroupMax = 8;     // rows per node block in the fused SpMM
+constexpr int kSigmaStride = 128;
+
+// ------------------------------------------------------------------------------------------
+// a1: fused six-array CSR SpMM
+// ------------------------------------------------------------------------------------------
+enum SpmmMode { SPMM_S2STEP = 0, SPMM_PLAIN3 = 1, SPMM_SINGLE = 2, SPMM_DENSE = 3 };
+
+struct SpmmArgs {
+  int M;
+  int ngroups;
+  const int* group_ptr;     // [ngroups+1] first row of each node block
+  const int* row_ptr;
+  const int* col_idx;
+  const double* v[6];       // A0, A1, A2, Jrho, Jmu, Jlam
+  double rho, lam;
+  const double* U;          // M x r input (row-major, ld ldu)
+  int ldu;
+  const int* d_r;           // r = d_r ? *d_r : r_fixed   (device-resident rank)
+  int r_fixed;
+  double* out;              // outputs at out[row*ldo + out_off + t*r + c]
+  int ldo;
+  int out_off;
+  double gamma;             // S2STEP: out0 = U - gamma * W0
+  int single_t;             // SINGLE: output c_t A_t U
+  const double* dmu;        // DENSE: per-column scalings
+  const double* dnu;
+};
+cudaError_t launch_spmm(int mode, const SpmmArgs& a, int rmax, cudaStream_t s);
+
+// ------------------------------------------------------------------------------------------
+// a3/a4/a6: tall-skinny DMMA kernels over the logical concatenation Ucat = [A | B]
+// ------------------------------------------------------------------------------------------
+struct UDesc {
+  const double* A; int lda; int wa_fixed; int wa_mul; int wa_idx;  // wa = wa_fixed + wa_mul*rk[wa_idx]
+  const double* B; int ldb; int wb_fixed; int wb_idx;              // wb = wb_idx>=0 ? rk[wb_idx] : wb_fixed
+};
+
+struct TsArgs {
+  int M;
+  UDesc u;
+  const int* rk;            // device rank array (may be null if no *_idx is used)
+  const double* T;          // w x p small right matrix (row-major, ld ldt)
+  int ldt;
+  const int* d_p;           // p = d_p ? *d_p : p_fixed
+  int p_fixed;
+  double* partials;         // GRAM: [gridDim.x][pmax*pmax]
+  double* out;              // STORE: M x p (ld ldo)
+  int ldo;
+};
+// mode 0 = GRAM (partial X^T X, X = Ucat T), 1 = STORE (out = Ucat T)
+cudaError_t launch_ts(int mode, const TsArgs& a, int pmax, int grid, cudaStream_t s);
+int ts_pmax_for(int p);          // padded width used by the instantiations
+int ts_grid_for(int M);          // persistent grid size
+// G = sum_b partials[b] (fixed order), full symmetric pmax x pmax
+cudaError_t launch_gram_reduce(const double* partials, int nblocks, int pmax, double* G,
+                               cudaStream_t s);
+
+// ------------------------------------------------------------------------------------------
+// a2/a5: small dense kernels (single CTA)
+// ------------------------------------------------------------------------------------------
+struct VBlock {
+  const double* ptr; int ld;
+  int w_fixed; int w_idx; int w_mul;   // width = w_idx>=0 ? w_mul*rk[w_idx] : w_fixed ... (see kernel)
+  double scale;                        // block multiplier
+  int diag;                            // 0: none, 1: d_mu, 2: d_nu
+  int use_omega;                       // 0: scale, 1: scale*omega, 2: scale*(1-omega)
+};
+struct VDesc { VBlock b[5]; int nb; };
+
+struct State {          // device-resident per-solve state
+  int* rk;              // rank array, rk[j] = rank of X_{j-1} (j = 0..N+1)
+  int* p;               // current Gram width p = min(n, w)
+  int* w;               // current concatenation width
+  int* flags;           // error bits (1: Cholesky failed after escalations, 2: NaN)
+  int* esc;             // shift escalations
+  double* sigma;        // [N][kSigmaStride]
+  double* scal;         // scalar slots: [0] ||B||^2, [1] ||R||^2 residual
+};
+
+struct SmallBufs {
+  double* Vcat_unused;
+  double* T1;     // w x pmax   (R_V^T)
+  double* QV;     // n x pmax   (Q_V[:, :p])
+  double* G;      // pmax x pmax reduced Gram
+  double* R1;     // pmax x pmax
+  double* T2;     // w x pmax   (R_V^T R1^{-1})
+  double* Z;      // w x capp   (R_V^T W_r Sigma_r^{-1})
+  int ldT;        // = pmax
+  int ldZ;        // = capp
+};
+
+// vside: build Vcat (n x w) from the descriptor, Householder QR, write T1 = R_V^T and Q_V.
+cudaError_t launch_vside(const VDesc& d, int n, const double* dmu, const double* dnu,
+                         const double* omega, int k, State st, SmallBufs b, int wmax,
+                         cudaStream_t s);
+// chol1: R1 = chol(G + s1 I) (escalating), T2 = T1 R1^{-1}
+cudaError_t launch_chol1(State st, SmallBufs b, int pmax, int wmax, cudaStream_t s);
+// chol2 + SVD: R2 = chol(G + s2 I), R = R2 R1, Jacobi SVD, rank rule, Z, V'
+cudaError_t launch_chol2_svd(State st, SmallBufs b, int pmax, int wmax, int n, double tol,
+                             int cap, int rank_slot, int sigma_row, double* Vout, int ldv,
+                             cudaStream_t s);
+// scal[slot] = trace(G) over p (for ||X||_F^2)
+cudaError_t launch_trace(State st, const double* G, int pmax, int slot, cudaStream_t s);
+
+// misc
+cudaError_t launch_fill_int(int* p, int v, int n, cudaStream_t s);
+cudaError_t launch_zero_cols(double* X, int rows, int ld, const int* d_r, int r_fixed, int cols,
+                             cudaStream_t s);
+
+}  // namespace lrc

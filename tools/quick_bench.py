@@ -1,0 +1,45 @@
+"""Developer timing probe (not the contract bench): per-kernel-class timings on one config."""
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+from paper_2008_10275_b200 import lrcheb  # noqa: E402
+from synth import generator as gen  # noqa: E402
+
+
+def main(name="large", N=20):
+    t0 = time.time()
+    prob = gen.make_problem(name)
+    print(f"generate {name}: {time.time() - t0:.1f}s  M={prob.op.M} nnz={prob.op.nnz} "
+          f"bounds=[{prob.lam_min:.4f},{prob.lam_max:.4f}]", flush=True)
+    cfg, op = prob.cfg, prob.op
+    d_mu, d_nu, BU, BV = prob.subset(0)
+    dev = torch.device("cuda:0")
+    ctx = lrcheb.Context(0)
+    ctx.set_operator(torch.from_numpy(op.row_ptr).to(dev), torch.from_numpy(op.col_idx).to(dev),
+                     [torch.from_numpy(v).to(dev) for v in op.vals], op.rho_f, op.lambda_s)
+    ctx.set_params(d_mu, d_nu)
+    r = cfg.rank_cap
+    U = torch.randn(op.M, r, dtype=torch.float64, device=dev)
+    for _ in range(3):
+        ctx.apply_lowrank(U, lrcheb.LRC_APPLY_S2STEP, 0.1)
+    ms = []
+    for _ in range(5):
+        ctx.apply_lowrank(U, lrcheb.LRC_APPLY_S2STEP, 0.1)
+        ms.append(ctx.last_kernel_ms())
+    byts = 52 * op.nnz + 4 * (op.M + 1) + 32 * op.M * r
+    t = float(np.median(ms))
+    print(f"K1 S2STEP r={r}: {t:.3f} ms  {byts / t / 1e6:.0f} GB/s  ({byts / 1e9:.3f} GB)", flush=True)
+    bu, bv = torch.from_numpy(BU).to(dev), torch.from_numpy(BV).to(dev)
+    for it in range(3):
+        Uo, Vo, info = ctx.solve(bu, bv, prob.lam_min, prob.lam_max, cfg.tol, r, N, skip_residual=(it < 2))
+        print(f"solve N={N}: iters {info['ms_iterations']:.2f} ms ({info['ms_iterations'] / N:.3f} ms/it) "
+              f"total {info['ms_total']:.2f} ms ranks {info['rank_history'][:6]}..{info['rank_history'][-1]} "
+              f"rho={info['rel_residual']:.3e} esc={info['shift_escalations']}", flush=True)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "large", int(sys.argv[2]) if len(sys.argv) > 2 else 20)
