@@ -147,6 +147,17 @@ lrc_status lrc_get_iterate(lrc_ctx *ctx, int64_t k, double *U, double *V, int64_
  * call's kernel, for the bench's SpMM roofline. */
 float lrc_last_kernel_ms(const lrc_ctx *ctx);
 
+/* Number of liblrcheb kernels launched on ctx so far (a graph replay counts its kernel nodes). */
+int64_t lrc_kernel_launches(const lrc_ctx *ctx);
+
+/* Per-kernel-class profiling with CUDA events on the launching stream (bench roofline pass).
+ * on != 0 resets the accumulators and makes lrc_solve launch directly (no graph) with an event
+ * pair around every kernel.  lrc_get_profile(ctx, cls, &name, &ms, &count) returns the number of
+ * classes and, for 0 <= cls < that number, the class name, its accumulated device ms and launch
+ * count (classes: spmm, vside_qr, ts_gram, gram_reduce, chol1, chol2_svd, ts_store, trace, misc). */
+void lrc_set_profiling(lrc_ctx *ctx, int on);
+int  lrc_get_profile(const lrc_ctx *ctx, int cls, const char **name, double *ms_total, int64_t *count);
+
 #ifdef __cplusplus
 }
 #endif

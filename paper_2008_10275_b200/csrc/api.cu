@@ -54,6 +54,11 @@ struct Workspace {
   double* tmpC = nullptr; size_t tmpC_sz = 0;
 };
 
+enum ProfClass { P_SPMM = 0, P_VSIDE, P_TS_GRAM, P_REDUCE, P_CHOL1, P_CHOL2, P_TS_STORE, P_TRACE,
+                 P_MISC, P_NCLASS };
+const char* const kProfNames[P_NCLASS] = {"spmm", "vside_qr", "ts_gram", "gram_reduce", "chol1",
+                                          "chol2_svd", "ts_store", "trace", "misc"};
+
 struct GraphKey {
   int64_t gen = -1, N = 0; int rb = 0, cap = 0; double gamma = 0, tol = 0; uint32_t flags = 0;
   bool operator==(const GraphKey& o) const {
@@ -89,6 +94,16 @@ struct lrc_ctx {
   // last solve
   int64_t last_N = 0; bool last_record = false; int last_cap = 0;
   float last_kernel_ms = 0.f;
+  // kernel launch accounting + optional per-kernel CUDA-event profiling (direct launches only)
+  int64_t launches = 0;
+  bool capturing = false;
+  int64_t capture_count = 0, graph_kernels = 0;
+  bool profiling = false;
+  std::vector<cudaEvent_t> evpool;
+  size_t evused = 0;
+  std::vector<int> evcls;
+  double prof_ms[P_NCLASS] = {};
+  int64_t prof_n[P_NCLASS] = {};
 };
 
 namespace {
@@ -96,6 +111,39 @@ namespace {
 lrc_status fail(lrc_ctx* c, lrc_status s, const std::string& m) {
   if (c) c->err = m;
   return s;
+}
+
+#define KL(cls, strm, call)                                                              \
+  do {                                                                                    \
+    cudaEvent_t e0_ = prof_event(ctx, cls);                                               \
+    if (e0_) CK(cudaEventRecord(e0_, strm));                                              \
+    CK(call);                                                                             \
+    if (e0_) CK(cudaEventRecord(prof_event(ctx, -1), strm));                              \
+    if (ctx->capturing) ++ctx->capture_count; else ++ctx->launches;                       \
+  } while (0)
+
+// next event of the profiling pool (nullptr when profiling is off); cls < 0: the closing event
+cudaEvent_t prof_event(lrc_ctx* ctx, int cls) {
+  if (!ctx->profiling || ctx->capturing) return nullptr;
+  if (ctx->evused == ctx->evpool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    ctx->evpool.push_back(e);
+  }
+  if (cls >= 0) ctx->evcls.push_back(cls);
+  return ctx->evpool[ctx->evused++];
+}
+
+void prof_collect(lrc_ctx* ctx) {   // after a stream synchronize
+  for (size_t i = 0; i + 1 < ctx->evused && i / 2 < ctx->evcls.size(); i += 2) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ctx->evpool[i], ctx->evpool[i + 1]) == cudaSuccess) {
+      ctx->prof_ms[ctx->evcls[i / 2]] += ms;
+      ctx->prof_n[ctx->evcls[i / 2]] += 1;
+    }
+  }
+  ctx->evused = 0;
+  ctx->evcls.clear();
 }
 
 #define CK(call)                                                                          \
@@ -236,11 +284,11 @@ lrc_status enqueue_truncation(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, co
   SmallBufs b = make_bufs(w);
   if (fork_from_spmm) {
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-    CK(launch_vside(vd, (int)ctx->n, ctx->dmu, ctx->dnu, omega, k, st, b, w.wmax, ctx->side));
+    KL(P_VSIDE, ctx->side, launch_vside(vd, (int)ctx->n, ctx->dmu, ctx->dnu, omega, k, st, b, w.wmax, ctx->side));
     CK(cudaEventRecord(ctx->ev_join, ctx->side));
     CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
   } else {
-    CK(launch_vside(vd, (int)ctx->n, ctx->dmu, ctx->dnu, omega, k, st, b, w.wmax, s));
+    KL(P_VSIDE, s, launch_vside(vd, (int)ctx->n, ctx->dmu, ctx->dnu, omega, k, st, b, w.wmax, s));
   }
   TsArgs ta{};
   ta.M = (int)ctx->M;
@@ -250,13 +298,13 @@ lrc_status enqueue_truncation(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, co
   ta.ldt = w.pmax;
   ta.d_p = st.p;
   ta.partials = w.partials;
-  CK(launch_ts(0, ta, w.pmax, w.grid, s));
-  CK(launch_gram_reduce(w.partials, w.grid, w.pmax, w.G, s));
-  CK(launch_chol1(st, b, w.pmax, w.wmax, s));
+  KL((0 == 0 ? P_TS_GRAM : P_TS_STORE), s, launch_ts(0, ta, w.pmax, w.grid, s));
+  KL(P_REDUCE, s, launch_gram_reduce(w.partials, w.grid, w.pmax, w.G, s));
+  KL(P_CHOL1, s, launch_chol1(st, b, w.pmax, w.wmax, s));
   ta.T = w.T2;
-  CK(launch_ts(0, ta, w.pmax, w.grid, s));
-  CK(launch_gram_reduce(w.partials, w.grid, w.pmax, w.G, s));
-  CK(launch_chol2_svd(st, b, w.pmax, w.wmax, (int)ctx->n, tol, cap, rank_slot, sigma_row, Vout,
+  KL((0 == 0 ? P_TS_GRAM : P_TS_STORE), s, launch_ts(0, ta, w.pmax, w.grid, s));
+  KL(P_REDUCE, s, launch_gram_reduce(w.partials, w.grid, w.pmax, w.G, s));
+  KL(P_CHOL2, s, launch_chol2_svd(st, b, w.pmax, w.wmax, (int)ctx->n, tol, cap, rank_slot, sigma_row, Vout,
                       ldv_out, s));
   TsArgs tb{};
   tb.M = (int)ctx->M;
@@ -267,7 +315,7 @@ lrc_status enqueue_truncation(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, co
   tb.d_p = st.rk + rank_slot;
   tb.out = Uout;
   tb.ldo = ldu_out;
-  CK(launch_ts(1, tb, w.capp, w.grid, s));
+  KL((1 == 0 ? P_TS_GRAM : P_TS_STORE), s, launch_ts(1, tb, w.capp, w.grid, s));
   return LRC_OK;
 }
 
@@ -276,7 +324,7 @@ lrc_status enqueue_norm2(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, int slo
   Workspace& w = ctx->ws;
   State st = make_state(w);
   SmallBufs b = make_bufs(w);
-  CK(launch_vside(vd, (int)ctx->n, ctx->dmu, ctx->dnu, nullptr, 0, st, b, w.wmax, s));
+  KL(P_VSIDE, s, launch_vside(vd, (int)ctx->n, ctx->dmu, ctx->dnu, nullptr, 0, st, b, w.wmax, s));
   TsArgs ta{};
   ta.M = (int)ctx->M;
   ta.u = ud;
@@ -285,9 +333,9 @@ lrc_status enqueue_norm2(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, int slo
   ta.ldt = w.pmax;
   ta.d_p = st.p;
   ta.partials = w.partials;
-  CK(launch_ts(0, ta, w.pmax, w.grid, s));
-  CK(launch_gram_reduce(w.partials, w.grid, w.pmax, w.G, s));
-  CK(launch_trace(st, w.G, w.pmax, slot, s));
+  KL((0 == 0 ? P_TS_GRAM : P_TS_STORE), s, launch_ts(0, ta, w.pmax, w.grid, s));
+  KL(P_REDUCE, s, launch_gram_reduce(w.partials, w.grid, w.pmax, w.G, s));
+  KL(P_TRACE, s, launch_trace(st, w.G, w.pmax, slot, s));
   return LRC_OK;
 }
 
@@ -320,7 +368,7 @@ lrc_status enqueue_iteration(lrc_ctx* ctx, int k, int rb, int cap, double gamma,
   a.ldo = w.LDW;
   a.out_off = rb;
   a.gamma = gamma;
-  CK(launch_spmm(SPMM_S2STEP, a, cap, s));
+  KL(P_SPMM, s, launch_spmm(SPMM_S2STEP, a, cap, s));
 
   VDesc vd{};
   vd.nb = 5;
@@ -423,6 +471,7 @@ void lrc_destroy(lrc_ctx* ctx) {
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   for (int i = 0; i < 4; ++i) if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+  for (cudaEvent_t e : ctx->evpool) cudaEventDestroy(e);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -430,6 +479,24 @@ void lrc_destroy(lrc_ctx* ctx) {
 const char* lrc_last_error(const lrc_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
 
 float lrc_last_kernel_ms(const lrc_ctx* ctx) { return ctx ? ctx->last_kernel_ms : 0.f; }
+
+int64_t lrc_kernel_launches(const lrc_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+void lrc_set_profiling(lrc_ctx* ctx, int on) {
+  if (!ctx) return;
+  ctx->profiling = on != 0;
+  for (int i = 0; i < P_NCLASS; ++i) { ctx->prof_ms[i] = 0.0; ctx->prof_n[i] = 0; }
+  ctx->evused = 0;
+  ctx->evcls.clear();
+}
+
+int lrc_get_profile(const lrc_ctx* ctx, int cls, const char** name, double* ms_total, int64_t* count) {
+  if (cls < 0 || cls >= P_NCLASS) return P_NCLASS;
+  if (name) *name = kProfNames[cls];
+  if (ms_total) *ms_total = ctx ? ctx->prof_ms[cls] : 0.0;
+  if (count) *count = ctx ? ctx->prof_n[cls] : 0;
+  return P_NCLASS;
+}
 
 lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t* row_ptr,
                             const int32_t* col_idx, const double* const vals[6], double rho_f,
@@ -579,7 +646,7 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
   if (lrc::vside_smem_bytes((int)n, wmax, ts_pmax_for(p_need)) > kSmemLimit)
     return fail(ctx, LRC_ERR_ARG, "n x (r_B + 4 rank_cap) too large for the single-CTA V-side QR");
   const bool record = (opts->flags & LRC_RECORD_ITERATES) != 0;
-  const bool use_graph = (opts->flags & LRC_NO_GRAPH) == 0;
+  const bool use_graph = (opts->flags & LRC_NO_GRAPH) == 0 && !ctx->profiling;
   CK(cudaSetDevice(ctx->device));
   lrc_status st = ensure_ws(ctx, std::max(rb, 1), cap, N, wmax, record);
   if (st != LRC_OK) return st;
@@ -623,9 +690,12 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
       if (!(ctx->gexec && ctx->gkey == key)) {
         drop_graph(ctx);
         CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        ctx->capturing = true;
+        ctx->capture_count = 0;
         lrc_status es = LRC_OK;
         for (int k = 0; k < N && es == LRC_OK; ++k)
           es = enqueue_iteration(ctx, k, rb, cap, gamma, opts->tol, record);
+        ctx->capturing = false;
         cudaGraph_t g = nullptr;
         cudaError_t ce = cudaStreamEndCapture(s, &g);
         if (es != LRC_OK) { if (g) cudaGraphDestroy(g); return es; }
@@ -634,8 +704,10 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
         cudaGraphDestroy(g);
         if (ce != cudaSuccess) { ctx->gexec = nullptr; return fail(ctx, LRC_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce)); }
         ctx->gkey = key;
+        ctx->graph_kernels = ctx->capture_count;
       }
       CK(cudaGraphLaunch(ctx->gexec, s));
+      ctx->launches += ctx->graph_kernels;
     } else {
       for (int k = 0; k < N; ++k) {
         st = enqueue_iteration(ctx, k, rb, cap, gamma, opts->tol, record);
@@ -650,7 +722,7 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
       // residual factors: Ucat = [B_U | W0 | W1 | W2], Vcat = [B_V | -V | -d_mu V | -d_nu V]
       SpmmArgs a = spmm_base(ctx);
       a.U = UN; a.ldu = w.LDU; a.d_r = sd.rk + slotN; a.out = w.Wcat; a.ldo = w.LDW; a.out_off = rb;
-      CK(launch_spmm(SPMM_PLAIN3, a, cap, s));
+      KL(P_SPMM, s, launch_spmm(SPMM_PLAIN3, a, cap, s));
       UDesc ur{};
       ur.A = w.Wcat; ur.lda = w.LDW; ur.wa_fixed = rb; ur.wa_mul = 3; ur.wa_idx = slotN; ur.B = nullptr; ur.wb_idx = -1;
       VDesc vr{};
@@ -663,8 +735,8 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
       if (st != LRC_OK) return st;
     }
     // outputs (zero the columns >= rank)
-    CK(launch_zero_cols(UN, (int)M, w.LDU, sd.rk + slotN, 0, cap, s));
-    CK(launch_zero_cols(VN, (int)n, cap, sd.rk + slotN, 0, cap, s));
+    KL(P_MISC, s, launch_zero_cols(UN, (int)M, w.LDU, sd.rk + slotN, 0, cap, s));
+    KL(P_MISC, s, launch_zero_cols(VN, (int)n, cap, sd.rk + slotN, 0, cap, s));
     CK(cudaMemcpy2DAsync(U_out, sizeof(double) * ld_u, UN, sizeof(double) * w.LDU, sizeof(double) * cap, M, kind_out(where), s));
     CK(cudaMemcpy2DAsync(V_out, sizeof(double) * ld_v, VN, sizeof(double) * cap, sizeof(double) * cap, n, kind_out(where), s));
   } else {
@@ -690,6 +762,7 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
     CK(cudaMemcpyAsync(sig.data(), w.sigma, sizeof(double) * sig.size(), cudaMemcpyDeviceToHost, s));
   }
   CK(cudaStreamSynchronize(s));
+  prof_collect(ctx);
   ctx->last_N = N;
   ctx->last_record = record;
   ctx->last_cap = cap;
@@ -750,15 +823,16 @@ lrc_status lrc_apply_lowrank(lrc_ctx* ctx, const double* U, int64_t ld_u, int64_
     for (int t = 0; t < 6; ++t) {
       a.single_t = t;
       a.out_off = t * (int)r;
-      CK(launch_spmm(SPMM_SINGLE, a, (int)r, s));
+      KL(P_SPMM, s, launch_spmm(SPMM_SINGLE, a, (int)r, s));
     }
   } else {
-    CK(launch_spmm(mode == LRC_APPLY_S2STEP ? SPMM_S2STEP : SPMM_PLAIN3, a, (int)r, s));
+    KL(P_SPMM, s, launch_spmm(mode == LRC_APPLY_S2STEP ? SPMM_S2STEP : SPMM_PLAIN3, a, (int)r, s));
   }
   CK(cudaEventRecord(ctx->ev[1], s));
   if (where == LRC_MEM_HOST)
     CK(cudaMemcpy2DAsync(W, sizeof(double) * ld_w, Wd, sizeof(double) * ldw, sizeof(double) * nout * r, M, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  prof_collect(ctx);
   cudaEventElapsedTime(&ctx->last_kernel_ms, ctx->ev[0], ctx->ev[1]);
   return LRC_OK;
 }
@@ -792,11 +866,12 @@ lrc_status lrc_apply_dense(lrc_ctx* ctx, const double* S, int64_t ld_s, int64_t 
   a.U = Sd; a.ldu = lds; a.d_r = nullptr; a.r_fixed = (int)ncols; a.out = Yd; a.ldo = ldy;
   a.dmu = ctx->dmu; a.dnu = ctx->dnu;
   CK(cudaEventRecord(ctx->ev[0], s));
-  CK(launch_spmm(SPMM_DENSE, a, (int)ncols, s));
+  KL(P_SPMM, s, launch_spmm(SPMM_DENSE, a, (int)ncols, s));
   CK(cudaEventRecord(ctx->ev[1], s));
   if (where == LRC_MEM_HOST)
     CK(cudaMemcpy2DAsync(Y, sizeof(double) * ld_y, Yd, sizeof(double) * ldy, sizeof(double) * ncols, M, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  prof_collect(ctx);
   cudaEventElapsedTime(&ctx->last_kernel_ms, ctx->ev[0], ctx->ev[1]);
   return LRC_OK;
 }
@@ -847,7 +922,7 @@ lrc_status lrc_truncate(lrc_ctx* ctx, const double* U, int64_t ld_u, const doubl
   double* Vnew = ws.tmpB + (size_t)n * w;
   st = enqueue_truncation(ctx, ud, vd, nullptr, 0, tol, capi, slot, ws.N, ws.tmpC, capi, Vnew, capi, s, false);
   if (st != LRC_OK) return st;
-  CK(launch_zero_cols(ws.tmpC, (int)M, capi, sd.rk + slot, 0, capi, s));
+  KL(P_MISC, s, launch_zero_cols(ws.tmpC, (int)M, capi, sd.rk + slot, 0, capi, s));
   CK(cudaMemcpyAsync(U_out, ws.tmpC, sizeof(double) * M * capi, kind_out(where), s));
   CK(cudaMemcpyAsync(V_out, Vnew, sizeof(double) * n * capi, kind_out(where), s));
   int hr = 0, flags = 0;
@@ -856,6 +931,7 @@ lrc_status lrc_truncate(lrc_ctx* ctx, const double* U, int64_t ld_u, const doubl
   std::vector<double> sg(kSigmaStride);
   CK(cudaMemcpyAsync(sg.data(), ws.sigma + (size_t)ws.N * kSigmaStride, sizeof(double) * kSigmaStride, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  prof_collect(ctx);
   *rank = hr;
   if (sigma) std::memcpy(sigma, sg.data(), sizeof(double) * p_need);
   ctx->last_record = false;   // tmp state overwrote the iterate bookkeeping slots
@@ -879,7 +955,7 @@ lrc_status lrc_get_iterate(lrc_ctx* ctx, int64_t k, double* U, double* V, int64_
   int hr = 0;
   CK(cudaMemcpyAsync(&hr, w.ints + (k + 1), sizeof(int), cudaMemcpyDeviceToHost, s));
   double* Uk = w.Uh + (size_t)(k - 1) * M * w.LDU;
-  CK(launch_zero_cols(Uk, (int)M, w.LDU, w.ints + (k + 1), 0, cap, s));
+  KL(P_MISC, s, launch_zero_cols(Uk, (int)M, w.LDU, w.ints + (k + 1), 0, cap, s));
   const double* Vk = w.Vh + (size_t)(k - 1) * n * cap;
   CK(cudaMemcpy2DAsync(U, sizeof(double) * cap, Uk, sizeof(double) * w.LDU, sizeof(double) * cap, M, kind_out(where), s));
   CK(cudaMemcpyAsync(V, Vk, sizeof(double) * n * cap, kind_out(where), s));

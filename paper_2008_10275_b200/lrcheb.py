@@ -30,7 +30,7 @@ SIGMA_STRIDE = 128
 EXPORTS = (
     "lrc_create", "lrc_destroy", "lrc_last_error", "lrc_version", "lrc_set_operator",
     "lrc_set_params", "lrc_solve", "lrc_apply_lowrank", "lrc_apply_dense", "lrc_truncate",
-    "lrc_get_iterate", "lrc_last_kernel_ms",
+    "lrc_get_iterate", "lrc_last_kernel_ms", "lrc_kernel_launches", "lrc_set_profiling", "lrc_get_profile",
 )
 
 
@@ -75,6 +75,12 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.lrc_get_iterate.argtypes = [P, I64, P, P, ctypes.POINTER(I64), I32]
     lib.lrc_last_kernel_ms.argtypes = [P]
     lib.lrc_last_kernel_ms.restype = ctypes.c_float
+    lib.lrc_kernel_launches.argtypes = [P]
+    lib.lrc_kernel_launches.restype = I64
+    lib.lrc_set_profiling.argtypes = [P, I32]
+    lib.lrc_set_profiling.restype = None
+    lib.lrc_get_profile.argtypes = [P, I32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(D), ctypes.POINTER(I64)]
+    lib.lrc_get_profile.restype = I32
     for name in ("lrc_create", "lrc_set_operator", "lrc_set_params", "lrc_solve", "lrc_apply_lowrank",
                  "lrc_apply_dense", "lrc_truncate", "lrc_get_iterate"):
         getattr(lib, name).restype = I32
@@ -291,6 +297,22 @@ class Context:
 
     def last_kernel_ms(self) -> float:
         return float(self._lib.lrc_last_kernel_ms(self._h))
+
+    def kernel_launches(self) -> int:
+        return int(self._lib.lrc_kernel_launches(self._h))
+
+    def set_profiling(self, on: bool):
+        self._lib.lrc_set_profiling(self._h, 1 if on else 0)
+
+    def profile(self) -> dict:
+        """{class: (total device ms, launches)} accumulated since set_profiling(True)."""
+        out = {}
+        ncls = self._lib.lrc_get_profile(self._h, -1, None, None, None)
+        for c in range(ncls):
+            name, ms, cnt = ctypes.c_char_p(), ctypes.c_double(), ctypes.c_int64()
+            self._lib.lrc_get_profile(self._h, c, ctypes.byref(name), ctypes.byref(ms), ctypes.byref(cnt))
+            out[name.value.decode()] = (ms.value, cnt.value)
+        return out
 
 
 def version() -> str:
