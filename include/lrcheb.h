@@ -106,6 +106,8 @@ typedef struct {
   int64_t *rank_history;      /* caller array[n_iter] or NULL: rank of X_1..X_N */
   double *sigma_history;      /* caller array[n_iter * 128] or NULL: core singular values per
                                  iteration, descending, zero padded */
+  int64_t jacobi_sweeps;      /* total one-sided Jacobi sweeps over all truncations of the call */
+  double chol2_cycles[3];     /* SM cycles in the core step: Cholesky + R, Jacobi, rank/Z/V' (summed) */
 } lrc_solve_info;
 
 /* Solve F(S) = B for the current operator/params.

@@ -47,6 +47,7 @@ struct Workspace {
   double* scal = nullptr;     // 8
   double* T1 = nullptr; double* QV = nullptr; double* G = nullptr; double* R1 = nullptr;
   double* T2 = nullptr; double* Z = nullptr;
+  double* R1i = nullptr; double* Wz = nullptr; double* Wv = nullptr;
   double* partials = nullptr;
   double* Uh = nullptr; double* Vh = nullptr;   // iterate history
   double* tmpA = nullptr; size_t tmpA_sz = 0;   // hook scratch
@@ -55,9 +56,9 @@ struct Workspace {
 };
 
 enum ProfClass { P_SPMM = 0, P_VSIDE, P_TS_GRAM, P_REDUCE, P_CHOL1, P_CHOL2, P_TS_STORE, P_TRACE,
-                 P_MISC, P_NCLASS };
+                 P_MISC, P_TINY, P_NCLASS };
 const char* const kProfNames[P_NCLASS] = {"spmm", "vside_qr", "ts_gram", "gram_reduce", "chol1",
-                                          "chol2_svd", "ts_store", "trace", "misc"};
+                                          "chol2_svd", "ts_store", "trace", "misc", "tiny_gemm"};
 
 struct GraphKey {
   int64_t gen = -1, N = 0; int rb = 0, cap = 0; double gamma = 0, tol = 0; uint32_t flags = 0;
@@ -81,6 +82,7 @@ struct lrc_ctx {
   int64_t M = 0, nnz = 0;
   int* row_ptr = nullptr; int* col_idx = nullptr; double* vals[6] = {};
   int* group_ptr = nullptr; int ngroups = 0;
+  int* tile_ptr = nullptr; int ntiles = 0;
   double rho = 0, lam = 0;
   // params
   bool par_set = false;
@@ -168,6 +170,7 @@ void free_ws(Workspace& w) {
   for (int i = 0; i < 3; ++i) { dfree(w.Ubuf[i]); dfree(w.Vbuf[i]); }
   dfree(w.BV); dfree(w.omega); dfree(w.ints); dfree(w.sigma); dfree(w.scal);
   dfree(w.T1); dfree(w.QV); dfree(w.G); dfree(w.R1); dfree(w.T2); dfree(w.Z);
+  dfree(w.R1i); dfree(w.Wz); dfree(w.Wv);
   dfree(w.partials); dfree(w.Uh); dfree(w.Vh); dfree(w.tmpA); dfree(w.tmpB); dfree(w.tmpC);
   w = Workspace();
 }
@@ -218,6 +221,9 @@ lrc_status ensure_ws(lrc_ctx* ctx, int rb, int cap, int N, int wmax, bool record
   CK(dalloc(&w.R1, (size_t)pmax * pmax));
   CK(dalloc(&w.T2, (size_t)wmax * pmax));
   CK(dalloc(&w.Z, (size_t)wmax * capp));
+  CK(dalloc(&w.R1i, (size_t)pmax * pmax));
+  CK(dalloc(&w.Wz, (size_t)pmax * capp));
+  CK(dalloc(&w.Wv, (size_t)pmax * capp));
   CK(dalloc(&w.partials, (size_t)w.grid * pmax * pmax));
   if (record) {
     CK(dalloc(&w.Uh, (size_t)N * M * w.LDU));
@@ -248,6 +254,7 @@ State make_state(Workspace& w) {
   s.w = w.ints + w.N + 5;
   s.flags = w.ints + w.N + 6;
   s.esc = w.ints + w.N + 7;
+  s.sweeps = w.ints + w.N + 8;
   s.sigma = w.sigma;
   s.scal = w.scal;
   return s;
@@ -256,6 +263,7 @@ State make_state(Workspace& w) {
 SmallBufs make_bufs(Workspace& w) {
   SmallBufs b{};
   b.T1 = w.T1; b.QV = w.QV; b.G = w.G; b.R1 = w.R1; b.T2 = w.T2; b.Z = w.Z;
+  b.R1i = w.R1i; b.Wz = w.Wz; b.Wv = w.Wv;
   b.ldT = w.pmax; b.ldZ = w.capp;
   return b;
 }
@@ -265,6 +273,8 @@ SpmmArgs spmm_base(lrc_ctx* ctx) {
   a.M = (int)ctx->M;
   a.ngroups = ctx->ngroups;
   a.group_ptr = ctx->group_ptr;
+  a.ntiles = ctx->ntiles;
+  a.tile_ptr = ctx->tile_ptr;
   a.row_ptr = ctx->row_ptr;
   a.col_idx = ctx->col_idx;
   for (int t = 0; t < 6; ++t) a.v[t] = ctx->vals[t];
@@ -301,11 +311,17 @@ lrc_status enqueue_truncation(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, co
   KL((0 == 0 ? P_TS_GRAM : P_TS_STORE), s, launch_ts(0, ta, w.pmax, w.grid, s));
   KL(P_REDUCE, s, launch_gram_reduce(w.partials, w.grid, w.pmax, w.G, s));
   KL(P_CHOL1, s, launch_chol1(st, b, w.pmax, w.wmax, s));
+  KL(P_TINY, s, launch_tiny_gemm(w.T1, w.pmax, w.R1i, w.pmax, w.T2, w.pmax, w.pmax, st.w, 0, w.wmax,
+                                 st.p, 0, s));
   ta.T = w.T2;
   KL((0 == 0 ? P_TS_GRAM : P_TS_STORE), s, launch_ts(0, ta, w.pmax, w.grid, s));
   KL(P_REDUCE, s, launch_gram_reduce(w.partials, w.grid, w.pmax, w.G, s));
   KL(P_CHOL2, s, launch_chol2_svd(st, b, w.pmax, w.wmax, (int)ctx->n, tol, cap, rank_slot, sigma_row, Vout,
                       ldv_out, s));
+  KL(P_TINY, s, launch_tiny_gemm(w.T1, w.pmax, w.Wz, w.capp, w.Z, w.capp, w.capp, st.w, 0, w.wmax,
+                                 st.p, 0, s));
+  KL(P_TINY, s, launch_tiny_gemm(w.QV, w.pmax, w.Wv, w.capp, Vout, ldv_out, cap, nullptr,
+                                 (int)ctx->n, (int)ctx->n, st.p, 0, s));
   TsArgs tb{};
   tb.M = (int)ctx->M;
   tb.u = ud;
@@ -466,7 +482,7 @@ void lrc_destroy(lrc_ctx* ctx) {
     dfree(ctx->row_ptr); dfree(ctx->col_idx);
     for (int t = 0; t < 6; ++t) dfree(ctx->vals[t]);
   }
-  dfree(ctx->group_ptr); dfree(ctx->dmu); dfree(ctx->dnu);
+  dfree(ctx->group_ptr); dfree(ctx->tile_ptr); dfree(ctx->dmu); dfree(ctx->dnu);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
@@ -544,6 +560,22 @@ lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t*
     else { groups.push_back((int32_t)i); gsz = 1; }
   }
   groups.push_back((int32_t)M);
+  // CTA tiles of the fused SpMM: <= 8 node blocks and <= kSpmmCap nnz (a longer block is alone)
+  std::vector<int32_t> tiles;
+  tiles.push_back(0);
+  {
+    int cnt = 0;
+    int64_t tn = 0;
+    const int ng = (int)groups.size() - 1;
+    for (int gi = 0; gi < ng; ++gi) {
+      const int64_t gn = (int64_t)hrp[groups[gi + 1]] - hrp[groups[gi]];
+      if (cnt > 0 && (cnt == 8 || tn + gn > kSpmmCap)) { tiles.push_back(gi); cnt = 0; tn = 0; }
+      ++cnt;
+      tn += gn;
+      if (gn > kSpmmCap) { tiles.push_back(gi + 1); cnt = 0; tn = 0; }
+    }
+    if (cnt > 0) tiles.push_back(ng);
+  }
 
   CK(cudaStreamSynchronize(ctx->stream));
   drop_graph(ctx);
@@ -553,7 +585,8 @@ lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t*
     for (int t = 0; t < 6; ++t) dfree(ctx->vals[t]);
   }
   dfree(ctx->group_ptr);
-  ctx->row_ptr = nullptr; ctx->col_idx = nullptr; ctx->group_ptr = nullptr;
+  dfree(ctx->tile_ptr);
+  ctx->row_ptr = nullptr; ctx->col_idx = nullptr; ctx->group_ptr = nullptr; ctx->tile_ptr = nullptr;
   for (int t = 0; t < 6; ++t) ctx->vals[t] = nullptr;
   ctx->op_set = false;
   ctx->par_set = false;   // params depend on nothing here, but workspaces do; keep semantics simple
@@ -578,6 +611,9 @@ lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t*
   CK(dalloc(&ctx->group_ptr, groups.size()));
   CK(cudaMemcpy(ctx->group_ptr, groups.data(), sizeof(int32_t) * groups.size(), cudaMemcpyHostToDevice));
   ctx->ngroups = (int)groups.size() - 1;
+  CK(dalloc(&ctx->tile_ptr, tiles.size()));
+  CK(cudaMemcpy(ctx->tile_ptr, tiles.data(), sizeof(int32_t) * tiles.size(), cudaMemcpyHostToDevice));
+  ctx->ntiles = (int)tiles.size() - 1;
   ctx->M = M;
   ctx->nnz = nnz;
   ctx->rho = rho_f;
@@ -783,6 +819,8 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
     if (info->rank_history)
       for (int k = 0; k < N; ++k) info->rank_history[k] = rb > 0 ? ints[k + 2] : 0;
     if (info->sigma_history) std::memcpy(info->sigma_history, sig.data(), sizeof(double) * sig.size());
+    info->jacobi_sweeps = ints[w.N + 8];
+    info->chol2_cycles[0] = scal[4]; info->chol2_cycles[1] = scal[5]; info->chol2_cycles[2] = scal[6];
   }
   if (flags & 1) return fail(ctx, LRC_ERR_NUMERIC, "shifted Cholesky failed after all escalations");
   if (flags & 2) return fail(ctx, LRC_ERR_NUMERIC, "non-finite singular value in the core SVD");

@@ -10,6 +10,7 @@ constexpr int kMaxRank = 128;    // rank_cap limit
 constexpr int kMaxP = 128;       // max Gram width p = min(n, w)
 constexpr int kMaxW = 256;       // max concatenation width w = r_B + 4 r
 constexpr int kGroupMax = 8;     // rows per node block in the fused SpMM
+constexpr int kSpmmCap = 2048;   // nnz staged per SpMM CTA tile
 constexpr int kSigmaStride = 128;
 
 // ------------------------------------------------------------------------------------------
@@ -21,6 +22,9 @@ struct SpmmArgs {
   int M;
   int ngroups;
   const int* group_ptr;     // [ngroups+1] first row of each node block
+  int ntiles;
+  const int* tile_ptr;      // [ntiles+1] first node block of each CTA tile (<= 8 blocks, <= kSpmmCap nnz
+                            // unless a single block is longer)
   const int* row_ptr;
   const int* col_idx;
   const double* v[6];       // A0, A1, A2, Jrho, Jmu, Jlam
@@ -85,6 +89,7 @@ struct State {          // device-resident per-solve state
   int* w;               // current concatenation width
   int* flags;           // error bits (1: Cholesky failed after escalations, 2: NaN)
   int* esc;             // shift escalations
+  int* sweeps;          // Jacobi sweeps (summed over calls)
   double* sigma;        // [N][kSigmaStride]
   double* scal;         // scalar slots: [0] ||B||^2, [1] ||R||^2 residual
 };
@@ -96,6 +101,9 @@ struct SmallBufs {
   double* G;      // pmax x pmax reduced Gram
   double* R1;     // pmax x pmax
   double* T2;     // w x pmax   (R_V^T R1^{-1})
+  double* R1i;    // pmax x pmax (R1^{-1}, upper)
+  double* Wz;     // pmax x ldZ  (W_r Sigma_r^{-1})
+  double* Wv;     // pmax x ldZ  (W_r Sigma_r)
   double* Z;      // w x capp   (R_V^T W_r Sigma_r^{-1})
   int ldT;        // = pmax
   int ldZ;        // = capp
@@ -111,6 +119,10 @@ cudaError_t launch_chol1(State st, SmallBufs b, int pmax, int wmax, cudaStream_t
 cudaError_t launch_chol2_svd(State st, SmallBufs b, int pmax, int wmax, int n, double tol,
                              int cap, int rank_slot, int sigma_row, double* Vout, int ldv,
                              cudaStream_t s);
+// C (m x ncols) = A (m x k) B (k x ncols), m/k device-resident (d_m/d_k) or fixed; m_max bounds the grid
+cudaError_t launch_tiny_gemm(const double* A, int lda, const double* B, int ldb, double* C, int ldc,
+                             int ncols, const int* d_m, int m_fixed, int m_max, const int* d_k,
+                             int k_fixed, cudaStream_t s);
 // scal[slot] = trace(G) over p (for ||X||_F^2)
 cudaError_t launch_trace(State st, const double* G, int pmax, int slot, cudaStream_t s);
 

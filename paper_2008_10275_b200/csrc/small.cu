@@ -24,7 +24,8 @@ constexpr int kT = 1024;
 constexpr double kShiftRel = 1e-12;   // pass-1 shift s1 = kShiftRel * tr(G1)  (reading S17')
 constexpr int kMaxEsc = 3;            // escalations x100
 constexpr double kJacobiTol = 1e-14;  // rotate while |a_i.a_j| > tol ||a_i|| ||a_j||
-constexpr int kMaxSweeps = 60;
+constexpr double kJacobiFloor = 1e-30;   // (1e-15)^2: column-norm^2 floor relative to ||R||_F^2
+constexpr int kMaxSweeps = 40;
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -235,11 +236,12 @@ __global__ void __launch_bounds__(kT) chol1_kernel(State st, SmallBufs b, int pm
     }
     __syncthreads();
   }
-  // keep R1 (upper, zero below) for R = R2 R1
+  // keep R1 (upper, zero below) and the shift actually used (for the core step's floor correction)
   for (int e = tid; e < pmax * pmax; e += kT) {
     const int i = e / pmax, c = e - (e / pmax) * pmax;
     b.R1[e] = (i < p && c < p && c >= i) ? s_r[i * LD + c] : 0.0;
   }
+  if (tid == 0) st.scal[2] = ok ? shift : 0.0;
   __syncthreads();
   // in-place inverse: rows from the bottom, X[i][j] = -(sum_{k=i+1..j} R[i][k] X[k][j]) / R[i][i]
   for (int i = p - 1; i >= 0; --i) {
@@ -259,15 +261,10 @@ __global__ void __launch_bounds__(kT) chol1_kernel(State st, SmallBufs b, int pm
     for (int j = i + tid; j < p; j += kT) s_r[i * LD + j] = s_row[j];
     __syncthreads();
   }
-  // T2 = T1 X   (w x p), X upper triangular
-  for (int e = tid; e < w * b.ldT; e += kT) {
-    const int c = e / b.ldT, j = e - (e / b.ldT) * b.ldT;
-    double acc = 0.0;
-    if (j < p) {
-      const double* t1 = b.T1 + (size_t)c * b.ldT;
-      for (int kk = 0; kk <= j; ++kk) acc += t1[kk] * s_r[kk * LD + j];
-    }
-    b.T2[(size_t)c * b.ldT + j] = acc;
+  // R1^{-1} (upper) -> global; T2 = T1 R1^{-1} is a multi-CTA tiny GEMM (tiny_gemm_kernel)
+  for (int e = tid; e < pmax * pmax; e += kT) {
+    const int i = e / pmax, c = e - (e / pmax) * pmax;
+    b.R1i[e] = (i < p && c < p && c >= i) ? s_r[i * LD + c] : 0.0;
   }
 }
 
@@ -300,6 +297,7 @@ __global__ void __launch_bounds__(kT) chol2_svd_kernel(State st, SmallBufs b, in
     s_tr = tr;
   }
   __syncthreads();
+  long long tclk0 = clock64();
   // R2 = chol(G2 + s2 I): unshifted first (keeps R^T R = X^T X exactly), then escalate
   double shift = 0.0;
   bool ok = false;
@@ -325,60 +323,110 @@ __global__ void __launch_bounds__(kT) chol2_svd_kernel(State st, SmallBufs b, in
     }
     __syncthreads();
   }
-  // R = R2 R1 -> column-major s_a
+  const double s2_used = ok ? shift : 0.0;
+  // R1 (row-major) -> s_a
   for (int e = tid; e < p * p; e += kT) {
-    const int j = e / p, i = e - (e / p) * p;    // column j, row i
-    double acc = 0.0;
-    if (i <= j)
-      for (int kk = i; kk <= j; ++kk) acc += s_w[i * LD + kk] * b.R1[kk * pmax + j];
-    s_a[j * LD + i] = acc;
+    const int i = e / p, c = e - (e / p) * p;
+    s_a[i * LD + c] = b.R1[i * pmax + c];
+  }
+  __syncthreads();
+  // R = R2 R1, one warp per row, in place in s_w (row i of R needs only row i of R2)
+  for (int i = warp; i < p; i += kT / 32) {
+    double acc[kMaxP / 32];
+#pragma unroll
+    for (int t = 0; t < kMaxP / 32; ++t) acc[t] = 0.0;
+    for (int k = i; k < p; ++k) {
+      const double r2 = s_w[i * LD + k];
+#pragma unroll
+      for (int t = 0; t < kMaxP / 32; ++t) {
+        const int j = lane + 32 * t;
+        if (j < p) acc[t] = fma(r2, s_a[k * LD + j], acc[t]);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < kMaxP / 32; ++t) {
+      const int j = lane + 32 * t;
+      if (j < p) s_w[i * LD + j] = (j >= i) ? acc[t] : 0.0;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < p * p; e += kT) {          // column-major A = R
+    const int i = e / p, j = e - (e / p) * p;
+    s_a[j * LD + i] = s_w[i * LD + j];
   }
   __syncthreads();
   for (int e = tid; e < p * p; e += kT) {
     const int j = e / p, i = e - (e / p) * p;
     s_w[j * LD + i] = (i == j) ? 1.0 : 0.0;
   }
+  if (warp == 0) {
+    double ss = 0.0;
+    for (int e = lane; e < p * p; e += 32) {
+      const double x = s_a[(e / p) * LD + (e % p)];
+      ss += x * x;
+    }
+    ss = warp_sum(ss);
+    if (lane == 0) s_tr = ss;
+  }
   __syncthreads();
+  long long tclk1 = clock64();
 
-  // one-sided Jacobi, round-robin ordering
-  const int P = p + (p & 1);
+  // One-sided (Hestenes) Jacobi on the columns of R, round-robin ordering, 16 lanes per pair
+  // (all p/2 pairs of a round in flight at once).  Columns whose squared norm is below
+  // kJacobiFloor ||R||_F^2 are rounding noise and are not rotated.
+  const double floor2 = kJacobiFloor * s_tr;
+  const double tol2 = kJacobiTol * kJacobiTol;
+  const int half = lane >> 4, hl = lane & 15;
+  const int P = p + (p & 1), NP = P / 2;
+  int sweeps_done = 0;
   for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
+    ++sweeps_done;
     if (tid == 0) s_rot = 0;
     __syncthreads();
     for (int r = 0; r < P - 1; ++r) {
-      for (int q = warp; q < P / 2; q += kT / 32) {
-        int i, j;
-        if (q == 0) { i = P - 1; j = r; }
-        else { i = (r + q) % (P - 1); j = (r - q + P - 1) % (P - 1); }
-        if (i >= p || j >= p) continue;
-        if (i > j) { const int t = i; i = j; j = t; }
+      for (int qb = warp * 2; qb < NP; qb += kT / 16) {
+        const int q = qb + half;
+        int i = 0, j = 0;
+        bool act = q < NP;
+        if (act) {
+          if (q == 0) { i = P - 1; j = r; }
+          else { i = (r + q) % (P - 1); j = (r - q + P - 1) % (P - 1); }
+          act = (i < p) && (j < p);
+          if (i > j) { const int t = i; i = j; j = t; }
+        }
         double* ai = s_a + i * LD;
         double* aj = s_a + j * LD;
         double al = 0.0, be = 0.0, ga = 0.0;
-        for (int e = lane; e < p; e += 32) {
-          const double x = ai[e], y = aj[e];
-          al += x * x; be += y * y; ga += x * y;
-        }
-        al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
-        if (ga != 0.0 && al > 0.0 && be > 0.0 && fabs(ga) > kJacobiTol * sqrt(al) * sqrt(be)) {
-          const double zeta = (be - al) / (2.0 * ga);
-          double t;
-          if (fabs(zeta) > 1e150) t = 0.5 / zeta;
-          else t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-          for (int e = lane; e < p; e += 32) {
+        if (act)
+          for (int e = hl; e < p; e += 16) {
             const double x = ai[e], y = aj[e];
-            ai[e] = c * x - s * y;
-            aj[e] = s * x + c * y;
+            al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
+          }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (act && ga != 0.0 && al > floor2 && be > floor2 && ga * ga > tol2 * al * be) {
+          // tan of the rotation angle, smaller root: t = sgn(d) 2g / (|d| + sqrt(d^2 + 4 g^2))
+          const double dd = be - al;
+          const double t = ((dd >= 0.0) ? 2.0 * ga : -2.0 * ga) / (fabs(dd) + sqrt(fma(dd, dd, 4.0 * ga * ga)));
+          const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
+          for (int e = hl; e < p; e += 16) {
+            const double x = ai[e], y = aj[e];
+            ai[e] = c * x - sn * y;
+            aj[e] = sn * x + c * y;
           }
           double* wi = s_w + i * LD;
           double* wj = s_w + j * LD;
-          for (int e = lane; e < p; e += 32) {
+          for (int e = hl; e < p; e += 16) {
             const double x = wi[e], y = wj[e];
-            wi[e] = c * x - s * y;
-            wj[e] = s * x + c * y;
+            wi[e] = c * x - sn * y;
+            wj[e] = sn * x + c * y;
           }
-          if (lane == 0) s_rot = 1;
+          if (hl == 0) s_rot = 1;
         }
       }
       __syncthreads();
@@ -387,13 +435,17 @@ __global__ void __launch_bounds__(kT) chol2_svd_kernel(State st, SmallBufs b, in
     __syncthreads();
     if (rot == 0) break;
   }
-  // singular values, descending order
+  if (tid == 0) atomicAdd(st.sweeps, sweeps_done);
+  long long tclk2 = clock64();
+  // singular values of R, then of X:  R^T R = (1 + s2) X^T X + s1 s2 I  (exact for the shifted
+  // CholeskyQR2; same singular vectors), so sigma_X^2 = (sigma_R^2 - s1 s2) / (1 + s2).
+  const double s1s2 = st.scal[2] * s2_used;
   for (int j = warp; j < p; j += kT / 32) {
     const double* aj = s_a + j * LD;
     double ss = 0.0;
     for (int e = lane; e < p; e += 32) ss += aj[e] * aj[e];
     ss = warp_sum(ss);
-    if (lane == 0) s_sig[j] = sqrt(ss);
+    if (lane == 0) s_sig[j] = sqrt(fmax(ss - s1s2, 0.0) / (1.0 + s2_used));
   }
   __syncthreads();
   if (tid < p) {
@@ -423,31 +475,52 @@ __global__ void __launch_bounds__(kT) chol2_svd_kernel(State st, SmallBufs b, in
   if (sigma_row >= 0)
     for (int i = tid; i < kSigmaStride; i += kT)
       st.sigma[(size_t)sigma_row * kSigmaStride + i] = (i < p) ? s_sig[s_perm[i]] : 0.0;
-  // Z = T1 W_r Sigma_r^{-1}  (w x ldZ)
-  for (int e = tid; e < w * b.ldZ; e += kT) {
-    const int c = e / b.ldZ, q = e - (e / b.ldZ) * b.ldZ;
-    double acc = 0.0;
-    if (q < rr) {
+  // Wz = W_r Sigma_r^{-1}, Wv = W_r Sigma_r (p x ldZ) for the tiny GEMMs Z = T1 Wz, V' = Q_V Wv
+  for (int e = tid; e < pmax * b.ldZ; e += kT) {
+    const int k = e / b.ldZ, q = e - (e / b.ldZ) * b.ldZ;
+    double wz = 0.0, wv = 0.0;
+    if (q < rr && k < p) {
       const int jq = s_perm[q];
-      const double* t1 = b.T1 + (size_t)c * b.ldT;
-      const double* wq = s_w + jq * LD;
-      for (int kk = 0; kk < p; ++kk) acc += t1[kk] * wq[kk];
-      acc /= s_sig[jq];
+      const double wk = s_w[jq * LD + k];
+      wz = wk / s_sig[jq];
+      wv = wk * s_sig[jq];
     }
-    b.Z[(size_t)c * b.ldZ + q] = acc;
+    b.Wz[e] = wz;
+    b.Wv[e] = wv;
   }
-  // V' = Q_V W_r Sigma_r  (n x cap, ld ldv)
-  for (int e = tid; e < n * cap; e += kT) {
-    const int i = e / cap, q = e - (e / cap) * cap;
+  __syncthreads();
+  if (tid == 0 && st.scal) {   // phase cycle counters (DESIGN.md profiling notes)
+    long long tclk3 = clock64();
+    atomicAdd(st.scal + 4, (double)(tclk1 - tclk0));
+    atomicAdd(st.scal + 5, (double)(tclk2 - tclk1));
+    atomicAdd(st.scal + 6, (double)(tclk3 - tclk2));
+  }
+}
+
+// C (m x ncols, ldc) = A (m x k, lda) B (k x ncols, ldb); m, k device-resident or fixed.  8 rows of C
+// per CTA; the A rows are staged in shared memory, B rows stream from L2 coalesced.
+__global__ void __launch_bounds__(256) tiny_gemm_kernel(const double* __restrict__ A, int lda,
+                                                         const double* __restrict__ B, int ldb,
+                                                         double* __restrict__ C, int ldc, int ncols,
+                                                         const int* d_m, int m_fixed, const int* d_k,
+                                                         int k_fixed) {
+  const int m = d_m ? *d_m : m_fixed;
+  const int k = d_k ? *d_k : k_fixed;
+  const int r0 = blockIdx.x * 8;
+  if (r0 >= m) return;
+  __shared__ double s_a[8][kMaxW];
+  const int rows = min(8, m - r0);
+  for (int e = threadIdx.x; e < 8 * k; e += 256) {
+    const int i = e / k, kk = e - (e / k) * k;
+    s_a[i][kk] = (i < rows) ? A[(size_t)(r0 + i) * lda + kk] : 0.0;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < rows * ncols; e += 256) {
+    const int i = e / ncols, c = e - (e / ncols) * ncols;
     double acc = 0.0;
-    if (q < rr) {
-      const int jq = s_perm[q];
-      const double* qv = b.QV + (size_t)i * b.ldT;
-      const double* wq = s_w + jq * LD;
-      for (int kk = 0; kk < p; ++kk) acc += qv[kk] * wq[kk];
-      acc *= s_sig[jq];
-    }
-    Vout[(size_t)i * ldv + q] = acc;
+#pragma unroll 4
+    for (int kk = 0; kk < k; ++kk) acc = fma(s_a[i][kk], __ldg(B + (size_t)kk * ldb + c), acc);
+    C[(size_t)(r0 + i) * ldc + c] = acc;
   }
 }
 
@@ -489,6 +562,15 @@ cudaError_t small_prepare() {
   if ((e = set_smem(vside_kernel, kMax)) != cudaSuccess) return e;
   if ((e = set_smem(chol1_kernel, kMax)) != cudaSuccess) return e;
   return set_smem(chol2_svd_kernel, kMax);
+}
+
+cudaError_t launch_tiny_gemm(const double* A, int lda, const double* B, int ldb, double* C, int ldc,
+                             int ncols, const int* d_m, int m_fixed, int m_max, const int* d_k,
+                             int k_fixed, cudaStream_t s) {
+  if (m_max <= 0 || ncols <= 0) return cudaSuccess;
+  tiny_gemm_kernel<<<(m_max + 7) / 8, 256, 0, s>>>(A, lda, B, ldb, C, ldc, ncols, d_m, m_fixed, d_k,
+                                                    k_fixed);
+  return cudaGetLastError();
 }
 
 size_t vside_smem_bytes(int n, int wmax, int pmax) {

@@ -4,12 +4,17 @@
 // All three M-level passes of the truncation have the same shape: a row tile of the logical
 // concatenation Ucat = [A | B] (M x w, two strided blocks, widths read from device-resident ranks)
 // is multiplied by a small w x p matrix T held in L2, on the fp64 tensor pipe
-// (mma.sync.m8n8k4.f64, "DMMA"), and the p-wide tile is then either
-//   GRAM  : contracted with itself, G += X_tile^T X_tile (upper 8x8 tiles, DMMA), accumulated in
-//           registers across the CTA's tiles and written once as a per-CTA partial
+// (mma.sync.m8n8k4.f64, "DMMA"), and the p-wide tile X = Ucat_tile T is then either
+//   GRAM  : contracted with itself, G += X^T X (upper 8x8 tiles in 2x2 register blocks, DMMA),
+//           accumulated in registers across the CTA's tiles and written once as a per-CTA partial
 //           (deterministic fixed-order reduction in gram_reduce_kernel), or
 //   STORE : written out (U_{k+1} = Ucat Z, row-major).
 // Gram pass 1 uses T = R_V^T, pass 2 T = R_V^T R1^{-1}, the basis GEMM T = Z.
+//
+// Tile: 128 rows x p, 8 warps, warp w owns rows [16w, 16w+16) (two 8-row DMMA tiles) and all p
+// columns.  The K loop streams 32-column chunks of Ucat and 32-row chunks of T into a cp.async
+// double buffer (8-byte copies: the two Ucat blocks meet at an odd column; zero fill past M / w).
+// The X tile is parked in the (then idle) stage buffers for the Gram / store epilogue.
 #include "lrc_internal.cuh"
 
 namespace lrc {
@@ -17,9 +22,9 @@ namespace lrc {
 namespace {
 
 constexpr int kThreads = 256;   // 8 warps
-constexpr int kBM = 64;         // rows per tile
+constexpr int kBM = 128;        // rows per tile
 constexpr int kBK = 32;         // k chunk
-constexpr int kSU = kBK + 4;    // smem row stride of the U tile (== 4 mod 16 doubles: conflict free)
+constexpr int kSU = kBK + 4;    // smem row stride of the U chunk (== 4 mod 16 doubles: conflict free)
 
 __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -27,19 +32,61 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
 __device__ __forceinline__ int ucat_widths(const TsArgs& a, int& wa) {
   wa = a.u.wa_fixed + (a.u.wa_idx >= 0 ? a.u.wa_mul * a.rk[a.u.wa_idx] : 0);
   const int wb = a.u.B ? (a.u.wb_idx >= 0 ? a.rk[a.u.wb_idx] : a.u.wb_fixed) : 0;
   return wa + wb;
 }
 
+template <int PT>
+struct TsShape {
+  static constexpr int PMAX = PT * 8;
+  static constexpr int SX = PMAX + 4;                    // T chunk / X tile row stride
+  static constexpr int STAGE = kBM * kSU + kBK * SX;     // doubles per pipeline stage
+  static constexpr int SMEM = (2 * STAGE > kBM * SX ? 2 * STAGE : kBM * SX);
+  static constexpr int PT2 = (PT + 1) / 2;               // 2x2 super tiles of the Gram
+  static constexpr int NS = PT2 * (PT2 + 1) / 2;
+  static constexpr int SPW = (NS + 7) / 8;               // super tiles per warp
+};
+
+template <int PT>
+__device__ __forceinline__ void issue_chunk(const TsArgs& a, double* stage, int m0, int k0, int w, int wa,
+                                            int tid) {
+  using S = TsShape<PT>;
+  double* s_u = stage;
+  double* s_t = stage + kBM * kSU;
+#pragma unroll 4
+  for (int e = tid; e < kBM * kBK; e += kThreads) {
+    const int i = e >> 5, j = e & 31;
+    const int m = m0 + i, c = k0 + j;
+    const bool ok = (m < a.M) && (c < w);
+    const double* src = a.u.A;
+    if (ok) src = (c < wa) ? a.u.A + (size_t)m * a.u.lda + c : a.u.B + (size_t)m * a.u.ldb + (c - wa);
+    cp_async8(s_u + i * kSU + j, src, ok);
+  }
+#pragma unroll 4
+  for (int e = tid; e < kBK * S::PMAX; e += kThreads) {
+    const int i = e / S::PMAX, j = e - (e / S::PMAX) * S::PMAX;
+    const int c = k0 + i;
+    const bool ok = c < w;
+    cp_async8(s_t + i * S::SX + j, ok ? a.T + (size_t)c * a.ldt + j : a.T, ok);
+  }
+}
+
 template <int PT, int MODE>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 1)
 ts_kernel(TsArgs a) {
-  constexpr int PMAX = PT * 8;
-  constexpr int SX = PMAX + 4;                      // row stride of T chunk / X tile in smem
-  constexpr int NT = PT * (PT + 1) / 2;             // upper 8x8 tiles of the Gram
-  constexpr int TPW = (NT + 7) / 8;                 // Gram tiles per warp
+  using S = TsShape<PT>;
+  constexpr int PMAX = S::PMAX, SX = S::SX;
 
   int wa;
   const int w = ucat_widths(a, wa);
@@ -53,80 +100,83 @@ ts_kernel(TsArgs a) {
   }
 
   extern __shared__ double sm[];
-  double* s_u = sm;                        // [kBM][kSU]
-  double* s_t = s_u + kBM * kSU;           // [kBK][SX]
-  double* s_x = s_t + kBK * SX;            // [kBM][SX]
+  double* s_x = sm;                                      // aliases the two stages after the K loop
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, tig = lane & 3;
 
-  double gacc[TPW][2];
+  // Gram super tiles (I2, J2), I2 <= J2, of this warp
+  double gacc[S::SPW][4][2];
+  int sI[S::SPW], sJ[S::SPW];
 #pragma unroll
-  for (int s = 0; s < TPW; ++s) gacc[s][0] = gacc[s][1] = 0.0;
-  // Gram tile coordinates of this warp
-  int tI[TPW], tJ[TPW];
+  for (int s = 0; s < S::SPW; ++s) {
 #pragma unroll
-  for (int s = 0; s < TPW; ++s) {
+    for (int q = 0; q < 4; ++q) gacc[s][q][0] = gacc[s][q][1] = 0.0;
     int t = warp + 8 * s, I = 0;
-    if (t >= NT) { tI[s] = -1; tJ[s] = -1; continue; }
-    while (t >= PT - I) { t -= PT - I; ++I; }
-    tI[s] = I; tJ[s] = I + t;
+    if (t >= S::NS) { sI[s] = -1; sJ[s] = -1; continue; }
+    while (t >= S::PT2 - I) { t -= S::PT2 - I; ++I; }
+    sI[s] = I; sJ[s] = I + t;
   }
 
+  const int nk = (w + kBK - 1) / kBK;
   const int ntiles = (a.M + kBM - 1) / kBM;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int m0 = tile * kBM;
-    double xacc[PT][2];
+    double x0[PT][2], x1[PT][2];
 #pragma unroll
-    for (int n = 0; n < PT; ++n) xacc[n][0] = xacc[n][1] = 0.0;
+    for (int n = 0; n < PT; ++n) x0[n][0] = x0[n][1] = x1[n][0] = x1[n][1] = 0.0;
 
-    for (int k0 = 0; k0 < w; k0 += kBK) {
-      // stage the Ucat tile [m0, m0+64) x [k0, k0+32)
-      for (int e = tid; e < kBM * kBK; e += kThreads) {
-        const int i = e / kBK, j = e - (e / kBK) * kBK;
-        const int m = m0 + i, c = k0 + j;
-        double v = 0.0;
-        if (m < a.M && c < w) {
-          v = (c < wa) ? __ldg(a.u.A + (size_t)m * a.u.lda + c)
-                       : __ldg(a.u.B + (size_t)m * a.u.ldb + (c - wa));
-        }
-        s_u[i * kSU + j] = v;
-      }
-      // stage the T chunk [k0, k0+32) x [0, PMAX)
-      for (int e = tid; e < kBK * PMAX; e += kThreads) {
-        const int i = e / PMAX, j = e - (e / PMAX) * PMAX;
-        const int c = k0 + i;
-        s_t[i * SX + j] = (c < w && j < p) ? __ldg(a.T + (size_t)c * a.ldt + j) : 0.0;
+    issue_chunk<PT>(a, sm, m0, 0, w, wa, tid);
+    cp_commit();
+    for (int kc = 0; kc < nk; ++kc) {
+      if (kc + 1 < nk) {
+        issue_chunk<PT>(a, sm + ((kc + 1) & 1) * S::STAGE, m0, (kc + 1) * kBK, w, wa, tid);
+        cp_commit();
+        cp_wait<1>();
+      } else {
+        cp_wait<0>();
       }
       __syncthreads();
+      const double* s_u = sm + (kc & 1) * S::STAGE;
+      const double* s_t = s_u + kBM * kSU;
 #pragma unroll
       for (int kk = 0; kk < kBK; kk += 4) {
-        const double av = s_u[(warp * 8 + gid) * kSU + kk + tig];
+        const double a0 = s_u[(warp * 16 + gid) * kSU + kk + tig];
+        const double a1 = s_u[(warp * 16 + 8 + gid) * kSU + kk + tig];
 #pragma unroll
         for (int n = 0; n < PT; ++n) {
           const double bv = s_t[(kk + tig) * SX + n * 8 + gid];
-          dmma884(xacc[n], av, bv);
+          dmma884(x0[n], a0, bv);
+          dmma884(x1[n], a1, bv);
         }
       }
       __syncthreads();
     }
-    // X tile -> smem
+    // X tile -> smem (stage buffers are idle now)
 #pragma unroll
     for (int n = 0; n < PT; ++n) {
-      s_x[(warp * 8 + gid) * SX + n * 8 + 2 * tig] = xacc[n][0];
-      s_x[(warp * 8 + gid) * SX + n * 8 + 2 * tig + 1] = xacc[n][1];
+      const int c = n * 8 + 2 * tig;
+      *reinterpret_cast<double2*>(s_x + (warp * 16 + gid) * SX + c) = make_double2(x0[n][0], x0[n][1]);
+      *reinterpret_cast<double2*>(s_x + (warp * 16 + 8 + gid) * SX + c) = make_double2(x1[n][0], x1[n][1]);
     }
     __syncthreads();
     if constexpr (MODE == 0) {
-#pragma unroll 4
+#pragma unroll 2
       for (int k = 0; k < kBM; k += 4) {
+        const double* xr = s_x + (k + tig) * SX + gid;
 #pragma unroll
-        for (int s = 0; s < TPW; ++s) {
-          if (tI[s] >= 0) {
-            const double av = s_x[(k + tig) * SX + tI[s] * 8 + gid];
-            const double bv = s_x[(k + tig) * SX + tJ[s] * 8 + gid];
-            dmma884(gacc[s], av, bv);
+        for (int s = 0; s < S::SPW; ++s) {
+          if (sI[s] >= 0) {
+            const int I0 = 2 * sI[s], J0 = 2 * sJ[s];
+            const double a0 = xr[I0 * 8];
+            const double a1 = (I0 + 1 < PT) ? xr[(I0 + 1) * 8] : 0.0;
+            const double b0 = xr[J0 * 8];
+            const double b1 = (J0 + 1 < PT) ? xr[(J0 + 1) * 8] : 0.0;
+            dmma884(gacc[s][0], a0, b0);
+            dmma884(gacc[s][1], a0, b1);
+            if (sI[s] != sJ[s]) dmma884(gacc[s][2], a1, b0);
+            dmma884(gacc[s][3], a1, b1);
           }
         }
       }
@@ -137,22 +187,28 @@ ts_kernel(TsArgs a) {
         if (m < a.M && j < p) a.out[(size_t)m * a.ldo + j] = s_x[i * SX + j];
       }
     }
-    // the next tile's first k-chunk __syncthreads() orders these s_x reads before its writes
+    __syncthreads();   // s_x (= stage memory) is overwritten by the next tile's first chunk
   }
 
   if constexpr (MODE == 0) {
     double* part = a.partials + (size_t)blockIdx.x * PMAX * PMAX;
-    // zero the lower 8x8 tiles (never computed) so the reduction reads defined data
+    // lower 8x8 tiles are never computed: zero them so the reduction reads defined data
     for (int e = tid; e < PMAX * PMAX; e += kThreads) {
       const int i = e / PMAX, j = e - (e / PMAX) * PMAX;
       if ((i >> 3) > (j >> 3)) part[e] = 0.0;
     }
 #pragma unroll
-    for (int s = 0; s < TPW; ++s) {
-      if (tI[s] >= 0) {
-        const int row = tI[s] * 8 + gid, col = tJ[s] * 8 + 2 * tig;
-        part[row * PMAX + col] = gacc[s][0];
-        part[row * PMAX + col + 1] = gacc[s][1];
+    for (int s = 0; s < S::SPW; ++s) {
+      if (sI[s] >= 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int I = 2 * sI[s] + (q >> 1), J = 2 * sJ[s] + (q & 1);
+          if (I < PT && J < PT && I <= J) {
+            const int row = I * 8 + gid, col = J * 8 + 2 * tig;
+            part[row * PMAX + col] = gacc[s][q][0];
+            part[row * PMAX + col + 1] = gacc[s][q][1];
+          }
+        }
       }
     }
   }
@@ -160,49 +216,32 @@ ts_kernel(TsArgs a) {
 
 template <int PT, int MODE>
 cudaError_t launch_pt(const TsArgs& a, int grid, cudaStream_t s) {
-  constexpr int PMAX = PT * 8;
-  constexpr size_t smem = sizeof(double) * ((size_t)kBM * kSU + (size_t)kBK * (PMAX + 4) +
-                                            (size_t)kBM * (PMAX + 4));
-  ts_kernel<PT, MODE><<<grid, kThreads, smem, s>>>(a);
+  ts_kernel<PT, MODE><<<grid, kThreads, sizeof(double) * TsShape<PT>::SMEM, s>>>(a);
   return cudaGetLastError();
 }
 
 template <int PT, int MODE>
 cudaError_t prep_pt() {
-  constexpr int PMAX = PT * 8;
-  constexpr size_t smem = sizeof(double) * ((size_t)kBM * kSU + (size_t)kBK * (PMAX + 4) +
-                                            (size_t)kBM * (PMAX + 4));
   return cudaFuncSetAttribute(ts_kernel<PT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)smem);
+                              (int)(sizeof(double) * TsShape<PT>::SMEM));
 }
 
-template <int MODE>
-cudaError_t prep_mode() {
-  cudaError_t e;
-  if ((e = prep_pt<2, MODE>()) != cudaSuccess) return e;
-  if ((e = prep_pt<4, MODE>()) != cudaSuccess) return e;
-  if ((e = prep_pt<6, MODE>()) != cudaSuccess) return e;
-  if ((e = prep_pt<8, MODE>()) != cudaSuccess) return e;
-  if ((e = prep_pt<10, MODE>()) != cudaSuccess) return e;
-  if ((e = prep_pt<12, MODE>()) != cudaSuccess) return e;
-  if ((e = prep_pt<14, MODE>()) != cudaSuccess) return e;
-  return prep_pt<16, MODE>();
-}
-
-template <int MODE>
-cudaError_t launch_mode(const TsArgs& a, int pmax, int grid, cudaStream_t s) {
-  switch (pmax) {
-    case 16: return launch_pt<2, MODE>(a, grid, s);
-    case 32: return launch_pt<4, MODE>(a, grid, s);
-    case 48: return launch_pt<6, MODE>(a, grid, s);
-    case 64: return launch_pt<8, MODE>(a, grid, s);
-    case 80: return launch_pt<10, MODE>(a, grid, s);
-    case 96: return launch_pt<12, MODE>(a, grid, s);
-    case 112: return launch_pt<14, MODE>(a, grid, s);
-    case 128: return launch_pt<16, MODE>(a, grid, s);
+template <int MODE, int PT>
+struct Dispatch {
+  static cudaError_t launch(const TsArgs& a, int pt, int grid, cudaStream_t s) {
+    if (pt == PT) return launch_pt<PT, MODE>(a, grid, s);
+    return Dispatch<MODE, PT - 1>::launch(a, pt, grid, s);
   }
-  return cudaErrorInvalidValue;
-}
+  static cudaError_t prep() {
+    cudaError_t e = prep_pt<PT, MODE>();
+    return e != cudaSuccess ? e : Dispatch<MODE, PT - 1>::prep();
+  }
+};
+template <int MODE>
+struct Dispatch<MODE, 0> {
+  static cudaError_t launch(const TsArgs&, int, int, cudaStream_t) { return cudaErrorInvalidValue; }
+  static cudaError_t prep() { return cudaSuccess; }
+};
 
 __global__ void gram_reduce_kernel(const double* __restrict__ partials, int nblocks, int pmax,
                                    double* __restrict__ G) {
@@ -220,20 +259,13 @@ __global__ void gram_reduce_kernel(const double* __restrict__ partials, int nblo
 }  // namespace
 
 cudaError_t ts_prepare() {
-  cudaError_t e = prep_mode<0>();
-  return e != cudaSuccess ? e : prep_mode<1>();
+  cudaError_t e = Dispatch<0, 16>::prep();
+  return e != cudaSuccess ? e : Dispatch<1, 16>::prep();
 }
 
 int ts_pmax_for(int p) {
-  if (p <= 16) return 16;
-  if (p <= 32) return 32;
-  if (p <= 48) return 48;
-  if (p <= 64) return 64;
-  if (p <= 80) return 80;
-  if (p <= 96) return 96;
-  if (p <= 112) return 112;
-  if (p <= 128) return 128;
-  return -1;
+  if (p < 1 || p > 128) return -1;
+  return 8 * ((p + 7) / 8);
 }
 
 int ts_grid_for(int M) {
@@ -245,12 +277,13 @@ int ts_grid_for(int M) {
     if (sms <= 0) sms = 148;
   }
   const int ntiles = (M + kBM - 1) / kBM;
-  const int g = 2 * sms;
-  return ntiles < g ? (ntiles > 0 ? ntiles : 1) : g;
+  return ntiles < sms ? (ntiles > 0 ? ntiles : 1) : sms;
 }
 
 cudaError_t launch_ts(int mode, const TsArgs& a, int pmax, int grid, cudaStream_t s) {
-  return mode == 0 ? launch_mode<0>(a, pmax, grid, s) : launch_mode<1>(a, pmax, grid, s);
+  if (pmax % 8 || pmax < 8 || pmax > 128) return cudaErrorInvalidValue;
+  return mode == 0 ? Dispatch<0, 16>::launch(a, pmax / 8, grid, s)
+                   : Dispatch<1, 16>::launch(a, pmax / 8, grid, s);
 }
 
 cudaError_t launch_gram_reduce(const double* partials, int nblocks, int pmax, double* G,

@@ -51,7 +51,8 @@ class SolveInfo(ctypes.Structure):
                 ("diverged", ctypes.c_int32), ("shift_escalations", ctypes.c_int32),
                 ("ms_iterations", ctypes.c_float), ("ms_total", ctypes.c_float),
                 ("rank_history", ctypes.POINTER(ctypes.c_int64)),
-                ("sigma_history", ctypes.POINTER(ctypes.c_double))]
+                ("sigma_history", ctypes.POINTER(ctypes.c_double)), ("jacobi_sweeps", ctypes.c_int64),
+                ("chol2_cycles", ctypes.c_double * 3)]
 
 
 def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
@@ -229,7 +230,7 @@ class Context:
                                         ldvo, w1, ctypes.byref(info)))
         res = dict(rank=info.rank, rel_residual=info.rel_residual, b_norm=info.b_norm, diverged=bool(info.diverged),
                    shift_escalations=info.shift_escalations, ms_iterations=info.ms_iterations,
-                   ms_total=info.ms_total, rank_history=list(rh),
+                   ms_total=info.ms_total, rank_history=list(rh), jacobi_sweeps=info.jacobi_sweeps, chol2_cycles=list(info.chol2_cycles),
                    sigma_history=np.frombuffer(sh, dtype=np.float64).reshape(n_iter, SIGMA_STRIDE).copy())
         return Uo, Vo, res
 

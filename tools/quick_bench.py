@@ -41,5 +41,35 @@ def main(name="large", N=20):
               f"rho={info['rel_residual']:.3e} esc={info['shift_escalations']}", flush=True)
 
 
+
+
+def profile(name="large", N=20):
+    prob = gen.make_problem(name)
+    cfg, op = prob.cfg, prob.op
+    d_mu, d_nu, BU, BV = prob.subset(0)
+    dev = torch.device("cuda:0")
+    ctx = lrcheb.Context(0)
+    ctx.set_operator(torch.from_numpy(op.row_ptr).to(dev), torch.from_numpy(op.col_idx).to(dev),
+                     [torch.from_numpy(v).to(dev) for v in op.vals], op.rho_f, op.lambda_s)
+    ctx.set_params(d_mu, d_nu)
+    bu, bv = torch.from_numpy(BU).to(dev), torch.from_numpy(BV).to(dev)
+    ctx.solve(bu, bv, prob.lam_min, prob.lam_max, cfg.tol, cfg.rank_cap, N)
+    _, _, info = ctx.solve(bu, bv, prob.lam_min, prob.lam_max, cfg.tol, cfg.rank_cap, N)
+    print(f"[{name}] graph solve N={N}: {info['ms_iterations'] / N:.3f} ms/it, sweeps/it "
+          f"{info['jacobi_sweeps'] / N:.1f}, rho={info['rel_residual']:.3e} chol2 cycles/it (chol+R, jacobi, out) "
+          f"{[round(c / N) for c in info['chol2_cycles']]}", flush=True)
+    ctx.set_profiling(True)
+    ctx.solve(bu, bv, prob.lam_min, prob.lam_max, cfg.tol, cfg.rank_cap, N)
+    prof = ctx.profile()
+    ctx.set_profiling(False)
+    for k, (ms, cnt) in sorted(prof.items(), key=lambda kv: -kv[1][0]):
+        if cnt:
+            print(f"   {k:12s} {ms:9.2f} ms total  {cnt:5d} launches  {ms / cnt:8.4f} ms avg", flush=True)
+
+
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "large", int(sys.argv[2]) if len(sys.argv) > 2 else 20)
+    if len(sys.argv) > 1 and sys.argv[1] == "profile":
+        for nm in sys.argv[2:] or ["large"]:
+            profile(nm, {"tiny": 30, "small": 50, "medium": 80, "large": 20}[nm])
+    else:
+        main(sys.argv[1] if len(sys.argv) > 1 else "large", int(sys.argv[2]) if len(sys.argv) > 2 else 20)
