@@ -8,7 +8,9 @@
 //          ts STORE(Ucat, Z) -> U_{k+1}                                          (a6)
 // with Ucat = [Wcat | U_{k-1}] never copied (two strided blocks) and all ranks device-resident,
 // so the whole N-iteration loop is captured once into a CUDA graph and replayed.
+#include <algorithm>
 #include <cmath>
+#include <iterator>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -82,7 +84,9 @@ struct lrc_ctx {
   int64_t M = 0, nnz = 0;
   int* row_ptr = nullptr; int* col_idx = nullptr; double* vals[6] = {};
   int* group_ptr = nullptr; int ngroups = 0;
-  int* tile_ptr = nullptr; int ntiles = 0;
+  int* tdesc = nullptr; int ntiles = 0;
+  int* tlist_u = nullptr; int ntl_u = 0; int* tlist_g = nullptr; int ntl_g = 0;
+  size_t meta_bytes = 0;
   double rho = 0, lam = 0;
   // params
   bool par_set = false;
@@ -274,7 +278,10 @@ SpmmArgs spmm_base(lrc_ctx* ctx) {
   a.ngroups = ctx->ngroups;
   a.group_ptr = ctx->group_ptr;
   a.ntiles = ctx->ntiles;
-  a.tile_ptr = ctx->tile_ptr;
+  a.tdesc = ctx->tdesc;
+  a.tlist_u = ctx->tlist_u; a.ntl_u = ctx->ntl_u;
+  a.tlist_g = ctx->tlist_g; a.ntl_g = ctx->ntl_g;
+  a.tlist = nullptr;
   a.row_ptr = ctx->row_ptr;
   a.col_idx = ctx->col_idx;
   for (int t = 0; t < 6; ++t) a.v[t] = ctx->vals[t];
@@ -292,7 +299,7 @@ lrc_status enqueue_truncation(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, co
   Workspace& w = ctx->ws;
   State st = make_state(w);
   SmallBufs b = make_bufs(w);
-  if (fork_from_spmm) {
+  if (fork_from_spmm && !ctx->profiling) {   // profiling: serial, so per-kernel times are isolated
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
     KL(P_VSIDE, ctx->side, launch_vside(vd, (int)ctx->n, ctx->dmu, ctx->dnu, omega, k, st, b, w.wmax, ctx->side));
     CK(cudaEventRecord(ctx->ev_join, ctx->side));
@@ -482,7 +489,7 @@ void lrc_destroy(lrc_ctx* ctx) {
     dfree(ctx->row_ptr); dfree(ctx->col_idx);
     for (int t = 0; t < 6; ++t) dfree(ctx->vals[t]);
   }
-  dfree(ctx->group_ptr); dfree(ctx->tile_ptr); dfree(ctx->dmu); dfree(ctx->dnu);
+  dfree(ctx->group_ptr); dfree(ctx->tdesc); dfree(ctx->tlist_u); dfree(ctx->tlist_g); dfree(ctx->dmu); dfree(ctx->dnu);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
@@ -560,21 +567,83 @@ lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t*
     else { groups.push_back((int32_t)i); gsz = 1; }
   }
   groups.push_back((int32_t)M);
-  // CTA tiles of the fused SpMM: <= 8 node blocks and <= kSpmmCap nnz (a longer block is alone)
-  std::vector<int32_t> tiles;
-  tiles.push_back(0);
+  // CTA tiles of the fused SpMM: <= kTileBlocks node blocks, <= kSpmmCap nnz,
+  // <= kValCap staged doubles, and -- for the shared-memory U path -- the deduplicated set of U rows
+  // the tile's column lists touch (<= kUCap rows) with a 16-bit local index per column-list entry.
+  // Everything a CTA needs is packed into one kDescInts-word descriptor (one coalesced load).
+  // A block that alone exceeds a bound gets its own tile on the L2-gather path (nu = 0).
+  std::vector<int32_t> tdesc;
   {
-    int cnt = 0;
-    int64_t tn = 0;
     const int ng = (int)groups.size() - 1;
+    std::vector<int32_t> uni, merged;
+    std::vector<int> tb;                           // blocks of the open tile
+    int64_t tn = 0, tv = 0, tl = 0;
+    auto block_cols = [&](int gi, const int32_t*& c, int& L) {
+      c = hci.data() + hrp[groups[gi]];
+      L = hrp[groups[gi] + 1] - hrp[groups[gi]];
+    };
+    auto close_tile = [&](bool ushared) {
+      std::vector<int32_t> d(kDescInts, 0);
+      const int r0 = groups[tb.front()], r1 = groups[tb.back() + 1];
+      d[0] = hrp[r0];
+      d[1] = hrp[r1] - hrp[r0];
+      d[2] = (int)tb.size();
+      d[3] = ushared ? (int)uni.size() : 0;
+      d[4] = r0;
+      d[5] = r1;
+      uint16_t* lx = reinterpret_cast<uint16_t*>(d.data() + kDescLidx);
+      int lo = 0;
+      for (size_t b = 0; b < tb.size(); ++b) {
+        const int gi = tb[b];
+        const int32_t* c; int L;
+        block_cols(gi, c, L);
+        d[8 + b] = groups[gi];
+        d[12 + b] = groups[gi + 1] - groups[gi];
+        d[16 + b] = L;
+        d[20 + b] = -1;                    // local row of the block's first row in the staged U rows
+        if (ushared) {
+          auto it = std::lower_bound(uni.begin(), uni.end(), (int32_t)groups[gi]);
+          const int g = groups[gi + 1] - groups[gi];
+          if (it != uni.end() && *it == groups[gi] && (it - uni.begin()) + g <= (long)uni.size() &&
+              *(it + (g - 1)) == groups[gi] + g - 1)
+            d[20 + b] = (int32_t)(it - uni.begin());
+        }
+        if (ushared)
+          for (int j = 0; j < L; ++j)
+            lx[lo + j] = (uint16_t)(std::lower_bound(uni.begin(), uni.end(), c[j]) - uni.begin());
+        lo += L;
+      }
+      if (ushared)
+        for (size_t u = 0; u < uni.size(); ++u) d[kDescUrows + u] = uni[u];
+      tdesc.insert(tdesc.end(), d.begin(), d.end());
+      tb.clear(); uni.clear(); tn = tv = tl = 0;
+    };
     for (int gi = 0; gi < ng; ++gi) {
-      const int64_t gn = (int64_t)hrp[groups[gi + 1]] - hrp[groups[gi]];
-      if (cnt > 0 && (cnt == 8 || tn + gn > kSpmmCap)) { tiles.push_back(gi); cnt = 0; tn = 0; }
-      ++cnt;
-      tn += gn;
-      if (gn > kSpmmCap) { tiles.push_back(gi + 1); cnt = 0; tn = 0; }
+      const int g = groups[gi + 1] - groups[gi];
+      const int32_t* c; int L;
+      block_cols(gi, c, L);
+      const int64_t gn = (int64_t)g * L;
+      const int lp = L + ((20 - (L & 15)) & 15);     // row pitch of the staged values (spmm.cu)
+      const int64_t gv = (int64_t)3 * g * lp;
+      merged.clear();
+      std::set_union(uni.begin(), uni.end(), c, c + L, std::back_inserter(merged));
+      const bool fits = (int)tb.size() < kTileBlocks && tn + gn <= kSpmmCap && tv + gv <= kValCap &&
+                        tl + L <= kLidxCap && (int)merged.size() <= kUCap && g <= 5;
+      if (!fits && !tb.empty()) {
+        close_tile(true);
+        merged.assign(c, c + L);
+      }
+      const bool alone_ok = gn <= kSpmmCap && gv <= kValCap && L <= kUCap && L <= kLidxCap && g <= 5;
+      if (!alone_ok) {                       // generic long / tall block: L2-gather path, own tile
+        tb.push_back(gi);
+        close_tile(false);
+        continue;
+      }
+      uni.swap(merged);
+      tb.push_back(gi);
+      tn += gn; tv += gv; tl += L;
     }
-    if (cnt > 0) tiles.push_back(ng);
+    if (!tb.empty()) close_tile(true);
   }
 
   CK(cudaStreamSynchronize(ctx->stream));
@@ -585,8 +654,9 @@ lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t*
     for (int t = 0; t < 6; ++t) dfree(ctx->vals[t]);
   }
   dfree(ctx->group_ptr);
-  dfree(ctx->tile_ptr);
-  ctx->row_ptr = nullptr; ctx->col_idx = nullptr; ctx->group_ptr = nullptr; ctx->tile_ptr = nullptr;
+  dfree(ctx->tdesc); dfree(ctx->tlist_u); dfree(ctx->tlist_g);
+  ctx->tlist_u = ctx->tlist_g = nullptr;
+  ctx->row_ptr = nullptr; ctx->col_idx = nullptr; ctx->group_ptr = nullptr; ctx->tdesc = nullptr;
   for (int t = 0; t < 6; ++t) ctx->vals[t] = nullptr;
   ctx->op_set = false;
   ctx->par_set = false;   // params depend on nothing here, but workspaces do; keep semantics simple
@@ -611,9 +681,20 @@ lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t*
   CK(dalloc(&ctx->group_ptr, groups.size()));
   CK(cudaMemcpy(ctx->group_ptr, groups.data(), sizeof(int32_t) * groups.size(), cudaMemcpyHostToDevice));
   ctx->ngroups = (int)groups.size() - 1;
-  CK(dalloc(&ctx->tile_ptr, tiles.size()));
-  CK(cudaMemcpy(ctx->tile_ptr, tiles.data(), sizeof(int32_t) * tiles.size(), cudaMemcpyHostToDevice));
-  ctx->ntiles = (int)tiles.size() - 1;
+  CK(dalloc(&ctx->tdesc, tdesc.size()));
+  CK(cudaMemcpy(ctx->tdesc, tdesc.data(), sizeof(int32_t) * tdesc.size(), cudaMemcpyHostToDevice));
+  ctx->ntiles = (int)(tdesc.size() / kDescInts);
+  {
+    std::vector<int32_t> lu, lg;
+    for (int t = 0; t < ctx->ntiles; ++t) (tdesc[(size_t)t * kDescInts + 3] > 0 ? lu : lg).push_back(t);
+    CK(dalloc(&ctx->tlist_u, lu.size()));
+    CK(dalloc(&ctx->tlist_g, lg.size()));
+    if (!lu.empty()) CK(cudaMemcpy(ctx->tlist_u, lu.data(), sizeof(int32_t) * lu.size(), cudaMemcpyHostToDevice));
+    if (!lg.empty()) CK(cudaMemcpy(ctx->tlist_g, lg.data(), sizeof(int32_t) * lg.size(), cudaMemcpyHostToDevice));
+    ctx->ntl_u = (int)lu.size();
+    ctx->ntl_g = (int)lg.size();
+  }
+  ctx->meta_bytes = sizeof(int32_t) * tdesc.size();
   ctx->M = M;
   ctx->nnz = nnz;
   ctx->rho = rho_f;

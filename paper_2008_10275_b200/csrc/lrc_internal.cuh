@@ -10,7 +10,19 @@ constexpr int kMaxRank = 128;    // rank_cap limit
 constexpr int kMaxP = 128;       // max Gram width p = min(n, w)
 constexpr int kMaxW = 256;       // max concatenation width w = r_B + 4 r
 constexpr int kGroupMax = 8;     // rows per node block in the fused SpMM
-constexpr int kSpmmCap = 2048;   // nnz staged per SpMM CTA tile
+constexpr int kSpmmCap = 1024;   // nnz staged per SpMM CTA tile
+constexpr int kValCap = 3200;    // staged (combined, row-padded) doubles per SpMM tile
+constexpr int kTileBlocks = 4;   // node blocks per SpMM tile
+constexpr int kUCap = 90;        // deduplicated U rows staged in shared memory per SpMM tile
+// SpMM tile descriptor (int32 words): [0] e0 (first nnz) [1] tot (nnz) [2] nb (blocks) [3] nu (U rows
+// staged; 0 = L2-gather tile) [4] rbeg [5] rend [6..7] pad, [8+b] row0, [12+b] g, [16+b] L, [20+b] local U row of the block's
+// first row (-1: not staged)
+// (b < 4); [24 .. 24+kUCap) U row ids; [kDescLidx ..) uint16 local column indices of the blocks'
+// column lists, concatenated (<= kLidxCap entries).
+constexpr int kDescInts = 256;
+constexpr int kDescUrows = 24;
+constexpr int kDescLidx = kDescUrows + kUCap;                 // 114
+constexpr int kLidxCap = 2 * (kDescInts - kDescLidx);         // 284
 constexpr int kSigmaStride = 128;
 
 // ------------------------------------------------------------------------------------------
@@ -23,8 +35,13 @@ struct SpmmArgs {
   int ngroups;
   const int* group_ptr;     // [ngroups+1] first row of each node block
   int ntiles;
-  const int* tile_ptr;      // [ntiles+1] first node block of each CTA tile (<= 8 blocks, <= kSpmmCap nnz
-                            // unless a single block is longer)
+  const int* tdesc;         // [ntiles][kDescInts] packed tile descriptors (see spmm.cu)
+  const int* tlist_u;       // tiles with shared-memory U rows (nu > 0), for the pipelined hot kernel
+  int ntl_u;
+  const int* tlist_g;       // L2-gather tiles (nu = 0)
+  int ntl_g;
+  const int* tlist;         // (set by the launcher) tile list, or null for all tiles
+  int u_aligned16;          // (set by the launcher) U rows may be copied in 16-byte chunks
   const int* row_ptr;
   const int* col_idx;
   const double* v[6];       // A0, A1, A2, Jrho, Jmu, Jlam

@@ -1,19 +1,21 @@
 // a1 -- fused six-array CSR SpMM (`equation_intro_mat1`).
 //
-// One pass over the shared CSR pattern reads col_idx once and each of the six fp64 value arrays
-// once, and produces the operator grouped by right diagonal (exact, Kronecker identity
-// I(x)(A0+rho Jrho+lam Jlam) + Dmu(x)(A1+Jmu) + Dnu(x)(rho A2)):
+// One pass over the shared CSR pattern reads each of the six fp64 value arrays once and the shared
+// column indices once per node block, and produces the operator grouped by right diagonal (exact,
+// Kronecker identity I(x)(A0+rho Jrho+lam Jlam) + Dmu(x)(A1+Jmu) + Dnu(x)(rho A2)):
 //     W0 = (A0 + rho Jrho + lam Jlam) U,  W1 = (A1 + Jmu) U,  W2 = rho A2 U,
 // with the Chebyshev-step epilogue W0' = U - gamma W0 fused (S2STEP).  The D_mu / D_nu scaling
 // of the terms lives on the V side (n rows), never on the M side (vside kernel).
 //
 // Mapping: rows come in node blocks -- runs of <= 8 consecutive rows with
 // identical column lists (the 5 field rows of an FE node share one list), detected at
-// set_operator -- and node blocks are packed into CTA tiles of <= kSpmmCap nnz.  A CTA streams its
-// tile's contiguous CSR segment (six value arrays + col_idx, coalesced, evict-first so U keeps
-// L1/L2) into shared memory, combining the six arrays into the three grouped streams on the way,
-// then each warp computes one node block: every U row (lanes over the r columns, read-only path)
-// is loaded once per block and reused by all its rows and all three groups (15 FMA per load).
+// set_operator -- packed into CTA tiles of <= 8 blocks / kSpmmCap nnz.  A 16-warp CTA streams the
+// tile's contiguous CSR segment (six value arrays, coalesced, evict-first so U keeps L1/L2) into
+// shared memory, combining the six arrays into the three grouped streams and interleaving them
+// per column-list entry ([j][row][stream], 16-byte aligned rows) on the way; the column list of a
+// block is read from its first row only.  Each warp then owns one (node block, 32-column slice):
+// every gathered U element (a 4-deep register prefetch ring hides the L2 latency) feeds
+// 3 x (rows of the block) FMAs.
 #include "lrc_internal.cuh"
 
 namespace lrc {
@@ -22,219 +24,455 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+constexpr int kPre = 4;                 // U gather prefetch depth
 
 template <int MODE>
 struct Nacc { static constexpr int v = (MODE == SPMM_S2STEP || MODE == SPMM_PLAIN3) ? 3 : 1; };
 template <int MODE>
 struct Nstage { static constexpr int v = (MODE == SPMM_SINGLE) ? 1 : 3; };
 
+// Staged values are laid out [slot][j] (slot = row*NV + stream, j = column-list entry) with a row
+// pitch == 4 (mod 16) doubles: the staging stores (consecutive j) and the DMMA fragment loads
+// (8 slots x 4 entries) are both bank-conflict free.
+__device__ __forceinline__ int row_pitch(int L) { return L + ((20 - (L & 15)) & 15); }
+
 template <int MODE>
-__device__ __forceinline__ void stage_entry(const SpmmArgs& a, int idx, int slot, double* s_v, double cs) {
+__device__ __forceinline__ void stage_entry(const SpmmArgs& a, int idx, double* dst, int lp, double cs) {
   if constexpr (MODE == SPMM_SINGLE) {
-    s_v[slot] = cs * __ldcs(a.v[a.single_t] + idx);
+    dst[0] = cs * __ldcs(a.v[a.single_t] + idx);
   } else {
     const double v0 = __ldcs(a.v[0] + idx), v1 = __ldcs(a.v[1] + idx), v2 = __ldcs(a.v[2] + idx);
     const double v3 = __ldcs(a.v[3] + idx), v4 = __ldcs(a.v[4] + idx), v5 = __ldcs(a.v[5] + idx);
-    s_v[slot] = fma(a.lam, v5, fma(a.rho, v3, v0));      // A0 + rho Jrho + lam Jlam
-    s_v[kSpmmCap + slot] = v1 + v4;                      // A1 + Jmu
-    s_v[2 * kSpmmCap + slot] = a.rho * v2;               // rho A2
+    dst[0] = fma(a.lam, v5, fma(a.rho, v3, v0));   // A0 + rho Jrho + lam Jlam
+    dst[lp] = v1 + v4;                             // A1 + Jmu
+    dst[2 * lp] = a.rho * v2;                      // rho A2
   }
 }
 
-// acc[q][t][i] += sum_j vals_t[q, j] * U[col_j, lane + 32 i] over the staged entries
-template <int MODE, int NC, int GM>
-__device__ __forceinline__ void block_accumulate(const SpmmArgs& a, int r, int lane, int g, int jn,
-                                                 int off, int rstride, const double* s_v,
-                                                 const int* s_col, const double (&dmu_c)[NC],
-                                                 const double (&dnu_c)[NC],
-                                                 double (&acc)[GM][Nacc<MODE>::v][NC]) {
-#pragma unroll 2
-  for (int j = 0; j < jn; ++j) {
-    const int col = s_col[j];
-    const double* urow = a.U + (size_t)col * a.ldu;
-    double u[NC];
+// One warp: rows [row0, row0 + gs) of a node block (their staged entries at
+// vals[((qo + q) * NV + t) * lp + j]), columns c = c0 + lane, over the jn staged column-list entries.
+template <int MODE, int GM>
+__device__ __forceinline__ void block_task(const SpmmArgs& a, int r, int c, int row0, int gs, int qo,
+                                           int jn, int lp, const double* vals, const int* cols,
+                                           double (&acc)[GM][Nacc<MODE>::v]) {
+  constexpr int NV = Nstage<MODE>::v;
+  const bool act = c < r;
+  double dmu_c = 0.0, dnu_c = 0.0;
+  if constexpr (MODE == SPMM_DENSE) {
+    if (act) { dmu_c = a.dmu[c]; dnu_c = a.dnu[c]; }
+  }
+  double ring[kPre];
 #pragma unroll
-    for (int i = 0; i < NC; ++i) {
-      const int c = lane + 32 * i;
-      u[i] = (c < r) ? __ldg(urow + c) : 0.0;
+  for (int d = 0; d < kPre; ++d) ring[d] = (d < jn && act) ? __ldg(a.U + (size_t)cols[d] * a.ldu + c) : 0.0;
+  for (int j0 = 0; j0 < jn; j0 += kPre) {
+#pragma unroll
+    for (int t = 0; t < kPre; ++t) {
+      const int j = j0 + t;
+      if (j >= jn) break;
+      const double u = ring[t];
+      const int jp = j + kPre;
+      ring[t] = (jp < jn && act) ? __ldg(a.U + (size_t)cols[jp] * a.ldu + c) : 0.0;
+      const double* vj = vals + qo * NV * lp + j;
+#pragma unroll
+      for (int q = 0; q < GM; ++q) {
+        if (q < gs) {
+          if constexpr (MODE == SPMM_S2STEP || MODE == SPMM_PLAIN3) {
+            acc[q][0] = fma(vj[(q * 3 + 0) * lp], u, acc[q][0]);
+            acc[q][1] = fma(vj[(q * 3 + 1) * lp], u, acc[q][1]);
+            acc[q][2] = fma(vj[(q * 3 + 2) * lp], u, acc[q][2]);
+          } else if constexpr (MODE == SPMM_DENSE) {
+            const double coef = fma(dnu_c, vj[(q * 3 + 2) * lp], fma(dmu_c, vj[(q * 3 + 1) * lp], vj[(q * 3) * lp]));
+            acc[q][0] = fma(coef, u, acc[q][0]);
+          } else {
+            acc[q][0] = fma(vj[q * lp], u, acc[q][0]);
+          }
+        }
+      }
     }
+  }
+  (void)row0;
+}
+
+__device__ __forceinline__ void dmma1684(double (&d)[4], double a0, double a1, double b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a0), "d"(a1), "d"(b));
+}
+
+// Hot modes (S2STEP / PLAIN3) on the fp64 tensor pipe: a node sub-block of gs <= 5 rows is the
+// dense contraction  [3 gs x L] (rows q*3 + stream, staged values) x [L x 32] (gathered U rows),
+// done as m16n8k4 DMMA over 4-entry k steps with the next step's U gather in flight.  Writes the
+// three grouped outputs (and the S2STEP epilogue) straight from the accumulator fragments.
+template <int MODE>
+__device__ __forceinline__ void block_task_mma(const SpmmArgs& a, int r, int n0, int row0, int gs, int qo,
+                                               int L, int lp, const double* vals, const int* cols,
+                                               int lane) {
+  const int gid = lane >> 2, tig = lane & 3;
+  const int nrow = gs * 3;
+  const int ra = gid, rb = gid + 8;
+  double acc[4][4];
 #pragma unroll
-    for (int q = 0; q < GM; ++q) {
-      if (q < g) {
-        const int e = off + q * rstride + j;
-        if constexpr (MODE == SPMM_S2STEP || MODE == SPMM_PLAIN3) {
-          const double va = s_v[e], vb = s_v[kSpmmCap + e], vc = s_v[2 * kSpmmCap + e];
+  for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.0;
+  // prologue: gather for k step 0
+  double bnext[4];
+  {
+    const int j = tig;
+    const bool jv = j < L;
+    const double* urow = a.U + (size_t)(jv ? cols[j] : 0) * a.ldu;
 #pragma unroll
-          for (int i = 0; i < NC; ++i) {
-            acc[q][0][i] = fma(va, u[i], acc[q][0][i]);
-            acc[q][1][i] = fma(vb, u[i], acc[q][1][i]);
-            acc[q][2][i] = fma(vc, u[i], acc[q][2][i]);
-          }
-        } else if constexpr (MODE == SPMM_DENSE) {
-          const double va = s_v[e], vb = s_v[kSpmmCap + e], vc = s_v[2 * kSpmmCap + e];
+    for (int nt = 0; nt < 4; ++nt) {
+      const int c = n0 + nt * 8 + gid;
+      bnext[nt] = (jv && c < r) ? __ldg(urow + c) : 0.0;
+    }
+  }
+  for (int k0 = 0; k0 < L; k0 += 4) {
+    double b[4];
 #pragma unroll
-          for (int i = 0; i < NC; ++i) {
-            const double coef = fma(dnu_c[i], vc, fma(dmu_c[i], vb, va));
-            acc[q][0][i] = fma(coef, u[i], acc[q][0][i]);
-          }
-        } else {
-          const double va = s_v[e];
+    for (int nt = 0; nt < 4; ++nt) b[nt] = bnext[nt];
+    {
+      const int j = k0 + 4 + tig;
+      const bool jv = j < L;
+      const double* urow = a.U + (size_t)(jv ? cols[j] : 0) * a.ldu;
 #pragma unroll
-          for (int i = 0; i < NC; ++i) acc[q][0][i] = fma(va, u[i], acc[q][0][i]);
+      for (int nt = 0; nt < 4; ++nt) {
+        const int c = n0 + nt * 8 + gid;
+        bnext[nt] = (jv && c < r) ? __ldg(urow + c) : 0.0;
+      }
+    }
+    const int j = k0 + tig;
+    const bool jv = j < L;
+    const double* vj = vals + qo * 3 * lp + j;
+    const double a0 = (jv && ra < nrow) ? vj[ra * lp] : 0.0;
+    const double a1 = (jv && rb < nrow) ? vj[rb * lp] : 0.0;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) dmma1684(acc[nt], a0, a1, b[nt]);
+  }
+  // epilogue: fragment (R, C) -> output row row0 + R/3, stream R%3, column n0 + nt*8 + 2 tig + {0,1}
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int R = h ? rb : ra;
+    if (R >= nrow) continue;
+    const int q = R / 3, st = R - (R / 3) * 3;
+    const size_t row = (size_t)(row0 + q);
+    double* orow = a.out + row * a.ldo + a.out_off + st * r;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = n0 + nt * 8 + 2 * tig + e;
+        if (c < r) {
+          double v = acc[nt][h * 2 + e];
+          if (MODE == SPMM_S2STEP && st == 0) v = fma(-a.gamma, v, __ldg(a.U + row * a.ldu + c));
+          __stcs(orow + c, v);
         }
       }
     }
   }
 }
 
-template <int MODE, int NC, int GM>
-__device__ __forceinline__ void block_store(const SpmmArgs& a, int r, int lane, int row0, int g,
-                                            const double (&acc)[GM][Nacc<MODE>::v][NC]) {
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+// rows of U (r columns, ldu even, 16-byte aligned) -> s_u (row stride ust even) in 16-byte chunks
+__device__ __forceinline__ void stage_u_rows(const SpmmArgs& a, int r, const int* ids, int nu, double* su,
+                                             int ust, int tid, int nthreads) {
+  if (a.u_aligned16) {
+    const int nch = (r + 1) >> 1;   // an odd r copies one element of padding (r + 1 <= ldu)
+    for (int e = tid; e < nu * nch; e += nthreads) {
+      const int u = e / nch, ch = e - (e / nch) * nch;
+      cp_async16(su + u * ust + 2 * ch, a.U + (size_t)ids[u] * a.ldu + 2 * ch);
+    }
+  } else {
+    for (int e = tid; e < nu * r; e += nthreads) {
+      const int u = e / r, c = e - (e / r) * r;
+      cp_async8(su + u * ust + c, a.U + (size_t)ids[u] * a.ldu + c);
+    }
+  }
+}
+
+// Same contraction with the tile's deduplicated U rows already in shared memory (row stride ust),
+// computed transposed so stores are full sectors:  D^T (32 cols x 3 gs) = U_tile^T (32 x L) Vals^T.
+// m16n8k4: M = 16 U columns (A = U^T from s_u, lcols[j] = local row of entry j), N = 8 row*3+stream
+// slots (B = staged values), K = 4 column-list entries.  lrow0 = local row of the block's first row
+// in s_u (for the S2STEP epilogue), -1 if absent.
+template <int MODE>
+__device__ __forceinline__ void block_task_mma_smem(const SpmmArgs& a, int r, int n0, int row0, int gs,
+                                                    int qo, int L, int lp, const double* vals,
+                                                    const unsigned short* lcols, const double* s_u, int ust,
+                                                    int lrow0, int lane) {
+  const int gid = lane >> 2, tig = lane & 3;
+  const int nrow = gs * 3;
+  double acc[2][2][4];   // [m tile (16 cols)][n tile (8 slots)][frag]
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.0;
+  for (int k0 = 0; k0 < L; k0 += 4) {
+    const int j = k0 + tig;
+    const bool jv = j < L;
+    const double* vj = vals + qo * 3 * lp + j;
+    const double b0 = (jv && gid < nrow) ? vj[gid * lp] : 0.0;
+    const double b1 = (jv && gid + 8 < nrow) ? vj[(gid + 8) * lp] : 0.0;
+    const double* urow = s_u + (jv ? lcols[j] : 0) * ust;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int cA = n0 + mt * 16 + gid, cB = cA + 8;
+      const double a0 = (jv && cA < r) ? urow[cA] : 0.0;
+      const double a1 = (jv && cB < r) ? urow[cB] : 0.0;
+      dmma1684(acc[mt][0], a0, a1, b0);
+      dmma1684(acc[mt][1], a0, a1, b1);
+    }
+  }
+  // epilogue: frag (m, n) -> column n0 + mt*16 + m, slot R = nt*8 + n = q*3 + stream
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int R = nt * 8 + 2 * tig + e;
+      if (R >= nrow) continue;
+      const int q = R / 3, st = R - (R / 3) * 3;
+      const size_t row = (size_t)(row0 + q);
+      double* orow = a.out + row * a.ldo + a.out_off + st * r;
+      const double* urow_self = (lrow0 >= 0) ? s_u + (lrow0 + qo + q) * ust : a.U + row * a.ldu;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+        for (int hm = 0; hm < 2; ++hm) {
+          const int c = n0 + mt * 16 + gid + hm * 8;
+          if (c < r) {
+            double v = acc[mt][nt][hm * 2 + e];
+            if (MODE == SPMM_S2STEP && st == 0) v = fma(-a.gamma, v, urow_self[c]);
+            __stcs(orow + c, v);
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int MODE, int GM>
+__device__ __forceinline__ void block_store(const SpmmArgs& a, int r, int c, int row0, int gs,
+                                            const double (&acc)[GM][Nacc<MODE>::v]) {
+  if (c >= r) return;
 #pragma unroll
   for (int q = 0; q < GM; ++q) {
-    if (q < g) {
+    if (q < gs) {
       const size_t row = (size_t)(row0 + q);
       double* orow = a.out + row * a.ldo + a.out_off;
-#pragma unroll
-      for (int i = 0; i < NC; ++i) {
-        const int c = lane + 32 * i;
-        if (c < r) {
-          if constexpr (MODE == SPMM_S2STEP) {
-            const double uk = __ldg(a.U + row * a.ldu + c);
-            __stcs(orow + c, fma(-a.gamma, acc[q][0][i], uk));
-            __stcs(orow + r + c, acc[q][1][i]);
-            __stcs(orow + 2 * r + c, acc[q][2][i]);
-          } else if constexpr (MODE == SPMM_PLAIN3) {
-            __stcs(orow + c, acc[q][0][i]);
-            __stcs(orow + r + c, acc[q][1][i]);
-            __stcs(orow + 2 * r + c, acc[q][2][i]);
-          } else {
-            __stcs(orow + c, acc[q][0][i]);
-          }
-        }
+      if constexpr (MODE == SPMM_S2STEP) {
+        const double uk = __ldg(a.U + row * a.ldu + c);
+        __stcs(orow + c, fma(-a.gamma, acc[q][0], uk));
+        __stcs(orow + r + c, acc[q][1]);
+        __stcs(orow + 2 * r + c, acc[q][2]);
+      } else if constexpr (MODE == SPMM_PLAIN3) {
+        __stcs(orow + c, acc[q][0]);
+        __stcs(orow + r + c, acc[q][1]);
+        __stcs(orow + 2 * r + c, acc[q][2]);
+      } else {
+        __stcs(orow + c, acc[q][0]);
       }
     }
   }
 }
 
-template <int MODE, int NC, int GM>
+template <int MODE, int GM>
+__device__ __forceinline__ void zero_acc(double (&acc)[GM][Nacc<MODE>::v]) {
+#pragma unroll
+  for (int q = 0; q < GM; ++q)
+#pragma unroll
+    for (int t = 0; t < Nacc<MODE>::v; ++t) acc[q][t] = 0.0;
+}
+
+template <int MODE, int GM>
 __global__ void __launch_bounds__(kThreads, 2)
-spmm_kernel(SpmmArgs a) {
+spmm_kernel(SpmmArgs a, int ust) {
   const int r = a.d_r ? *a.d_r : a.r_fixed;
   if (r <= 0) return;
+  constexpr int NV = Nstage<MODE>::v;
   constexpr int NACC = Nacc<MODE>::v;
   extern __shared__ double smem_dyn[];
-  double* s_v = smem_dyn;                                          // [NSTAGE][kSpmmCap]
-  int* s_col = reinterpret_cast<int*>(smem_dyn + Nstage<MODE>::v * kSpmmCap);
+  constexpr bool HOT = (MODE == SPMM_S2STEP || MODE == SPMM_PLAIN3);
+  double* s_v = smem_dyn;                                     // [kValCap]
+  double* s_u = smem_dyn + kValCap;                           // [kUCap][ust]   (HOT modes)
+  int* s_col = reinterpret_cast<int*>(smem_dyn + kValCap + (HOT ? kUCap * ust : 0));   // [kSpmmCap]
+  __shared__ int s_desc[kDescInts];
+  __shared__ int s_bstart[kGroupMax + 1], s_vbase[kGroupMax], s_cbase[kGroupMax];
+  __shared__ int s_L[kGroupMax], s_g[kGroupMax], s_js[kGroupMax], s_row0[kGroupMax];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int CT = (r + 31) >> 5;                               // 32-column slices
 
-  double dmu_c[NC], dnu_c[NC];
-#pragma unroll
-  for (int i = 0; i < NC; ++i) {
-    const int c = lane + 32 * i;
-    dmu_c[i] = (MODE == SPMM_DENSE && c < r) ? a.dmu[c] : 0.0;
-    dnu_c[i] = (MODE == SPMM_DENSE && c < r) ? a.dnu[c] : 0.0;
-  }
   double cs = 1.0;
   if constexpr (MODE == SPMM_SINGLE)
     cs = (a.single_t == 2 || a.single_t == 3) ? a.rho : (a.single_t == 5 ? a.lam : 1.0);
 
-  const int t = blockIdx.x;
-  const int g0 = a.tile_ptr[t], g1 = a.tile_ptr[t + 1];
-  const int rbeg = a.group_ptr[g0], rend = a.group_ptr[g1];
-  const int e0 = a.row_ptr[rbeg], e1 = a.row_ptr[rend];
-  const int tot = e1 - e0;
+  // one coalesced load of the tile's packed descriptor
+  const int t = a.tlist ? a.tlist[blockIdx.x] : blockIdx.x;
+  for (int i = tid; i < kDescInts; i += kThreads) s_desc[i] = __ldg(a.tdesc + (size_t)t * kDescInts + i);
+  __syncthreads();
+  const int e0 = s_desc[0], tot = s_desc[1], nb = s_desc[2];
+  const int rbeg = s_desc[4], rend = s_desc[5];
+  const unsigned short* s_lx = reinterpret_cast<const unsigned short*>(s_desc + kDescLidx);
 
   if (tot <= kSpmmCap) {
-    // ---- whole tile staged at once (the common case: <= 8 node blocks)
-    for (int e = tid; e < tot; e += kThreads) {
-      s_col[e] = __ldcs(a.col_idx + e0 + e);
-      stage_entry<MODE>(a, e0 + e, e, s_v, cs);
+    if (tid == 0) {
+      int vb = 0, cb = 0, eb = 0;
+      for (int b = 0; b < nb; ++b) {
+        const int g = s_desc[12 + b], L = s_desc[16 + b];
+        s_bstart[b] = eb;
+        s_row0[b] = s_desc[8 + b]; s_g[b] = g; s_L[b] = L;
+        s_js[b] = row_pitch(L);
+        s_vbase[b] = vb; s_cbase[b] = cb;
+        vb += g * NV * s_js[b];
+        cb += L;
+        eb += g * L;
+      }
+      s_bstart[nb] = tot;
     }
     __syncthreads();
-    const int grp = g0 + warp;
-    if (grp < g1) {
-      const int gr0 = a.group_ptr[grp], gr1 = a.group_ptr[grp + 1];
-      const int gb = a.row_ptr[gr0] - e0;
-      const int L = a.row_ptr[gr0 + 1] - a.row_ptr[gr0];
-      for (int sb = gr0; sb < gr1; sb += GM) {
-        const int g = min(GM, gr1 - sb);
-        double acc[GM][NACC][NC];
+    const int nu = HOT ? s_desc[3] : 0;
+    // ---- the tile's deduplicated U rows -> shared memory (cp.async, overlaps the value stream)
+    if (HOT && nu > 0) {
+      stage_u_rows(a, r, s_desc + kDescUrows, nu, s_u, ust, tid, kThreads);
+      asm volatile("cp.async.commit_group;\n" ::);
+    }
+    // ---- stage: coalesced over the tile's contiguous nnz range.  Every thread first issues all the
+    //      loads of its (<= kStg) entries, then combines and stores them, so the DRAM latency is
+    //      paid once per tile rather than once per entry.
+    constexpr int kStg = (kSpmmCap + kThreads - 1) / kThreads;
+    constexpr int NRAW = (MODE == SPMM_SINGLE) ? 1 : 6;
+    double raw[kStg][NRAW];
 #pragma unroll
-        for (int q = 0; q < GM; ++q)
+    for (int k = 0; k < kStg; ++k) {
+      const int e = tid + k * kThreads;
+      if (e < tot) {
+        if constexpr (MODE == SPMM_SINGLE) {
+          raw[k][0] = __ldcs(a.v[a.single_t] + e0 + e);
+        } else {
 #pragma unroll
-          for (int tt = 0; tt < NACC; ++tt)
+          for (int v = 0; v < 6; ++v) raw[k][v] = __ldcs(a.v[v] + e0 + e);
+        }
+      }
+    }
 #pragma unroll
-            for (int i = 0; i < NC; ++i) acc[q][tt][i] = 0.0;
-        const int off = gb + (sb - gr0) * L;
-        block_accumulate<MODE, NC, GM>(a, r, lane, g, L, off, L, s_v, s_col + gb, dmu_c, dnu_c, acc);
-        block_store<MODE, NC, GM>(a, r, lane, sb, g, acc);
+    for (int k = 0; k < kStg; ++k) {
+      const int e = tid + k * kThreads;
+      if (e < tot) {
+        int b = 0;
+#pragma unroll
+        for (int kk = 1; kk < kGroupMax; ++kk) b += (kk < nb && e >= s_bstart[kk]);
+        const int L = s_L[b];
+        const int rel = e - s_bstart[b];
+        const int q = rel / L, j = rel - (rel / L) * L;
+        const int lp = s_js[b];
+        double* dst = s_v + s_vbase[b] + q * NV * lp + j;
+        if constexpr (MODE == SPMM_SINGLE) {
+          dst[0] = cs * raw[k][0];
+        } else {
+          dst[0] = fma(a.lam, raw[k][5], fma(a.rho, raw[k][3], raw[k][0]));   // A0 + rho Jrho + lam Jlam
+          dst[lp] = raw[k][1] + raw[k][4];                                   // A1 + Jmu
+          dst[2 * lp] = a.rho * raw[k][2];                                    // rho A2
+        }
+        if (q == 0 && !(HOT && nu > 0)) s_col[s_cbase[b] + j] = __ldcs(a.col_idx + e0 + e);
+      }
+    }
+    if (HOT && nu > 0) asm volatile("cp.async.wait_all;\n" ::);
+    __syncthreads();
+    // ---- compute: one warp per (node block, 32-column slice)
+    for (int task = warp; task < nb * CT; task += kWarps) {
+      const int b = task / CT, ct = task - (task / CT) * CT;
+      const int c = ct * 32 + lane;
+      const int g = s_g[b];
+      if constexpr (HOT) {
+        for (int qo = 0; qo < g; qo += 5) {
+          if (nu > 0)
+            block_task_mma_smem<MODE>(a, r, ct * 32, s_row0[b] + qo, min(5, g - qo), qo, s_L[b], s_js[b],
+                                      s_v + s_vbase[b], s_lx + s_cbase[b], s_u, ust, s_desc[20 + b], lane);
+          else
+            block_task_mma<MODE>(a, r, ct * 32, s_row0[b] + qo, min(5, g - qo), qo, s_L[b], s_js[b],
+                                 s_v + s_vbase[b], s_col + s_cbase[b], lane);
+        }
+        continue;
+      }
+      for (int qo = 0; qo < g; qo += GM) {
+        const int gs = min(GM, g - qo);
+        double acc[GM][NACC];
+        zero_acc<MODE, GM>(acc);
+        block_task<MODE, GM>(a, r, c, s_row0[b] + qo, gs, qo, s_L[b], s_js[b], s_v + s_vbase[b],
+                             s_col + s_cbase[b], acc);
+        block_store<MODE, GM>(a, r, c, s_row0[b] + qo, gs, acc);
       }
     }
   } else {
-    // ---- one group longer than the stage (generic long rows): chunks over its column list,
-    //      warp 0 accumulates, the whole CTA stages
-    const int L = a.row_ptr[rbeg + 1] - e0;
-    for (int sb = rbeg; sb < rend; sb += GM) {
-      const int g = min(GM, rend - sb);
-      const int jc = kSpmmCap / g;
-      double acc[GM][NACC][NC];
-#pragma unroll
-      for (int q = 0; q < GM; ++q)
-#pragma unroll
-        for (int tt = 0; tt < NACC; ++tt)
-#pragma unroll
-          for (int i = 0; i < NC; ++i) acc[q][tt][i] = 0.0;
-      const int base = e0 + (sb - rbeg) * L;
+    // ---- one block longer than the stage (generic long rows): chunks of its column list; the
+    //      whole CTA stages, warp ct < CT accumulates column slice ct
+    const int g = rend - rbeg;
+    const int L = s_desc[16];
+    const int jc = min(kSpmmCap, kValCap / (g * NV) - 16);   // row_pitch(jc) * g * NV <= kValCap
+    for (int qo = 0; qo < g; qo += GM) {
+      const int gs = min(GM, g - qo);
+      double acc[GM][NACC];
+      zero_acc<MODE, GM>(acc);
       for (int j0 = 0; j0 < L; j0 += jc) {
         const int jn = min(jc, L - j0);
+        const int lp = row_pitch(jn);
         __syncthreads();
-        for (int e = tid; e < jn; e += kThreads) s_col[e] = __ldcs(a.col_idx + base + j0 + e);
         for (int e = tid; e < g * jn; e += kThreads) {
           const int q = e / jn, j = e - (e / jn) * jn;
-          stage_entry<MODE>(a, base + q * L + j0 + j, q * jn + j, s_v, cs);
+          stage_entry<MODE>(a, e0 + q * L + j0 + j, s_v + q * NV * lp + j, lp, cs);
+          if (q == 0) s_col[j] = __ldcs(a.col_idx + e0 + j0 + j);
         }
         __syncthreads();
-        if (warp == 0)
-          block_accumulate<MODE, NC, GM>(a, r, lane, g, jn, 0, jn, s_v, s_col, dmu_c, dnu_c, acc);
+        if (warp < CT) block_task<MODE, GM>(a, r, warp * 32 + lane, rbeg + qo, gs, qo, jn, lp, s_v, s_col, acc);
       }
-      if (warp == 0) block_store<MODE, NC, GM>(a, r, lane, sb, g, acc);
+      if (warp < CT) block_store<MODE, GM>(a, r, warp * 32 + lane, rbeg + qo, gs, acc);
     }
   }
 }
 
-template <int MODE>
-constexpr size_t smem_bytes() {
-  return (size_t)kSpmmCap * (Nstage<MODE>::v * sizeof(double) + sizeof(int));
+
+int ust_for(int rmax) { return ((rmax + 11) / 16) * 16 + 4; }   // >= rmax + 1, == 4 mod 16 (even)
+
+size_t smem_for(int mode, int rmax) {
+  const bool hot = (mode == SPMM_S2STEP || mode == SPMM_PLAIN3);
+  return sizeof(double) * (kValCap + (hot ? (size_t)kUCap * ust_for(rmax) : 0)) + sizeof(int) * kSpmmCap;
 }
 
-template <int MODE, int NC, int GM>
-cudaError_t launch_t(const SpmmArgs& a, cudaStream_t s) {
+int sm_count() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+template <int MODE>
+cudaError_t launch_m(const SpmmArgs& a0, int rmax, cudaStream_t s) {
+  SpmmArgs a = a0;
+  // 16-byte U row copies need 16-byte aligned rows and room for the padding element of an odd r
+  a.u_aligned16 = ((reinterpret_cast<uintptr_t>(a.U) & 15) == 0) && (a.ldu % 2 == 0) && (rmax < a.ldu || rmax % 2 == 0);
+  constexpr bool HOT = (MODE == SPMM_S2STEP || MODE == SPMM_PLAIN3);
+  (void)HOT;
   if (a.ntiles == 0) return cudaSuccess;
-  spmm_kernel<MODE, NC, GM><<<a.ntiles, kThreads, smem_bytes<MODE>(), s>>>(a);
+  a.tlist = nullptr;
+  spmm_kernel<MODE, 5><<<a.ntiles, kThreads, smem_for(MODE, rmax), s>>>(a, ust_for(rmax));
   return cudaGetLastError();
 }
 
 template <int MODE>
-cudaError_t launch_m(const SpmmArgs& a, int rmax, cudaStream_t s) {
-  if (rmax <= 32) return launch_t<MODE, 1, 8>(a, s);
-  if (rmax <= 64) return launch_t<MODE, 2, 5>(a, s);
-  if (rmax <= 128) return launch_t<MODE, 4, 3>(a, s);
-  return cudaErrorInvalidValue;
-}
-
-template <int MODE, int NC, int GM>
-cudaError_t prep_t() {
-  return cudaFuncSetAttribute(spmm_kernel<MODE, NC, GM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)smem_bytes<MODE>());
-}
-
-template <int MODE>
 cudaError_t prep_m() {
-  cudaError_t e;
-  if ((e = prep_t<MODE, 1, 8>()) != cudaSuccess) return e;
-  if ((e = prep_t<MODE, 2, 5>()) != cudaSuccess) return e;
-  return prep_t<MODE, 4, 3>();
+  cudaError_t e = cudaFuncSetAttribute(spmm_kernel<MODE, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem_for(MODE, kMaxRank));
+  if (e != cudaSuccess) return e;
+  return e;
 }
 
 }  // namespace
@@ -245,19 +483,16 @@ cudaError_t spmm_prepare() {
   if ((e = prep_m<SPMM_S2STEP>()) != cudaSuccess) return e;
   if ((e = prep_m<SPMM_PLAIN3>()) != cudaSuccess) return e;
   if ((e = prep_m<SPMM_SINGLE>()) != cudaSuccess) return e;
-  if ((e = prep_m<SPMM_DENSE>()) != cudaSuccess) return e;
-  return prep_t<SPMM_DENSE, 8, 4>();
+  return prep_m<SPMM_DENSE>();
 }
 
 cudaError_t launch_spmm(int mode, const SpmmArgs& a, int rmax, cudaStream_t s) {
+  if (rmax > (mode == SPMM_DENSE ? 256 : kMaxRank)) return cudaErrorInvalidValue;
   switch (mode) {
     case SPMM_S2STEP: return launch_m<SPMM_S2STEP>(a, rmax, s);
     case SPMM_PLAIN3: return launch_m<SPMM_PLAIN3>(a, rmax, s);
     case SPMM_SINGLE: return launch_m<SPMM_SINGLE>(a, rmax, s);
-    case SPMM_DENSE:
-      if (rmax <= 128) return launch_m<SPMM_DENSE>(a, rmax, s);
-      if (rmax <= 256) return launch_t<SPMM_DENSE, 8, 4>(a, s);
-      return cudaErrorInvalidValue;
+    case SPMM_DENSE: return launch_m<SPMM_DENSE>(a, rmax, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -11,7 +11,7 @@
 //   STORE : written out (U_{k+1} = Ucat Z, row-major).
 // Gram pass 1 uses T = R_V^T, pass 2 T = R_V^T R1^{-1}, the basis GEMM T = Z.
 //
-// Tile: 128 rows x p, 8 warps, warp w owns rows [16w, 16w+16) (two 8-row DMMA tiles) and all p
+// Tile: 128 rows x p, 16 warps, warp w owns rows [8w, 8w+8) (one 8-row DMMA tile) and all p
 // columns.  The K loop streams 32-column chunks of Ucat and 32-row chunks of T into a cp.async
 // double buffer (8-byte copies: the two Ucat blocks meet at an odd column; zero fill past M / w).
 // The X tile is parked in the (then idle) stage buffers for the Gram / store epilogue.
@@ -21,7 +21,8 @@ namespace lrc {
 
 namespace {
 
-constexpr int kThreads = 256;   // 8 warps
+constexpr int kThreads = 512;   // 16 warps
+constexpr int kWarps = kThreads / 32;
 constexpr int kBM = 128;        // rows per tile
 constexpr int kBK = 32;         // k chunk
 constexpr int kSU = kBK + 4;    // smem row stride of the U chunk (== 4 mod 16 doubles: conflict free)
@@ -55,7 +56,7 @@ struct TsShape {
   static constexpr int SMEM = (2 * STAGE > kBM * SX ? 2 * STAGE : kBM * SX);
   static constexpr int PT2 = (PT + 1) / 2;               // 2x2 super tiles of the Gram
   static constexpr int NS = PT2 * (PT2 + 1) / 2;
-  static constexpr int SPW = (NS + 7) / 8;               // super tiles per warp
+  static constexpr int SPW = (NS + kWarps - 1) / kWarps;  // super tiles per warp
 };
 
 template <int PT>
@@ -113,7 +114,7 @@ ts_kernel(TsArgs a) {
   for (int s = 0; s < S::SPW; ++s) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) gacc[s][q][0] = gacc[s][q][1] = 0.0;
-    int t = warp + 8 * s, I = 0;
+    int t = warp + kWarps * s, I = 0;
     if (t >= S::NS) { sI[s] = -1; sJ[s] = -1; continue; }
     while (t >= S::PT2 - I) { t -= S::PT2 - I; ++I; }
     sI[s] = I; sJ[s] = I + t;
@@ -123,9 +124,9 @@ ts_kernel(TsArgs a) {
   const int ntiles = (a.M + kBM - 1) / kBM;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int m0 = tile * kBM;
-    double x0[PT][2], x1[PT][2];
+    double x0[PT][2];
 #pragma unroll
-    for (int n = 0; n < PT; ++n) x0[n][0] = x0[n][1] = x1[n][0] = x1[n][1] = 0.0;
+    for (int n = 0; n < PT; ++n) x0[n][0] = x0[n][1] = 0.0;
 
     issue_chunk<PT>(a, sm, m0, 0, w, wa, tid);
     cp_commit();
@@ -142,13 +143,11 @@ ts_kernel(TsArgs a) {
       const double* s_t = s_u + kBM * kSU;
 #pragma unroll
       for (int kk = 0; kk < kBK; kk += 4) {
-        const double a0 = s_u[(warp * 16 + gid) * kSU + kk + tig];
-        const double a1 = s_u[(warp * 16 + 8 + gid) * kSU + kk + tig];
+        const double a0 = s_u[(warp * 8 + gid) * kSU + kk + tig];
 #pragma unroll
         for (int n = 0; n < PT; ++n) {
           const double bv = s_t[(kk + tig) * SX + n * 8 + gid];
           dmma884(x0[n], a0, bv);
-          dmma884(x1[n], a1, bv);
         }
       }
       __syncthreads();
@@ -157,8 +156,7 @@ ts_kernel(TsArgs a) {
 #pragma unroll
     for (int n = 0; n < PT; ++n) {
       const int c = n * 8 + 2 * tig;
-      *reinterpret_cast<double2*>(s_x + (warp * 16 + gid) * SX + c) = make_double2(x0[n][0], x0[n][1]);
-      *reinterpret_cast<double2*>(s_x + (warp * 16 + 8 + gid) * SX + c) = make_double2(x1[n][0], x1[n][1]);
+      *reinterpret_cast<double2*>(s_x + (warp * 8 + gid) * SX + c) = make_double2(x0[n][0], x0[n][1]);
     }
     __syncthreads();
     if constexpr (MODE == 0) {

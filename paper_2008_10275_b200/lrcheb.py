@@ -55,7 +55,8 @@ class SolveInfo(ctypes.Structure):
                 ("chol2_cycles", ctypes.c_double * 3)]
 
 
-def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+def load_library(path: str = None) -> ctypes.CDLL:
+    path = path or os.environ.get("LRCHEB_LIB") or LIB_PATH   # LRCHEB_LIB: an alternative in-tree build
     if not os.path.exists(path):
         raise ImportError(f"liblrcheb.so not built at {path}: run `python -c 'import __graft_entry__ as g; g.build()'`")
     lib = ctypes.CDLL(path)
