@@ -42,6 +42,22 @@ def parse():
     return ap.parse_args()
 
 
+def shard_subsets(K: int, rank: int, world: int):
+    """Subsets of this rank: round-robin over ranks (subsets are independent given the
+    operator), at least one per rank so every rank does a step of work."""
+    return [k for k in range(K) if k % world == rank] or [rank % K]
+
+
+def max_over_ranks(ms: float, dist, device=None) -> float:
+    """Max-over-ranks of a device time (the contract's timing rule); identity at world size 1."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return ms
+    import torch
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -170,7 +186,7 @@ def main():
     ctx = lrcheb.Context(local)
     ctx.set_operator(torch.from_numpy(op.row_ptr).to(dev), torch.from_numpy(op.col_idx).to(dev),
                      [torch.from_numpy(v).to(dev) for v in op.vals], op.rho_f, op.lambda_s, borrow=True)
-    my_subsets = [k for k in range(cfg.K) if k % world == rank] or [rank % cfg.K]
+    my_subsets = shard_subsets(cfg.K, rank, world)
     inputs = []
     for k in my_subsets:
         d_mu, d_nu, BU, BV = prob.subset(k)
@@ -205,12 +221,9 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         launches = ctx.kernel_launches() - launches0
+        ms = max_over_ranks(ms, dist if world > 1 else None, dev)
         if world > 1:
-            t = torch.tensor([ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-            if world > 1:
-                dist.barrier()
+            dist.barrier()
         return ms, infos, launches
 
     clk = ClockSampler(local)

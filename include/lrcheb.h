@@ -59,6 +59,8 @@ typedef enum { LRC_MEM_HOST = 0, LRC_MEM_DEVICE = 1, LRC_MEM_DEVICE_BORROW = 2 }
 #define LRC_RECORD_ITERATES      1u  /* keep every X_k = U_k V_k^T on the device for lrc_get_iterate */
 #define LRC_SKIP_FINAL_RESIDUAL  2u  /* do not compute info->rel_residual (set to NaN) */
 #define LRC_NO_GRAPH             4u  /* launch the iteration kernels directly instead of a CUDA graph */
+#define LRC_NO_WARM_START        8u  /* start every core Jacobi SVD from W = I (default: warm start from the
+                                        previous iteration's right singular basis when p == n) */
 
 /* lrc_apply_lowrank modes */
 #define LRC_APPLY_PLAIN3  0u  /* W = [W0 | W1 | W2], W0 = (A0+rho Jrho+lam Jlam)U, W1 = (A1+Jmu)U, W2 = rho A2 U */
@@ -92,7 +94,7 @@ typedef struct {
   int64_t rank_cap;               /* R, 1 <= R <= min(M, n, 128) */
   int64_t n_iter;                 /* N >= 1 updates X_1..X_N from X_0 = 0 (readings S6, S7) */
   int64_t restart_every;          /* 0: no restart; else the omega sequence restarts every k iterations (S8) */
-  uint32_t flags;                 /* LRC_RECORD_ITERATES | LRC_SKIP_FINAL_RESIDUAL | LRC_NO_GRAPH */
+  uint32_t flags;                 /* LRC_RECORD_ITERATES | LRC_SKIP_FINAL_RESIDUAL | LRC_NO_GRAPH | LRC_NO_WARM_START */
 } lrc_solve_opts;
 
 typedef struct {

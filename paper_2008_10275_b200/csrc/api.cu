@@ -50,6 +50,7 @@ struct Workspace {
   double* T1 = nullptr; double* QV = nullptr; double* G = nullptr; double* R1 = nullptr;
   double* T2 = nullptr; double* Z = nullptr;
   double* R1i = nullptr; double* Wz = nullptr; double* Wv = nullptr;
+  double* W0 = nullptr; double* Wfull = nullptr; double* Bprev = nullptr;
   double* partials = nullptr;
   double* Uh = nullptr; double* Vh = nullptr;   // iterate history
   double* tmpA = nullptr; size_t tmpA_sz = 0;   // hook scratch
@@ -100,6 +101,7 @@ struct lrc_ctx {
   // last solve
   int64_t last_N = 0; bool last_record = false; int last_cap = 0;
   float last_kernel_ms = 0.f;
+  bool warm_start = true;   // LRC_NO_WARM_START clears it per solve
   // kernel launch accounting + optional per-kernel CUDA-event profiling (direct launches only)
   int64_t launches = 0;
   bool capturing = false;
@@ -174,7 +176,7 @@ void free_ws(Workspace& w) {
   for (int i = 0; i < 3; ++i) { dfree(w.Ubuf[i]); dfree(w.Vbuf[i]); }
   dfree(w.BV); dfree(w.omega); dfree(w.ints); dfree(w.sigma); dfree(w.scal);
   dfree(w.T1); dfree(w.QV); dfree(w.G); dfree(w.R1); dfree(w.T2); dfree(w.Z);
-  dfree(w.R1i); dfree(w.Wz); dfree(w.Wv);
+  dfree(w.R1i); dfree(w.Wz); dfree(w.Wv); dfree(w.W0); dfree(w.Wfull); dfree(w.Bprev);
   dfree(w.partials); dfree(w.Uh); dfree(w.Vh); dfree(w.tmpA); dfree(w.tmpB); dfree(w.tmpC);
   w = Workspace();
 }
@@ -228,6 +230,9 @@ lrc_status ensure_ws(lrc_ctx* ctx, int rb, int cap, int N, int wmax, bool record
   CK(dalloc(&w.R1i, (size_t)pmax * pmax));
   CK(dalloc(&w.Wz, (size_t)pmax * capp));
   CK(dalloc(&w.Wv, (size_t)pmax * capp));
+  CK(dalloc(&w.W0, (size_t)pmax * pmax));
+  CK(dalloc(&w.Wfull, (size_t)pmax * pmax));
+  CK(dalloc(&w.Bprev, n * pmax));
   CK(dalloc(&w.partials, (size_t)w.grid * pmax * pmax));
   if (record) {
     CK(dalloc(&w.Uh, (size_t)N * M * w.LDU));
@@ -259,6 +264,7 @@ State make_state(Workspace& w) {
   s.flags = w.ints + w.N + 6;
   s.esc = w.ints + w.N + 7;
   s.sweeps = w.ints + w.N + 8;
+  s.prevp = w.ints + w.N + 9;
   s.sigma = w.sigma;
   s.scal = w.scal;
   return s;
@@ -268,6 +274,7 @@ SmallBufs make_bufs(Workspace& w) {
   SmallBufs b{};
   b.T1 = w.T1; b.QV = w.QV; b.G = w.G; b.R1 = w.R1; b.T2 = w.T2; b.Z = w.Z;
   b.R1i = w.R1i; b.Wz = w.Wz; b.Wv = w.Wv;
+  b.W0 = nullptr; b.Wfull = w.Wfull; b.Bprev = w.Bprev;
   b.ldT = w.pmax; b.ldZ = w.capp;
   return b;
 }
@@ -295,17 +302,26 @@ SpmmArgs spmm_base(lrc_ctx* ctx) {
 lrc_status enqueue_truncation(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, const double* omega,
                               int k, double tol, int cap, int rank_slot, int sigma_row,
                               double* Uout, int ldu_out, double* Vout, int ldv_out,
-                              cudaStream_t s, bool fork_from_spmm) {
+                              cudaStream_t s, bool fork_from_spmm, bool warm = false) {
   Workspace& w = ctx->ws;
   State st = make_state(w);
   SmallBufs b = make_bufs(w);
+  // warm start of the core Jacobi SVD (p == n only, n <= 256 for the tiny GEMM staging)
+  const bool use_warm = warm && ctx->n <= kMaxW;
+  if (use_warm) b.W0 = w.W0;
   if (fork_from_spmm && !ctx->profiling) {   // profiling: serial, so per-kernel times are isolated
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
     KL(P_VSIDE, ctx->side, launch_vside(vd, (int)ctx->n, ctx->dmu, ctx->dnu, omega, k, st, b, w.wmax, ctx->side));
+    if (use_warm)   // W0 = Q_V^T B_prev (p x p, p = n), overlapping the SpMM
+      KL(P_TINY, ctx->side, launch_tiny_gemm(w.QV, w.pmax, w.Bprev, w.pmax, w.W0, w.pmax, w.pmax, st.p, 0,
+                                             w.pmax, nullptr, (int)ctx->n, ctx->side, 1));
     CK(cudaEventRecord(ctx->ev_join, ctx->side));
     CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
   } else {
     KL(P_VSIDE, s, launch_vside(vd, (int)ctx->n, ctx->dmu, ctx->dnu, omega, k, st, b, w.wmax, s));
+    if (use_warm)
+      KL(P_TINY, s, launch_tiny_gemm(w.QV, w.pmax, w.Bprev, w.pmax, w.W0, w.pmax, w.pmax, st.p, 0,
+                                     w.pmax, nullptr, (int)ctx->n, s, 1));
   }
   TsArgs ta{};
   ta.M = (int)ctx->M;
@@ -329,6 +345,9 @@ lrc_status enqueue_truncation(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, co
                                  st.p, 0, s));
   KL(P_TINY, s, launch_tiny_gemm(w.QV, w.pmax, w.Wv, w.capp, Vout, ldv_out, cap, nullptr,
                                  (int)ctx->n, (int)ctx->n, st.p, 0, s));
+  if (use_warm)   // B = Q_V W (n x p): the right singular basis of X for the next warm start
+    KL(P_TINY, s, launch_tiny_gemm(w.QV, w.pmax, w.Wfull, w.pmax, w.Bprev, w.pmax, w.pmax, nullptr,
+                                   (int)ctx->n, (int)ctx->n, st.p, 0, s));
   TsArgs tb{};
   tb.M = (int)ctx->M;
   tb.u = ud;
@@ -404,7 +423,7 @@ lrc_status enqueue_iteration(lrc_ctx* ctx, int k, int rb, int cap, double gamma,
   ud.A = w.Wcat; ud.lda = w.LDW; ud.wa_fixed = rb; ud.wa_mul = 3; ud.wa_idx = k + 1;
   ud.B = Uprev; ud.ldb = w.LDU; ud.wb_fixed = 0; ud.wb_idx = k;
   lrc_status r = enqueue_truncation(ctx, ud, vd, w.omega, k, tol, cap, k + 2, k, Unext, w.LDU,
-                                    Vnext, cap, s, true);
+                                    Vnext, cap, s, true, ctx->warm_start);
   if (r != LRC_OK) return r;
   if (record) {
     CK(cudaMemcpyAsync(w.Uh + (size_t)k * ctx->M * w.LDU, Unext,
@@ -764,6 +783,7 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
     return fail(ctx, LRC_ERR_ARG, "n x (r_B + 4 rank_cap) too large for the single-CTA V-side QR");
   const bool record = (opts->flags & LRC_RECORD_ITERATES) != 0;
   const bool use_graph = (opts->flags & LRC_NO_GRAPH) == 0 && !ctx->profiling;
+  ctx->warm_start = (opts->flags & LRC_NO_WARM_START) == 0;
   CK(cudaSetDevice(ctx->device));
   lrc_status st = ensure_ws(ctx, std::max(rb, 1), cap, N, wmax, record);
   if (st != LRC_OK) return st;
@@ -799,7 +819,7 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
     if (st != LRC_OK) return st;
 
     CK(cudaEventRecord(ctx->ev[1], s));
-    const uint32_t gflags = opts->flags & (LRC_RECORD_ITERATES);
+    const uint32_t gflags = opts->flags & (LRC_RECORD_ITERATES | LRC_NO_WARM_START);
     GraphKey key;
     key.gen = ctx->gen; key.N = N; key.rb = rb; key.cap = cap; key.gamma = gamma; key.tol = opts->tol;
     key.flags = gflags;

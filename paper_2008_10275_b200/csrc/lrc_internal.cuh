@@ -107,6 +107,7 @@ struct State {          // device-resident per-solve state
   int* flags;           // error bits (1: Cholesky failed after escalations, 2: NaN)
   int* esc;             // shift escalations
   int* sweeps;          // Jacobi sweeps (summed over calls)
+  int* prevp;           // p of the previous core SVD (warm-start validity)
   double* sigma;        // [N][kSigmaStride]
   double* scal;         // scalar slots: [0] ||B||^2, [1] ||R||^2 residual
 };
@@ -121,6 +122,9 @@ struct SmallBufs {
   double* R1i;    // pmax x pmax (R1^{-1}, upper)
   double* Wz;     // pmax x ldZ  (W_r Sigma_r^{-1})
   double* Wv;     // pmax x ldZ  (W_r Sigma_r)
+  double* W0;     // pmax x pmax (warm-start basis Q_V^T B_prev), null: warm start off
+  double* Wfull;  // pmax x pmax (full right basis W of the core)
+  double* Bprev;  // n x pmax    (Q_V W of the previous iteration)
   double* Z;      // w x capp   (R_V^T W_r Sigma_r^{-1})
   int ldT;        // = pmax
   int ldZ;        // = capp
@@ -139,7 +143,7 @@ cudaError_t launch_chol2_svd(State st, SmallBufs b, int pmax, int wmax, int n, d
 // C (m x ncols) = A (m x k) B (k x ncols), m/k device-resident (d_m/d_k) or fixed; m_max bounds the grid
 cudaError_t launch_tiny_gemm(const double* A, int lda, const double* B, int ldb, double* C, int ldc,
                              int ncols, const int* d_m, int m_fixed, int m_max, const int* d_k,
-                             int k_fixed, cudaStream_t s);
+                             int k_fixed, cudaStream_t s, int transA = 0);
 // scal[slot] = trace(G) over p (for ||X||_F^2)
 cudaError_t launch_trace(State st, const double* G, int pmax, int slot, cudaStream_t s);
 

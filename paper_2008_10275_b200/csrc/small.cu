@@ -351,19 +351,64 @@ __global__ void __launch_bounds__(kT) chol2_svd_kernel(State st, SmallBufs b, in
     }
   }
   __syncthreads();
-  for (int e = tid; e < p * p; e += kT) {          // column-major A = R
-    const int i = e / p, j = e - (e / p) * p;
-    s_a[j * LD + i] = s_w[i * LD + j];
-  }
-  __syncthreads();
-  for (int e = tid; e < p * p; e += kT) {
-    const int j = e / p, i = e - (e / p) * p;
-    s_w[j * LD + i] = (i == j) ? 1.0 : 0.0;
+  // Jacobi start.  Cold: A = R, W = I.  Warm (p == n in this and the previous iteration): the previous
+  // right singular basis B = Q_V,prev W_prev of X in R^n maps into the new coordinates exactly
+  // orthogonally, W0 = Q_V^T B (tiny_gemm on the V-side stream), and A0 = R W0 is nearly column-
+  // orthogonal once the iteration settles, so far fewer sweeps are needed (R9).
+  const bool warm = (b.W0 != nullptr) && (*st.prevp == n) && (p == n);
+  double* A = s_a;
+  double* Wm = s_w;
+  if (warm) {
+    for (int e = tid; e < p * p; e += kT) {
+      const int i = e / p, c = e - (e / p) * p;
+      s_a[i * LD + c] = b.W0[i * pmax + c];
+    }
+    __syncthreads();
+    for (int i = warp; i < p; i += kT / 32) {     // A0 = R W0, row i in place (R upper triangular)
+      double acc[kMaxP / 32];
+#pragma unroll
+      for (int t = 0; t < kMaxP / 32; ++t) acc[t] = 0.0;
+      for (int k = i; k < p; ++k) {
+        const double rk = s_w[i * LD + k];
+#pragma unroll
+        for (int t = 0; t < kMaxP / 32; ++t) {
+          const int j = lane + 32 * t;
+          if (j < p) acc[t] = fma(rk, s_a[k * LD + j], acc[t]);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < kMaxP / 32; ++t) {
+        const int j = lane + 32 * t;
+        if (j < p) s_w[i * LD + j] = acc[t];
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < p * p; e += kT) {        // in-place transposes -> column-major
+      const int i = e / p, j = e - (e / p) * p;
+      if (i < j) {
+        double t0 = s_w[i * LD + j]; s_w[i * LD + j] = s_w[j * LD + i]; s_w[j * LD + i] = t0;
+        double t1 = s_a[i * LD + j]; s_a[i * LD + j] = s_a[j * LD + i]; s_a[j * LD + i] = t1;
+      }
+    }
+    A = s_w;
+    Wm = s_a;
+    __syncthreads();
+  } else {
+    for (int e = tid; e < p * p; e += kT) {          // column-major A = R
+      const int i = e / p, j = e - (e / p) * p;
+      s_a[j * LD + i] = s_w[i * LD + j];
+    }
+    __syncthreads();
+    for (int e = tid; e < p * p; e += kT) {
+      const int j = e / p, i = e - (e / p) * p;
+      s_w[j * LD + i] = (i == j) ? 1.0 : 0.0;
+    }
   }
   if (warp == 0) {
     double ss = 0.0;
     for (int e = lane; e < p * p; e += 32) {
-      const double x = s_a[(e / p) * LD + (e % p)];
+      const double x = A[(e / p) * LD + (e % p)];
       ss += x * x;
     }
     ss = warp_sum(ss);
@@ -395,8 +440,8 @@ __global__ void __launch_bounds__(kT) chol2_svd_kernel(State st, SmallBufs b, in
           act = (i < p) && (j < p);
           if (i > j) { const int t = i; i = j; j = t; }
         }
-        double* ai = s_a + i * LD;
-        double* aj = s_a + j * LD;
+        double* ai = A + i * LD;
+        double* aj = A + j * LD;
         double al = 0.0, be = 0.0, ga = 0.0;
         if (act)
           for (int e = hl; e < p; e += 16) {
@@ -419,8 +464,8 @@ __global__ void __launch_bounds__(kT) chol2_svd_kernel(State st, SmallBufs b, in
             ai[e] = c * x - sn * y;
             aj[e] = sn * x + c * y;
           }
-          double* wi = s_w + i * LD;
-          double* wj = s_w + j * LD;
+          double* wi = Wm + i * LD;
+          double* wj = Wm + j * LD;
           for (int e = hl; e < p; e += 16) {
             const double x = wi[e], y = wj[e];
             wi[e] = c * x - sn * y;
@@ -441,7 +486,7 @@ __global__ void __launch_bounds__(kT) chol2_svd_kernel(State st, SmallBufs b, in
   // CholeskyQR2; same singular vectors), so sigma_X^2 = (sigma_R^2 - s1 s2) / (1 + s2).
   const double s1s2 = st.scal[2] * s2_used;
   for (int j = warp; j < p; j += kT / 32) {
-    const double* aj = s_a + j * LD;
+    const double* aj = A + j * LD;
     double ss = 0.0;
     for (int e = lane; e < p; e += 32) ss += aj[e] * aj[e];
     ss = warp_sum(ss);
@@ -481,13 +526,20 @@ __global__ void __launch_bounds__(kT) chol2_svd_kernel(State st, SmallBufs b, in
     double wz = 0.0, wv = 0.0;
     if (q < rr && k < p) {
       const int jq = s_perm[q];
-      const double wk = s_w[jq * LD + k];
+      const double wk = Wm[jq * LD + k];
       wz = wk / s_sig[jq];
       wv = wk * s_sig[jq];
     }
     b.Wz[e] = wz;
     b.Wv[e] = wv;
   }
+  if (b.Wfull) {                                   // full right basis W (for the next warm start)
+    for (int e = tid; e < pmax * pmax; e += kT) {
+      const int i = e / pmax, j = e - (e / pmax) * pmax;
+      b.Wfull[e] = (i < p && j < p) ? Wm[j * LD + i] : 0.0;
+    }
+  }
+  if (tid == 0) *st.prevp = p;
   __syncthreads();
   if (tid == 0 && st.scal) {   // phase cycle counters (DESIGN.md profiling notes)
     long long tclk3 = clock64();
@@ -503,7 +555,7 @@ __global__ void __launch_bounds__(256) tiny_gemm_kernel(const double* __restrict
                                                          const double* __restrict__ B, int ldb,
                                                          double* __restrict__ C, int ldc, int ncols,
                                                          const int* d_m, int m_fixed, const int* d_k,
-                                                         int k_fixed) {
+                                                         int k_fixed, int transA) {
   const int m = d_m ? *d_m : m_fixed;
   const int k = d_k ? *d_k : k_fixed;
   const int r0 = blockIdx.x * 8;
@@ -512,7 +564,7 @@ __global__ void __launch_bounds__(256) tiny_gemm_kernel(const double* __restrict
   const int rows = min(8, m - r0);
   for (int e = threadIdx.x; e < 8 * k; e += 256) {
     const int i = e / k, kk = e - (e / k) * k;
-    s_a[i][kk] = (i < rows) ? A[(size_t)(r0 + i) * lda + kk] : 0.0;
+    s_a[i][kk] = (i < rows) ? (transA ? A[(size_t)kk * lda + r0 + i] : A[(size_t)(r0 + i) * lda + kk]) : 0.0;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < rows * ncols; e += 256) {
@@ -566,10 +618,10 @@ cudaError_t small_prepare() {
 
 cudaError_t launch_tiny_gemm(const double* A, int lda, const double* B, int ldb, double* C, int ldc,
                              int ncols, const int* d_m, int m_fixed, int m_max, const int* d_k,
-                             int k_fixed, cudaStream_t s) {
+                             int k_fixed, cudaStream_t s, int transA) {
   if (m_max <= 0 || ncols <= 0) return cudaSuccess;
   tiny_gemm_kernel<<<(m_max + 7) / 8, 256, 0, s>>>(A, lda, B, ldb, C, ldc, ncols, d_m, m_fixed, d_k,
-                                                    k_fixed);
+                                                    k_fixed, transA);
   return cudaGetLastError();
 }
 

@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(_HERE, "liblrcheb.so")
 
 LRC_OK, LRC_ERR_ARG, LRC_ERR_SHAPE, LRC_ERR_STATE, LRC_ERR_NOMEM, LRC_ERR_CUDA, LRC_ERR_NUMERIC = range(7)
 LRC_MEM_HOST, LRC_MEM_DEVICE, LRC_MEM_DEVICE_BORROW = 0, 1, 2
-LRC_RECORD_ITERATES, LRC_SKIP_FINAL_RESIDUAL, LRC_NO_GRAPH = 1, 2, 4
+LRC_RECORD_ITERATES, LRC_SKIP_FINAL_RESIDUAL, LRC_NO_GRAPH, LRC_NO_WARM_START = 1, 2, 4, 8
 LRC_APPLY_PLAIN3, LRC_APPLY_SIX, LRC_APPLY_S2STEP = 0, 1, 2
 SIGMA_STRIDE = 128
 
@@ -197,7 +197,7 @@ class Context:
     # ------------------------------------------------------------------------------------
     def solve(self, B_U, B_V, lambda_min: float, lambda_max: float, tol: float, rank_cap: int,
               n_iter: int, restart_every: int = 0, record_iterates: bool = False,
-              skip_residual: bool = False, no_graph: bool = False, out=None):
+              skip_residual: bool = False, no_graph: bool = False, warm_start: bool = True, out=None):
         """Returns (U, V, info).  Outputs live where the inputs live (torch CUDA tensors for device
         inputs, numpy for host inputs) unless ``out=(U_out, V_out)`` is given."""
         pu, ldbu, w1, ku = _mat(B_U)
@@ -219,7 +219,7 @@ class Context:
         pVo, ldvo, w4, _ = _mat(Vo)
         assert w3 == w1 and w4 == w1
         flags = ((LRC_RECORD_ITERATES if record_iterates else 0) | (LRC_SKIP_FINAL_RESIDUAL if skip_residual else 0)
-                 | (LRC_NO_GRAPH if no_graph else 0))
+                 | (LRC_NO_GRAPH if no_graph else 0) | (0 if warm_start else LRC_NO_WARM_START))
         opts = SolveOpts(float(lambda_min), float(lambda_max), float(tol), int(rank_cap), int(n_iter),
                          int(restart_every), flags)
         rh = (ctypes.c_int64 * n_iter)()
