@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--config", default="large")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--streams", type=int, default=2, help="concurrent subset solves per GPU")
+    ap.add_argument("--reserve-sms", type=int, default=2, help="SMs the persistent kernels leave free")
     return ap.parse_args()
 
 
@@ -183,9 +185,21 @@ def main():
     prob = gen.make_problem(args.config)
     cfg, op = prob.cfg, prob.op
     N = cfg.n_iter
-    ctx = lrcheb.Context(local)
-    ctx.set_operator(torch.from_numpy(op.row_ptr).to(dev), torch.from_numpy(op.col_idx).to(dev),
-                     [torch.from_numpy(v).to(dev) for v in op.vals], op.rho_f, op.lambda_s, borrow=True)
+    # S concurrent subset solves (subsets are independent): one lrc context,
+    # CUDA stream and host thread each, all sharing the borrowed operator.  The persistent M-level
+    # kernels leave `reserve` SMs free so one solve's single-CTA core steps overlap the other's
+    # M-level work.  Steps are dealt round-robin to the streams.
+    S = max(1, args.streams)
+    reserve = args.reserve_sms if S > 1 else 0
+    rp_d, ci_d = torch.from_numpy(op.row_ptr).to(dev), torch.from_numpy(op.col_idx).to(dev)
+    vals_d = [torch.from_numpy(v).to(dev) for v in op.vals]
+    ctxs = []
+    for _ in range(S):
+        c = lrcheb.Context(local)
+        c.set_reserved_sms(reserve)
+        c.set_operator(rp_d, ci_d, vals_d, op.rho_f, op.lambda_s, borrow=True)
+        ctxs.append(c)
+    ctx = ctxs[0]
     my_subsets = shard_subsets(cfg.K, rank, world)
     inputs = []
     for k in my_subsets:
@@ -193,34 +207,55 @@ def main():
         inputs.append((d_mu, d_nu, torch.from_numpy(BU).to(dev), torch.from_numpy(BV).to(dev),
                        torch.from_numpy(BU).pin_memory(), torch.from_numpy(BV).pin_memory()))
     n = len(inputs[0][0])
-    Uo = torch.empty((op.M, cfg.rank_cap), dtype=torch.float64, device=dev)
-    Vo = torch.empty((n, cfg.rank_cap), dtype=torch.float64, device=dev)
-    Uh = torch.empty((op.M, cfg.rank_cap), dtype=torch.float64).pin_memory()
-    Vh = torch.empty((n, cfg.rank_cap), dtype=torch.float64).pin_memory()
+    outs = [(torch.empty((op.M, cfg.rank_cap), dtype=torch.float64, device=dev),
+             torch.empty((n, cfg.rank_cap), dtype=torch.float64, device=dev),
+             torch.empty((op.M, cfg.rank_cap), dtype=torch.float64).pin_memory(),
+             torch.empty((n, cfg.rank_cap), dtype=torch.float64).pin_memory()) for _ in range(S)]
 
-    def step(i, host=False):
+    def step(i, host=False, c=None):
+        si = (i % S) if c is None else c
+        cx = ctxs[si]
+        Uo, Vo, Uh, Vh = outs[si]
         d_mu, d_nu, bu, bv, bu_h, bv_h = inputs[i % len(inputs)]
-        ctx.set_params(d_mu, d_nu)
+        cx.set_params(d_mu, d_nu)
         if host:
-            return ctx.solve(bu_h, bv_h, prob.lam_min, prob.lam_max, cfg.tol, cfg.rank_cap, N, out=(Uh, Vh))[2]
-        return ctx.solve(bu, bv, prob.lam_min, prob.lam_max, cfg.tol, cfg.rank_cap, N, out=(Uo, Vo))[2]
+            return cx.solve(bu_h, bv_h, prob.lam_min, prob.lam_max, cfg.tol, cfg.rank_cap, N, out=(Uh, Vh))[2]
+        return cx.solve(bu, bv, prob.lam_min, prob.lam_max, cfg.tol, cfg.rank_cap, N, out=(Uo, Vo))[2]
 
-    for i in range(args.warmup):
-        step(i)
-    s = ctx.stream
+    def run_steps(nsteps, host):
+        """nsteps solves dealt round-robin to the S streams, one host thread per stream."""
+        infos = [None] * nsteps
+        def worker(si):
+            for i in range(si, nsteps, S):
+                infos[i] = step(i, host, si)
+        ths = [threading.Thread(target=worker, args=(si,)) for si in range(S)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        return infos
+
+    run_steps(max(args.warmup, S), False)           # >= 1 warm-up per stream (graph capture)
+    main_s = torch.cuda.Stream(device=dev)
 
     def timed(host):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        launches0 = ctx.kernel_launches()
-        e0.record(s)
-        infos = [step(i, host) for i in range(args.steps)]
-        e1.record(s)
+        launches0 = sum(c.kernel_launches() for c in ctxs)
+        e0.record(main_s)
+        for c in ctxs:
+            c.stream.wait_event(e0)
+        infos = run_steps(args.steps, host)
+        for c in ctxs:
+            ev = torch.cuda.Event()
+            ev.record(c.stream)
+            main_s.wait_event(ev)
+        e1.record(main_s)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
-        launches = ctx.kernel_launches() - launches0
+        launches = sum(c.kernel_launches() for c in ctxs) - launches0
         ms = max_over_ranks(ms, dist if world > 1 else None, dev)
         if world > 1:
             dist.barrier()
@@ -236,11 +271,11 @@ def main():
     e2e_value = iters / (ms_e2e / 1e3)
     h2d = sum(inputs[i % len(inputs)][4].numel() * 8 + inputs[i % len(inputs)][5].numel() * 8
               for i in range(args.steps)) / args.steps
-    d2h = (Uh.numel() + Vh.numel()) * 8 + 64
+    d2h = (outs[0][2].numel() + outs[0][3].numel()) * 8 + 64
 
     # ---- roofline pass: per-kernel CUDA events on the launching streams (same workload, no graph)
     ctx.set_profiling(True)
-    step(0)
+    step(0, c=0)
     prof = ctx.profile()
     ctx.set_profiling(False)
     step_ms = sum(v[0] for v in prof.values())
@@ -279,6 +314,7 @@ def main():
                                f"N={N} iterations per subset solve",
                    "step": "one full ChebyshevT solve of one parameter subset (N iterations + final residual)",
                    "subsets_per_rank": len(my_subsets), "parallelism": f"subsets round-robin over {world} GPU(s)",
+                   "concurrent_subsets_per_gpu": S, "reserved_sms": reserve,
                    "l2": "inputs larger than L2 (operator 3.06 GB >> 126 MB)"},
         "e2e": {"value": e2e_value, "unit": "iterations/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},

@@ -151,6 +151,11 @@ lrc_status lrc_get_iterate(lrc_ctx *ctx, int64_t k, double *U, double *V, int64_
  * call's kernel, for the bench's SpMM roofline. */
 float lrc_last_kernel_ms(const lrc_ctx *ctx);
 
+/* Concurrent subset solves: the persistent M-level kernels of this ctx use
+ * (SM count - n) CTAs so that n SMs stay free for the single-CTA core steps of other contexts
+ * solving other subsets on other streams (subsets are independent).  Default 0. */
+lrc_status lrc_set_reserved_sms(lrc_ctx *ctx, int n);
+
 /* Number of liblrcheb kernels launched on ctx so far (a graph replay counts its kernel nodes). */
 int64_t lrc_kernel_launches(const lrc_ctx *ctx);
 

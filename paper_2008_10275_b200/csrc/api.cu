@@ -102,6 +102,7 @@ struct lrc_ctx {
   int64_t last_N = 0; bool last_record = false; int last_cap = 0;
   float last_kernel_ms = 0.f;
   bool warm_start = true;   // LRC_NO_WARM_START clears it per solve
+  int reserved_sms = 0;     // SMs the persistent kernels leave free (concurrent subset solves)
   // kernel launch accounting + optional per-kernel CUDA-event profiling (direct launches only)
   int64_t launches = 0;
   bool capturing = false;
@@ -210,7 +211,7 @@ lrc_status ensure_ws(lrc_ctx* ctx, int rb, int cap, int N, int wmax, bool record
   w.capp = capp; w.record = record;
   w.LDW = rb + 3 * cap; w.LDW += (w.LDW & 1);
   w.LDU = cap + (cap & 1);
-  w.grid = ts_grid_for((int)ctx->M);
+  w.grid = ts_grid_for((int)ctx->M, ctx->reserved_sms);
   CK(dalloc(&w.Wcat, M * w.LDW));
   for (int i = 0; i < 3; ++i) {
     CK(dalloc(&w.Ubuf[i], M * w.LDU));
@@ -331,12 +332,14 @@ lrc_status enqueue_truncation(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, co
   ta.ldt = w.pmax;
   ta.d_p = st.p;
   ta.partials = w.partials;
+  ta.t_lower = 1;
   KL((0 == 0 ? P_TS_GRAM : P_TS_STORE), s, launch_ts(0, ta, w.pmax, w.grid, s));
   KL(P_REDUCE, s, launch_gram_reduce(w.partials, w.grid, w.pmax, w.G, s));
   KL(P_CHOL1, s, launch_chol1(st, b, w.pmax, w.wmax, s));
   KL(P_TINY, s, launch_tiny_gemm(w.T1, w.pmax, w.R1i, w.pmax, w.T2, w.pmax, w.pmax, st.w, 0, w.wmax,
                                  st.p, 0, s));
   ta.T = w.T2;
+  ta.t_lower = 0;
   KL((0 == 0 ? P_TS_GRAM : P_TS_STORE), s, launch_ts(0, ta, w.pmax, w.grid, s));
   KL(P_REDUCE, s, launch_gram_reduce(w.partials, w.grid, w.pmax, w.G, s));
   KL(P_CHOL2, s, launch_chol2_svd(st, b, w.pmax, w.wmax, (int)ctx->n, tol, cap, rank_slot, sigma_row, Vout,
@@ -375,6 +378,7 @@ lrc_status enqueue_norm2(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, int slo
   ta.ldt = w.pmax;
   ta.d_p = st.p;
   ta.partials = w.partials;
+  ta.t_lower = 1;
   KL((0 == 0 ? P_TS_GRAM : P_TS_STORE), s, launch_ts(0, ta, w.pmax, w.grid, s));
   KL(P_REDUCE, s, launch_gram_reduce(w.partials, w.grid, w.pmax, w.G, s));
   KL(P_TRACE, s, launch_trace(st, w.G, w.pmax, slot, s));
@@ -523,6 +527,19 @@ const char* lrc_last_error(const lrc_ctx* ctx) { return ctx ? ctx->err.c_str() :
 float lrc_last_kernel_ms(const lrc_ctx* ctx) { return ctx ? ctx->last_kernel_ms : 0.f; }
 
 int64_t lrc_kernel_launches(const lrc_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+lrc_status lrc_set_reserved_sms(lrc_ctx* ctx, int n) {
+  if (!ctx) return LRC_ERR_ARG;
+  if (n < 0 || n > 64) return fail(ctx, LRC_ERR_ARG, "reserved SMs must be in [0, 64]");
+  if (n != ctx->reserved_sms) {
+    cudaStreamSynchronize(ctx->stream);
+    drop_graph(ctx);
+    free_ws(ctx->ws);      // the persistent grid (and its partial buffers) are sized from it
+    ++ctx->gen;
+    ctx->reserved_sms = n;
+  }
+  return LRC_OK;
+}
 
 void lrc_set_profiling(lrc_ctx* ctx, int on) {
   if (!ctx) return;

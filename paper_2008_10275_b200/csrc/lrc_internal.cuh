@@ -79,11 +79,12 @@ struct TsArgs {
   double* partials;         // GRAM: [gridDim.x][pmax*pmax]
   double* out;              // STORE: M x p (ld ldo)
   int ldo;
+  int t_lower;              // T[c][i] == 0 for i > c (T1 = R_V^T): skip the zero blocks
 };
 // mode 0 = GRAM (partial X^T X, X = Ucat T), 1 = STORE (out = Ucat T)
 cudaError_t launch_ts(int mode, const TsArgs& a, int pmax, int grid, cudaStream_t s);
 int ts_pmax_for(int p);          // padded width used by the instantiations
-int ts_grid_for(int M);          // persistent grid size
+int ts_grid_for(int M, int reserved = 0);   // persistent grid size (SM count minus reserved SMs)
 // G = sum_b partials[b] (fixed order), full symmetric pmax x pmax
 cudaError_t launch_gram_reduce(const double* partials, int nblocks, int pmax, double* G,
                                cudaStream_t s);

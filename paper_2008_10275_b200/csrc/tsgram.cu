@@ -141,11 +141,14 @@ ts_kernel(TsArgs a) {
       __syncthreads();
       const double* s_u = sm + (kc & 1) * S::STAGE;
       const double* s_t = s_u + kBM * kSU;
+      const int k0 = kc * kBK;
 #pragma unroll
       for (int kk = 0; kk < kBK; kk += 4) {
         const double a0 = s_u[(warp * 8 + gid) * kSU + kk + tig];
 #pragma unroll
         for (int n = 0; n < PT; ++n) {
+          // T1 = R_V^T is lower trapezoidal: blocks with all i > c are zero (warp-uniform skip)
+          if (a.t_lower && n * 8 > k0 + kk + 3) continue;
           const double bv = s_t[(kk + tig) * SX + n * 8 + gid];
           dmma884(x0[n], a0, bv);
         }
@@ -266,7 +269,7 @@ int ts_pmax_for(int p) {
   return 8 * ((p + 7) / 8);
 }
 
-int ts_grid_for(int M) {
+int ts_grid_for(int M, int reserved) {
   static int sms = 0;
   if (sms == 0) {
     int dev = 0;
@@ -275,7 +278,9 @@ int ts_grid_for(int M) {
     if (sms <= 0) sms = 148;
   }
   const int ntiles = (M + kBM - 1) / kBM;
-  return ntiles < sms ? (ntiles > 0 ? ntiles : 1) : sms;
+  int g = sms - (reserved > 0 ? reserved : 0);
+  if (g < 1) g = 1;
+  return ntiles < g ? (ntiles > 0 ? ntiles : 1) : g;
 }
 
 cudaError_t launch_ts(int mode, const TsArgs& a, int pmax, int grid, cudaStream_t s) {

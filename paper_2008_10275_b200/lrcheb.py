@@ -31,6 +31,7 @@ EXPORTS = (
     "lrc_create", "lrc_destroy", "lrc_last_error", "lrc_version", "lrc_set_operator",
     "lrc_set_params", "lrc_solve", "lrc_apply_lowrank", "lrc_apply_dense", "lrc_truncate",
     "lrc_get_iterate", "lrc_last_kernel_ms", "lrc_kernel_launches", "lrc_set_profiling", "lrc_get_profile",
+    "lrc_set_reserved_sms",
 )
 
 
@@ -77,6 +78,8 @@ def load_library(path: str = None) -> ctypes.CDLL:
     lib.lrc_get_iterate.argtypes = [P, I64, P, P, ctypes.POINTER(I64), I32]
     lib.lrc_last_kernel_ms.argtypes = [P]
     lib.lrc_last_kernel_ms.restype = ctypes.c_float
+    lib.lrc_set_reserved_sms.argtypes = [P, I32]
+    lib.lrc_set_reserved_sms.restype = I32
     lib.lrc_kernel_launches.argtypes = [P]
     lib.lrc_kernel_launches.restype = I64
     lib.lrc_set_profiling.argtypes = [P, I32]
@@ -299,6 +302,9 @@ class Context:
 
     def last_kernel_ms(self) -> float:
         return float(self._lib.lrc_last_kernel_ms(self._h))
+
+    def set_reserved_sms(self, n: int):
+        self._check(self._lib.lrc_set_reserved_sms(self._h, int(n)))
 
     def kernel_launches(self) -> int:
         return int(self._lib.lrc_kernel_launches(self._h))

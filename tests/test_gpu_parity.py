@@ -188,3 +188,9 @@ def test_solve_medium_first_iterations():
 def test_solve_restart_and_tau0():
     require_gpu()
     _solve_parity("tiny", 0, 14, restart_every=6, tau=0.0, cap=16)
+
+
+def test_solve_small_cold_jacobi_start():
+    """Same parity with the core SVD started from W = I every iteration (LRC_NO_WARM_START)."""
+    require_gpu()
+    _solve_parity("small", 1, 30, warm_start=False)

@@ -43,7 +43,7 @@ def main(name="large", N=20):
 
 
 
-def profile(name="large", N=20):
+def profile(name="large", N=20, warm=True):
     prob = gen.make_problem(name)
     cfg, op = prob.cfg, prob.op
     d_mu, d_nu, BU, BV = prob.subset(0)
@@ -53,13 +53,13 @@ def profile(name="large", N=20):
                      [torch.from_numpy(v).to(dev) for v in op.vals], op.rho_f, op.lambda_s)
     ctx.set_params(d_mu, d_nu)
     bu, bv = torch.from_numpy(BU).to(dev), torch.from_numpy(BV).to(dev)
-    ctx.solve(bu, bv, prob.lam_min, prob.lam_max, cfg.tol, cfg.rank_cap, N)
-    _, _, info = ctx.solve(bu, bv, prob.lam_min, prob.lam_max, cfg.tol, cfg.rank_cap, N)
-    print(f"[{name}] graph solve N={N}: {info['ms_iterations'] / N:.3f} ms/it, sweeps/it "
+    ctx.solve(bu, bv, prob.lam_min, prob.lam_max, cfg.tol, cfg.rank_cap, N, warm_start=warm)
+    _, _, info = ctx.solve(bu, bv, prob.lam_min, prob.lam_max, cfg.tol, cfg.rank_cap, N, warm_start=warm)
+    print(f"[{name} warm={warm}] graph solve N={N}: {info['ms_iterations'] / N:.3f} ms/it, sweeps/it "
           f"{info['jacobi_sweeps'] / N:.1f}, rho={info['rel_residual']:.3e} chol2 cycles/it (chol+R, jacobi, out) "
           f"{[round(c / N) for c in info['chol2_cycles']]}", flush=True)
     ctx.set_profiling(True)
-    ctx.solve(bu, bv, prob.lam_min, prob.lam_max, cfg.tol, cfg.rank_cap, N)
+    ctx.solve(bu, bv, prob.lam_min, prob.lam_max, cfg.tol, cfg.rank_cap, N, warm_start=warm)
     prof = ctx.profile()
     ctx.set_profiling(False)
     for k, (ms, cnt) in sorted(prof.items(), key=lambda kv: -kv[1][0]):
@@ -70,6 +70,7 @@ def profile(name="large", N=20):
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "profile":
         for nm in sys.argv[2:] or ["large"]:
-            profile(nm, {"tiny": 30, "small": 50, "medium": 80, "large": 20}[nm])
+            for warm in (True, False):
+                profile(nm, {"tiny": 30, "small": 50, "medium": 80, "large": 100}[nm], warm)
     else:
         main(sys.argv[1] if len(sys.argv) > 1 else "large", int(sys.argv[2]) if len(sys.argv) > 2 else 20)
