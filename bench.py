@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--streams", type=int, default=2, help="concurrent subset solves per GPU")
+    ap.add_argument("--no-dense", dest="dense", action="store_false", help="skip the config-5 measurement")
     ap.add_argument("--reserve-sms", type=int, default=2, help="SMs the persistent kernels leave free")
     return ap.parse_args()
 
@@ -305,6 +306,32 @@ def main():
         roof["peak_source"] = ("MEASURED_PEAKS.json hbm_gbs" if roof["unit"] == "GB/s" else
                                "measured DMMA m8n8k4 fp64 (profiles/r01_phase0_fp64_peaks.jsonl)")
 
+    # ---- BASELINE config 5 (full-rank direct approach): fused six-term operator on a dense M x 256 S,
+    #      D_mu / D_nu from a 16 x 16 parameter grid, 20 repetitions, HBM GB/s vs the same roofline
+    dense = None
+    if args.dense and rank == 0:
+        cfg5 = gen.config_by_name("fullrank")
+        mu5, nu5 = gen.parameter_grid(cfg5)
+        ctx5 = lrcheb.Context(local)
+        ctx5.set_operator(rp_d, ci_d, vals_d, op.rho_f, op.lambda_s, borrow=True)
+        ctx5.set_params(mu5, nu5)
+        g = torch.Generator(device=dev).manual_seed(cfg5.seed)
+        S5 = torch.randn((op.M, cfg5.dense_cols), dtype=torch.float64, device=dev, generator=g)
+        for _ in range(3):
+            Y5 = ctx5.apply_dense(S5)
+        kms = []
+        for _ in range(cfg5.reps):
+            Y5 = ctx5.apply_dense(S5)
+            kms.append(ctx5.last_kernel_ms())
+        avg = float(np.mean(kms))
+        byts = 52.0 * nnz + 4.0 * (M + 1) + 16.0 * M * cfg5.dense_cols
+        dense = {"workload": f"config 5: M={M} dense S M x {cfg5.dense_cols}, {cfg5.reps} repetitions",
+                 "avg_ms": avg, "achieved": byts / (avg / 1e3) / 1e9, "unit": "GB/s", "peak": hbm_peak(),
+                 "frac": byts / (avg / 1e3) / 1e9 / hbm_peak(),
+                 "tflops": 6.0 * nnz * cfg5.dense_cols / (avg / 1e3) / 1e12}
+        del S5, Y5
+        ctx5.close()
+
     result = {
         "metric": "ChebyshevT iterations/sec (fused-SpMM HBM GB/s in roofline_spmm)",
         "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -322,6 +349,7 @@ def main():
         "clocks": clocks,
         "roofline": roof,
         "roofline_spmm": kernel_entry("spmm"),
+        "config5_dense_spmm": dense,
         "kernel_ms_per_step": {k: v[0] for k, v in prof.items()},
         "final_rel_residual": infos[-1]["rel_residual"],
         "ranks_final": infos[-1]["rank"],

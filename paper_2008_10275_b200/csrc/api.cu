@@ -1,12 +1,12 @@
 // liblrcheb C ABI (include/lrcheb.h): context, validation, workspaces, and the ChebyshevT driver.
 //
 // One iteration k (X_k -> X_{k+1}, reading S1) is enqueued as
-//   fork:  [s0] K1 spmm S2STEP(U_k) -> Wcat = [B_U | U_k - g W0 | W1 | W2]        (a1)
+//   fork:  [s0] K1 spmm S2STEP(U_k) -> W3 = [U_k - g W0], [W1], [W2] (three contiguous arrays) (a1)
 //          [s1] vside: Vcat, Householder QR -> T1 = R_V^T, Q_V                    (a2)
 //   join:  ts GRAM(Ucat, T1) -> reduce -> chol1 -> T2                            (a3)
 //          ts GRAM(Ucat, T2) -> reduce -> chol2 + Jacobi + rank -> Z, V_{k+1}    (a4, a5)
 //          ts STORE(Ucat, Z) -> U_{k+1}                                          (a6)
-// with Ucat = [Wcat | U_{k-1}] never copied (two strided blocks) and all ranks device-resident,
+// with Ucat = [B_U | W0' | W1 | W2 | U_{k-1}] never copied (five strided blocks), ranks device-resident,
 // so the whole N-iteration loop is captured once into a CUDA graph and replayed.
 #include <algorithm>
 #include <cmath>
@@ -38,8 +38,9 @@ struct Workspace {
   int64_t M = 0, n = 0;
   int rb = 0, cap = 0, N = 0, pmax = 0, wmax = 0, capp = 0, grid = 0;
   bool record = false;
-  int LDW = 0, LDU = 0;
-  double* Wcat = nullptr;
+  int LDB = 0, LDU = 0;
+  double* BUb = nullptr;      // B_U (M x r_B, ld LDB)
+  double* W3 = nullptr;       // [W0' | W1 | W2]: three contiguous M x LDU blocks (stream stride M*LDU)
   double* Ubuf[3] = {nullptr, nullptr, nullptr};
   double* Vbuf[3] = {nullptr, nullptr, nullptr};
   double* BV = nullptr;
@@ -173,7 +174,7 @@ cudaMemcpyKind kind_out(lrc_mem where) {
 }
 
 void free_ws(Workspace& w) {
-  dfree(w.Wcat);
+  dfree(w.BUb); dfree(w.W3);
   for (int i = 0; i < 3; ++i) { dfree(w.Ubuf[i]); dfree(w.Vbuf[i]); }
   dfree(w.BV); dfree(w.omega); dfree(w.ints); dfree(w.sigma); dfree(w.scal);
   dfree(w.T1); dfree(w.QV); dfree(w.G); dfree(w.R1); dfree(w.T2); dfree(w.Z);
@@ -199,7 +200,7 @@ lrc_status ensure_ws(lrc_ctx* ctx, int rb, int cap, int N, int wmax, bool record
   const int p_need = (int)std::min<int64_t>(ctx->n, wmax);
   const int pmax = ts_pmax_for(p_need < 1 ? 1 : p_need);
   const int capp = ts_pmax_for(cap);
-  if (w.Wcat && w.M == ctx->M && w.n == ctx->n && w.rb >= rb && w.cap == cap && w.N >= N &&
+  if (w.W3 && w.M == ctx->M && w.n == ctx->n && w.rb >= rb && w.cap == cap && w.N >= N &&
       w.wmax >= wmax && w.pmax == pmax && (!record || w.record))
     return LRC_OK;
   cudaStreamSynchronize(ctx->stream);
@@ -209,10 +210,11 @@ lrc_status ensure_ws(lrc_ctx* ctx, int rb, int cap, int N, int wmax, bool record
   const size_t M = (size_t)ctx->M, n = (size_t)ctx->n;
   w.M = ctx->M; w.n = ctx->n; w.rb = rb; w.cap = cap; w.N = N; w.pmax = pmax; w.wmax = wmax;
   w.capp = capp; w.record = record;
-  w.LDW = rb + 3 * cap; w.LDW += (w.LDW & 1);
+  w.LDB = rb + (rb & 1);
   w.LDU = cap + (cap & 1);
   w.grid = ts_grid_for((int)ctx->M, ctx->reserved_sms);
-  CK(dalloc(&w.Wcat, M * w.LDW));
+  CK(dalloc(&w.BUb, M * w.LDB));
+  CK(dalloc(&w.W3, 3 * M * w.LDU));
   for (int i = 0; i < 3; ++i) {
     CK(dalloc(&w.Ubuf[i], M * w.LDU));
     CK(dalloc(&w.Vbuf[i], n * cap));
@@ -239,7 +241,8 @@ lrc_status ensure_ws(lrc_ctx* ctx, int rb, int cap, int N, int wmax, bool record
     CK(dalloc(&w.Uh, (size_t)N * M * w.LDU));
     CK(dalloc(&w.Vh, (size_t)N * n * cap));
   }
-  CK(cudaMemsetAsync(w.Wcat, 0, sizeof(double) * M * w.LDW, ctx->stream));
+  CK(cudaMemsetAsync(w.BUb, 0, sizeof(double) * M * w.LDB, ctx->stream));
+  CK(cudaMemsetAsync(w.W3, 0, sizeof(double) * 3 * M * w.LDU, ctx->stream));
   for (int i = 0; i < 3; ++i) {
     CK(cudaMemsetAsync(w.Ubuf[i], 0, sizeof(double) * M * w.LDU, ctx->stream));
     CK(cudaMemsetAsync(w.Vbuf[i], 0, sizeof(double) * n * cap, ctx->stream));
@@ -385,6 +388,23 @@ lrc_status enqueue_norm2(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, int slo
   return LRC_OK;
 }
 
+UBlock ublock(const double* p, int ld, int w_fixed, int w_idx) {
+  UBlock b{};
+  b.p = p; b.ld = ld; b.w_fixed = w_fixed; b.w_idx = w_idx;
+  return b;
+}
+
+// Ucat = [B_U | W0' | W1 | W2 | extra]: the three W blocks have width rk[ridx]
+UDesc ucat_desc(const Workspace& w, int64_t M, int rb, int ridx, const double* extra, int extra_idx) {
+  UDesc u{};
+  u.nb = 0;
+  u.b[u.nb++] = ublock(w.BUb, w.LDB, rb, -1);
+  if (ridx >= 0)
+    for (int t = 0; t < 3; ++t) u.b[u.nb++] = ublock(w.W3 + (size_t)t * M * w.LDU, w.LDU, 0, ridx);
+  if (extra) u.b[u.nb++] = ublock(extra, w.LDU, 0, extra_idx);
+  return u;
+}
+
 VBlock vblock(const double* ptr, int ld, int w_fixed, int w_idx, double scale, int diag, int use_omega) {
   VBlock v{};
   v.ptr = ptr; v.ld = ld; v.w_fixed = w_fixed; v.w_idx = w_idx; v.w_mul = 1;
@@ -410,9 +430,10 @@ lrc_status enqueue_iteration(lrc_ctx* ctx, int k, int rb, int cap, double gamma,
   a.U = Ucur;
   a.ldu = w.LDU;
   a.d_r = st.rk + (k + 1);
-  a.out = w.Wcat;
-  a.ldo = w.LDW;
-  a.out_off = rb;
+  a.out = w.W3;
+  a.ldo = w.LDU;
+  a.out_off = 0;
+  a.out_sstride = (long long)ctx->M * w.LDU;
   a.gamma = gamma;
   KL(P_SPMM, s, launch_spmm(SPMM_S2STEP, a, cap, s));
 
@@ -423,9 +444,7 @@ lrc_status enqueue_iteration(lrc_ctx* ctx, int k, int rb, int cap, double gamma,
   vd.b[2] = vblock(Vcur, cap, 0, k + 1, -gamma, 1, 1);         // -w g d_mu * V_k
   vd.b[3] = vblock(Vcur, cap, 0, k + 1, -gamma, 2, 1);         // -w g d_nu * V_k
   vd.b[4] = vblock(Vprev, cap, 0, k, 1.0, 0, 2);               // (1-w) V_{k-1}
-  UDesc ud{};
-  ud.A = w.Wcat; ud.lda = w.LDW; ud.wa_fixed = rb; ud.wa_mul = 3; ud.wa_idx = k + 1;
-  ud.B = Uprev; ud.ldb = w.LDU; ud.wb_fixed = 0; ud.wb_idx = k;
+  const UDesc ud = ucat_desc(w, ctx->M, rb, k + 1, Uprev, k);
   lrc_status r = enqueue_truncation(ctx, ud, vd, w.omega, k, tol, cap, k + 2, k, Unext, w.LDU,
                                     Vnext, cap, s, true, ctx->warm_start);
   if (r != LRC_OK) return r;
@@ -812,9 +831,9 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
   const double gamma = 1.0 / d_;
 
   CK(cudaEventRecord(ctx->ev[0], s));
-  // inputs: B_U into Wcat[:, :rb], B_V into BV
+  // inputs: B_U into BUb, B_V into BV
   if (rb > 0) {
-    CK(cudaMemcpy2DAsync(w.Wcat, sizeof(double) * w.LDW, B_U, sizeof(double) * ld_bu,
+    CK(cudaMemcpy2DAsync(w.BUb, sizeof(double) * w.LDB, B_U, sizeof(double) * ld_bu,
                          sizeof(double) * rb, M, kind_in(where), s));
     CK(cudaMemcpy2DAsync(w.BV, sizeof(double) * rb, B_V, sizeof(double) * ld_bv,
                          sizeof(double) * rb, n, kind_in(where), s));
@@ -827,8 +846,7 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
 
   if (rb > 0) {
     // ||B||_F^2 -> scal[0]
-    UDesc ub{};
-    ub.A = w.Wcat; ub.lda = w.LDW; ub.wa_fixed = rb; ub.wa_idx = -1; ub.B = nullptr; ub.wb_idx = -1;
+    const UDesc ub = ucat_desc(w, M, rb, -1, nullptr, -1);
     VDesc vb{};
     vb.nb = 1;
     vb.b[0] = vblock(w.BV, rb, rb, -1, 1.0, 0, 0);
@@ -875,10 +893,10 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
     if (!(opts->flags & LRC_SKIP_FINAL_RESIDUAL)) {
       // residual factors: Ucat = [B_U | W0 | W1 | W2], Vcat = [B_V | -V | -d_mu V | -d_nu V]
       SpmmArgs a = spmm_base(ctx);
-      a.U = UN; a.ldu = w.LDU; a.d_r = sd.rk + slotN; a.out = w.Wcat; a.ldo = w.LDW; a.out_off = rb;
+      a.U = UN; a.ldu = w.LDU; a.d_r = sd.rk + slotN; a.out = w.W3; a.ldo = w.LDU; a.out_off = 0;
+      a.out_sstride = (long long)M * w.LDU;
       KL(P_SPMM, s, launch_spmm(SPMM_PLAIN3, a, cap, s));
-      UDesc ur{};
-      ur.A = w.Wcat; ur.lda = w.LDW; ur.wa_fixed = rb; ur.wa_mul = 3; ur.wa_idx = slotN; ur.B = nullptr; ur.wb_idx = -1;
+      const UDesc ur = ucat_desc(w, M, rb, slotN, nullptr, -1);
       VDesc vr{};
       vr.nb = 4;
       vr.b[0] = vblock(w.BV, rb, rb, -1, 1.0, 0, 0);
@@ -1071,7 +1089,8 @@ lrc_status lrc_truncate(lrc_ctx* ctx, const double* U, int64_t ld_u, const doubl
   CK(cudaMemsetAsync(ws.ints, 0, sizeof(int) * (ws.N + 16), s));
   CK(cudaMemsetAsync(ws.sigma, 0, sizeof(double) * (size_t)(ws.N + 4) * kSigmaStride, s));
   UDesc ud{};
-  ud.A = ws.tmpA; ud.lda = w; ud.wa_fixed = w; ud.wa_idx = -1; ud.B = nullptr; ud.wb_idx = -1;
+  ud.nb = 1;
+  ud.b[0] = ublock(ws.tmpA, w, w, -1);
   VDesc vd{};
   vd.nb = 1;
   vd.b[0] = vblock(ws.tmpB, w, w, -1, 1.0, 0, 0);

@@ -42,6 +42,9 @@ struct SpmmArgs {
   int ntl_g;
   const int* tlist;         // (set by the launcher) tile list, or null for all tiles
   int u_aligned16;          // (set by the launcher) U rows may be copied in 16-byte chunks
+  int dbg;                  // (developer bisection, env LRCHEB_SPMM_DBG) 1: no DMMA, 2: no U staging,
+                            // 4: no value loads, 8: no output stores; 32 (env LRCHEB_SPMM_TMA): use
+                            // the experimental persistent TMA pipeline kernel
   const int* row_ptr;
   const int* col_idx;
   const double* v[6];       // A0, A1, A2, Jrho, Jmu, Jlam
@@ -50,9 +53,10 @@ struct SpmmArgs {
   int ldu;
   const int* d_r;           // r = d_r ? *d_r : r_fixed   (device-resident rank)
   int r_fixed;
-  double* out;              // outputs at out[row*ldo + out_off + t*r + c]
+  double* out;              // outputs at out[t*out_sstride + row*ldo + out_off + c] (t = stream)
   int ldo;
   int out_off;
+  long long out_sstride;    // element offset between the three output streams; 0 = r (interleaved)
   double gamma;             // S2STEP: out0 = U - gamma * W0
   int single_t;             // SINGLE: output c_t A_t U
   const double* dmu;        // DENSE: per-column scalings
@@ -63,10 +67,11 @@ cudaError_t launch_spmm(int mode, const SpmmArgs& a, int rmax, cudaStream_t s);
 // ------------------------------------------------------------------------------------------
 // a3/a4/a6: tall-skinny DMMA kernels over the logical concatenation Ucat = [A | B]
 // ------------------------------------------------------------------------------------------
-struct UDesc {
-  const double* A; int lda; int wa_fixed; int wa_mul; int wa_idx;  // wa = wa_fixed + wa_mul*rk[wa_idx]
-  const double* B; int ldb; int wb_fixed; int wb_idx;              // wb = wb_idx>=0 ? rk[wb_idx] : wb_fixed
-};
+// Logical concatenation Ucat = [block 0 | ... | block nb-1] of row-major M-row blocks; block width =
+// w_fixed + (w_idx >= 0 ? rk[w_idx] : 0) (device-resident ranks).
+struct UBlock { const double* p; int ld; int w_fixed; int w_idx; };
+constexpr int kMaxUBlocks = 5;
+struct UDesc { UBlock b[kMaxUBlocks]; int nb; };
 
 struct TsArgs {
   int M;

@@ -16,6 +16,7 @@
 // block is read from its first row only.  Each warp then owns one (node block, 32-column slice):
 // every gathered U element (a 4-deep register prefetch ring hides the L2 latency) feeds
 // 3 x (rows of the block) FMAs.
+#include <cstdlib>
 #include "lrc_internal.cuh"
 
 namespace lrc {
@@ -155,7 +156,7 @@ __device__ __forceinline__ void block_task_mma(const SpmmArgs& a, int r, int n0,
     if (R >= nrow) continue;
     const int q = R / 3, st = R - (R / 3) * 3;
     const size_t row = (size_t)(row0 + q);
-    double* orow = a.out + row * a.ldo + a.out_off + st * r;
+    double* orow = a.out + st * (a.out_sstride ? a.out_sstride : r) + row * a.ldo + a.out_off;
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
 #pragma unroll
@@ -213,7 +214,7 @@ __device__ __forceinline__ void block_task_mma_smem(const SpmmArgs& a, int r, in
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.0;
-  for (int k0 = 0; k0 < L; k0 += 4) {
+  for (int k0 = 0; k0 < ((a.dbg & 1) ? 0 : L); k0 += 4) {
     const int j = k0 + tig;
     const bool jv = j < L;
     const double* vj = vals + qo * 3 * lp + j;
@@ -238,7 +239,7 @@ __device__ __forceinline__ void block_task_mma_smem(const SpmmArgs& a, int r, in
       if (R >= nrow) continue;
       const int q = R / 3, st = R - (R / 3) * 3;
       const size_t row = (size_t)(row0 + q);
-      double* orow = a.out + row * a.ldo + a.out_off + st * r;
+      double* orow = a.out + st * (a.out_sstride ? a.out_sstride : r) + row * a.ldo + a.out_off;
       const double* urow_self = (lrow0 >= 0) ? s_u + (lrow0 + qo + q) * ust : a.U + row * a.ldu;
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
@@ -248,7 +249,7 @@ __device__ __forceinline__ void block_task_mma_smem(const SpmmArgs& a, int r, in
           if (c < r) {
             double v = acc[mt][nt][hm * 2 + e];
             if (MODE == SPMM_S2STEP && st == 0) v = fma(-a.gamma, v, urow_self[c]);
-            __stcs(orow + c, v);
+            if (!(a.dbg & 8)) __stcs(orow + c, v);
           }
         }
       }
@@ -265,15 +266,16 @@ __device__ __forceinline__ void block_store(const SpmmArgs& a, int r, int c, int
     if (q < gs) {
       const size_t row = (size_t)(row0 + q);
       double* orow = a.out + row * a.ldo + a.out_off;
+      const long long sst = a.out_sstride ? a.out_sstride : r;
       if constexpr (MODE == SPMM_S2STEP) {
         const double uk = __ldg(a.U + row * a.ldu + c);
         __stcs(orow + c, fma(-a.gamma, acc[q][0], uk));
-        __stcs(orow + r + c, acc[q][1]);
-        __stcs(orow + 2 * r + c, acc[q][2]);
+        __stcs(orow + sst + c, acc[q][1]);
+        __stcs(orow + 2 * sst + c, acc[q][2]);
       } else if constexpr (MODE == SPMM_PLAIN3) {
         __stcs(orow + c, acc[q][0]);
-        __stcs(orow + r + c, acc[q][1]);
-        __stcs(orow + 2 * r + c, acc[q][2]);
+        __stcs(orow + sst + c, acc[q][1]);
+        __stcs(orow + 2 * sst + c, acc[q][2]);
       } else {
         __stcs(orow + c, acc[q][0]);
       }
@@ -436,6 +438,235 @@ spmm_kernel(SpmmArgs a, int ust) {
 }
 
 
+// Lean hot kernel (S2STEP / PLAIN3) for the shared-memory-U tiles only: same stages as the U path of
+// spmm_kernel without the gather / scalar code, so it fits 3 CTAs per SM (registers and ~76 KB smem).
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 3)
+spmm_u_kernel(SpmmArgs a, int ust) {
+  const int r = a.d_r ? *a.d_r : a.r_fixed;
+  if (r <= 0) return;
+  extern __shared__ double smem_dyn[];
+  double* s_v = smem_dyn;                        // [kValCap]
+  double* s_u = smem_dyn + kValCap;              // [kUCap][ust]
+  __shared__ int s_desc[kDescInts];
+  __shared__ int s_bstart[kTileBlocks + 1], s_vbase[kTileBlocks], s_lp[kTileBlocks];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int CT = (r + 31) >> 5;
+  const int t = a.tlist_u[blockIdx.x];
+  for (int i = tid; i < kDescInts; i += kThreads) s_desc[i] = __ldg(a.tdesc + (size_t)t * kDescInts + i);
+  __syncthreads();
+  const int e0 = s_desc[0], tot = s_desc[1], nb = s_desc[2], nu = s_desc[3];
+  if (!(a.dbg & 2)) stage_u_rows(a, r, s_desc + kDescUrows, nu, s_u, ust, tid, kThreads);
+  asm volatile("cp.async.commit_group;\n" ::);
+  if (tid == 0) {
+    int vb = 0, eb = 0;
+    for (int b = 0; b < nb; ++b) {
+      const int g = s_desc[12 + b], L = s_desc[16 + b];
+      s_bstart[b] = eb; s_lp[b] = row_pitch(L); s_vbase[b] = vb;
+      vb += g * 3 * s_lp[b];
+      eb += g * L;
+    }
+    s_bstart[nb] = tot;
+  }
+  constexpr int kStg = (kSpmmCap + kThreads - 1) / kThreads;
+  double raw[kStg][6];
+#pragma unroll
+  for (int k = 0; k < kStg; ++k) {
+    const int e = tid + k * kThreads;
+    if (e < tot && !(a.dbg & 4)) {
+#pragma unroll
+      for (int v = 0; v < 6; ++v) raw[k][v] = __ldcs(a.v[v] + e0 + e);
+    } else {
+#pragma unroll
+      for (int v = 0; v < 6; ++v) raw[k][v] = 0.0;
+    }
+  }
+  __syncthreads();                               // block table
+#pragma unroll
+  for (int k = 0; k < kStg; ++k) {
+    const int e = tid + k * kThreads;
+    if (e < tot) {
+      int b = 0;
+#pragma unroll
+      for (int kk = 1; kk < kTileBlocks; ++kk) b += (kk < nb && e >= s_bstart[kk]);
+      const int L = s_desc[16 + b];
+      const int rel = e - s_bstart[b];
+      const int q = rel / L, j = rel - (rel / L) * L;
+      const int lp = s_lp[b];
+      double* dst = s_v + s_vbase[b] + q * 3 * lp + j;
+      dst[0] = fma(a.lam, raw[k][5], fma(a.rho, raw[k][3], raw[k][0]));   // A0 + rho Jrho + lam Jlam
+      dst[lp] = raw[k][1] + raw[k][4];                                   // A1 + Jmu
+      dst[2 * lp] = a.rho * raw[k][2];                                    // rho A2
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::);
+  __syncthreads();
+  const unsigned short* lx = reinterpret_cast<const unsigned short*>(s_desc + kDescLidx);
+  int cb = 0;
+  for (int b = 0, task0 = 0; b < nb; ++b) {
+    const int g = s_desc[12 + b], L = s_desc[16 + b];
+    for (int ct = 0; ct < CT; ++ct, ++task0) {
+      if ((task0 % kWarps) != warp) continue;
+      for (int qo = 0; qo < g; qo += 5)
+        block_task_mma_smem<MODE>(a, r, ct * 32, s_desc[8 + b] + qo, min(5, g - qo), qo, L, s_lp[b],
+                                  s_v + s_vbase[b], lx + cb, s_u, ust, s_desc[20 + b], lane);
+    }
+    cb += L;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Persistent warp-specialised TMA kernel (S2STEP / PLAIN3, shared-memory-U tiles).  One CTA per SM:
+// warp 8 is the producer -- per tile it copies the 1 KB descriptor, then one elected lane issues
+// cp.async.bulk copies of the six contiguous value segments and of the tile's deduplicated U rows
+// into a double-buffered stage, completing on the stage's `full` mbarrier (expect-tx bytes).  Warps
+// 0-7 consume: combine the six raw streams into the conflict-free [slot][j] layout, contract on
+// the fp64 tensor pipe, store, and release the stage through its `empty` mbarrier.  Tile k+1 is in
+// flight while tile k is combined and contracted.
+// ---------------------------------------------------------------------------------------------
+constexpr int kTmaStages = 2;
+constexpr int kRawCap = kSpmmCap + 2;              // doubles per staged raw value array (alignment slack)
+constexpr int kTmaThreads = 288;                   // 8 consumer warps + 1 producer warp
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
+  unsigned ok;
+  asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+               : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  while (!mbar_try(b, parity)) {}
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
+
+size_t tma_stage_doubles(int ust) { return (size_t)kDescInts / 2 + 6 * (size_t)kRawCap + (size_t)kUCap * ust; }
+
+template <int MODE>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+spmm_tma_kernel(SpmmArgs a, int ust) {
+  const int r = a.d_r ? *a.d_r : a.r_fixed;
+  if (r <= 0) return;
+  extern __shared__ __align__(128) double smem_dyn[];
+  const int stage_d = kDescInts / 2 + 6 * kRawCap + kUCap * ust;
+  double* s_v = smem_dyn + kTmaStages * stage_d;
+  __shared__ __align__(8) unsigned long long full[kTmaStages], empty[kTmaStages];
+  __shared__ int s_bstart[kTileBlocks + 1], s_vbase[kTileBlocks], s_lp[kTileBlocks];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    // full: 1 expect-tx arrival (elected lane) + 32 cp.async arrivals (producer lanes)
+    for (int i = 0; i < kTmaStages; ++i) { mbar_init(&full[i], 33); mbar_init(&empty[i], 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int G = gridDim.x;
+  const int ntl = a.ntl_u;
+
+  if (warp == 8) {
+    // ------------------------------------------------------------------ producer
+    for (int k = 0;; ++k) {
+      const int idx = blockIdx.x + k * G;
+      if (idx >= ntl) break;
+      const int st = k % kTmaStages;
+      if (k >= kTmaStages) mbar_wait(&empty[st], ((k / kTmaStages) - 1) & 1);
+      double* stage = smem_dyn + st * stage_d;
+      int* d = reinterpret_cast<int*>(stage);
+      const int t = __ldg(a.tlist_u + idx);
+      for (int i = lane; i < kDescInts; i += 32) d[i] = __ldg(a.tdesc + (size_t)t * kDescInts + i);
+      __syncwarp();
+      const int e0 = d[0], tot = d[1], nu = d[3];
+      const int e0a = e0 & ~1, end = e0 + tot, enda = end & ~1;
+      double* raw = stage + kDescInts / 2;
+      double* su = raw + 6 * kRawCap;
+      if (lane == 0) {
+        const unsigned vbytes = (unsigned)(enda - e0a) * 8u;
+        if (end & 1)      // odd tail element: plain load (never read past the array end)
+          for (int v = 0; v < 6; ++v) raw[v * kRawCap + (end - 1 - e0a)] = __ldg(a.v[v] + end - 1);
+        mbar_expect_tx(&full[st], 6u * vbytes);
+        if (vbytes)
+          for (int v = 0; v < 6; ++v) bulk_g2s(raw + v * kRawCap, a.v[v] + e0a, vbytes, &full[st]);
+      }
+      // U rows: 16-byte cp.async by all producer lanes, tracked by the same mbarrier
+      const int nch = (r + 1) >> 1;
+      for (int e = lane; e < nu * nch; e += 32) {
+        const int u = e / nch, ch = e - (e / nch) * nch;
+        cp_async16(su + u * ust + 2 * ch, a.U + (size_t)d[kDescUrows + u] * a.ldu + 2 * ch);
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[st])) : "memory");
+      __syncwarp();
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------------- consumers (warps 0-7)
+  const int CT = (r + 31) >> 5;
+  for (int k = 0;; ++k) {
+    const int idx = blockIdx.x + k * G;
+    if (idx >= ntl) break;
+    const int st = k % kTmaStages;
+    mbar_wait(&full[st], (k / kTmaStages) & 1);
+    const double* stage = smem_dyn + st * stage_d;
+    const int* d = reinterpret_cast<const int*>(stage);
+    const double* raw = stage + kDescInts / 2;
+    const double* su = raw + 6 * kRawCap;
+    const int e0 = d[0], tot = d[1], nb = d[2];
+    const int off = e0 - (e0 & ~1);
+    if (tid == 0) {
+      int vb = 0, eb = 0;
+      for (int b = 0; b < nb; ++b) {
+        const int g = d[12 + b], L = d[16 + b];
+        s_bstart[b] = eb; s_lp[b] = row_pitch(L); s_vbase[b] = vb;
+        vb += g * 3 * s_lp[b];
+        eb += g * L;
+      }
+      s_bstart[nb] = tot;
+    }
+    consumer_sync();
+    for (int e = tid; e < tot; e += 256) {
+      int b = 0;
+#pragma unroll
+      for (int kk = 1; kk < kTileBlocks; ++kk) b += (kk < nb && e >= s_bstart[kk]);
+      const int L = d[16 + b];
+      const int rel = e - s_bstart[b];
+      const int q = rel / L, j = rel - (rel / L) * L;
+      const int lp = s_lp[b];
+      const double* rv = raw + off + e;
+      double* dst = s_v + s_vbase[b] + q * 3 * lp + j;
+      dst[0] = fma(a.lam, rv[5 * kRawCap], fma(a.rho, rv[3 * kRawCap], rv[0]));   // A0 + rho Jrho + lam Jlam
+      dst[lp] = rv[1 * kRawCap] + rv[4 * kRawCap];                               // A1 + Jmu
+      dst[2 * lp] = a.rho * rv[2 * kRawCap];                                      // rho A2
+    }
+    consumer_sync();
+    const unsigned short* lx = reinterpret_cast<const unsigned short*>(d + kDescLidx);
+    int cb = 0;
+    for (int b = 0, task0 = 0; b < nb; ++b) {
+      const int g = d[12 + b], L = d[16 + b];
+      for (int ct = 0; ct < CT; ++ct, ++task0) {
+        if ((task0 & 7) != warp) continue;
+        for (int qo = 0; qo < g; qo += 5)
+          block_task_mma_smem<MODE>(a, r, ct * 32, d[8 + b] + qo, min(5, g - qo), qo, L, s_lp[b],
+                                    s_v + s_vbase[b], lx + cb, su, ust, d[20 + b], lane);
+      }
+      cb += L;
+    }
+    consumer_sync();                   // stage st and s_v fully consumed
+    if (tid == 0) mbar_arrive(&empty[st]);
+  }
+}
+
 int ust_for(int rmax) { return ((rmax + 11) / 16) * 16 + 4; }   // >= rmax + 1, == 4 mod 16 (even)
 
 size_t smem_for(int mode, int rmax) {
@@ -457,10 +688,51 @@ int sm_count() {
 template <int MODE>
 cudaError_t launch_m(const SpmmArgs& a0, int rmax, cudaStream_t s) {
   SpmmArgs a = a0;
+  {
+    static int dbg = -1;
+    if (dbg < 0) {
+      const char* e = getenv("LRCHEB_SPMM_DBG");
+      dbg = e ? atoi(e) : 0;
+      if (getenv("LRCHEB_SPMM_TMA")) dbg |= 32;
+    }
+    a.dbg = dbg;
+  }
   // 16-byte U row copies need 16-byte aligned rows and room for the padding element of an odd r
   a.u_aligned16 = ((reinterpret_cast<uintptr_t>(a.U) & 15) == 0) && (a.ldu % 2 == 0) && (rmax < a.ldu || rmax % 2 == 0);
   constexpr bool HOT = (MODE == SPMM_S2STEP || MODE == SPMM_PLAIN3);
-  (void)HOT;
+  if constexpr (HOT) {
+    // persistent TMA pipeline when the stage fits and every stream is 16-byte aligned
+    const size_t sm_t = sizeof(double) * (kTmaStages * tma_stage_doubles(ust_for(rmax)) + kValCap);
+    bool al = a.u_aligned16 && ((reinterpret_cast<uintptr_t>(a.U) & 15) == 0);
+    for (int v = 0; v < 6; ++v) al = al && ((reinterpret_cast<uintptr_t>(a.v[v]) & 15) == 0);
+    // experimental (slower than spmm_u_kernel on B200 so far): opt-in via dbg bit 32
+    if (al && sm_t <= 232448 - 1024 && (a.dbg & 32)) {
+      if (a.ntl_u > 0) {
+        const int grid = a.ntl_u < sm_count() ? a.ntl_u : sm_count();
+        spmm_tma_kernel<MODE><<<grid, kTmaThreads, sm_t, s>>>(a, ust_for(rmax));
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+      }
+      if (a.ntl_g > 0) {
+        a.tlist = a.tlist_g;
+        spmm_kernel<MODE, 5><<<a.ntl_g, kThreads, smem_for(MODE, rmax), s>>>(a, ust_for(rmax));
+      }
+      return cudaGetLastError();
+    }
+    const size_t sm_u = sizeof(double) * (kValCap + (size_t)kUCap * ust_for(rmax));
+    if (sm_u <= 75 * 1024) {                       // 3 CTAs / SM
+      if (a.ntl_u > 0) {
+        spmm_u_kernel<MODE><<<a.ntl_u, kThreads, sm_u, s>>>(a, ust_for(rmax));
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+      }
+      if (a.ntl_g > 0) {
+        a.tlist = a.tlist_g;
+        spmm_kernel<MODE, 5><<<a.ntl_g, kThreads, smem_for(MODE, rmax), s>>>(a, ust_for(rmax));
+      }
+      return cudaGetLastError();
+    }
+  }
   if (a.ntiles == 0) return cudaSuccess;
   a.tlist = nullptr;
   spmm_kernel<MODE, 5><<<a.ntiles, kThreads, smem_for(MODE, rmax), s>>>(a, ust_for(rmax));
@@ -472,6 +744,15 @@ cudaError_t prep_m() {
   cudaError_t e = cudaFuncSetAttribute(spmm_kernel<MODE, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem_for(MODE, kMaxRank));
   if (e != cudaSuccess) return e;
+  if constexpr (MODE == SPMM_S2STEP || MODE == SPMM_PLAIN3) {
+    e = cudaFuncSetAttribute(spmm_u_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 75 * 1024);
+    if (e != cudaSuccess) return e;
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, spmm_tma_kernel<MODE>);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(spmm_tma_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(232448 - fa.sharedSizeBytes));
+  }
   return e;
 }
 

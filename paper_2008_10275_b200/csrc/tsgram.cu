@@ -42,10 +42,16 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-__device__ __forceinline__ int ucat_widths(const TsArgs& a, int& wa) {
-  wa = a.u.wa_fixed + (a.u.wa_idx >= 0 ? a.u.wa_mul * a.rk[a.u.wa_idx] : 0);
-  const int wb = a.u.B ? (a.u.wb_idx >= 0 ? a.rk[a.u.wb_idx] : a.u.wb_fixed) : 0;
-  return wa + wb;
+// column offsets of the Ucat blocks (off[nb] = w)
+__device__ __forceinline__ int ucat_offsets(const TsArgs& a, int (&off)[kMaxUBlocks + 1]) {
+  int o = 0;
+#pragma unroll
+  for (int bi = 0; bi < kMaxUBlocks; ++bi) {
+    off[bi] = o;
+    if (bi < a.u.nb) o += a.u.b[bi].w_fixed + (a.u.b[bi].w_idx >= 0 ? a.rk[a.u.b[bi].w_idx] : 0);
+  }
+  off[kMaxUBlocks] = o;
+  return o;
 }
 
 template <int PT>
@@ -60,8 +66,8 @@ struct TsShape {
 };
 
 template <int PT>
-__device__ __forceinline__ void issue_chunk(const TsArgs& a, double* stage, int m0, int k0, int w, int wa,
-                                            int tid) {
+__device__ __forceinline__ void issue_chunk(const TsArgs& a, double* stage, int m0, int k0, int w,
+                                            const int (&off)[kMaxUBlocks + 1], int tid) {
   using S = TsShape<PT>;
   double* s_u = stage;
   double* s_t = stage + kBM * kSU;
@@ -70,8 +76,13 @@ __device__ __forceinline__ void issue_chunk(const TsArgs& a, double* stage, int 
     const int i = e >> 5, j = e & 31;
     const int m = m0 + i, c = k0 + j;
     const bool ok = (m < a.M) && (c < w);
-    const double* src = a.u.A;
-    if (ok) src = (c < wa) ? a.u.A + (size_t)m * a.u.lda + c : a.u.B + (size_t)m * a.u.ldb + (c - wa);
+    const double* src = a.u.b[0].p;
+    if (ok) {
+      int bi = 0;
+#pragma unroll
+      for (int q = 1; q < kMaxUBlocks; ++q) bi += (c >= off[q]);
+      src = a.u.b[bi].p + (size_t)m * a.u.b[bi].ld + (c - off[bi]);
+    }
     cp_async8(s_u + i * kSU + j, src, ok);
   }
 #pragma unroll 4
@@ -89,8 +100,8 @@ ts_kernel(TsArgs a) {
   using S = TsShape<PT>;
   constexpr int PMAX = S::PMAX, SX = S::SX;
 
-  int wa;
-  const int w = ucat_widths(a, wa);
+  int off[kMaxUBlocks + 1];
+  const int w = ucat_offsets(a, off);
   const int p = a.d_p ? *a.d_p : a.p_fixed;
   if (w <= 0 || p <= 0) {
     if (MODE == 0) {   // still publish a zero partial so the reduction is well defined
@@ -128,11 +139,11 @@ ts_kernel(TsArgs a) {
 #pragma unroll
     for (int n = 0; n < PT; ++n) x0[n][0] = x0[n][1] = 0.0;
 
-    issue_chunk<PT>(a, sm, m0, 0, w, wa, tid);
+    issue_chunk<PT>(a, sm, m0, 0, w, off, tid);
     cp_commit();
     for (int kc = 0; kc < nk; ++kc) {
       if (kc + 1 < nk) {
-        issue_chunk<PT>(a, sm + ((kc + 1) & 1) * S::STAGE, m0, (kc + 1) * kBK, w, wa, tid);
+        issue_chunk<PT>(a, sm + ((kc + 1) & 1) * S::STAGE, m0, (kc + 1) * kBK, w, off, tid);
         cp_commit();
         cp_wait<1>();
       } else {
