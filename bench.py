@@ -39,9 +39,9 @@ def parse():
     ap.add_argument("--config", default="large")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--streams", type=int, default=2, help="concurrent subset solves per GPU")
+    ap.add_argument("--streams", type=int, default=3, help="concurrent subset solves per GPU")
     ap.add_argument("--no-dense", dest="dense", action="store_false", help="skip the config-5 measurement")
-    ap.add_argument("--reserve-sms", type=int, default=2, help="SMs the persistent kernels leave free")
+    ap.add_argument("--reserve-sms", type=int, default=3, help="SMs the persistent kernels leave free")
     return ap.parse_args()
 
 
