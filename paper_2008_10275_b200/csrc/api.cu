@@ -398,6 +398,7 @@ UBlock ublock(const double* p, int ld, int w_fixed, int w_idx) {
 UDesc ucat_desc(const Workspace& w, int64_t M, int rb, int ridx, const double* extra, int extra_idx) {
   UDesc u{};
   u.nb = 0;
+  u.pad_even = 1;      // every block at an even column: 16-byte Ucat copies in the ts kernels
   u.b[u.nb++] = ublock(w.BUb, w.LDB, rb, -1);
   if (ridx >= 0)
     for (int t = 0; t < 3; ++t) u.b[u.nb++] = ublock(w.W3 + (size_t)t * M * w.LDU, w.LDU, 0, ridx);
@@ -439,6 +440,7 @@ lrc_status enqueue_iteration(lrc_ctx* ctx, int k, int rb, int cap, double gamma,
 
   VDesc vd{};
   vd.nb = 5;
+  vd.pad_even = 1;
   vd.b[0] = vblock(w.BV, rb, rb, -1, gamma, 0, 1);             // w g B_V
   vd.b[1] = vblock(Vcur, cap, 0, k + 1, 1.0, 0, 1);            // w V_k
   vd.b[2] = vblock(Vcur, cap, 0, k + 1, -gamma, 1, 1);         // -w g d_mu * V_k
@@ -811,7 +813,8 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
   if (!U_out || !V_out) return fail(ctx, LRC_ERR_ARG, "null output");
   if (ld_u < cap || ld_v < cap) return fail(ctx, LRC_ERR_SHAPE, "ld_u / ld_v < rank_cap");
   const int rb = (int)r_B, N = (int)opts->n_iter;
-  const int wmax = std::max(rb + 4 * cap, 3 * cap + rb);
+  // widest concatenation: every block padded to an even width (UDesc::pad_even)
+  const int wmax = (rb + (rb & 1)) + 4 * (cap + (cap & 1));
   if (wmax > kMaxW) return fail(ctx, LRC_ERR_ARG, "r_B + 4 rank_cap must be <= 256");
   const int p_need = (int)std::min<int64_t>(n, wmax);
   if (p_need > 112) return fail(ctx, LRC_ERR_ARG, "min(n, r_B + 4 rank_cap) must be <= 112 in this build");
@@ -849,6 +852,7 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
     const UDesc ub = ucat_desc(w, M, rb, -1, nullptr, -1);
     VDesc vb{};
     vb.nb = 1;
+    vb.pad_even = 1;
     vb.b[0] = vblock(w.BV, rb, rb, -1, 1.0, 0, 0);
     st = enqueue_norm2(ctx, ub, vb, 0, s);
     if (st != LRC_OK) return st;
@@ -899,6 +903,7 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
       const UDesc ur = ucat_desc(w, M, rb, slotN, nullptr, -1);
       VDesc vr{};
       vr.nb = 4;
+      vr.pad_even = 1;
       vr.b[0] = vblock(w.BV, rb, rb, -1, 1.0, 0, 0);
       vr.b[1] = vblock(VN, cap, 0, slotN, -1.0, 0, 0);
       vr.b[2] = vblock(VN, cap, 0, slotN, -1.0, 1, 0);

@@ -71,7 +71,10 @@ cudaError_t launch_spmm(int mode, const SpmmArgs& a, int rmax, cudaStream_t s);
 // w_fixed + (w_idx >= 0 ? rk[w_idx] : 0) (device-resident ranks).
 struct UBlock { const double* p; int ld; int w_fixed; int w_idx; };
 constexpr int kMaxUBlocks = 5;
-struct UDesc { UBlock b[kMaxUBlocks]; int nb; };
+struct UDesc { UBlock b[kMaxUBlocks]; int nb; int pad_even; };   // pad_even: every block's logical
+                                                                   // width rounded up to even (the pad
+                                                                   // column holds zeros / finite data
+                                                                   // met by a zero row of T)
 
 struct TsArgs {
   int M;
@@ -85,6 +88,7 @@ struct TsArgs {
   double* out;              // STORE: M x p (ld ldo)
   int ldo;
   int t_lower;              // T[c][i] == 0 for i > c (T1 = R_V^T): skip the zero blocks
+  int u16;                  // (set by launch_ts) all Ucat blocks 16-byte aligned with even ld/offsets
 };
 // mode 0 = GRAM (partial X^T X, X = Ucat T), 1 = STORE (out = Ucat T)
 cudaError_t launch_ts(int mode, const TsArgs& a, int pmax, int grid, cudaStream_t s);
@@ -104,7 +108,7 @@ struct VBlock {
   int diag;                            // 0: none, 1: d_mu, 2: d_nu
   int use_omega;                       // 0: scale, 1: scale*omega, 2: scale*(1-omega)
 };
-struct VDesc { VBlock b[5]; int nb; };
+struct VDesc { VBlock b[5]; int nb; int pad_even; };   // pad_even: as UDesc (zero pad columns)
 
 struct State {          // device-resident per-solve state
   int* rk;              // rank array, rk[j] = rank of X_{j-1} (j = 0..N+1)

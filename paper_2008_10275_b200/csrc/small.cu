@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kT) vside_kernel(VDesc d, int n, const double*
       const VBlock& B = d.b[bi];
       const int wdt = B.w_fixed + (B.w_idx >= 0 ? B.w_mul * st.rk[B.w_idx] : 0);
       s_off[bi] = off;
-      off += wdt;
+      off += d.pad_even ? wdt + (wdt & 1) : wdt;     // zero pad column (see UDesc::pad_even)
     }
     s_off[d.nb] = off;
   }
@@ -95,13 +95,17 @@ __global__ void __launch_bounds__(kT) vside_kernel(VDesc d, int n, const double*
   const double om = omega ? omega[k] : 1.0;
   for (int bi = 0; bi < d.nb; ++bi) {
     const VBlock& B = d.b[bi];
-    const int o = s_off[bi], wdt = s_off[bi + 1] - o;
+    const int o = s_off[bi], wlog = s_off[bi + 1] - o;
+    const int wdt = B.w_fixed + (B.w_idx >= 0 ? B.w_mul * st.rk[B.w_idx] : 0);
     const double sc = B.use_omega == 0 ? B.scale : (B.use_omega == 1 ? B.scale * om : B.scale * (1.0 - om));
-    for (int e = tid; e < wdt * n; e += kT) {
+    for (int e = tid; e < wlog * n; e += kT) {
       const int c = e / n, i = e - (e / n) * n;
-      double v = sc * B.ptr[(size_t)i * B.ld + c];
-      if (B.diag == 1) v *= dmu[i];
-      else if (B.diag == 2) v *= dnu[i];
+      double v = 0.0;                                   // pad column: exactly zero
+      if (c < wdt) {
+        v = sc * B.ptr[(size_t)i * B.ld + c];
+        if (B.diag == 1) v *= dmu[i];
+        else if (B.diag == 2) v *= dnu[i];
+      }
       s_v[(o + c) * NL + i] = v;
     }
   }

@@ -166,6 +166,8 @@ __device__ __forceinline__ void block_task_mma(const SpmmArgs& a, int r, int n0,
           double v = acc[nt][h * 2 + e];
           if (MODE == SPMM_S2STEP && st == 0) v = fma(-a.gamma, v, __ldg(a.U + row * a.ldu + c));
           __stcs(orow + c, v);
+        } else if (c == r && (r & 1) && a.out_sstride) {
+          __stcs(orow + c, 0.0);          // zero pad column of the (even-padded) Ucat block
         }
       }
     }
@@ -250,6 +252,8 @@ __device__ __forceinline__ void block_task_mma_smem(const SpmmArgs& a, int r, in
             double v = acc[mt][nt][hm * 2 + e];
             if (MODE == SPMM_S2STEP && st == 0) v = fma(-a.gamma, v, urow_self[c]);
             if (!(a.dbg & 8)) __stcs(orow + c, v);
+          } else if (c == r && (r & 1) && a.out_sstride) {
+            __stcs(orow + c, 0.0);        // zero pad column of the (even-padded) Ucat block
           }
         }
       }
@@ -267,6 +271,9 @@ __device__ __forceinline__ void block_store(const SpmmArgs& a, int r, int c, int
       const size_t row = (size_t)(row0 + q);
       double* orow = a.out + row * a.ldo + a.out_off;
       const long long sst = a.out_sstride ? a.out_sstride : r;
+      if (MODE != SPMM_SINGLE && MODE != SPMM_DENSE && a.out_sstride && (r & 1) && c + 1 == r) {
+        __stcs(orow + r, 0.0); __stcs(orow + sst + r, 0.0); __stcs(orow + 2 * sst + r, 0.0);
+      }
       if constexpr (MODE == SPMM_S2STEP) {
         const double uk = __ldg(a.U + row * a.ldu + c);
         __stcs(orow + c, fma(-a.gamma, acc[q][0], uk));

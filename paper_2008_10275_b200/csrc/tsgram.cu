@@ -48,7 +48,10 @@ __device__ __forceinline__ int ucat_offsets(const TsArgs& a, int (&off)[kMaxUBlo
 #pragma unroll
   for (int bi = 0; bi < kMaxUBlocks; ++bi) {
     off[bi] = o;
-    if (bi < a.u.nb) o += a.u.b[bi].w_fixed + (a.u.b[bi].w_idx >= 0 ? a.rk[a.u.b[bi].w_idx] : 0);
+    if (bi < a.u.nb) {
+      const int wd = a.u.b[bi].w_fixed + (a.u.b[bi].w_idx >= 0 ? a.rk[a.u.b[bi].w_idx] : 0);
+      o += a.u.pad_even ? wd + (wd & 1) : wd;
+    }
   }
   off[kMaxUBlocks] = o;
   return o;
@@ -71,26 +74,49 @@ __device__ __forceinline__ void issue_chunk(const TsArgs& a, double* stage, int 
   using S = TsShape<PT>;
   double* s_u = stage;
   double* s_t = stage + kBM * kSU;
+  if (a.u16) {
+    // 16-byte copies: every block starts at an even logical column with an even ld
 #pragma unroll 4
-  for (int e = tid; e < kBM * kBK; e += kThreads) {
-    const int i = e >> 5, j = e & 31;
-    const int m = m0 + i, c = k0 + j;
-    const bool ok = (m < a.M) && (c < w);
-    const double* src = a.u.b[0].p;
-    if (ok) {
-      int bi = 0;
+    for (int e = tid; e < kBM * kBK / 2; e += kThreads) {
+      const int i = e >> 4, j = (e & 15) * 2;
+      const int m = m0 + i, c = k0 + j;
+      const bool ok = (m < a.M) && (c < w);
+      const double* src = a.u.b[0].p;
+      if (ok) {
+        int bi = 0;
 #pragma unroll
-      for (int q = 1; q < kMaxUBlocks; ++q) bi += (c >= off[q]);
-      src = a.u.b[bi].p + (size_t)m * a.u.b[bi].ld + (c - off[bi]);
+        for (int q = 1; q < kMaxUBlocks; ++q) bi += (c >= off[q]);
+        src = a.u.b[bi].p + (size_t)m * a.u.b[bi].ld + (c - off[bi]);
+      }
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(s_u + i * kSU + j);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(ok ? 16 : 0));
     }
-    cp_async8(s_u + i * kSU + j, src, ok);
-  }
+  } else {
 #pragma unroll 4
-  for (int e = tid; e < kBK * S::PMAX; e += kThreads) {
-    const int i = e / S::PMAX, j = e - (e / S::PMAX) * S::PMAX;
+    for (int e = tid; e < kBM * kBK; e += kThreads) {
+      const int i = e >> 5, j = e & 31;
+      const int m = m0 + i, c = k0 + j;
+      const bool ok = (m < a.M) && (c < w);
+      const double* src = a.u.b[0].p;
+      if (ok) {
+        int bi = 0;
+#pragma unroll
+        for (int q = 1; q < kMaxUBlocks; ++q) bi += (c >= off[q]);
+        src = a.u.b[bi].p + (size_t)m * a.u.b[bi].ld + (c - off[bi]);
+      }
+      cp_async8(s_u + i * kSU + j, src, ok);
+    }
+  }
+  // T rows are 16-byte aligned (ldt even): two doubles per copy
+  constexpr int HP = S::PMAX / 2;
+#pragma unroll 4
+  for (int e = tid; e < kBK * HP; e += kThreads) {
+    const int i = e / HP, j2 = e - (e / HP) * HP;
     const int c = k0 + i;
     const bool ok = c < w;
-    cp_async8(s_t + i * S::SX + j, ok ? a.T + (size_t)c * a.ldt + j : a.T, ok);
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(s_t + i * S::SX + 2 * j2);
+    const double* g = ok ? a.T + (size_t)c * a.ldt + 2 * j2 : a.T;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 16 : 0));
   }
 }
 
@@ -196,7 +222,8 @@ ts_kernel(TsArgs a) {
       for (int e = tid; e < kBM * PMAX; e += kThreads) {
         const int i = e / PMAX, j = e - (e / PMAX) * PMAX;
         const int m = m0 + i;
-        if (m < a.M && j < p) a.out[(size_t)m * a.ldo + j] = s_x[i * SX + j];
+        // padded (solver) mode also writes the zero pad column of an odd-width U block
+        if (m < a.M && j < p + (a.u.pad_even ? (p & 1) : 0)) a.out[(size_t)m * a.ldo + j] = s_x[i * SX + j];
       }
     }
     __syncthreads();   // s_x (= stage memory) is overwritten by the next tile's first chunk
@@ -294,8 +321,13 @@ int ts_grid_for(int M, int reserved) {
   return ntiles < g ? (ntiles > 0 ? ntiles : 1) : g;
 }
 
-cudaError_t launch_ts(int mode, const TsArgs& a, int pmax, int grid, cudaStream_t s) {
+cudaError_t launch_ts(int mode, const TsArgs& a0, int pmax, int grid, cudaStream_t s) {
   if (pmax % 8 || pmax < 8 || pmax > 128) return cudaErrorInvalidValue;
+  TsArgs a = a0;
+  bool u16 = a.u.pad_even != 0;
+  for (int bi = 0; bi < a.u.nb; ++bi)
+    u16 = u16 && (a.u.b[bi].ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(a.u.b[bi].p) & 15) == 0);
+  a.u16 = u16 ? 1 : 0;
   return mode == 0 ? Dispatch<0, 16>::launch(a, pmax / 8, grid, s)
                    : Dispatch<1, 16>::launch(a, pmax / 8, grid, s);
 }
