@@ -208,7 +208,6 @@ __global__ void __launch_bounds__(kT) chol1_kernel(State st, SmallBufs b, int pm
   __shared__ double s_tr;
   const int tid = threadIdx.x;
   const int p = *st.p;
-  const int w = *st.w;
   if (p <= 0) return;
   if (tid == 0) {
     double tr = 0.0;
@@ -289,7 +288,6 @@ __global__ void __launch_bounds__(kT) chol2_svd_kernel(State st, SmallBufs b, in
   __shared__ double s_tr;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int p = *st.p;
-  const int w = *st.w;
   if (p <= 0) {
     if (tid == 0) st.rk[rank_slot] = 0;
     for (int e = tid; e < n * cap; e += kT) Vout[(e / cap) * (size_t)ldv + e % cap] = 0.0;

@@ -406,15 +406,15 @@ spmm_kernel(SpmmArgs a, int ust) {
             block_task_mma<MODE>(a, r, ct * 32, s_row0[b] + qo, min(5, g - qo), qo, s_L[b], s_js[b],
                                  s_v + s_vbase[b], s_col + s_cbase[b], lane);
         }
-        continue;
-      }
-      for (int qo = 0; qo < g; qo += GM) {
-        const int gs = min(GM, g - qo);
-        double acc[GM][NACC];
-        zero_acc<MODE, GM>(acc);
-        block_task<MODE, GM>(a, r, c, s_row0[b] + qo, gs, qo, s_L[b], s_js[b], s_v + s_vbase[b],
-                             s_col + s_cbase[b], acc);
-        block_store<MODE, GM>(a, r, c, s_row0[b] + qo, gs, acc);
+      } else {
+        for (int qo = 0; qo < g; qo += GM) {
+          const int gs = min(GM, g - qo);
+          double acc[GM][NACC];
+          zero_acc<MODE, GM>(acc);
+          block_task<MODE, GM>(a, r, c, s_row0[b] + qo, gs, qo, s_L[b], s_js[b], s_v + s_vbase[b],
+                               s_col + s_cbase[b], acc);
+          block_store<MODE, GM>(a, r, c, s_row0[b] + qo, gs, acc);
+        }
       }
     }
   } else {

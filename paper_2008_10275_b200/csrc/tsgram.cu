@@ -33,11 +33,6 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  const int sz = valid ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -62,61 +57,75 @@ struct TsShape {
   static constexpr int PMAX = PT * 8;
   static constexpr int SX = PMAX + 4;                    // T chunk / X tile row stride
   static constexpr int STAGE = kBM * kSU + kBK * SX;     // doubles per pipeline stage
-  static constexpr int SMEM = (2 * STAGE > kBM * SX ? 2 * STAGE : kBM * SX);
+  static constexpr int NSTAGE = 3;
+  static constexpr int SMEM = NSTAGE * STAGE;
+  static constexpr int XH = (kBM / 2) * SX;              // half X tile (64 rows), fits one stage
+  static_assert(XH <= STAGE, "half X tile must fit a stage");
   static constexpr int PT2 = (PT + 1) / 2;               // 2x2 super tiles of the Gram
   static constexpr int NS = PT2 * (PT2 + 1) / 2;
   static constexpr int SPW = (NS + kWarps - 1) / kWarps;  // super tiles per warp
+  static constexpr int HP = PMAX / 2;                    // 16-byte pieces per T row
+};
+
+// Per-thread copy plan of one chunk (tile rows m0.., logical Ucat columns k0..k0+kBK) into a stage.
+//   Ucat, 16-byte mode: thread copies column pair 2*(tid&15) of rows (tid>>4) + 32q, q = 0..3
+//   Ucat,  8-byte mode: thread copies column tid&31 of rows (tid>>5) + 16q, q = 0..7
+//   T: warp wp copies T rows k0+2wp, k0+2wp+1; lane the 16-byte pieces lane, lane+32 (< HP)
+// The copies are issued in 8 parts interleaved with the DMMA steps of the previous chunk, so no
+// warp ever stalls the tensor pipe on a block of address arithmetic.
+struct ChunkPlan {
+  const double* ub;   // Ucat source of this thread's column at row m0 (null: column past w)
+  int ld;
+  int m0, k0;
+  unsigned st;        // stage base (shared address)
 };
 
 template <int PT>
-__device__ __forceinline__ void issue_chunk(const TsArgs& a, double* stage, int m0, int k0, int w,
-                                            const int (&off)[kMaxUBlocks + 1], int tid) {
-  using S = TsShape<PT>;
-  double* s_u = stage;
-  double* s_t = stage + kBM * kSU;
-  if (a.u16) {
-    // 16-byte copies: every block starts at an even logical column with an even ld
-#pragma unroll 4
-    for (int e = tid; e < kBM * kBK / 2; e += kThreads) {
-      const int i = e >> 4, j = (e & 15) * 2;
-      const int m = m0 + i, c = k0 + j;
-      const bool ok = (m < a.M) && (c < w);
-      const double* src = a.u.b[0].p;
-      if (ok) {
-        int bi = 0;
+__device__ __forceinline__ ChunkPlan plan_chunk(const TsArgs& a, unsigned stage, int m0, int k0, int w,
+                                                const int* off, int tid) {
+  ChunkPlan c;
+  c.m0 = m0; c.k0 = k0; c.st = stage;
+  const int col = k0 + (a.u16 ? (tid & 15) * 2 : (tid & 31));
+  c.ub = nullptr; c.ld = 0;
+  if (col < w) {
+    int bi = 0;
 #pragma unroll
-        for (int q = 1; q < kMaxUBlocks; ++q) bi += (c >= off[q]);
-        src = a.u.b[bi].p + (size_t)m * a.u.b[bi].ld + (c - off[bi]);
-      }
-      const unsigned sa = (unsigned)__cvta_generic_to_shared(s_u + i * kSU + j);
+    for (int q = 1; q < kMaxUBlocks; ++q) bi += (col >= off[q]);
+    c.ld = a.u.b[bi].ld;
+    c.ub = a.u.b[bi].p + (size_t)m0 * c.ld + (col - off[bi]);
+  }
+  return c;
+}
+
+template <int PT>
+__device__ __forceinline__ void issue_part(const TsArgs& a, const ChunkPlan& c, int part, int w, int tid) {
+  using S = TsShape<PT>;
+  if (a.u16) {
+    if (part < 4) {
+      const int i = (tid >> 4) + 32 * part, j = (tid & 15) * 2;
+      const bool ok = c.ub != nullptr && (c.m0 + i < a.M);
+      const double* src = ok ? c.ub + (size_t)i * c.ld : a.u.b[0].p;
+      const unsigned sa = c.st + 8u * (i * kSU + j);
       asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(ok ? 16 : 0));
     }
   } else {
-#pragma unroll 4
-    for (int e = tid; e < kBM * kBK; e += kThreads) {
-      const int i = e >> 5, j = e & 31;
-      const int m = m0 + i, c = k0 + j;
-      const bool ok = (m < a.M) && (c < w);
-      const double* src = a.u.b[0].p;
-      if (ok) {
-        int bi = 0;
-#pragma unroll
-        for (int q = 1; q < kMaxUBlocks; ++q) bi += (c >= off[q]);
-        src = a.u.b[bi].p + (size_t)m * a.u.b[bi].ld + (c - off[bi]);
-      }
-      cp_async8(s_u + i * kSU + j, src, ok);
-    }
+    const int i = (tid >> 5) + 16 * part, j = tid & 31;
+    const bool ok = c.ub != nullptr && (c.m0 + i < a.M);
+    const double* src = ok ? c.ub + (size_t)i * c.ld : a.u.b[0].p;
+    const unsigned sa = c.st + 8u * (i * kSU + j);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src), "r"(ok ? 8 : 0));
   }
-  // T rows are 16-byte aligned (ldt even): two doubles per copy
-  constexpr int HP = S::PMAX / 2;
-#pragma unroll 4
-  for (int e = tid; e < kBK * HP; e += kThreads) {
-    const int i = e / HP, j2 = e - (e / HP) * HP;
-    const int c = k0 + i;
-    const bool ok = c < w;
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(s_t + i * S::SX + 2 * j2);
-    const double* g = ok ? a.T + (size_t)c * a.ldt + 2 * j2 : a.T;
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 16 : 0));
+  if (part >= 4) {
+    const int q = part - 4;
+    const int wp = tid >> 5, lane = tid & 31;
+    const int row = 2 * wp + (q >> 1), piece = lane + 32 * (q & 1);
+    if (piece < S::HP) {
+      const int cr = c.k0 + row;
+      const bool ok = cr < w;
+      const double* g = ok ? a.T + (size_t)cr * a.ldt + 2 * piece : a.T;
+      const unsigned sa = c.st + 8u * (kBM * kSU + row * S::SX + 2 * piece);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 16 : 0));
+    }
   }
 }
 
@@ -126,10 +135,17 @@ ts_kernel(TsArgs a) {
   using S = TsShape<PT>;
   constexpr int PMAX = S::PMAX, SX = S::SX;
 
-  int off[kMaxUBlocks + 1];
-  const int w = ucat_offsets(a, off);
+  // block column offsets in shared memory (keeps them out of the register budget)
+  __shared__ int off[kMaxUBlocks + 1];
+  int w;
+  {
+    int o[kMaxUBlocks + 1];
+    w = ucat_offsets(a, o);
+    if (threadIdx.x <= kMaxUBlocks) off[threadIdx.x] = o[threadIdx.x];
+  }
   const int p = a.d_p ? *a.d_p : a.p_fixed;
-  if (w <= 0 || p <= 0) {
+  const int ntiles = (a.M + kBM - 1) / kBM;
+  if (w <= 0 || p <= 0 || (int)blockIdx.x >= ntiles) {
     if (MODE == 0) {   // still publish a zero partial so the reduction is well defined
       double* part = a.partials + (size_t)blockIdx.x * PMAX * PMAX;
       for (int e = threadIdx.x; e < PMAX * PMAX; e += kThreads) part[e] = 0.0;
@@ -138,7 +154,7 @@ ts_kernel(TsArgs a) {
   }
 
   extern __shared__ double sm[];
-  double* s_x = sm;                                      // aliases the two stages after the K loop
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(sm);
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -158,25 +174,50 @@ ts_kernel(TsArgs a) {
   }
 
   const int nk = (w + kBK - 1) / kBK;
-  const int ntiles = (a.M + kBM - 1) / kBM;
+  // Chunks of all this CTA's tiles form one sequence g = 0, 1, ...; chunk g lives in stage g % 3.
+  // Chunk g+1 is in flight while g is computed and g+2 is issued during g's DMMA steps, except that
+  // at most the next tile's chunk 0 is prefetched across a tile boundary: the X tile of the
+  // epilogue is parked (as two 64-row halves) in the two stages that chunk does not use.
+  int g = 0, issued = 0;
+  __syncthreads();   // off[]
+  {
+    const ChunkPlan c0 = plan_chunk<PT>(a, sbase, blockIdx.x * kBM, 0, w, off, tid);
+#pragma unroll
+    for (int part = 0; part < 8; ++part) issue_part<PT>(a, c0, part, w, tid);
+    cp_commit();
+  }
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int m0 = tile * kBM;
+    const bool has_next = tile + (int)gridDim.x < ntiles;
     double x0[PT][2];
 #pragma unroll
     for (int n = 0; n < PT; ++n) x0[n][0] = x0[n][1] = 0.0;
 
-    issue_chunk<PT>(a, sm, m0, 0, w, off, tid);
-    cp_commit();
-    for (int kc = 0; kc < nk; ++kc) {
-      if (kc + 1 < nk) {
-        issue_chunk<PT>(a, sm + ((kc + 1) & 1) * S::STAGE, m0, (kc + 1) * kBK, w, off, tid);
-        cp_commit();
-        cp_wait<1>();
-      } else {
-        cp_wait<0>();
+    for (int kc = 0; kc < nk; ++kc, ++g) {
+      if (issued > g) cp_wait<1>(); else cp_wait<0>();
+      __syncthreads();   // chunk g visible to all; every warp is done with chunk g-1 (and the X tile)
+      if (issued == g) {
+        // (tile start without prefetch) chunk g+1 now, before computing g
+        int nm0 = -1, nk0 = 0;
+        if (kc + 1 < nk) { nm0 = m0; nk0 = (kc + 1) * kBK; }
+        else if (has_next) { nm0 = m0 + gridDim.x * kBM; nk0 = 0; }
+        if (nm0 >= 0) {
+          const ChunkPlan c1 = plan_chunk<PT>(a, sbase + 8u * S::STAGE * ((g + 1) % 3), nm0, nk0, w, off, tid);
+#pragma unroll
+          for (int part = 0; part < 8; ++part) issue_part<PT>(a, c1, part, w, tid);
+          cp_commit();
+          issued = g + 1;
+        }
       }
-      __syncthreads();
-      const double* s_u = sm + (kc & 1) * S::STAGE;
+      // chunk g+2 (this tile's kc+2, or the next tile's chunk 0) is issued during the DMMA steps
+      int pm0 = -1, pk0 = 0;
+      if (issued == g + 1) {
+        if (kc + 2 < nk) { pm0 = m0; pk0 = (kc + 2) * kBK; }
+        else if (kc + 2 == nk && has_next) { pm0 = m0 + gridDim.x * kBM; pk0 = 0; }
+      }
+      ChunkPlan c2;
+      if (pm0 >= 0) c2 = plan_chunk<PT>(a, sbase + 8u * S::STAGE * ((g + 2) % 3), pm0, pk0, w, off, tid);
+      const double* s_u = sm + (g % 3) * S::STAGE;
       const double* s_t = s_u + kBM * kSU;
       const int k0 = kc * kBK;
 #pragma unroll
@@ -189,44 +230,64 @@ ts_kernel(TsArgs a) {
           const double bv = s_t[(kk + tig) * SX + n * 8 + gid];
           dmma884(x0[n], a0, bv);
         }
+        if (pm0 >= 0) issue_part<PT>(a, c2, kk / 4, w, tid);
       }
-      __syncthreads();
+      if (pm0 >= 0) { cp_commit(); issued = g + 2; }
     }
-    // X tile -> smem (stage buffers are idle now)
+    // X tile -> the two stages not holding the next tile's chunk 0 (chunk g, if issued)
+    __syncthreads();   // every warp is done with the last chunk
+    double* xh0 = sm + ((g + 1) % 3) * S::STAGE;   // rows 0..63
+    double* xh1 = sm + ((g + 2) % 3) * S::STAGE;   // rows 64..127
+    {
+      double* xr = (warp < 8 ? xh0 : xh1) + ((warp & 7) * 8 + gid) * SX;
 #pragma unroll
-    for (int n = 0; n < PT; ++n) {
-      const int c = n * 8 + 2 * tig;
-      *reinterpret_cast<double2*>(s_x + (warp * 8 + gid) * SX + c) = make_double2(x0[n][0], x0[n][1]);
+      for (int n = 0; n < PT; ++n)
+        *reinterpret_cast<double2*>(xr + n * 8 + 2 * tig) = make_double2(x0[n][0], x0[n][1]);
     }
     __syncthreads();
     if constexpr (MODE == 0) {
 #pragma unroll 2
       for (int k = 0; k < kBM; k += 4) {
-        const double* xr = s_x + (k + tig) * SX + gid;
+        const double* xr = (k < 64 ? xh0 : xh1) + ((k & 63) + tig) * SX + gid;
 #pragma unroll
         for (int s = 0; s < S::SPW; ++s) {
           if (sI[s] >= 0) {
             const int I0 = 2 * sI[s], J0 = 2 * sJ[s];
+            const bool i1 = I0 + 1 < PT, j1 = J0 + 1 < PT;   // odd PT: the last super row/column is half
             const double a0 = xr[I0 * 8];
-            const double a1 = (I0 + 1 < PT) ? xr[(I0 + 1) * 8] : 0.0;
+            const double a1 = i1 ? xr[(I0 + 1) * 8] : 0.0;
             const double b0 = xr[J0 * 8];
-            const double b1 = (J0 + 1 < PT) ? xr[(J0 + 1) * 8] : 0.0;
+            const double b1 = j1 ? xr[(J0 + 1) * 8] : 0.0;
             dmma884(gacc[s][0], a0, b0);
-            dmma884(gacc[s][1], a0, b1);
-            if (sI[s] != sJ[s]) dmma884(gacc[s][2], a1, b0);
-            dmma884(gacc[s][3], a1, b1);
+            if (j1) dmma884(gacc[s][1], a0, b1);
+            if (i1 && sI[s] != sJ[s]) dmma884(gacc[s][2], a1, b0);
+            if (i1 && j1) dmma884(gacc[s][3], a1, b1);
           }
         }
       }
     } else {
-      for (int e = tid; e < kBM * PMAX; e += kThreads) {
-        const int i = e / PMAX, j = e - (e / PMAX) * PMAX;
-        const int m = m0 + i;
-        // padded (solver) mode also writes the zero pad column of an odd-width U block
-        if (m < a.M && j < p + (a.u.pad_even ? (p & 1) : 0)) a.out[(size_t)m * a.ldo + j] = s_x[i * SX + j];
+      // rows of U_{k+1}: 16-byte stores when the output rows are 16-byte aligned
+      const int pw = p + (a.u.pad_even ? (p & 1) : 0);   // padded (solver) mode also writes the zero pad column
+      if (a.o16) {
+        constexpr int HP = S::HP;
+        for (int e = tid; e < kBM * HP; e += kThreads) {
+          const int i = e / HP, j = 2 * (e - (e / HP) * HP);
+          const int m = m0 + i;
+          const double* xr = (i < 64 ? xh0 : xh1) + (i & 63) * SX + j;
+          if (m < a.M && j < pw) {
+            if (j + 1 < pw) *reinterpret_cast<double2*>(a.out + (size_t)m * a.ldo + j) = *reinterpret_cast<const double2*>(xr);
+            else a.out[(size_t)m * a.ldo + j] = xr[0];
+          }
+        }
+      } else {
+        for (int e = tid; e < kBM * PMAX; e += kThreads) {
+          const int i = e / PMAX, j = e - (e / PMAX) * PMAX;
+          const int m = m0 + i;
+          if (m < a.M && j < pw) a.out[(size_t)m * a.ldo + j] = ((i < 64 ? xh0 : xh1) + (i & 63) * SX)[j];
+        }
       }
     }
-    __syncthreads();   // s_x (= stage memory) is overwritten by the next tile's first chunk
+    // the next tile's first barrier protects the X halves before chunk g+1 overwrites one of them
   }
 
   if constexpr (MODE == 0) {
@@ -328,6 +389,7 @@ cudaError_t launch_ts(int mode, const TsArgs& a0, int pmax, int grid, cudaStream
   for (int bi = 0; bi < a.u.nb; ++bi)
     u16 = u16 && (a.u.b[bi].ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(a.u.b[bi].p) & 15) == 0);
   a.u16 = u16 ? 1 : 0;
+  a.o16 = (mode == 1 && a.out && a.ldo % 2 == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0) ? 1 : 0;
   return mode == 0 ? Dispatch<0, 16>::launch(a, pmax / 8, grid, s)
                    : Dispatch<1, 16>::launch(a, pmax / 8, grid, s);
 }

@@ -38,8 +38,6 @@ def test_two_rank_sharding_and_max_timing(K):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, _free_port() if False else None, K, q))
-             for r in range(0)]
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, K, q)) for r in range(world)]
     for p in procs:

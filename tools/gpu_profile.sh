@@ -1,0 +1,31 @@
+#!/bin/bash
+# One GPU round trip: the GPU test suite, the contract bench, the ncu launch list of the same bench
+# command and one `--set full` capture each of the SpMM and the tall-skinny kernels.
+# Usage (from the repo root, under gpurun):  bash tools/gpu_profile.sh TAG [skip-tests]
+set -u
+TAG=${1:-run}
+OUT=gpurun_out/$TAG
+mkdir -p "$OUT"
+NCU=/usr/local/cuda/bin/ncu
+if [ "${2:-}" != "skip-tests" ]; then
+  timeout 900 python -m pytest tests -m gpu -x -q > "$OUT/pytest_gpu.log" 2>&1
+  echo "pytest_exit=$?"; tail -2 "$OUT/pytest_gpu.log"
+fi
+timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"
+rc=$?
+echo "bench_exit=$rc"; cat "$OUT/bench.json"
+[ $rc -eq 0 ] || exit $rc
+timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none -c 800 --csv \
+  --log-file "$OUT/launches.csv" python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-dense \
+  > "$OUT/ncu_launches.log" 2>&1
+echo "ncu_launches_exit=$?"
+timeout 900 $NCU --set full --clock-control none --import-source on -k regex:spmm_u_kernel -s 3 -c 1 \
+  -o "$OUT/spmm_full" -f python tools/quick_bench.py large 4 > "$OUT/ncu_spmm.log" 2>&1
+echo "ncu_spmm_exit=$?"
+timeout 900 $NCU --set full --clock-control none --import-source on -k regex:ts_kernel -s 6 -c 3 \
+  -o "$OUT/ts_full" -f python tools/quick_bench.py large 4 > "$OUT/ncu_ts.log" 2>&1
+echo "ncu_ts_exit=$?"
+for r in spmm_full ts_full; do
+  [ -f "$OUT/$r.ncu-rep" ] && $NCU -i "$OUT/$r.ncu-rep" --page raw --csv > "$OUT/${r}_raw.csv" 2>/dev/null
+done
+ls -la "$OUT"
