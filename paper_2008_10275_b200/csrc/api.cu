@@ -60,9 +60,9 @@ struct Workspace {
 };
 
 enum ProfClass { P_SPMM = 0, P_VSIDE, P_TS_GRAM, P_REDUCE, P_CHOL1, P_CHOL2, P_TS_STORE, P_TRACE,
-                 P_MISC, P_TINY, P_NCLASS };
+                 P_MISC, P_TINY, P_TS_GRAM2, P_NCLASS };
 const char* const kProfNames[P_NCLASS] = {"spmm", "vside_qr", "ts_gram", "gram_reduce", "chol1",
-                                          "chol2_svd", "ts_store", "trace", "misc", "tiny_gemm"};
+                                          "chol2_svd", "ts_store", "trace", "misc", "tiny_gemm", "ts_gram2"};
 
 struct GraphKey {
   int64_t gen = -1, N = 0; int rb = 0, cap = 0; double gamma = 0, tol = 0; uint32_t flags = 0;
@@ -336,14 +336,14 @@ lrc_status enqueue_truncation(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, co
   ta.d_p = st.p;
   ta.partials = w.partials;
   ta.t_lower = 1;
-  KL((0 == 0 ? P_TS_GRAM : P_TS_STORE), s, launch_ts(0, ta, w.pmax, w.grid, s));
+  KL(P_TS_GRAM, s, launch_ts(0, ta, w.pmax, w.grid, s));
   KL(P_REDUCE, s, launch_gram_reduce(w.partials, w.grid, w.pmax, w.G, s));
   KL(P_CHOL1, s, launch_chol1(st, b, w.pmax, w.wmax, s));
   KL(P_TINY, s, launch_tiny_gemm(w.T1, w.pmax, w.R1i, w.pmax, w.T2, w.pmax, w.pmax, st.w, 0, w.wmax,
                                  st.p, 0, s));
   ta.T = w.T2;
   ta.t_lower = 0;
-  KL((0 == 0 ? P_TS_GRAM : P_TS_STORE), s, launch_ts(0, ta, w.pmax, w.grid, s));
+  KL(P_TS_GRAM2, s, launch_ts(0, ta, w.pmax, w.grid, s));
   KL(P_REDUCE, s, launch_gram_reduce(w.partials, w.grid, w.pmax, w.G, s));
   KL(P_CHOL2, s, launch_chol2_svd(st, b, w.pmax, w.wmax, (int)ctx->n, tol, cap, rank_slot, sigma_row, Vout,
                       ldv_out, s));
@@ -363,7 +363,7 @@ lrc_status enqueue_truncation(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, co
   tb.d_p = st.rk + rank_slot;
   tb.out = Uout;
   tb.ldo = ldu_out;
-  KL((1 == 0 ? P_TS_GRAM : P_TS_STORE), s, launch_ts(1, tb, w.capp, w.grid, s));
+  KL(P_TS_STORE, s, launch_ts(1, tb, w.capp, w.grid, s));
   return LRC_OK;
 }
 
@@ -382,7 +382,7 @@ lrc_status enqueue_norm2(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, int slo
   ta.d_p = st.p;
   ta.partials = w.partials;
   ta.t_lower = 1;
-  KL((0 == 0 ? P_TS_GRAM : P_TS_STORE), s, launch_ts(0, ta, w.pmax, w.grid, s));
+  KL(P_TS_GRAM, s, launch_ts(0, ta, w.pmax, w.grid, s));
   KL(P_REDUCE, s, launch_gram_reduce(w.partials, w.grid, w.pmax, w.G, s));
   KL(P_TRACE, s, launch_trace(st, w.G, w.pmax, slot, s));
   return LRC_OK;

@@ -129,6 +129,63 @@ __device__ __forceinline__ void issue_part(const TsArgs& a, const ChunkPlan& c, 
   }
 }
 
+// One k4 step of a warp's 8-row X slice against n-tiles [0, nact) of the staged T chunk.  nact < PT
+// (lower-trapezoidal T1, zero tail of the last chunk) jumps into a fall-through sequence, so the
+// skipped DMMAs are not issued at all (predicated-off DMMAs still occupy the tensor pipe).
+#define LRC_TS_MMA(n) if constexpr ((n) < PT) dmma884(x0[n], a0, bt[(n) * 8])
+template <int PT>
+__device__ __forceinline__ void mma_row(double (&x0)[PT][2], double a0, const double* bt, int nact) {
+  if (nact >= PT) {
+#pragma unroll
+    for (int n = 0; n < PT; ++n) dmma884(x0[n], a0, bt[n * 8]);
+    return;
+  }
+  switch (nact) {
+    case 15: LRC_TS_MMA(14); [[fallthrough]];
+    case 14: LRC_TS_MMA(13); [[fallthrough]];
+    case 13: LRC_TS_MMA(12); [[fallthrough]];
+    case 12: LRC_TS_MMA(11); [[fallthrough]];
+    case 11: LRC_TS_MMA(10); [[fallthrough]];
+    case 10: LRC_TS_MMA(9); [[fallthrough]];
+    case 9: LRC_TS_MMA(8); [[fallthrough]];
+    case 8: LRC_TS_MMA(7); [[fallthrough]];
+    case 7: LRC_TS_MMA(6); [[fallthrough]];
+    case 6: LRC_TS_MMA(5); [[fallthrough]];
+    case 5: LRC_TS_MMA(4); [[fallthrough]];
+    case 4: LRC_TS_MMA(3); [[fallthrough]];
+    case 3: LRC_TS_MMA(2); [[fallthrough]];
+    case 2: LRC_TS_MMA(1); [[fallthrough]];
+    case 1: LRC_TS_MMA(0); [[fallthrough]];
+    default: break;
+  }
+}
+#undef LRC_TS_MMA
+
+// Gram contribution of the parked 128-row X tile to one 2x2 super tile (I0, J0) of G (8x8 tiles):
+// KIND 0 full, 1 diagonal (the lower tile is skipped), 2 last column of odd PT (J0+1 absent),
+// 3 last diagonal of odd PT (one tile).
+template <int KIND, int SX>
+__device__ __forceinline__ void gram_tile(double (&acc)[4][2], const double* xh0, const double* xh1, int I0,
+                                          int J0, int tig, int gid) {
+#pragma unroll 4
+  for (int k = 0; k < kBM; k += 4) {
+    const double* xr = (k < 64 ? xh0 : xh1) + ((k & 63) + tig) * SX + gid;
+    const double a0 = xr[I0 * 8], b0 = xr[J0 * 8];
+    if constexpr (KIND == 0) {
+      const double a1 = xr[(I0 + 1) * 8], b1 = xr[(J0 + 1) * 8];
+      dmma884(acc[0], a0, b0); dmma884(acc[1], a0, b1); dmma884(acc[2], a1, b0); dmma884(acc[3], a1, b1);
+    } else if constexpr (KIND == 1) {
+      const double a1 = xr[(I0 + 1) * 8], b1 = xr[(J0 + 1) * 8];
+      dmma884(acc[0], a0, b0); dmma884(acc[1], a0, b1); dmma884(acc[3], a1, b1);
+    } else if constexpr (KIND == 2) {
+      const double a1 = xr[(I0 + 1) * 8];
+      dmma884(acc[0], a0, b0); dmma884(acc[2], a1, b0);
+    } else {
+      dmma884(acc[0], a0, b0);
+    }
+  }
+}
+
 template <int PT, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 ts_kernel(TsArgs a) {
@@ -222,14 +279,12 @@ ts_kernel(TsArgs a) {
       const int k0 = kc * kBK;
 #pragma unroll
       for (int kk = 0; kk < kBK; kk += 4) {
+        // active n-tiles: none in the zero-filled tail of the last chunk; for T1 = R_V^T (lower
+        // trapezoidal) the tiles with all i > c are zero
+        int nact = (k0 + kk < w) ? PT : 0;
+        if (a.t_lower) nact = min(nact, (k0 + kk + 3) / 8 + 1);
         const double a0 = s_u[(warp * 8 + gid) * kSU + kk + tig];
-#pragma unroll
-        for (int n = 0; n < PT; ++n) {
-          // T1 = R_V^T is lower trapezoidal: blocks with all i > c are zero (warp-uniform skip)
-          if (a.t_lower && n * 8 > k0 + kk + 3) continue;
-          const double bv = s_t[(kk + tig) * SX + n * 8 + gid];
-          dmma884(x0[n], a0, bv);
-        }
+        mma_row<PT>(x0, a0, s_t + (kk + tig) * SX + gid, nact);
         if (pm0 >= 0) issue_part<PT>(a, c2, kk / 4, w, tid);
       }
       if (pm0 >= 0) { cp_commit(); issued = g + 2; }
@@ -246,24 +301,18 @@ ts_kernel(TsArgs a) {
     }
     __syncthreads();
     if constexpr (MODE == 0) {
-#pragma unroll 2
-      for (int k = 0; k < kBM; k += 4) {
-        const double* xr = (k < 64 ? xh0 : xh1) + ((k & 63) + tig) * SX + gid;
 #pragma unroll
-        for (int s = 0; s < S::SPW; ++s) {
-          if (sI[s] >= 0) {
-            const int I0 = 2 * sI[s], J0 = 2 * sJ[s];
-            const bool i1 = I0 + 1 < PT, j1 = J0 + 1 < PT;   // odd PT: the last super row/column is half
-            const double a0 = xr[I0 * 8];
-            const double a1 = i1 ? xr[(I0 + 1) * 8] : 0.0;
-            const double b0 = xr[J0 * 8];
-            const double b1 = j1 ? xr[(J0 + 1) * 8] : 0.0;
-            dmma884(gacc[s][0], a0, b0);
-            if (j1) dmma884(gacc[s][1], a0, b1);
-            if (i1 && sI[s] != sJ[s]) dmma884(gacc[s][2], a1, b0);
-            if (i1 && j1) dmma884(gacc[s][3], a1, b1);
-          }
-        }
+      for (int s = 0; s < S::SPW; ++s) {
+        if (sI[s] < 0) continue;
+        const int I0 = 2 * sI[s], J0 = 2 * sJ[s];
+        // odd PT: the last super row/column is half; the kind is warp-uniform and fixed, so each
+        // kind runs its own loop (no predicated-off DMMAs)
+        const bool i1 = I0 + 1 < PT, j1 = J0 + 1 < PT;
+        const int kind = (sI[s] == sJ[s]) ? (i1 ? 1 : 3) : (j1 ? 0 : 2);
+        if (kind == 0) gram_tile<0, SX>(gacc[s], xh0, xh1, I0, J0, tig, gid);
+        else if (kind == 1) gram_tile<1, SX>(gacc[s], xh0, xh1, I0, J0, tig, gid);
+        else if (kind == 2) gram_tile<2, SX>(gacc[s], xh0, xh1, I0, J0, tig, gid);
+        else gram_tile<3, SX>(gacc[s], xh0, xh1, I0, J0, tig, gid);
       }
     } else {
       // rows of U_{k+1}: 16-byte stores when the output rows are 16-byte aligned
