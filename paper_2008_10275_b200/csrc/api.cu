@@ -88,6 +88,7 @@ struct lrc_ctx {
   int* group_ptr = nullptr; int ngroups = 0;
   int* tdesc = nullptr; int ntiles = 0;
   int* tlist_u = nullptr; int ntl_u = 0; int* tlist_g = nullptr; int ntl_g = 0;
+  int* tile_ev = nullptr;   // [ntiles][2] (first nnz, nnz count) of each tile (U tiles first)
   size_t meta_bytes = 0;
   double rho = 0, lam = 0;
   // params
@@ -291,6 +292,8 @@ SpmmArgs spmm_base(lrc_ctx* ctx) {
   a.ntiles = ctx->ntiles;
   a.tdesc = ctx->tdesc;
   a.tlist_u = ctx->tlist_u; a.ntl_u = ctx->ntl_u;
+  a.tile_ev = ctx->tile_ev;
+  a.reserved_sms = ctx->reserved_sms;
   a.tlist_g = ctx->tlist_g; a.ntl_g = ctx->ntl_g;
   a.tlist = nullptr;
   a.row_ptr = ctx->row_ptr;
@@ -533,7 +536,7 @@ void lrc_destroy(lrc_ctx* ctx) {
     dfree(ctx->row_ptr); dfree(ctx->col_idx);
     for (int t = 0; t < 6; ++t) dfree(ctx->vals[t]);
   }
-  dfree(ctx->group_ptr); dfree(ctx->tdesc); dfree(ctx->tlist_u); dfree(ctx->tlist_g); dfree(ctx->dmu); dfree(ctx->dnu);
+  dfree(ctx->group_ptr); dfree(ctx->tdesc); dfree(ctx->tlist_u); dfree(ctx->tlist_g); dfree(ctx->tile_ev); dfree(ctx->dmu); dfree(ctx->dnu);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
@@ -711,8 +714,8 @@ lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t*
     for (int t = 0; t < 6; ++t) dfree(ctx->vals[t]);
   }
   dfree(ctx->group_ptr);
-  dfree(ctx->tdesc); dfree(ctx->tlist_u); dfree(ctx->tlist_g);
-  ctx->tlist_u = ctx->tlist_g = nullptr;
+  dfree(ctx->tdesc); dfree(ctx->tlist_u); dfree(ctx->tlist_g); dfree(ctx->tile_ev);
+  ctx->tlist_u = ctx->tlist_g = nullptr; ctx->tile_ev = nullptr;
   ctx->row_ptr = nullptr; ctx->col_idx = nullptr; ctx->group_ptr = nullptr; ctx->tdesc = nullptr;
   for (int t = 0; t < 6; ++t) ctx->vals[t] = nullptr;
   ctx->op_set = false;
@@ -738,9 +741,26 @@ lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t*
   CK(dalloc(&ctx->group_ptr, groups.size()));
   CK(cudaMemcpy(ctx->group_ptr, groups.data(), sizeof(int32_t) * groups.size(), cudaMemcpyHostToDevice));
   ctx->ngroups = (int)groups.size() - 1;
+  ctx->ntiles = (int)(tdesc.size() / kDescInts);
+  {
+    // shared-memory-U tiles first (stable): the hot kernel then indexes tiles by blockIdx.x and
+    // reads the (e0, nnz) pair of its tile from a side array, in parallel with the descriptor
+    std::vector<int32_t> perm;
+    for (int t = 0; t < ctx->ntiles; ++t) if (tdesc[(size_t)t * kDescInts + 3] > 0) perm.push_back(t);
+    for (int t = 0; t < ctx->ntiles; ++t) if (tdesc[(size_t)t * kDescInts + 3] <= 0) perm.push_back(t);
+    std::vector<int32_t> sorted(tdesc.size()), ev(2 * (size_t)ctx->ntiles + 2, 0);
+    for (int i = 0; i < ctx->ntiles; ++i) {
+      std::copy(tdesc.begin() + (size_t)perm[i] * kDescInts, tdesc.begin() + (size_t)(perm[i] + 1) * kDescInts,
+                sorted.begin() + (size_t)i * kDescInts);
+      ev[2 * i] = sorted[(size_t)i * kDescInts + 0];
+      ev[2 * i + 1] = sorted[(size_t)i * kDescInts + 1];
+    }
+    tdesc.swap(sorted);
+    CK(dalloc(&ctx->tile_ev, ev.size()));
+    CK(cudaMemcpy(ctx->tile_ev, ev.data(), sizeof(int32_t) * ev.size(), cudaMemcpyHostToDevice));
+  }
   CK(dalloc(&ctx->tdesc, tdesc.size()));
   CK(cudaMemcpy(ctx->tdesc, tdesc.data(), sizeof(int32_t) * tdesc.size(), cudaMemcpyHostToDevice));
-  ctx->ntiles = (int)(tdesc.size() / kDescInts);
   {
     std::vector<int32_t> lu, lg;
     for (int t = 0; t < ctx->ntiles; ++t) (tdesc[(size_t)t * kDescInts + 3] > 0 ? lu : lg).push_back(t);

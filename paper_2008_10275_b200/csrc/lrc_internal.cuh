@@ -36,8 +36,9 @@ struct SpmmArgs {
   const int* group_ptr;     // [ngroups+1] first row of each node block
   int ntiles;
   const int* tdesc;         // [ntiles][kDescInts] packed tile descriptors (see spmm.cu)
-  const int* tlist_u;       // tiles with shared-memory U rows (nu > 0), for the pipelined hot kernel
+  const int* tlist_u;       // tiles with shared-memory U rows (nu > 0): 0 .. ntl_u-1 (stored first)
   int ntl_u;
+  const int* tile_ev;       // [ntiles][2] first nnz and nnz count of each tile
   const int* tlist_g;       // L2-gather tiles (nu = 0)
   int ntl_g;
   const int* tlist;         // (set by the launcher) tile list, or null for all tiles
@@ -61,6 +62,7 @@ struct SpmmArgs {
   int single_t;             // SINGLE: output c_t A_t U
   const double* dmu;        // DENSE: per-column scalings
   const double* dnu;
+  int reserved_sms;         // persistent hot kernel: SMs left free (concurrent solves)
 };
 cudaError_t launch_spmm(int mode, const SpmmArgs& a, int rmax, cudaStream_t s);
 

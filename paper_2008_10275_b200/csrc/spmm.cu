@@ -185,16 +185,18 @@ __device__ __forceinline__ void cp_async16(double* smem, const double* gmem) {
 // rows of U (r columns, ldu even, 16-byte aligned) -> s_u (row stride ust even) in 16-byte chunks
 __device__ __forceinline__ void stage_u_rows(const SpmmArgs& a, int r, const int* ids, int nu, double* su,
                                              int ust, int tid, int nthreads) {
+  // one warp per U row, lanes over the row (no per-copy integer division)
+  const int lane = tid & 31, wp = tid >> 5, nw = nthreads >> 5;
   if (a.u_aligned16) {
     const int nch = (r + 1) >> 1;   // an odd r copies one element of padding (r + 1 <= ldu)
-    for (int e = tid; e < nu * nch; e += nthreads) {
-      const int u = e / nch, ch = e - (e / nch) * nch;
-      cp_async16(su + u * ust + 2 * ch, a.U + (size_t)ids[u] * a.ldu + 2 * ch);
+    for (int u = wp; u < nu; u += nw) {
+      const double* src = a.U + (size_t)ids[u] * a.ldu;
+      for (int ch = lane; ch < nch; ch += 32) cp_async16(su + u * ust + 2 * ch, src + 2 * ch);
     }
   } else {
-    for (int e = tid; e < nu * r; e += nthreads) {
-      const int u = e / r, c = e - (e / r) * r;
-      cp_async8(su + u * ust + c, a.U + (size_t)ids[u] * a.ldu + c);
+    for (int u = wp; u < nu; u += nw) {
+      const double* src = a.U + (size_t)ids[u] * a.ldu;
+      for (int c = lane; c < r; c += 32) cp_async8(su + u * ust + c, src + c);
     }
   }
 }
@@ -256,6 +258,80 @@ __device__ __forceinline__ void block_task_mma_smem(const SpmmArgs& a, int r, in
             __stcs(orow + c, 0.0);        // zero pad column of the (even-padded) Ucat block
           }
         }
+      }
+    }
+  }
+}
+
+// block_task_mma_smem without per-step predicates (spmm_u_kernel): the staged values are
+// zero-filled up to the next multiple of 4 column-list entries, the local U row index is clamped,
+// and out-of-range slots / U columns only feed accumulator entries that are never stored.
+template <int MODE>
+__device__ __forceinline__ void block_task_mma_fast(const SpmmArgs& a, int r, int n0, int row0, int gs,
+                                                    int qo, int L, int lp, const double* vals,
+                                                    const unsigned short* lcols, const double* s_u, int ust,
+                                                    int lrow0, int lane) {
+  const int gid = lane >> 2, tig = lane & 3;
+  const int nrow = gs * 3;
+  double acc[2][2][4];   // [m tile (16 cols)][n tile (8 slots)][frag]
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.0;
+  const int L4 = (a.dbg & 1) ? 0 : ((L + 3) & ~3);
+  const double* vb = vals + (qo * 3 + gid) * lp + tig;
+  const double* ub = s_u + n0 + gid;
+  const unsigned short* lc = lcols + tig;
+  const int lmax = L - 1 - tig;
+#pragma unroll 2
+  for (int k0 = 0; k0 < L4; k0 += 4) {
+    const double b0 = vb[k0], b1 = vb[8 * lp + k0];
+    const double* urow = ub + (int)lc[min(k0, lmax)] * ust;
+    const double a00 = urow[0], a01 = urow[8], a10 = urow[16], a11 = urow[24];
+    dmma1684(acc[0][0], a00, a01, b0);
+    dmma1684(acc[0][1], a00, a01, b1);
+    dmma1684(acc[1][0], a10, a11, b0);
+    dmma1684(acc[1][1], a10, a11, b1);
+  }
+  // epilogue: frag (m, n) -> column n0 + mt*16 + m, slot R = nt*8 + n = q*3 + stream.  A lane's
+  // four values of one slot sit in one output row at columns n0 + gid + {0, 8, 16, 24}; the S2
+  // update out0 = U - gamma W0 is applied branch-free (alpha, beta) from the staged U row.
+  const long long sst = a.out_sstride ? a.out_sstride : r;
+  const bool full = n0 + 32 <= r;
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int R = nt * 8 + 2 * tig + e;
+      if (R >= nrow) continue;
+      const int q = R / 3, st = R - q * 3;
+      double* orow = a.out + st * sst + (size_t)(row0 + q) * a.ldo + a.out_off + n0 + gid;
+      const bool s2 = (MODE == SPMM_S2STEP) && st == 0;
+      const double alpha = s2 ? -a.gamma : 1.0, beta = s2 ? 1.0 : 0.0;
+      const double* us = s_u + (MODE == SPMM_S2STEP ? (lrow0 + qo + q) * ust : 0) + n0 + gid;
+      if (a.dbg & 8) continue;
+      if (full) {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int hm = 0; hm < 2; ++hm) {
+            const int o = mt * 16 + hm * 8;
+            const double u = (MODE == SPMM_S2STEP) ? us[o] : 0.0;
+            __stcs(orow + o, fma(alpha, acc[mt][nt][hm * 2 + e], beta * u));
+          }
+      } else {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int hm = 0; hm < 2; ++hm) {
+            const int o = mt * 16 + hm * 8, c = n0 + gid + o;
+            if (c < r) {
+              const double u = (MODE == SPMM_S2STEP) ? us[o] : 0.0;
+              __stcs(orow + o, fma(alpha, acc[mt][nt][hm * 2 + e], beta * u));
+            } else if (c == r && (r & 1) && a.out_sstride) {
+              __stcs(orow + o, 0.0);        // zero pad column of the (even-padded) Ucat block
+            }
+          }
       }
     }
   }
@@ -455,26 +531,18 @@ spmm_u_kernel(SpmmArgs a, int ust) {
   extern __shared__ double smem_dyn[];
   double* s_v = smem_dyn;                        // [kValCap]
   double* s_u = smem_dyn + kValCap;              // [kUCap][ust]
-  __shared__ int s_desc[kDescInts];
+  __shared__ __align__(16) int s_desc[kDescInts];
   __shared__ int s_bstart[kTileBlocks + 1], s_vbase[kTileBlocks], s_lp[kTileBlocks];
+  __shared__ float s_invL[kTileBlocks];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int CT = (r + 31) >> 5;
-  const int t = a.tlist_u[blockIdx.x];
-  for (int i = tid; i < kDescInts; i += kThreads) s_desc[i] = __ldg(a.tdesc + (size_t)t * kDescInts + i);
-  __syncthreads();
-  const int e0 = s_desc[0], tot = s_desc[1], nb = s_desc[2], nu = s_desc[3];
-  if (!(a.dbg & 2)) stage_u_rows(a, r, s_desc + kDescUrows, nu, s_u, ust, tid, kThreads);
-  asm volatile("cp.async.commit_group;\n" ::);
-  if (tid == 0) {
-    int vb = 0, eb = 0;
-    for (int b = 0; b < nb; ++b) {
-      const int g = s_desc[12 + b], L = s_desc[16 + b];
-      s_bstart[b] = eb; s_lp[b] = row_pitch(L); s_vbase[b] = vb;
-      vb += g * 3 * s_lp[b];
-      eb += g * L;
-    }
-    s_bstart[nb] = tot;
-  }
+  // U tiles are stored first (tile = blockIdx.x); the value loads need only (e0, tot), fetched in
+  // parallel with the descriptor, so they are issued before the descriptor arrives
+  const int t = blockIdx.x;
+  const int2 et = __ldg(reinterpret_cast<const int2*>(a.tile_ev) + t);
+  const int e0 = et.x, tot = et.y;
+  if (tid < kDescInts / 4)
+    *reinterpret_cast<int4*>(s_desc + 4 * tid) = __ldg(reinterpret_cast<const int4*>(a.tdesc + (size_t)t * kDescInts) + tid);
   constexpr int kStg = (kSpmmCap + kThreads - 1) / kThreads;
   double raw[kStg][6];
 #pragma unroll
@@ -488,6 +556,20 @@ spmm_u_kernel(SpmmArgs a, int ust) {
       for (int v = 0; v < 6; ++v) raw[k][v] = 0.0;
     }
   }
+  __syncthreads();
+  const int nb = s_desc[2], nu = s_desc[3];
+  if (!(a.dbg & 2)) stage_u_rows(a, r, s_desc + kDescUrows, nu, s_u, ust, tid, kThreads);
+  asm volatile("cp.async.commit_group;\n" ::);
+  if (tid == 0) {
+    int vb = 0, eb = 0;
+    for (int b = 0; b < nb; ++b) {
+      const int g = s_desc[12 + b], L = s_desc[16 + b];
+      s_bstart[b] = eb; s_lp[b] = row_pitch(L); s_vbase[b] = vb; s_invL[b] = 1.0f / (float)L;
+      vb += g * 3 * s_lp[b];
+      eb += g * L;
+    }
+    s_bstart[nb] = tot;
+  }
   __syncthreads();                               // block table
 #pragma unroll
   for (int k = 0; k < kStg; ++k) {
@@ -498,12 +580,22 @@ spmm_u_kernel(SpmmArgs a, int ust) {
       for (int kk = 1; kk < kTileBlocks; ++kk) b += (kk < nb && e >= s_bstart[kk]);
       const int L = s_desc[16 + b];
       const int rel = e - s_bstart[b];
-      const int q = rel / L, j = rel - (rel / L) * L;
+      // q = rel / L exactly: (rel + 1/2) / L is >= 1/(2L) away from an integer, far above the
+      // float rounding error for rel, L <= 1024
+      const int q = __float2int_rz(((float)rel + 0.5f) * s_invL[b]), j = rel - q * L;
       const int lp = s_lp[b];
       double* dst = s_v + s_vbase[b] + q * 3 * lp + j;
       dst[0] = fma(a.lam, raw[k][5], fma(a.rho, raw[k][3], raw[k][0]));   // A0 + rho Jrho + lam Jlam
       dst[lp] = raw[k][1] + raw[k][4];                                   // A1 + Jmu
       dst[2 * lp] = a.rho * raw[k][2];                                    // rho A2
+    }
+  }
+  // zero the staged entries L .. round4(L)-1 of every slot (the contraction runs in steps of 4)
+  for (int b = 0; b < nb; ++b) {
+    const int g = s_desc[12 + b], L = s_desc[16 + b], lp = s_lp[b];
+    for (int i = tid; i < g * 3 * 4; i += kThreads) {
+      const int j = L + (i & 3);
+      if (j < ((L + 3) & ~3)) s_v[s_vbase[b] + (i >> 2) * lp + j] = 0.0;
     }
   }
   asm volatile("cp.async.wait_all;\n" ::);
@@ -514,33 +606,194 @@ spmm_u_kernel(SpmmArgs a, int ust) {
     const int g = s_desc[12 + b], L = s_desc[16 + b];
     for (int ct = 0; ct < CT; ++ct, ++task0) {
       if ((task0 % kWarps) != warp) continue;
-      for (int qo = 0; qo < g; qo += 5)
-        block_task_mma_smem<MODE>(a, r, ct * 32, s_desc[8 + b] + qo, min(5, g - qo), qo, L, s_lp[b],
-                                  s_v + s_vbase[b], lx + cb, s_u, ust, s_desc[20 + b], lane);
+      const int lrow0 = s_desc[20 + b];
+      for (int qo = 0; qo < g; qo += 5) {
+        if (MODE == SPMM_S2STEP && lrow0 < 0)   // the block's own U rows are not staged (no diagonal)
+          block_task_mma_smem<MODE>(a, r, ct * 32, s_desc[8 + b] + qo, min(5, g - qo), qo, L, s_lp[b],
+                                    s_v + s_vbase[b], lx + cb, s_u, ust, lrow0, lane);
+        else
+          block_task_mma_fast<MODE>(a, r, ct * 32, s_desc[8 + b] + qo, min(5, g - qo), qo, L, s_lp[b],
+                                    s_v + s_vbase[b], lx + cb, s_u, ust, lrow0, lane);
+      }
     }
     cb += L;
   }
 }
 
+// Config-5 dense application Y = sum_t c_t A_t S diag(e_t) (S dense M x ncols, ncols <= 256) on the
+// fp64 tensor pipe, shared-memory-U tiles.  Per tile the six value streams are combined once into
+// the three grouped streams; S is then processed in 64-column chunks: the chunk of the tile's
+// deduplicated S rows is staged (16-byte cp.async), every warp contracts one (node block, 32-column
+// half) exactly like the hot kernel (transposed m16n8k4, D = S_chunk^T Vals^T), parks its D tile in
+// its own shared-memory slab and writes Y[row][c] = D[c][3q] + d_mu[c] D[c][3q+1] + d_nu[c] D[c][3q+2]
+// with coalesced row stores.
+constexpr int kDenseChunk = 64;
+constexpr int kDenseUst = kDenseChunk + 4;          // == 4 mod 16 doubles
+constexpr int kDenseDst = 17;                       // per-warp D slab row stride (odd: conflict free)
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 2)
+spmm_dense_kernel(SpmmArgs a) {
+  const int ncols = a.r_fixed;
+  extern __shared__ __align__(16) double smem_dyn[];
+  double* s_v = smem_dyn;                                     // [kValCap]
+  double* s_u = s_v + kValCap;                                // [kUCap][kDenseUst] (+32 slack)
+  double* s_d = s_u + kUCap * kDenseUst + 32;                 // [8 warps][32][kDenseDst]
+  __shared__ __align__(16) int s_desc[kDescInts];
+  __shared__ int s_bstart[kTileBlocks + 1], s_vbase[kTileBlocks], s_lp[kTileBlocks];
+  __shared__ float s_invL[kTileBlocks];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int t = blockIdx.x;
+  const int2 et = __ldg(reinterpret_cast<const int2*>(a.tile_ev) + t);
+  const int e0 = et.x, tot = et.y;
+  if (tid < kDescInts / 4)
+    *reinterpret_cast<int4*>(s_desc + 4 * tid) = __ldg(reinterpret_cast<const int4*>(a.tdesc + (size_t)t * kDescInts) + tid);
+  constexpr int kStg = (kSpmmCap + kThreads - 1) / kThreads;
+  double raw[kStg][6];
+#pragma unroll
+  for (int k = 0; k < kStg; ++k) {
+    const int e = tid + k * kThreads;
+    if (e < tot) {
+#pragma unroll
+      for (int v = 0; v < 6; ++v) raw[k][v] = __ldcs(a.v[v] + e0 + e);
+    } else {
+#pragma unroll
+      for (int v = 0; v < 6; ++v) raw[k][v] = 0.0;
+    }
+  }
+  __syncthreads();
+  const int nb = s_desc[2], nu = s_desc[3];
+  if (tid == 0) {
+    int vb = 0, eb = 0;
+    for (int b = 0; b < nb; ++b) {
+      const int g = s_desc[12 + b], L = s_desc[16 + b];
+      s_bstart[b] = eb; s_lp[b] = row_pitch(L); s_vbase[b] = vb; s_invL[b] = 1.0f / (float)L;
+      vb += g * 3 * s_lp[b];
+      eb += g * L;
+    }
+    s_bstart[nb] = tot;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kStg; ++k) {
+    const int e = tid + k * kThreads;
+    if (e < tot) {
+      int b = 0;
+#pragma unroll
+      for (int kk = 1; kk < kTileBlocks; ++kk) b += (kk < nb && e >= s_bstart[kk]);
+      const int L = s_desc[16 + b];
+      const int rel = e - s_bstart[b];
+      const int q = __float2int_rz(((float)rel + 0.5f) * s_invL[b]), j = rel - q * L;
+      const int lp = s_lp[b];
+      double* dst = s_v + s_vbase[b] + q * 3 * lp + j;
+      dst[0] = fma(a.lam, raw[k][5], fma(a.rho, raw[k][3], raw[k][0]));   // A0 + rho Jrho + lam Jlam
+      dst[lp] = raw[k][1] + raw[k][4];                                   // A1 + Jmu
+      dst[2 * lp] = a.rho * raw[k][2];                                    // rho A2
+    }
+  }
+  for (int b = 0; b < nb; ++b) {
+    const int g = s_desc[12 + b], L = s_desc[16 + b], lp = s_lp[b];
+    for (int i = tid; i < g * 3 * 4; i += kThreads) {
+      const int j = L + (i & 3);
+      if (j < ((L + 3) & ~3)) s_v[s_vbase[b] + (i >> 2) * lp + j] = 0.0;
+    }
+  }
+  const unsigned short* lx = reinterpret_cast<const unsigned short*>(s_desc + kDescLidx);
+  double* slab = s_d + warp * 32 * kDenseDst;
+  for (int c0 = 0; c0 < ncols; c0 += kDenseChunk) {
+    const int cw = min(kDenseChunk, ncols - c0);
+    __syncthreads();   // previous chunk fully consumed (and the staged values visible)
+    if (a.u_aligned16) {
+      const int nch = (cw + 1) >> 1;
+      for (int u = warp; u < nu; u += kWarps) {
+        const double* src = a.U + (size_t)s_desc[kDescUrows + u] * a.ldu + c0;
+        for (int ch = lane; ch < nch; ch += 32) cp_async16(s_u + u * kDenseUst + 2 * ch, src + 2 * ch);
+      }
+    } else {
+      for (int u = warp; u < nu; u += kWarps) {
+        const double* src = a.U + (size_t)s_desc[kDescUrows + u] * a.ldu + c0;
+        for (int c = lane; c < cw; c += 32) cp_async8(s_u + u * kDenseUst + c, src + c);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncthreads();
+    const int CT = (cw + 31) >> 5;
+    int cb = 0, bprev = 0;
+    for (int task = warp; task < nb * CT; task += kWarps) {
+      const int b = task / CT, ct = task - (task / CT) * CT;
+      for (; bprev < b; ++bprev) cb += s_desc[16 + bprev];
+      const int g = s_desc[12 + b], L = s_desc[16 + b], lp = s_lp[b];
+      const int n0 = ct * 32;
+      const double dm_lo = 0.0;
+      (void)dm_lo;
+      for (int qo = 0; qo < g; qo += 5) {
+        const int gs = min(5, g - qo);
+        double acc[2][2][4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.0;
+        const int L4 = (L + 3) & ~3;
+        const double* vb = s_v + s_vbase[b] + (qo * 3 + gid) * lp + tig;
+        const double* ub = s_u + n0 + gid;
+        const unsigned short* lc = lx + cb + tig;
+        const int lmax = L - 1 - tig;
+#pragma unroll 2
+        for (int k0 = 0; k0 < L4; k0 += 4) {
+          const double b0 = vb[k0], b1 = vb[8 * lp + k0];
+          const double* urow = ub + (int)lc[min(k0, lmax)] * kDenseUst;
+          const double a00 = urow[0], a01 = urow[8], a10 = urow[16], a11 = urow[24];
+          dmma1684(acc[0][0], a00, a01, b0);
+          dmma1684(acc[0][1], a00, a01, b1);
+          dmma1684(acc[1][0], a10, a11, b0);
+          dmma1684(acc[1][1], a10, a11, b1);
+        }
+        // D[col m][slot n] -> slab[m][n]
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int hm = 0; hm < 2; ++hm) {
+              const int m = mt * 16 + gid + hm * 8;
+              slab[m * kDenseDst + nt * 8 + 2 * tig] = acc[mt][nt][hm * 2];
+              slab[m * kDenseDst + nt * 8 + 2 * tig + 1] = acc[mt][nt][hm * 2 + 1];
+            }
+        __syncwarp();
+        const int c = c0 + n0 + lane;
+        if (n0 + lane < cw) {
+          const double dm = __ldg(a.dmu + c), dn = __ldg(a.dnu + c);
+          const double* sr = slab + lane * kDenseDst;
+          for (int q = 0; q < gs; ++q) {
+            const double y = fma(dn, sr[3 * q + 2], fma(dm, sr[3 * q + 1], sr[3 * q]));
+            __stcs(a.out + (size_t)(s_desc[8 + b] + qo + q) * a.ldo + a.out_off + c, y);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------------------------
-// Persistent warp-specialised TMA kernel (S2STEP / PLAIN3, shared-memory-U tiles).  One CTA per SM:
-// warp 8 is the producer -- per tile it copies the 1 KB descriptor, then one elected lane issues
-// cp.async.bulk copies of the six contiguous value segments and of the tile's deduplicated U rows
-// into a double-buffered stage, completing on the stage's `full` mbarrier (expect-tx bytes).  Warps
-// 0-7 consume: combine the six raw streams into the conflict-free [slot][j] layout, contract on
-// the fp64 tensor pipe, store, and release the stage through its `empty` mbarrier.  Tile k+1 is in
-// flight while tile k is combined and contracted.
+// Persistent warp-specialised kernel (S2STEP / PLAIN3, shared-memory-U tiles), one CTA per SM.
+// Warps 8-11 produce: per tile they fetch the (e0, nnz) pair and issue all six value streams into
+// registers at once, copy the descriptor and the tile's deduplicated U rows (16-byte cp.async) into
+// a double-buffered stage, combine the six streams into the three grouped [slot][j] streams and
+// publish the stage on its `full` mbarrier.  Warps 0-7 consume: contract on the fp64 tensor pipe
+// (block_task_mma_fast), store, and release the stage on its `empty` mbarrier.  Tile k+1 is loaded
+// and combined while tile k is contracted, so the HBM stream and the DMMA work overlap.
 // ---------------------------------------------------------------------------------------------
-constexpr int kTmaStages = 2;
-constexpr int kRawCap = kSpmmCap + 2;              // doubles per staged raw value array (alignment slack)
-constexpr int kTmaThreads = 288;                   // 8 consumer warps + 1 producer warp
+constexpr int kWsStages = 2;
+constexpr int kWsConsumers = 256;                  // 8 warps
+constexpr int kWsProducers = 128;                  // 4 warps
+constexpr int kWsThreads = kWsConsumers + kWsProducers;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
@@ -554,127 +807,158 @@ __device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity)
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
   while (!mbar_try(b, parity)) {}
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
 
-size_t tma_stage_doubles(int ust) { return (size_t)kDescInts / 2 + 6 * (size_t)kRawCap + (size_t)kUCap * ust; }
+
+// doubles per stage: descriptor (1 KB) + grouped values + U rows (+ slack of the predicate-free
+// contraction), rounded to a multiple of 2 (16-byte alignment)
+size_t ws_stage_doubles(int ust, int slack) {
+  return (((size_t)kDescInts / 2 + kValCap + (size_t)kUCap * ust + slack) + 1) & ~(size_t)1;
+}
 
 template <int MODE>
-__global__ void __launch_bounds__(kTmaThreads, 1)
-spmm_tma_kernel(SpmmArgs a, int ust) {
+__global__ void __launch_bounds__(kWsThreads, 1)
+spmm_ws_kernel(SpmmArgs a, int ust, int stage_d) {
   const int r = a.d_r ? *a.d_r : a.r_fixed;
   if (r <= 0) return;
-  extern __shared__ __align__(128) double smem_dyn[];
-  const int stage_d = kDescInts / 2 + 6 * kRawCap + kUCap * ust;
-  double* s_v = smem_dyn + kTmaStages * stage_d;
-  __shared__ __align__(8) unsigned long long full[kTmaStages], empty[kTmaStages];
-  __shared__ int s_bstart[kTileBlocks + 1], s_vbase[kTileBlocks], s_lp[kTileBlocks];
+  extern __shared__ __align__(16) double smem_dyn[];
+  __shared__ __align__(8) unsigned long long full[kWsStages], empty[kWsStages];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
-    // full: 1 expect-tx arrival (elected lane) + 32 cp.async arrivals (producer lanes)
-    for (int i = 0; i < kTmaStages; ++i) { mbar_init(&full[i], 33); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < kWsStages; ++i) { mbar_init(&full[i], kWsProducers); mbar_init(&empty[i], kWsConsumers / 32); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  const int G = gridDim.x;
-  const int ntl = a.ntl_u;
+  const int G = gridDim.x, ntl = a.ntl_u;
+  const int CT = (r + 31) >> 5;
 
-  if (warp == 8) {
-    // ------------------------------------------------------------------ producer
+  if (tid >= kWsConsumers) {
+    // ------------------------------------------------------------------------------ producers
+    const int p = tid - kWsConsumers, pw = p >> 5;
+    constexpr int kStg = (kSpmmCap + kWsProducers - 1) / kWsProducers;   // 8 entries per thread
     for (int k = 0;; ++k) {
       const int idx = blockIdx.x + k * G;
       if (idx >= ntl) break;
-      const int st = k % kTmaStages;
-      if (k >= kTmaStages) mbar_wait(&empty[st], ((k / kTmaStages) - 1) & 1);
-      double* stage = smem_dyn + st * stage_d;
+      const int st = k % kWsStages;
+      const int2 et = __ldg(reinterpret_cast<const int2*>(a.tile_ev) + idx);
+      const int e0 = et.x, tot = et.y;
+      double raw[kStg][6];
+#pragma unroll
+      for (int i = 0; i < kStg; ++i) {
+        const int e = p + i * kWsProducers;
+        if (e < tot && !(a.dbg & 4)) {
+#pragma unroll
+          for (int v = 0; v < 6; ++v) raw[i][v] = __ldcs(a.v[v] + e0 + e);
+        } else {
+#pragma unroll
+          for (int v = 0; v < 6; ++v) raw[i][v] = 0.0;
+        }
+      }
+      int4 dq = make_int4(0, 0, 0, 0);
+      if (p < kDescInts / 4) dq = __ldg(reinterpret_cast<const int4*>(a.tdesc + (size_t)idx * kDescInts) + p);
+      if (k >= kWsStages) mbar_wait(&empty[st], ((k / kWsStages) - 1) & 1);
+      double* stage = smem_dyn + (size_t)st * stage_d;
       int* d = reinterpret_cast<int*>(stage);
-      const int t = __ldg(a.tlist_u + idx);
-      for (int i = lane; i < kDescInts; i += 32) d[i] = __ldg(a.tdesc + (size_t)t * kDescInts + i);
-      __syncwarp();
-      const int e0 = d[0], tot = d[1], nu = d[3];
-      const int e0a = e0 & ~1, end = e0 + tot, enda = end & ~1;
-      double* raw = stage + kDescInts / 2;
-      double* su = raw + 6 * kRawCap;
-      if (lane == 0) {
-        const unsigned vbytes = (unsigned)(enda - e0a) * 8u;
-        if (end & 1)      // odd tail element: plain load (never read past the array end)
-          for (int v = 0; v < 6; ++v) raw[v * kRawCap + (end - 1 - e0a)] = __ldg(a.v[v] + end - 1);
-        mbar_expect_tx(&full[st], 6u * vbytes);
-        if (vbytes)
-          for (int v = 0; v < 6; ++v) bulk_g2s(raw + v * kRawCap, a.v[v] + e0a, vbytes, &full[st]);
+      double* s_v = stage + kDescInts / 2;
+      double* s_u = s_v + kValCap;
+      if (p < kDescInts / 4) *reinterpret_cast<int4*>(d + 4 * p) = dq;
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");          // producers: descriptor visible
+      const int nb = d[2], nu = d[3];
+      // U rows: one warp per row, lanes over 16-byte chunks
+      if (!(a.dbg & 2)) {
+        const int nch = (r + 1) >> 1;
+        for (int u = pw; u < nu; u += kWsProducers / 32) {
+          const double* src = a.U + (size_t)d[kDescUrows + u] * a.ldu;
+          for (int ch = lane; ch < nch; ch += 32) cp_async16(s_u + u * ust + 2 * ch, src + 2 * ch);
+        }
       }
-      // U rows: 16-byte cp.async by all producer lanes, tracked by the same mbarrier
-      const int nch = (r + 1) >> 1;
-      for (int e = lane; e < nu * nch; e += 32) {
-        const int u = e / nch, ch = e - (e / nch) * nch;
-        cp_async16(su + u * ust + 2 * ch, a.U + (size_t)d[kDescUrows + u] * a.ldu + 2 * ch);
+      // block table (registers)
+      int bst[kTileBlocks + 1], vbs[kTileBlocks], lps[kTileBlocks], Ls[kTileBlocks];
+      {
+        int vb = 0, eb = 0;
+#pragma unroll
+        for (int b = 0; b < kTileBlocks; ++b) {
+          const int g = b < nb ? d[12 + b] : 0, L = b < nb ? d[16 + b] : 1;
+          bst[b] = eb; vbs[b] = vb; Ls[b] = L; lps[b] = row_pitch(L);
+          vb += g * 3 * lps[b];
+          eb += g * L;
+        }
+        bst[kTileBlocks] = 0x7fffffff;
       }
-      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[st])) : "memory");
-      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < kStg; ++i) {
+        const int e = p + i * kWsProducers;
+        if (e < tot) {
+          int eb = bst[0], vb = vbs[0], L = Ls[0], lp = lps[0];
+#pragma unroll
+          for (int b = 1; b < kTileBlocks; ++b)
+            if (b < nb && e >= bst[b]) { eb = bst[b]; vb = vbs[b]; L = Ls[b]; lp = lps[b]; }
+          const int rel = e - eb;
+          // q = rel / L exactly (see spmm_u_kernel)
+          const int q = __float2int_rz(((float)rel + 0.5f) / (float)L), j = rel - q * L;
+          double* dst = s_v + vb + q * 3 * lp + j;
+          dst[0] = fma(a.lam, raw[i][5], fma(a.rho, raw[i][3], raw[i][0]));   // A0 + rho Jrho + lam Jlam
+          dst[lp] = raw[i][1] + raw[i][4];                                   // A1 + Jmu
+          dst[2 * lp] = a.rho * raw[i][2];                                    // rho A2
+        }
+      }
+      // zero the staged entries L .. round4(L)-1 of every slot
+#pragma unroll
+      for (int b = 0; b < kTileBlocks; ++b) {
+        if (b < nb) {
+          const int g = d[12 + b], L = Ls[b];
+          for (int i = p; i < g * 3 * 4; i += kWsProducers) {
+            const int j = L + (i & 3);
+            if (j < ((L + 3) & ~3)) s_v[vbs[b] + (i >> 2) * lps[b] + j] = 0.0;
+          }
+        }
+      }
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      mbar_arrive(&full[st]);
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");          // descriptor reads done before reuse
     }
     return;
   }
 
-  // -------------------------------------------------------------------- consumers (warps 0-7)
-  const int CT = (r + 31) >> 5;
+  // ---------------------------------------------------------------------------------- consumers
   for (int k = 0;; ++k) {
     const int idx = blockIdx.x + k * G;
     if (idx >= ntl) break;
-    const int st = k % kTmaStages;
-    mbar_wait(&full[st], (k / kTmaStages) & 1);
-    const double* stage = smem_dyn + st * stage_d;
+    const int st = k % kWsStages;
+    mbar_wait(&full[st], (k / kWsStages) & 1);
+    const double* stage = smem_dyn + (size_t)st * stage_d;
     const int* d = reinterpret_cast<const int*>(stage);
-    const double* raw = stage + kDescInts / 2;
-    const double* su = raw + 6 * kRawCap;
-    const int e0 = d[0], tot = d[1], nb = d[2];
-    const int off = e0 - (e0 & ~1);
-    if (tid == 0) {
-      int vb = 0, eb = 0;
-      for (int b = 0; b < nb; ++b) {
-        const int g = d[12 + b], L = d[16 + b];
-        s_bstart[b] = eb; s_lp[b] = row_pitch(L); s_vbase[b] = vb;
-        vb += g * 3 * s_lp[b];
-        eb += g * L;
-      }
-      s_bstart[nb] = tot;
-    }
-    consumer_sync();
-    for (int e = tid; e < tot; e += 256) {
-      int b = 0;
-#pragma unroll
-      for (int kk = 1; kk < kTileBlocks; ++kk) b += (kk < nb && e >= s_bstart[kk]);
-      const int L = d[16 + b];
-      const int rel = e - s_bstart[b];
-      const int q = rel / L, j = rel - (rel / L) * L;
-      const int lp = s_lp[b];
-      const double* rv = raw + off + e;
-      double* dst = s_v + s_vbase[b] + q * 3 * lp + j;
-      dst[0] = fma(a.lam, rv[5 * kRawCap], fma(a.rho, rv[3 * kRawCap], rv[0]));   // A0 + rho Jrho + lam Jlam
-      dst[lp] = rv[1 * kRawCap] + rv[4 * kRawCap];                               // A1 + Jmu
-      dst[2 * lp] = a.rho * rv[2 * kRawCap];                                      // rho A2
-    }
-    consumer_sync();
+    const double* s_v = stage + kDescInts / 2;
+    const double* s_u = s_v + kValCap;
+    const int nb = d[2];
     const unsigned short* lx = reinterpret_cast<const unsigned short*>(d + kDescLidx);
-    int cb = 0;
-    for (int b = 0, task0 = 0; b < nb; ++b) {
-      const int g = d[12 + b], L = d[16 + b];
-      for (int ct = 0; ct < CT; ++ct, ++task0) {
-        if ((task0 & 7) != warp) continue;
-        for (int qo = 0; qo < g; qo += 5)
-          block_task_mma_smem<MODE>(a, r, ct * 32, d[8 + b] + qo, min(5, g - qo), qo, L, s_lp[b],
-                                    s_v + s_vbase[b], lx + cb, su, ust, d[20 + b], lane);
+    for (int task = warp; task < nb * CT; task += kWsConsumers / 32) {
+      const int b = task / CT, ct = task - (task / CT) * CT;
+      int vb = 0, cb = 0;
+      for (int bb = 0; bb < b; ++bb) {
+        const int Lb = d[16 + bb];
+        vb += d[12 + bb] * 3 * row_pitch(Lb);
+        cb += Lb;
       }
-      cb += L;
+      const int g = d[12 + b], L = d[16 + b], lrow0 = d[20 + b];
+      for (int qo = 0; qo < g; qo += 5) {
+        if (MODE == SPMM_S2STEP && lrow0 < 0)
+          block_task_mma_smem<MODE>(a, r, ct * 32, d[8 + b] + qo, min(5, g - qo), qo, L, row_pitch(L),
+                                    s_v + vb, lx + cb, s_u, ust, lrow0, lane);
+        else
+          block_task_mma_fast<MODE>(a, r, ct * 32, d[8 + b] + qo, min(5, g - qo), qo, L, row_pitch(L),
+                                    s_v + vb, lx + cb, s_u, ust, lrow0, lane);
+      }
     }
-    consumer_sync();                   // stage st and s_v fully consumed
-    if (tid == 0) mbar_arrive(&empty[st]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
   }
 }
 
 int ust_for(int rmax) { return ((rmax + 11) / 16) * 16 + 4; }   // >= rmax + 1, == 4 mod 16 (even)
+
+size_t dense_smem() {
+  return sizeof(double) * (kValCap + (size_t)kUCap * kDenseUst + 32 + (size_t)kWarps * 32 * kDenseDst);
+}
 
 size_t smem_for(int mode, int rmax) {
   const bool hot = (mode == SPMM_S2STEP || mode == SPMM_PLAIN3);
@@ -708,15 +992,14 @@ cudaError_t launch_m(const SpmmArgs& a0, int rmax, cudaStream_t s) {
   a.u_aligned16 = ((reinterpret_cast<uintptr_t>(a.U) & 15) == 0) && (a.ldu % 2 == 0) && (rmax < a.ldu || rmax % 2 == 0);
   constexpr bool HOT = (MODE == SPMM_S2STEP || MODE == SPMM_PLAIN3);
   if constexpr (HOT) {
-    // persistent TMA pipeline when the stage fits and every stream is 16-byte aligned
-    const size_t sm_t = sizeof(double) * (kTmaStages * tma_stage_doubles(ust_for(rmax)) + kValCap);
-    bool al = a.u_aligned16 && ((reinterpret_cast<uintptr_t>(a.U) & 15) == 0);
-    for (int v = 0; v < 6; ++v) al = al && ((reinterpret_cast<uintptr_t>(a.v[v]) & 15) == 0);
-    // experimental (slower than spmm_u_kernel on B200 so far): opt-in via dbg bit 32
-    if (al && sm_t <= 232448 - 1024 && (a.dbg & 32)) {
+    // slack: the predicate-free contraction reads up to 32*CT - 1 columns of the last staged U row
+    const int ust = ust_for(rmax), slack = max(0, 32 * ((rmax + 31) / 32) - ust);
+    // warp-specialised persistent pipeline (dbg bit 32 = env LRCHEB_SPMM_TMA selects it)
+    const size_t sd = ws_stage_doubles(ust, slack);
+    if ((a.dbg & 32) && a.u_aligned16 && sizeof(double) * kWsStages * sd <= 232448 - 1024) {
       if (a.ntl_u > 0) {
-        const int grid = a.ntl_u < sm_count() ? a.ntl_u : sm_count();
-        spmm_tma_kernel<MODE><<<grid, kTmaThreads, sm_t, s>>>(a, ust_for(rmax));
+        const int grid = min(a.ntl_u, max(1, sm_count() - max(0, a.reserved_sms)));
+        spmm_ws_kernel<MODE><<<grid, kWsThreads, sizeof(double) * kWsStages * sd, s>>>(a, ust, (int)sd);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
       }
@@ -726,10 +1009,10 @@ cudaError_t launch_m(const SpmmArgs& a0, int rmax, cudaStream_t s) {
       }
       return cudaGetLastError();
     }
-    const size_t sm_u = sizeof(double) * (kValCap + (size_t)kUCap * ust_for(rmax));
+    const size_t sm_u = sizeof(double) * (kValCap + (size_t)kUCap * ust + slack);
     if (sm_u <= 75 * 1024) {                       // 3 CTAs / SM
       if (a.ntl_u > 0) {
-        spmm_u_kernel<MODE><<<a.ntl_u, kThreads, sm_u, s>>>(a, ust_for(rmax));
+        spmm_u_kernel<MODE><<<a.ntl_u, kThreads, sm_u, s>>>(a, ust);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
       }
@@ -739,6 +1022,20 @@ cudaError_t launch_m(const SpmmArgs& a0, int rmax, cudaStream_t s) {
       }
       return cudaGetLastError();
     }
+  }
+  if constexpr (MODE == SPMM_DENSE) {
+    // shared-memory-S tiles on the tensor pipe, L2-gather tiles on the general kernel
+    if (a.ntl_u > 0) {
+      a.u_aligned16 = ((reinterpret_cast<uintptr_t>(a.U) & 15) == 0) && (a.ldu % 2 == 0);
+      spmm_dense_kernel<MODE><<<a.ntl_u, kThreads, dense_smem(), s>>>(a);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+    if (a.ntl_g > 0) {
+      a.tlist = a.tlist_g;
+      spmm_kernel<MODE, 5><<<a.ntl_g, kThreads, smem_for(MODE, rmax), s>>>(a, ust_for(rmax));
+    }
+    return cudaGetLastError();
   }
   if (a.ntiles == 0) return cudaSuccess;
   a.tlist = nullptr;
@@ -751,13 +1048,17 @@ cudaError_t prep_m() {
   cudaError_t e = cudaFuncSetAttribute(spmm_kernel<MODE, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem_for(MODE, kMaxRank));
   if (e != cudaSuccess) return e;
+  if constexpr (MODE == SPMM_DENSE) {
+    e = cudaFuncSetAttribute(spmm_dense_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dense_smem());
+    if (e != cudaSuccess) return e;
+  }
   if constexpr (MODE == SPMM_S2STEP || MODE == SPMM_PLAIN3) {
     e = cudaFuncSetAttribute(spmm_u_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 75 * 1024);
     if (e != cudaSuccess) return e;
     cudaFuncAttributes fa;
-    e = cudaFuncGetAttributes(&fa, spmm_tma_kernel<MODE>);
+    e = cudaFuncGetAttributes(&fa, spmm_ws_kernel<MODE>);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(spmm_tma_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(spmm_ws_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(232448 - fa.sharedSizeBytes));
   }
   return e;
