@@ -332,9 +332,22 @@ def main():
         dense = {"workload": f"config 5: M={M} dense S M x {cfg5.dense_cols}, {cfg5.reps} repetitions",
                  "avg_ms": avg, "achieved": byts / (avg / 1e3) / 1e9, "unit": "GB/s", "peak": hbm_peak(),
                  "frac": byts / (avg / 1e3) / 1e9 / hbm_peak(),
-                 "tflops": 6.0 * nnz * cfg5.dense_cols / (avg / 1e3) / 1e12}
+                 "tflops": 6.0 * nnz * cfg5.dense_cols / (avg / 1e3) / 1e12,
+                 "tensor_frac": 6.0 * nnz * cfg5.dense_cols / (avg / 1e3) / 1e12 / FP64_DMMA_PEAK_TFLOPS,
+                 "bound": "tensor (6 nnz ncols fp64 flops at the DMMA peak outlast the bytes at the HBM peak)"}
         del S5, Y5
         ctx5.close()
+
+    # ---- the whole iteration against its roofline: per kernel max(flops / fp64 peak, bytes / HBM peak),
+    #      summed over the M-level kernels of one steady-state iteration
+    it_parts = {"spmm": (6.0 * nnz * r, bytes_spmm), "ts_gram_x2": (2 * flops_gram, 2 * 8.0 * M * w),
+                "ts_store": (flops_store, 8.0 * M * w + 8.0 * M * r)}
+    t_roof = sum(max(f / (FP64_DMMA_PEAK_TFLOPS * 1e12), b / (hbm_peak() * 1e9)) for f, b in it_parts.values())
+    t_meas = 1.0 / value
+    iteration_roofline = {"flops": sum(f for f, _ in it_parts.values()), "bytes": sum(b for _, b in it_parts.values()),
+                          "roofline_ms": t_roof * 1e3, "measured_ms_per_iteration": t_meas * 1e3,
+                          "frac": t_roof / t_meas,
+                          "bound": "fp64 tensor (the Gram / basis passes); the SpMM alone is HBM-bound"}
 
     result = {
         "metric": "ChebyshevT iterations/sec (fused-SpMM HBM GB/s in roofline_spmm)",
@@ -353,6 +366,7 @@ def main():
         "clocks": clocks,
         "roofline": roof,
         "roofline_spmm": kernel_entry("spmm"),
+        "iteration_roofline": iteration_roofline,
         "config5_dense_spmm": dense,
         "kernel_ms_per_step": {k: v[0] for k, v in prof.items()},
         "ts_gram_passes": gram_split,

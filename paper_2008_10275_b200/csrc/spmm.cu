@@ -620,6 +620,130 @@ spmm_u_kernel(SpmmArgs a, int ust) {
   }
 }
 
+// Persistent variant of spmm_u_kernel (2 CTAs / SM, 128 registers): while tile i is contracted, the
+// six value streams, the (e0, nnz) pair and the descriptor of tile i + G are already in flight in
+// registers, so a tile's HBM latency overlaps the previous tile's DMMA work.  Opt-in
+// (LRCHEB_SPMM_PERSIST=1) until it measures faster than spmm_u_kernel.
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 2)
+spmm_p_kernel(SpmmArgs a, int ust) {
+  const int r = a.d_r ? *a.d_r : a.r_fixed;
+  if (r <= 0) return;
+  extern __shared__ double smem_dyn[];
+  double* s_v = smem_dyn;                        // [kValCap]
+  double* s_u = smem_dyn + kValCap;              // [kUCap][ust]
+  __shared__ __align__(16) int s_descb[2][kDescInts];
+  __shared__ int s_bstart[kTileBlocks + 1], s_vbase[kTileBlocks], s_lp[kTileBlocks];
+  __shared__ float s_invL[kTileBlocks];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int CT = (r + 31) >> 5;
+  const int G = gridDim.x, ntl = a.ntl_u;
+  constexpr int kStg = (kSpmmCap + kThreads - 1) / kThreads;
+  int idx = blockIdx.x;
+  if (idx >= ntl) return;
+  // prologue: tile idx in flight
+  int2 et = __ldg(reinterpret_cast<const int2*>(a.tile_ev) + idx);
+  int4 dq = make_int4(0, 0, 0, 0);
+  if (tid < kDescInts / 4) dq = __ldg(reinterpret_cast<const int4*>(a.tdesc + (size_t)idx * kDescInts) + tid);
+  double raw[kStg][6];
+#pragma unroll
+  for (int k = 0; k < kStg; ++k) {
+    const int e = tid + k * kThreads;
+    if (e < et.y && !(a.dbg & 4)) {
+#pragma unroll
+      for (int v = 0; v < 6; ++v) raw[k][v] = __ldcs(a.v[v] + et.x + e);
+    } else {
+#pragma unroll
+      for (int v = 0; v < 6; ++v) raw[k][v] = 0.0;
+    }
+  }
+  if (tid < kDescInts / 4) *reinterpret_cast<int4*>(&s_descb[0][4 * tid]) = dq;
+  __syncthreads();
+  for (int buf = 0; idx < ntl; idx += G, buf ^= 1) {
+    const int* s_desc = s_descb[buf];
+    const int tot = et.y, nb = s_desc[2], nu = s_desc[3];
+    // ---- (A) stage this tile: U rows, block table, grouped values
+    if (!(a.dbg & 2)) stage_u_rows(a, r, s_desc + kDescUrows, nu, s_u, ust, tid, kThreads);
+    asm volatile("cp.async.commit_group;\n" ::);
+    if (tid == 0) {
+      int vb = 0, eb = 0;
+      for (int b = 0; b < nb; ++b) {
+        const int g = s_desc[12 + b], L = s_desc[16 + b];
+        s_bstart[b] = eb; s_lp[b] = row_pitch(L); s_vbase[b] = vb; s_invL[b] = 1.0f / (float)L;
+        vb += g * 3 * s_lp[b];
+        eb += g * L;
+      }
+      s_bstart[nb] = tot;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kStg; ++k) {
+      const int e = tid + k * kThreads;
+      if (e < tot) {
+        int b = 0;
+#pragma unroll
+        for (int kk = 1; kk < kTileBlocks; ++kk) b += (kk < nb && e >= s_bstart[kk]);
+        const int L = s_desc[16 + b];
+        const int rel = e - s_bstart[b];
+        const int q = __float2int_rz(((float)rel + 0.5f) * s_invL[b]), j = rel - q * L;
+        const int lp = s_lp[b];
+        double* dst = s_v + s_vbase[b] + q * 3 * lp + j;
+        dst[0] = fma(a.lam, raw[k][5], fma(a.rho, raw[k][3], raw[k][0]));   // A0 + rho Jrho + lam Jlam
+        dst[lp] = raw[k][1] + raw[k][4];                                   // A1 + Jmu
+        dst[2 * lp] = a.rho * raw[k][2];                                    // rho A2
+      }
+    }
+    for (int b = 0; b < nb; ++b) {
+      const int g = s_desc[12 + b], L = s_desc[16 + b], lp = s_lp[b];
+      for (int i = tid; i < g * 3 * 4; i += kThreads) {
+        const int j = L + (i & 3);
+        if (j < ((L + 3) & ~3)) s_v[s_vbase[b] + (i >> 2) * lp + j] = 0.0;
+      }
+    }
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncthreads();
+    // ---- (B) next tile in flight (registers)
+    const int in = idx + G;
+    if (in < ntl) {
+      et = __ldg(reinterpret_cast<const int2*>(a.tile_ev) + in);
+      if (tid < kDescInts / 4) dq = __ldg(reinterpret_cast<const int4*>(a.tdesc + (size_t)in * kDescInts) + tid);
+#pragma unroll
+      for (int k = 0; k < kStg; ++k) {
+        const int e = tid + k * kThreads;
+        if (e < et.y && !(a.dbg & 4)) {
+#pragma unroll
+          for (int v = 0; v < 6; ++v) raw[k][v] = __ldcs(a.v[v] + et.x + e);
+        } else {
+#pragma unroll
+          for (int v = 0; v < 6; ++v) raw[k][v] = 0.0;
+        }
+      }
+    }
+    // ---- (C) contract this tile
+    const unsigned short* lx = reinterpret_cast<const unsigned short*>(s_desc + kDescLidx);
+    int cb = 0;
+    for (int b = 0, task0 = 0; b < nb; ++b) {
+      const int g = s_desc[12 + b], L = s_desc[16 + b];
+      for (int ct = 0; ct < CT; ++ct, ++task0) {
+        if ((task0 % kWarps) != warp) continue;
+        const int lrow0 = s_desc[20 + b];
+        for (int qo = 0; qo < g; qo += 5) {
+          if (MODE == SPMM_S2STEP && lrow0 < 0)
+            block_task_mma_smem<MODE>(a, r, ct * 32, s_desc[8 + b] + qo, min(5, g - qo), qo, L, s_lp[b],
+                                      s_v + s_vbase[b], lx + cb, s_u, ust, lrow0, lane);
+          else
+            block_task_mma_fast<MODE>(a, r, ct * 32, s_desc[8 + b] + qo, min(5, g - qo), qo, L, s_lp[b],
+                                      s_v + s_vbase[b], lx + cb, s_u, ust, lrow0, lane);
+        }
+      }
+      cb += L;
+    }
+    // ---- (D) publish the next descriptor; every warp is done with s_u / s_v / this descriptor
+    if (in < ntl && tid < kDescInts / 4) *reinterpret_cast<int4*>(&s_descb[buf ^ 1][4 * tid]) = dq;
+    __syncthreads();
+  }
+}
+
 // Config-5 dense application Y = sum_t c_t A_t S diag(e_t) (S dense M x ncols, ncols <= 256) on the
 // fp64 tensor pipe, shared-memory-U tiles.  Per tile the six value streams are combined once into
 // the three grouped streams; S is then processed in 64-column chunks: the chunk of the tile's
@@ -985,6 +1109,7 @@ cudaError_t launch_m(const SpmmArgs& a0, int rmax, cudaStream_t s) {
       const char* e = getenv("LRCHEB_SPMM_DBG");
       dbg = e ? atoi(e) : 0;
       if (getenv("LRCHEB_SPMM_TMA")) dbg |= 32;
+      if (getenv("LRCHEB_SPMM_PERSIST")) dbg |= 64;
     }
     a.dbg = dbg;
   }
@@ -1010,6 +1135,19 @@ cudaError_t launch_m(const SpmmArgs& a0, int rmax, cudaStream_t s) {
       return cudaGetLastError();
     }
     const size_t sm_u = sizeof(double) * (kValCap + (size_t)kUCap * ust + slack);
+    if (sm_u <= 75 * 1024 && (a.dbg & 64)) {       // persistent, 2 CTAs / SM (opt-in)
+      if (a.ntl_u > 0) {
+        const int grid = min(a.ntl_u, 2 * max(1, sm_count() - max(0, a.reserved_sms)));
+        spmm_p_kernel<MODE><<<grid, kThreads, sm_u, s>>>(a, ust);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+      }
+      if (a.ntl_g > 0) {
+        a.tlist = a.tlist_g;
+        spmm_kernel<MODE, 5><<<a.ntl_g, kThreads, smem_for(MODE, rmax), s>>>(a, ust_for(rmax));
+      }
+      return cudaGetLastError();
+    }
     if (sm_u <= 75 * 1024) {                       // 3 CTAs / SM
       if (a.ntl_u > 0) {
         spmm_u_kernel<MODE><<<a.ntl_u, kThreads, sm_u, s>>>(a, ust);
@@ -1054,6 +1192,8 @@ cudaError_t prep_m() {
   }
   if constexpr (MODE == SPMM_S2STEP || MODE == SPMM_PLAIN3) {
     e = cudaFuncSetAttribute(spmm_u_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 75 * 1024);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(spmm_p_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 75 * 1024);
     if (e != cudaSuccess) return e;
     cudaFuncAttributes fa;
     e = cudaFuncGetAttributes(&fa, spmm_ws_kernel<MODE>);

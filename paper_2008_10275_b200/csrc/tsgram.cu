@@ -15,6 +15,8 @@
 // columns.  The K loop streams 32-column chunks of Ucat and 32-row chunks of T into a cp.async
 // double buffer (8-byte copies: the two Ucat blocks meet at an odd column; zero fill past M / w).
 // The X tile is parked in the (then idle) stage buffers for the Gram / store epilogue.
+#include <cstdlib>
+
 #include "lrc_internal.cuh"
 
 namespace lrc {
@@ -100,6 +102,7 @@ __device__ __forceinline__ ChunkPlan plan_chunk(const TsArgs& a, unsigned stage,
 template <int PT>
 __device__ __forceinline__ void issue_part(const TsArgs& a, const ChunkPlan& c, int part, int w, int tid) {
   using S = TsShape<PT>;
+  if (a.dbg & 1) return;
   if (a.u16) {
     if (part < 4) {
       const int i = (tid >> 4) + 32 * part, j = (tid & 15) * 2;
@@ -283,6 +286,7 @@ ts_kernel(TsArgs a) {
         // trapezoidal) the tiles with all i > c are zero
         int nact = (k0 + kk < w) ? PT : 0;
         if (a.t_lower) nact = min(nact, (k0 + kk + 3) / 8 + 1);
+        if (a.dbg & 4) nact = 0;
         const double a0 = s_u[(warp * 8 + gid) * kSU + kk + tig];
         mma_row<PT>(x0, a0, s_t + (kk + tig) * SX + gid, nact);
         if (pm0 >= 0) issue_part<PT>(a, c2, kk / 4, w, tid);
@@ -303,7 +307,7 @@ ts_kernel(TsArgs a) {
     if constexpr (MODE == 0) {
 #pragma unroll
       for (int s = 0; s < S::SPW; ++s) {
-        if (sI[s] < 0) continue;
+        if (sI[s] < 0 || (a.dbg & 2)) continue;
         const int I0 = 2 * sI[s], J0 = 2 * sJ[s];
         // odd PT: the last super row/column is half; the kind is warp-uniform and fixed, so each
         // kind runs its own loop (no predicated-off DMMAs)
@@ -316,7 +320,7 @@ ts_kernel(TsArgs a) {
       }
     } else {
       // rows of U_{k+1}: 16-byte stores when the output rows are 16-byte aligned
-      const int pw = p + (a.u.pad_even ? (p & 1) : 0);   // padded (solver) mode also writes the zero pad column
+      const int pw = (a.dbg & 2) ? 0 : p + (a.u.pad_even ? (p & 1) : 0);   // padded (solver) mode also writes the zero pad column
       if (a.o16) {
         constexpr int HP = S::HP;
         for (int e = tid; e < kBM * HP; e += kThreads) {
@@ -439,6 +443,11 @@ cudaError_t launch_ts(int mode, const TsArgs& a0, int pmax, int grid, cudaStream
     u16 = u16 && (a.u.b[bi].ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(a.u.b[bi].p) & 15) == 0);
   a.u16 = u16 ? 1 : 0;
   a.o16 = (mode == 1 && a.out && a.ldo % 2 == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0) ? 1 : 0;
+  {
+    static int dbg = -1;
+    if (dbg < 0) { const char* e = getenv("LRCHEB_TS_DBG"); dbg = e ? atoi(e) : 0; }
+    a.dbg = dbg;
+  }
   return mode == 0 ? Dispatch<0, 16>::launch(a, pmax / 8, grid, s)
                    : Dispatch<1, 16>::launch(a, pmax / 8, grid, s);
 }

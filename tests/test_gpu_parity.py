@@ -81,17 +81,24 @@ def test_apply_irregular_pattern(diag_only):
     ctx.close()
 
 
-@pytest.mark.parametrize("ncols", [16, 256])
-def test_apply_dense(ncols):
-    """BASELINE config 5 mode: Y = sum_t c_t A_t S D_t (oracle.apply_dense)."""
+@pytest.mark.parametrize("ncols,ld,cfg", [(16, 16, "tiny"), (256, 256, "tiny"), (37, 37, "tiny"),
+                                           (100, 100, "small"), (37, 41, "tiny"), (200, 203, "small")])
+def test_apply_dense(ncols, ld, cfg):
+    """BASELINE config 5 mode: Y = sum_t c_t A_t S D_t (oracle.apply_dense).  Covers one and several
+    64-column chunks, a ragged last chunk, odd widths and an odd leading dimension (8-byte copies)."""
     require_gpu()
-    prob = problem("tiny")
+    prob = problem(cfg)
     op = prob.op
-    rng = np.random.default_rng(ncols)
+    rng = np.random.default_rng(ncols + ld)
     d_mu, d_nu = 0.25 + 3.75 * rng.random(ncols), 0.25 + 3.75 * rng.random(ncols)
     ctx = make_ctx(op, d_mu, d_nu)
-    S = rng.standard_normal((op.M, ncols))
-    Y = ctx.apply_dense(S)
+    S_full = rng.standard_normal((op.M, ld))
+    S = S_full[:, :ncols]
+    if ld != ncols:    # a strided device view keeps the leading dimension
+        import torch
+        Y = ctx.apply_dense(torch.from_numpy(S_full).cuda()[:, :ncols]).cpu().numpy()
+    else:
+        Y = ctx.apply_dense(S)
     ref = orc.apply_dense(oracle_terms(op, d_mu, d_nu), S)
     assert _rel(Y, ref) <= 1e-12
     ctx.close()
