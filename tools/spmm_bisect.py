@@ -1,6 +1,6 @@
 """Developer probe: K1 S2STEP time on one config with phases of the SpMM switched off
 (LRCHEB_SPMM_DBG bits: 1 no DMMA, 2 no U staging, 4 no value loads, 8 no stores; 32 = warp-specialised
-kernel, 64 = persistent 2-CTA kernel).
+kernel, 64 = persistent 2-CTA kernel, 128 = deep-prefetch kernel).
 Each setting runs in its own process (the switch is read once per process).
 
     python tools/spmm_bisect.py large 0 15 9      # settings to compare
@@ -51,5 +51,7 @@ if __name__ == "__main__":
             env["LRCHEB_SPMM_TMA"] = "1"
         if dbg & 64:
             env["LRCHEB_SPMM_PERSIST"] = "1"
+        if dbg & 128:
+            env["LRCHEB_SPMM_DEEP"] = "1"
         out = subprocess.run([sys.executable, __file__, "once", cfg], env=env, capture_output=True, text=True)
         print(f"dbg={dbg:3d}: {out.stdout.strip() or out.stderr.strip()[-300:]}", flush=True)
