@@ -902,18 +902,20 @@ spmm_dense_kernel(SpmmArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// Persistent warp-specialised kernel (S2STEP / PLAIN3, shared-memory-U tiles), one CTA per SM.
-// Warps 8-11 produce: per tile they fetch the (e0, nnz) pair and issue all six value streams into
-// registers at once, copy the descriptor and the tile's deduplicated U rows (16-byte cp.async) into
-// a double-buffered stage, combine the six streams into the three grouped [slot][j] streams and
-// publish the stage on its `full` mbarrier.  Warps 0-7 consume: contract on the fp64 tensor pipe
-// (block_task_mma_fast), store, and release the stage on its `empty` mbarrier.  Tile k+1 is loaded
-// and combined while tile k is contracted, so the HBM stream and the DMMA work overlap.
+// Persistent TMA-fed pipeline (S2STEP / PLAIN3, shared-memory-U tiles), one CTA per SM; opt-in
+// (env LRCHEB_SPMM_TMA=1), slower than spmm_u_kernel on B200 so far.
+//   producer warp (8): per tile, the descriptor (loaded one tile ahead into registers, written to a
+//       4-deep ring), then TMA bulk copies (cp.async.bulk + mbarrier complete_tx) of the six raw value
+//       segments and of the tile's deduplicated U rows into double-buffered stages;
+//   compute warps (0-7): combine the raw six streams into the grouped [slot][j] values, contract on
+//       the fp64 tensor pipe, store.
+// Tile k+1's copies overlap tile k's combine and contraction; hand-offs are mbarriers (parity = use
+// count & 1).  With a single CTA per SM the per-tile critical path (combine, two barriers, one task
+// per warp) is ~2.3 us, which bounds it above the 3-CTA lean kernel.
 // ---------------------------------------------------------------------------------------------
-constexpr int kWsStages = 2;
-constexpr int kWsConsumers = 256;                  // 8 warps
-constexpr int kWsProducers = 128;                  // 4 warps
-constexpr int kWsThreads = kWsConsumers + kWsProducers;
+constexpr int kTRaw = kSpmmCap + 2;                // doubles per raw value stream (alignment slack)
+constexpr int kTCompute = 256, kTThreads = kTCompute + 32;
+constexpr int kTRing = 4;                          // descriptor ring depth
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
@@ -933,148 +935,168 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 }
 
 
-// doubles per stage: descriptor (1 KB) + grouped values + U rows (+ slack of the predicate-free
-// contraction), rounded to a multiple of 2 (16-byte alignment)
-size_t ws_stage_doubles(int ust, int slack) {
-  return (((size_t)kDescInts / 2 + kValCap + (size_t)kUCap * ust + slack) + 1) & ~(size_t)1;
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// dynamic shared memory: raw[2][6][kTRaw] | ustage[2][ustage] | sv[kValCap]
+size_t t_smem(int ustage) {
+  return sizeof(double) * (2 * 6 * (size_t)kTRaw + 2 * (size_t)ustage + kValCap);
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kWsThreads, 1)
-spmm_ws_kernel(SpmmArgs a, int ust, int stage_d) {
+__global__ void __launch_bounds__(kTThreads, 1)
+spmm_t_kernel(SpmmArgs a, int ust, int ustage) {
   const int r = a.d_r ? *a.d_r : a.r_fixed;
   if (r <= 0) return;
   extern __shared__ __align__(16) double smem_dyn[];
-  __shared__ __align__(8) unsigned long long full[kWsStages], empty[kWsStages];
+  double* s_raw = smem_dyn;
+  double* s_ust = s_raw + 2 * 6 * kTRaw;
+  double* s_v = s_ust + 2 * ustage;
+  __shared__ __align__(16) int s_ring[kTRing][kDescInts];
+  __shared__ __align__(8) unsigned long long raw_full[2], raw_empty[2], u_full[2], u_empty[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
-    for (int i = 0; i < kWsStages; ++i) { mbar_init(&full[i], kWsProducers); mbar_init(&empty[i], kWsConsumers / 32); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&raw_full[i], 1); mbar_init(&raw_empty[i], 1);
+      mbar_init(&u_full[i], 1); mbar_init(&u_empty[i], kTCompute / 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
   const int G = gridDim.x, ntl = a.ntl_u;
   const int CT = (r + 31) >> 5;
+  const int2* ev = reinterpret_cast<const int2*>(a.tile_ev);
 
-  if (tid >= kWsConsumers) {
-    // ------------------------------------------------------------------------------ producers
-    const int p = tid - kWsConsumers, pw = p >> 5;
-    constexpr int kStg = (kSpmmCap + kWsProducers - 1) / kWsProducers;   // 8 entries per thread
+  if (warp == kTCompute / 32) {
+    // ------------------------------------------------------------------------------ producer
+    const unsigned ubytes = (unsigned)((r + 1) >> 1) * 16u;
+    // the descriptor words and (e0, nnz) of the next tile are loaded one tile ahead (registers), so
+    // no DRAM latency sits on the producer's per-tile path
+    int4 dq[kDescInts / 128];
+    int2 e;
+    {
+      const int4* gd = reinterpret_cast<const int4*>(a.tdesc + (size_t)blockIdx.x * kDescInts);
+#pragma unroll
+      for (int i = 0; i < kDescInts / 128; ++i) dq[i] = __ldg(gd + lane + 32 * i);
+      e = __ldg(ev + blockIdx.x);
+    }
     for (int k = 0;; ++k) {
       const int idx = blockIdx.x + k * G;
       if (idx >= ntl) break;
-      const int st = k % kWsStages;
-      const int2 et = __ldg(reinterpret_cast<const int2*>(a.tile_ev) + idx);
-      const int e0 = et.x, tot = et.y;
-      double raw[kStg][6];
+      int4 nq[kDescInts / 128];
+      int2 ne = make_int2(0, 0);
+      if (idx + G < ntl) {
+        const int4* gd = reinterpret_cast<const int4*>(a.tdesc + (size_t)(idx + G) * kDescInts);
 #pragma unroll
-      for (int i = 0; i < kStg; ++i) {
-        const int e = p + i * kWsProducers;
-        if (e < tot && !(a.dbg & 4)) {
-#pragma unroll
-          for (int v = 0; v < 6; ++v) raw[i][v] = __ldcs(a.v[v] + e0 + e);
-        } else {
-#pragma unroll
-          for (int v = 0; v < 6; ++v) raw[i][v] = 0.0;
-        }
+        for (int i = 0; i < kDescInts / 128; ++i) nq[i] = __ldg(gd + lane + 32 * i);
+        ne = __ldg(ev + idx + G);
       }
-      int4 dq = make_int4(0, 0, 0, 0);
-      if (p < kDescInts / 4) dq = __ldg(reinterpret_cast<const int4*>(a.tdesc + (size_t)idx * kDescInts) + p);
-      if (k >= kWsStages) mbar_wait(&empty[st], ((k / kWsStages) - 1) & 1);
-      double* stage = smem_dyn + (size_t)st * stage_d;
-      int* d = reinterpret_cast<int*>(stage);
-      double* s_v = stage + kDescInts / 2;
-      double* s_u = s_v + kValCap;
-      if (p < kDescInts / 4) *reinterpret_cast<int4*>(d + 4 * p) = dq;
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");          // producers: descriptor visible
-      const int nb = d[2], nu = d[3];
-      // U rows: one warp per row, lanes over 16-byte chunks
-      if (!(a.dbg & 2)) {
-        const int nch = (r + 1) >> 1;
-        for (int u = pw; u < nu; u += kWsProducers / 32) {
-          const double* src = a.U + (size_t)d[kDescUrows + u] * a.ldu;
-          for (int ch = lane; ch < nch; ch += 32) cp_async16(s_u + u * ust + 2 * ch, src + 2 * ch);
-        }
-      }
-      // block table (registers)
-      int bst[kTileBlocks + 1], vbs[kTileBlocks], lps[kTileBlocks], Ls[kTileBlocks];
-      {
-        int vb = 0, eb = 0;
+      const int st = k & 1;
+      // descriptor of tile k first (ring slot of tile k-4, free once tile k-2 is contracted): the
+      // combiners read it as soon as the raw values land
+      if (k >= 2) mbar_wait(&u_empty[st], ((k >> 1) - 1) & 1);
+      int* d = s_ring[k % kTRing];
 #pragma unroll
-        for (int b = 0; b < kTileBlocks; ++b) {
-          const int g = b < nb ? d[12 + b] : 0, L = b < nb ? d[16 + b] : 1;
-          bst[b] = eb; vbs[b] = vb; Ls[b] = L; lps[b] = row_pitch(L);
-          vb += g * 3 * lps[b];
-          eb += g * L;
-        }
-        bst[kTileBlocks] = 0x7fffffff;
+      for (int i = 0; i < kDescInts / 128; ++i) *reinterpret_cast<int4*>(d + 4 * (lane + 32 * i)) = dq[i];
+      __syncwarp();
+      // raw value segments of tile k (buffer st, free once the combiners are done with tile k-2)
+      if (k >= 2) mbar_wait(&raw_empty[st], ((k >> 1) - 1) & 1);
+      const int e0a = e.x & ~1, end = e.x + e.y, enda = end & ~1;
+      double* raw = s_raw + st * 6 * kTRaw;
+      if (lane == 0) {
+        if ((end & 1) && !(a.dbg & 4))   // odd tail element: plain load (never read past the array)
+          for (int v = 0; v < 6; ++v) raw[v * kTRaw + (end - 1 - e0a)] = __ldg(a.v[v] + end - 1);
+        mbar_expect_tx(&raw_full[st], (a.dbg & 4) ? 0u : 6u * 8u * (unsigned)(enda - e0a));
       }
+      __syncwarp();
+      if (lane < 6 && enda > e0a && !(a.dbg & 4))
+        bulk_g2s(raw + lane * kTRaw, a.v[lane] + e0a, 8u * (unsigned)(enda - e0a), &raw_full[st]);
+      // U rows of tile k (buffer st)
+      const int nu = (a.dbg & 2) ? 0 : d[3];
+      double* su = s_ust + st * ustage;
+      if (lane == 0) mbar_expect_tx(&u_full[st], ubytes * (unsigned)nu);
+      __syncwarp();
+      for (int u = lane; u < nu; u += 32)
+        bulk_g2s(su + u * ust, a.U + (size_t)d[kDescUrows + u] * a.ldu, ubytes, &u_full[st]);
 #pragma unroll
-      for (int i = 0; i < kStg; ++i) {
-        const int e = p + i * kWsProducers;
-        if (e < tot) {
-          int eb = bst[0], vb = vbs[0], L = Ls[0], lp = lps[0];
-#pragma unroll
-          for (int b = 1; b < kTileBlocks; ++b)
-            if (b < nb && e >= bst[b]) { eb = bst[b]; vb = vbs[b]; L = Ls[b]; lp = lps[b]; }
-          const int rel = e - eb;
-          // q = rel / L exactly (see spmm_u_kernel)
-          const int q = __float2int_rz(((float)rel + 0.5f) / (float)L), j = rel - q * L;
-          double* dst = s_v + vb + q * 3 * lp + j;
-          dst[0] = fma(a.lam, raw[i][5], fma(a.rho, raw[i][3], raw[i][0]));   // A0 + rho Jrho + lam Jlam
-          dst[lp] = raw[i][1] + raw[i][4];                                   // A1 + Jmu
-          dst[2 * lp] = a.rho * raw[i][2];                                    // rho A2
-        }
-      }
-      // zero the staged entries L .. round4(L)-1 of every slot
-#pragma unroll
-      for (int b = 0; b < kTileBlocks; ++b) {
-        if (b < nb) {
-          const int g = d[12 + b], L = Ls[b];
-          for (int i = p; i < g * 3 * 4; i += kWsProducers) {
-            const int j = L + (i & 3);
-            if (j < ((L + 3) & ~3)) s_v[vbs[b] + (i >> 2) * lps[b] + j] = 0.0;
-          }
-        }
-      }
-      asm volatile("cp.async.wait_all;\n" ::: "memory");
-      mbar_arrive(&full[st]);
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");          // descriptor reads done before reuse
+      for (int i = 0; i < kDescInts / 128; ++i) dq[i] = nq[i];
+      e = ne;
     }
     return;
   }
 
-  // ---------------------------------------------------------------------------------- consumers
+  // ------------------------------------------------------------------- compute (combine + contract)
+  const int c = tid;
   for (int k = 0;; ++k) {
     const int idx = blockIdx.x + k * G;
     if (idx >= ntl) break;
-    const int st = k % kWsStages;
-    mbar_wait(&full[st], (k / kWsStages) & 1);
-    const double* stage = smem_dyn + (size_t)st * stage_d;
-    const int* d = reinterpret_cast<const int*>(stage);
-    const double* s_v = stage + kDescInts / 2;
-    const double* s_u = s_v + kValCap;
-    const int nb = d[2];
-    const unsigned short* lx = reinterpret_cast<const unsigned short*>(d + kDescLidx);
-    for (int task = warp; task < nb * CT; task += kWsConsumers / 32) {
-      const int b = task / CT, ct = task - (task / CT) * CT;
-      int vb = 0, cb = 0;
-      for (int bb = 0; bb < b; ++bb) {
-        const int Lb = d[16 + bb];
-        vb += d[12 + bb] * 3 * row_pitch(Lb);
-        cb += Lb;
+    const int st = k & 1;
+    mbar_wait(&raw_full[st], (k >> 1) & 1);
+    asm volatile("bar.sync 1, %0;\n" ::"n"(kTCompute) : "memory");   // s_v of tile k-1 fully consumed
+    const int* d = s_ring[k % kTRing];
+    const double* raw = s_raw + st * 6 * kTRaw;
+    const int e0 = d[0], tot = d[1], nb = d[2];
+    const int off = e0 - (e0 & ~1);
+    int bs[kTileBlocks], vbs[kTileBlocks];
+    {
+      int eb = 0, vb = 0;
+#pragma unroll
+      for (int b = 0; b < kTileBlocks; ++b) {
+        bs[b] = b < nb ? eb : 0x7fffffff;
+        vbs[b] = vb;
+        if (b < nb) { const int g = d[12 + b], L = d[16 + b]; eb += g * L; vb += 3 * g * row_pitch(L); }
       }
+    }
+    for (int e = c; e < tot; e += kTCompute) {
+      int b = 0;
+#pragma unroll
+      for (int kk = 1; kk < kTileBlocks; ++kk) b += (e >= bs[kk]);
+      int eb = bs[0], vb = vbs[0];
+#pragma unroll
+      for (int kk = 1; kk < kTileBlocks; ++kk) if (b == kk) { eb = bs[kk]; vb = vbs[kk]; }
+      const int L = d[16 + b];
+      const int rel = e - eb;
+      const int q = __float2int_rz(((float)rel + 0.5f) / (float)L), j = rel - q * L;
+      const int lp = row_pitch(L);
+      const double* rv = raw + off + e;
+      double* dst = s_v + vb + q * 3 * lp + j;
+      dst[0] = fma(a.lam, rv[5 * kTRaw], fma(a.rho, rv[3 * kTRaw], rv[0]));   // A0 + rho Jrho + lam Jlam
+      dst[lp] = rv[1 * kTRaw] + rv[4 * kTRaw];                             // A1 + Jmu
+      dst[2 * lp] = a.rho * rv[2 * kTRaw];                                  // rho A2
+    }
+    for (int b = 0; b < nb; ++b) {
+      const int g = d[12 + b], L = d[16 + b], lp = row_pitch(L);
+      for (int i = c; i < g * 3 * 4; i += kTCompute) {
+        const int j = L + (i & 3);
+        if (j < ((L + 3) & ~3)) s_v[vbs[b] + (i >> 2) * lp + j] = 0.0;
+      }
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"n"(kTCompute) : "memory");   // grouped values ready
+    if (c == 0) mbar_arrive(&raw_empty[st]);
+    mbar_wait(&u_full[st], (k >> 1) & 1);
+    const double* s_u = s_ust + st * ustage;
+    const unsigned short* lx = reinterpret_cast<const unsigned short*>(d + kDescLidx);
+    for (int task = warp; task < nb * CT; task += kTCompute / 32) {
+      const int b = task / CT, ct = task - (task / CT) * CT;
+      int cb = 0;
+      for (int bb = 0; bb < b; ++bb) cb += d[16 + bb];
       const int g = d[12 + b], L = d[16 + b], lrow0 = d[20 + b];
       for (int qo = 0; qo < g; qo += 5) {
         if (MODE == SPMM_S2STEP && lrow0 < 0)
           block_task_mma_smem<MODE>(a, r, ct * 32, d[8 + b] + qo, min(5, g - qo), qo, L, row_pitch(L),
-                                    s_v + vb, lx + cb, s_u, ust, lrow0, lane);
+                                    s_v + vbs[b], lx + cb, s_u, ust, lrow0, lane);
         else
           block_task_mma_fast<MODE>(a, r, ct * 32, d[8 + b] + qo, min(5, g - qo), qo, L, row_pitch(L),
-                                    s_v + vb, lx + cb, s_u, ust, lrow0, lane);
+                                    s_v + vbs[b], lx + cb, s_u, ust, lrow0, lane);
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
+    if (lane == 0) mbar_arrive(&u_empty[st]);
   }
 }
 
@@ -1119,12 +1141,14 @@ cudaError_t launch_m(const SpmmArgs& a0, int rmax, cudaStream_t s) {
   if constexpr (HOT) {
     // slack: the predicate-free contraction reads up to 32*CT - 1 columns of the last staged U row
     const int ust = ust_for(rmax), slack = max(0, 32 * ((rmax + 31) / 32) - ust);
-    // warp-specialised persistent pipeline (dbg bit 32 = env LRCHEB_SPMM_TMA selects it)
-    const size_t sd = ws_stage_doubles(ust, slack);
-    if ((a.dbg & 32) && a.u_aligned16 && sizeof(double) * kWsStages * sd <= 232448 - 1024) {
+    // three-role TMA pipeline (dbg bit 32 = env LRCHEB_SPMM_TMA selects it)
+    const int ustage = (kUCap * ust + slack + 1) & ~1;
+    bool al = a.u_aligned16;
+    for (int v = 0; v < 6; ++v) al = al && ((reinterpret_cast<uintptr_t>(a.v[v]) & 15) == 0);
+    if ((a.dbg & 32) && al && t_smem(ustage) <= 232448 - 8192) {
       if (a.ntl_u > 0) {
         const int grid = min(a.ntl_u, max(1, sm_count() - max(0, a.reserved_sms)));
-        spmm_ws_kernel<MODE><<<grid, kWsThreads, sizeof(double) * kWsStages * sd, s>>>(a, ust, (int)sd);
+        spmm_t_kernel<MODE><<<grid, kTThreads, t_smem(ustage), s>>>(a, ust, ustage);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
       }
@@ -1196,9 +1220,9 @@ cudaError_t prep_m() {
     e = cudaFuncSetAttribute(spmm_p_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 75 * 1024);
     if (e != cudaSuccess) return e;
     cudaFuncAttributes fa;
-    e = cudaFuncGetAttributes(&fa, spmm_ws_kernel<MODE>);
+    e = cudaFuncGetAttributes(&fa, spmm_t_kernel<MODE>);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(spmm_ws_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(spmm_t_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(232448 - fa.sharedSizeBytes));
   }
   return e;
