@@ -201,3 +201,42 @@ def test_solve_small_cold_jacobi_start():
     """Same parity with the core SVD started from W = I every iteration (LRC_NO_WARM_START)."""
     require_gpu()
     _solve_parity("small", 1, 30, warm_start=False)
+
+
+# The opt-in SpMM variants (persistent 2-CTA register prefetch, TMA-fed pipeline) are selected by
+# environment variables read once per process, so each runs in a child process.
+_VARIANT_CODE = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+from paper_2008_10275_b200 import lrcheb
+from gpu_common import make_ctx, oracle_terms, problem
+prob = problem(sys.argv[2]); op = prob.op
+d_mu, d_nu, _, _ = prob.subset(0)
+ctx = make_ctx(op, d_mu, d_nu)
+r = int(sys.argv[3]); rng = np.random.default_rng(r)
+U = rng.standard_normal((op.M, r))
+A = [t[1] for t in oracle_terms(op, d_mu, d_nu)]
+ref = [A[0] @ U + op.rho_f * (A[3] @ U) + op.lambda_s * (A[5] @ U), A[1] @ U + A[4] @ U, op.rho_f * (A[2] @ U)]
+g = 0.037
+W = ctx.apply_lowrank(torch.from_numpy(U).cuda(), lrcheb.LRC_APPLY_S2STEP, g).cpu().numpy()
+W3 = ctx.apply_lowrank(torch.from_numpy(U).cuda(), lrcheb.LRC_APPLY_PLAIN3).cpu().numpy()
+refs = [U - g * ref[0], ref[1], ref[2]]
+err = max(max(np.linalg.norm(W[:, t*r:(t+1)*r] - refs[t]) / np.linalg.norm(refs[t]) for t in range(3)),
+          max(np.linalg.norm(W3[:, t*r:(t+1)*r] - ref[t]) / np.linalg.norm(ref[t]) for t in range(3)))
+print("ERR", err)
+"""
+
+
+@pytest.mark.parametrize("env", ["LRCHEB_SPMM_TMA", "LRCHEB_SPMM_PERSIST"])
+@pytest.mark.parametrize("name,r", [("small", 60), ("small", 33), ("tiny", 10)])
+def test_apply_lowrank_optin_variants(env, name, r):
+    require_gpu()
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", _VARIANT_CODE, root, name, str(r)], capture_output=True,
+                         text=True, env=dict(os.environ, **{env: "1"}), timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    err = float(out.stdout.split("ERR")[-1])
+    assert err <= 1e-12
