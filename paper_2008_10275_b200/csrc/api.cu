@@ -3,9 +3,9 @@
 // One iteration k (X_k -> X_{k+1}, reading S1) is enqueued as
 //   fork:  [s0] K1 spmm S2STEP(U_k) -> W3 = [U_k - g W0], [W1], [W2] (three contiguous arrays) (a1)
 //          [s1] vside: Vcat, Householder QR -> T1 = R_V^T, Q_V                    (a2)
-//   join:  ts GRAM(Ucat, T1) -> reduce -> chol1 -> T2                            (a3)
-//          ts GRAM(Ucat, T2) -> reduce -> chol2 + Jacobi + rank -> Z, V_{k+1}    (a4, a5)
-//          ts STORE(Ucat, Z) -> U_{k+1}                                          (a6)
+//   join:  ts GRAM(Ucat, T1 = R_V^T) -> Y (stored, M x p), G1 -> reduce -> chol1 -> R1^{-1}   (a3)
+//          ts GRAM(Y, R1^{-1}) -> G2 -> reduce -> chol2 + Jacobi + rank -> W_r, V_{k+1}       (a4, a5)
+//          ts STORE(Y, W_r Sigma_r^{-1}) -> U_{k+1}                                          (a6)
 // with Ucat = [B_U | W0' | W1 | W2 | U_{k-1}] never copied (five strided blocks), ranks device-resident,
 // so the whole N-iteration loop is captured once into a CUDA graph and replayed.
 #include <algorithm>
@@ -53,6 +53,7 @@ struct Workspace {
   double* R1i = nullptr; double* Wz = nullptr; double* Wv = nullptr;
   double* W0 = nullptr; double* Wfull = nullptr; double* Bprev = nullptr;
   double* partials = nullptr;
+  double* Y = nullptr;                          // M x pmax: Y = Ucat R_V^T of the current truncation
   double* Uh = nullptr; double* Vh = nullptr;   // iterate history
   double* tmpA = nullptr; size_t tmpA_sz = 0;   // hook scratch
   double* tmpB = nullptr; size_t tmpB_sz = 0;
@@ -178,7 +179,7 @@ void free_ws(Workspace& w) {
   dfree(w.BUb); dfree(w.W3);
   for (int i = 0; i < 3; ++i) { dfree(w.Ubuf[i]); dfree(w.Vbuf[i]); }
   dfree(w.BV); dfree(w.omega); dfree(w.ints); dfree(w.sigma); dfree(w.scal);
-  dfree(w.T1); dfree(w.QV); dfree(w.G); dfree(w.R1); dfree(w.T2); dfree(w.Z);
+  dfree(w.T1); dfree(w.QV); dfree(w.G); dfree(w.R1); dfree(w.T2); dfree(w.Z); dfree(w.Y);
   dfree(w.R1i); dfree(w.Wz); dfree(w.Wv); dfree(w.W0); dfree(w.Wfull); dfree(w.Bprev);
   dfree(w.partials); dfree(w.Uh); dfree(w.Vh); dfree(w.tmpA); dfree(w.tmpB); dfree(w.tmpC);
   w = Workspace();
@@ -238,6 +239,7 @@ lrc_status ensure_ws(lrc_ctx* ctx, int rb, int cap, int N, int wmax, bool record
   CK(dalloc(&w.Wfull, (size_t)pmax * pmax));
   CK(dalloc(&w.Bprev, n * pmax));
   CK(dalloc(&w.partials, (size_t)w.grid * pmax * pmax));
+  CK(dalloc(&w.Y, M * pmax));
   if (record) {
     CK(dalloc(&w.Uh, (size_t)N * M * w.LDU));
     CK(dalloc(&w.Vh, (size_t)N * n * cap));
@@ -330,6 +332,7 @@ lrc_status enqueue_truncation(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, co
       KL(P_TINY, s, launch_tiny_gemm(w.QV, w.pmax, w.Bprev, w.pmax, w.W0, w.pmax, w.pmax, st.p, 0,
                                      w.pmax, nullptr, (int)ctx->n, s, 1));
   }
+  // pass 1 over Ucat: Y = Ucat R_V^T (kept: M x pmax), G1 = Y^T Y
   TsArgs ta{};
   ta.M = (int)ctx->M;
   ta.u = ud;
@@ -339,29 +342,44 @@ lrc_status enqueue_truncation(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, co
   ta.d_p = st.p;
   ta.partials = w.partials;
   ta.t_lower = 1;
+  ta.yout = w.Y;
+  ta.ldy = w.pmax;
   KL(P_TS_GRAM, s, launch_ts(0, ta, w.pmax, w.grid, s));
   KL(P_REDUCE, s, launch_gram_reduce(w.partials, w.grid, w.pmax, w.G, s));
   KL(P_CHOL1, s, launch_chol1(st, b, w.pmax, w.wmax, s));
-  KL(P_TINY, s, launch_tiny_gemm(w.T1, w.pmax, w.R1i, w.pmax, w.T2, w.pmax, w.pmax, st.w, 0, w.wmax,
-                                 st.p, 0, s));
-  ta.T = w.T2;
-  ta.t_lower = 0;
-  KL(P_TS_GRAM2, s, launch_ts(0, ta, w.pmax, w.grid, s));
+  // pass 2 over Y (textbook CholeskyQR2: Q1 = Y R1^{-1} from the stored Y), G2 = Q1^T Q1.  The Y block
+  // is p wide (p read from the device state); its pad column (odd p) is an exact zero column.
+  UDesc yd{};
+  yd.nb = 1;
+  yd.pad_even = ud.pad_even;
+  yd.b[0].p = w.Y;
+  yd.b[0].ld = w.pmax;
+  yd.b[0].w_fixed = 0;
+  yd.b[0].w_idx = (int)(st.p - st.rk);
+  TsArgs t2{};
+  t2.M = (int)ctx->M;
+  t2.u = yd;
+  t2.rk = st.rk;
+  t2.T = w.R1i;
+  t2.ldt = w.pmax;
+  t2.d_p = st.p;
+  t2.partials = w.partials;
+  t2.t_upper = 1;
+  KL(P_TS_GRAM2, s, launch_ts(0, t2, w.pmax, w.grid, s));
   KL(P_REDUCE, s, launch_gram_reduce(w.partials, w.grid, w.pmax, w.G, s));
   KL(P_CHOL2, s, launch_chol2_svd(st, b, w.pmax, w.wmax, (int)ctx->n, tol, cap, rank_slot, sigma_row, Vout,
                       ldv_out, s));
-  KL(P_TINY, s, launch_tiny_gemm(w.T1, w.pmax, w.Wz, w.capp, w.Z, w.capp, w.capp, st.w, 0, w.wmax,
-                                 st.p, 0, s));
   KL(P_TINY, s, launch_tiny_gemm(w.QV, w.pmax, w.Wv, w.capp, Vout, ldv_out, cap, nullptr,
                                  (int)ctx->n, (int)ctx->n, st.p, 0, s));
   if (use_warm)   // B = Q_V W (n x p): the right singular basis of X for the next warm start
     KL(P_TINY, s, launch_tiny_gemm(w.QV, w.pmax, w.Wfull, w.pmax, w.Bprev, w.pmax, w.pmax, nullptr,
                                    (int)ctx->n, (int)ctx->n, st.p, 0, s));
+  // basis pass: U' = Y W_r Sigma_r^{-1}
   TsArgs tb{};
   tb.M = (int)ctx->M;
-  tb.u = ud;
+  tb.u = yd;
   tb.rk = st.rk;
-  tb.T = w.Z;
+  tb.T = w.Wz;
   tb.ldt = w.capp;
   tb.d_p = st.rk + rank_slot;
   tb.out = Uout;

@@ -90,6 +90,9 @@ struct TsArgs {
   double* out;              // STORE: M x p (ld ldo)
   int ldo;
   int t_lower;              // T[c][i] == 0 for i > c (T1 = R_V^T): skip the zero blocks
+  int t_upper;              // T[c][i] == 0 for c > i (T = R1^{-1}): skip the zero blocks
+  double* yout;             // GRAM: optional copy of the X tile (M x pmax, ld ldy, columns >= p are 0)
+  int ldy;
   int u16;                  // (set by launch_ts) all Ucat blocks 16-byte aligned with even ld/offsets
   int o16;                  // (set by launch_ts) STORE rows 16-byte aligned (even ldo)
   int dbg;                  // (set by launch_ts; developer bisection, env LRCHEB_TS_DBG) 1: no copies,

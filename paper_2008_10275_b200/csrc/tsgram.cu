@@ -163,6 +163,31 @@ __device__ __forceinline__ void mma_row(double (&x0)[PT][2], double a0, const do
   }
 }
 #undef LRC_TS_MMA
+// Same for n-tiles [nstart, PT) (T upper triangular: tiles with all i < c are zero).
+#define LRC_TS_MMA(n) if constexpr ((n) < PT) dmma884(x0[n], a0, bt[(n) * 8])
+template <int PT>
+__device__ __forceinline__ void mma_row_from(double (&x0)[PT][2], double a0, const double* bt, int nstart) {
+  switch (nstart) {
+    case 0: LRC_TS_MMA(0); [[fallthrough]];
+    case 1: LRC_TS_MMA(1); [[fallthrough]];
+    case 2: LRC_TS_MMA(2); [[fallthrough]];
+    case 3: LRC_TS_MMA(3); [[fallthrough]];
+    case 4: LRC_TS_MMA(4); [[fallthrough]];
+    case 5: LRC_TS_MMA(5); [[fallthrough]];
+    case 6: LRC_TS_MMA(6); [[fallthrough]];
+    case 7: LRC_TS_MMA(7); [[fallthrough]];
+    case 8: LRC_TS_MMA(8); [[fallthrough]];
+    case 9: LRC_TS_MMA(9); [[fallthrough]];
+    case 10: LRC_TS_MMA(10); [[fallthrough]];
+    case 11: LRC_TS_MMA(11); [[fallthrough]];
+    case 12: LRC_TS_MMA(12); [[fallthrough]];
+    case 13: LRC_TS_MMA(13); [[fallthrough]];
+    case 14: LRC_TS_MMA(14); [[fallthrough]];
+    case 15: LRC_TS_MMA(15); [[fallthrough]];
+    default: break;
+  }
+}
+#undef LRC_TS_MMA
 
 // Gram contribution of the parked 128-row X tile to one 2x2 super tile (I0, J0) of G (8x8 tiles):
 // KIND 0 full, 1 diagonal (the lower tile is skipped), 2 last column of odd PT (J0+1 absent),
@@ -288,7 +313,10 @@ ts_kernel(TsArgs a) {
         if (a.t_lower) nact = min(nact, (k0 + kk + 3) / 8 + 1);
         if (a.dbg & 4) nact = 0;
         const double a0 = s_u[(warp * 8 + gid) * kSU + kk + tig];
-        mma_row<PT>(x0, a0, s_t + (kk + tig) * SX + gid, nact);
+        if (a.t_upper && nact > 0 && k0 + kk >= 8)   // T = R1^{-1}: tiles with all i < c are zero
+          mma_row_from<PT>(x0, a0, s_t + (kk + tig) * SX + gid, (k0 + kk) >> 3);
+        else
+          mma_row<PT>(x0, a0, s_t + (kk + tig) * SX + gid, nact);
         if (pm0 >= 0) issue_part<PT>(a, c2, kk / 4, w, tid);
       }
       if (pm0 >= 0) { cp_commit(); issued = g + 2; }
@@ -305,6 +333,15 @@ ts_kernel(TsArgs a) {
     }
     __syncthreads();
     if constexpr (MODE == 0) {
+      if (a.yout) {   // Y = this X tile (all PMAX columns; the ones >= p are exact zeros)
+        constexpr int HP = S::HP;
+        for (int e = tid; e < kBM * HP; e += kThreads) {
+          const int i = e / HP, j = 2 * (e - (e / HP) * HP);
+          if (m0 + i < a.M)
+            *reinterpret_cast<double2*>(a.yout + (size_t)(m0 + i) * a.ldy + j) =
+                *reinterpret_cast<const double2*>((i < 64 ? xh0 : xh1) + (i & 63) * SX + j);
+        }
+      }
 #pragma unroll
       for (int s = 0; s < S::SPW; ++s) {
         if (sI[s] < 0 || (a.dbg & 2)) continue;
