@@ -279,19 +279,24 @@ def main():
     step(0, c=0)
     prof = ctx.profile()
     ctx.set_profiling(False)
-    # the roofline entry "ts_gram" covers both Gram passes (pass 1 T = R_V^T, pass 2 T = R_V^T R1^-1)
-    g1, g2 = prof.pop("ts_gram", (0.0, 0)), prof.pop("ts_gram2", (0.0, 0))
-    prof["ts_gram"] = (g1[0] + g2[0], g1[1] + g2[1])
+    g1, g2 = prof.get("ts_gram", (0.0, 0)), prof.get("ts_gram2", (0.0, 0))
     gram_split = {"pass1_avg_ms": g1[0] / max(g1[1], 1), "pass2_avg_ms": g2[0] / max(g2[1], 1)}
     step_ms = sum(v[0] for v in prof.values())
-    dom = max(prof.items(), key=lambda kv: kv[1][0])
     M, nnz, r, rB = op.M, op.nnz, cfg.rank_cap, cfg.r_B
     w = rB + 4 * r
     p = min(n, w)
-    # algorithmic work per launch at steady state
-    flops_gram = 2.0 * M * w * p + 1.0 * M * p * (p + 1)
-    flops_store = 2.0 * M * w * r
-    bytes_spmm = 52.0 * nnz + 4.0 * (M + 1) + 32.0 * M * r
+    # algorithmic (structurally necessary) work per launch at steady state:
+    #   pass 1  Y = Ucat R_V^T (R_V^T lower trapezoidal) + G1 = Y^T Y (symmetric)
+    #   pass 2  Q1 = Y R1^{-1} (upper triangular) + G2 = Q1^T Q1
+    #   basis   U' = Y W_r Sigma_r^{-1}
+    flops = {"spmm": 6.0 * nnz * r,
+             "ts_gram": 2.0 * M * (w * p - p * (p - 1) / 2.0) + 1.0 * M * p * (p + 1),
+             "ts_gram2": 1.0 * M * p * (p + 1) + 1.0 * M * p * (p + 1),
+             "ts_store": 2.0 * M * p * r}
+    byts = {"spmm": 52.0 * nnz + 4.0 * (M + 1) + 32.0 * M * r,
+            "ts_gram": 8.0 * M * w + 8.0 * M * p, "ts_gram2": 8.0 * M * p, "ts_store": 8.0 * M * p + 8.0 * M * r}
+    bytes_spmm = byts["spmm"]
+
     def kernel_entry(name):
         ms_tot, cnt = prof[name]
         avg = ms_tot / max(cnt, 1)
@@ -299,16 +304,17 @@ def main():
             ach = bytes_spmm / (avg / 1e3) / 1e9
             return {"bound": "hbm", "achieved": ach, "peak": hbm_peak(), "unit": "GB/s",
                     "frac": ach / hbm_peak(), "avg_ms": avg, "launches": cnt, "share": ms_tot / step_ms}
-        fl = flops_gram if name == "ts_gram" else flops_store
-        ach = fl / (avg / 1e3) / 1e12
+        ach = flops[name] / (avg / 1e3) / 1e12
         return {"bound": "tensor", "achieved": ach, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": ach / FP64_DMMA_PEAK_TFLOPS, "avg_ms": avg, "launches": cnt, "share": ms_tot / step_ms}
-    roof = kernel_entry(dom[0]) if dom[0] in ("spmm", "ts_gram", "ts_store") else None
-    if roof:
-        roof["kernel"] = dom[0]
-        roof["traffic"] = ncu_traffic(dom[0])
-        roof["peak_source"] = ("MEASURED_PEAKS.json hbm_gbs" if roof["unit"] == "GB/s" else
-                               "measured DMMA m8n8k4 fp64 (profiles/r01_phase0_fp64_peaks.jsonl)")
+    cand = {k: v for k, v in prof.items() if k in flops}
+    dom = max(cand.items(), key=lambda kv: kv[1][0])
+    roof = kernel_entry(dom[0])
+    roof["kernel"] = dom[0]
+    roof["traffic"] = ncu_traffic(dom[0])
+    roof["peak_source"] = ("MEASURED_PEAKS.json hbm_gbs" if roof["unit"] == "GB/s" else
+                           "measured DMMA m8n8k4 fp64 (profiles/r01_phase0_fp64_peaks.jsonl)")
+    kernels = {k: kernel_entry(k) for k in cand}
 
     # ---- BASELINE config 5 (full-rank direct approach): fused six-term operator on a dense M x 256 S,
     #      D_mu / D_nu from a 16 x 16 parameter grid, 20 repetitions, HBM GB/s vs the same roofline
@@ -340,13 +346,14 @@ def main():
 
     # ---- the whole iteration against its roofline: per kernel max(flops / fp64 peak, bytes / HBM peak),
     #      summed over the M-level kernels of one steady-state iteration
-    it_parts = {"spmm": (6.0 * nnz * r, bytes_spmm), "ts_gram_x2": (2 * flops_gram, 2 * 8.0 * M * w),
-                "ts_store": (flops_store, 8.0 * M * w + 8.0 * M * r)}
+    it_parts = {k: (flops[k], byts[k]) for k in flops}
     t_roof = sum(max(f / (FP64_DMMA_PEAK_TFLOPS * 1e12), b / (hbm_peak() * 1e9)) for f, b in it_parts.values())
     t_meas = 1.0 / value
     iteration_roofline = {"flops": sum(f for f, _ in it_parts.values()), "bytes": sum(b for _, b in it_parts.values()),
                           "roofline_ms": t_roof * 1e3, "measured_ms_per_iteration": t_meas * 1e3,
                           "frac": t_roof / t_meas,
+                          "per_kernel_ms": {k: max(f / (FP64_DMMA_PEAK_TFLOPS * 1e9), b / (hbm_peak() * 1e6))
+                                            for k, (f, b) in it_parts.items()},
                           "bound": "fp64 tensor (the Gram / basis passes); the SpMM alone is HBM-bound"}
 
     result = {
@@ -366,6 +373,7 @@ def main():
         "clocks": clocks,
         "roofline": roof,
         "roofline_spmm": kernel_entry("spmm"),
+        "roofline_kernels": kernels,
         "iteration_roofline": iteration_roofline,
         "config5_dense_spmm": dense,
         "kernel_ms_per_step": {k: v[0] for k, v in prof.items()},

@@ -321,6 +321,32 @@ ts_kernel(TsArgs a) {
       }
       if (pm0 >= 0) { cp_commit(); issued = g + 2; }
     }
+    if (MODE == 0 && a.yout) {
+      // Y = this X tile straight from the accumulators (all PMAX columns; the ones >= p are exact
+      // zeros): fire-and-forget 16-byte evict-first stores, full 32-byte sectors per quad
+      const int row = m0 + warp * 8 + gid;
+      if (row < a.M) {
+        double* yr = a.yout + (size_t)row * a.ldy + 2 * tig;
+#pragma unroll
+        for (int n = 0; n < PT; ++n) __stcs(reinterpret_cast<double2*>(yr + n * 8), make_double2(x0[n][0], x0[n][1]));
+      }
+    }
+    if (MODE == 1 && a.o16) {
+      // rows of U_{k+1} straight from the accumulators (16-byte evict-first stores, full sectors);
+      // the padded (solver) mode also writes the zero pad column of an odd rank
+      const int pw = (a.dbg & 2) ? 0 : p + (a.u.pad_even ? (p & 1) : 0);
+      const int row = m0 + warp * 8 + gid;
+      if (row < a.M) {
+        double* orow = a.out + (size_t)row * a.ldo;
+#pragma unroll
+        for (int n = 0; n < PT; ++n) {
+          const int c = n * 8 + 2 * tig;
+          if (c + 1 < pw) __stcs(reinterpret_cast<double2*>(orow + c), make_double2(x0[n][0], x0[n][1]));
+          else if (c < pw) __stcs(orow + c, x0[n][0]);
+        }
+      }
+      continue;
+    }
     // X tile -> the two stages not holding the next tile's chunk 0 (chunk g, if issued)
     __syncthreads();   // every warp is done with the last chunk
     double* xh0 = sm + ((g + 1) % 3) * S::STAGE;   // rows 0..63
@@ -333,15 +359,6 @@ ts_kernel(TsArgs a) {
     }
     __syncthreads();
     if constexpr (MODE == 0) {
-      if (a.yout) {   // Y = this X tile (all PMAX columns; the ones >= p are exact zeros)
-        constexpr int HP = S::HP;
-        for (int e = tid; e < kBM * HP; e += kThreads) {
-          const int i = e / HP, j = 2 * (e - (e / HP) * HP);
-          if (m0 + i < a.M)
-            *reinterpret_cast<double2*>(a.yout + (size_t)(m0 + i) * a.ldy + j) =
-                *reinterpret_cast<const double2*>((i < 64 ? xh0 : xh1) + (i & 63) * SX + j);
-        }
-      }
 #pragma unroll
       for (int s = 0; s < S::SPW; ++s) {
         if (sI[s] < 0 || (a.dbg & 2)) continue;
@@ -365,8 +382,8 @@ ts_kernel(TsArgs a) {
           const int m = m0 + i;
           const double* xr = (i < 64 ? xh0 : xh1) + (i & 63) * SX + j;
           if (m < a.M && j < pw) {
-            if (j + 1 < pw) *reinterpret_cast<double2*>(a.out + (size_t)m * a.ldo + j) = *reinterpret_cast<const double2*>(xr);
-            else a.out[(size_t)m * a.ldo + j] = xr[0];
+            if (j + 1 < pw) __stcs(reinterpret_cast<double2*>(a.out + (size_t)m * a.ldo + j), *reinterpret_cast<const double2*>(xr));
+            else __stcs(a.out + (size_t)m * a.ldo + j, xr[0]);
           }
         }
       } else {
