@@ -49,7 +49,6 @@ struct Workspace {
   double* sigma = nullptr;    // (N+2) x 128
   double* scal = nullptr;     // 8
   double* T1 = nullptr; double* QV = nullptr; double* G = nullptr; double* R1 = nullptr;
-  double* T2 = nullptr; double* Z = nullptr;
   double* R1i = nullptr; double* Wz = nullptr; double* Wv = nullptr;
   double* W0 = nullptr; double* Wfull = nullptr; double* Bprev = nullptr;
   double* partials = nullptr;
@@ -179,7 +178,7 @@ void free_ws(Workspace& w) {
   dfree(w.BUb); dfree(w.W3);
   for (int i = 0; i < 3; ++i) { dfree(w.Ubuf[i]); dfree(w.Vbuf[i]); }
   dfree(w.BV); dfree(w.omega); dfree(w.ints); dfree(w.sigma); dfree(w.scal);
-  dfree(w.T1); dfree(w.QV); dfree(w.G); dfree(w.R1); dfree(w.T2); dfree(w.Z); dfree(w.Y);
+  dfree(w.T1); dfree(w.QV); dfree(w.G); dfree(w.R1); dfree(w.Y);
   dfree(w.R1i); dfree(w.Wz); dfree(w.Wv); dfree(w.W0); dfree(w.Wfull); dfree(w.Bprev);
   dfree(w.partials); dfree(w.Uh); dfree(w.Vh); dfree(w.tmpA); dfree(w.tmpB); dfree(w.tmpC);
   w = Workspace();
@@ -230,8 +229,6 @@ lrc_status ensure_ws(lrc_ctx* ctx, int rb, int cap, int N, int wmax, bool record
   CK(dalloc(&w.QV, n * pmax));
   CK(dalloc(&w.G, (size_t)pmax * pmax));
   CK(dalloc(&w.R1, (size_t)pmax * pmax));
-  CK(dalloc(&w.T2, (size_t)wmax * pmax));
-  CK(dalloc(&w.Z, (size_t)wmax * capp));
   CK(dalloc(&w.R1i, (size_t)pmax * pmax));
   CK(dalloc(&w.Wz, (size_t)pmax * capp));
   CK(dalloc(&w.Wv, (size_t)pmax * capp));
@@ -279,7 +276,7 @@ State make_state(Workspace& w) {
 
 SmallBufs make_bufs(Workspace& w) {
   SmallBufs b{};
-  b.T1 = w.T1; b.QV = w.QV; b.G = w.G; b.R1 = w.R1; b.T2 = w.T2; b.Z = w.Z;
+  b.T1 = w.T1; b.QV = w.QV; b.G = w.G; b.R1 = w.R1;
   b.R1i = w.R1i; b.Wz = w.Wz; b.Wv = w.Wv;
   b.W0 = nullptr; b.Wfull = w.Wfull; b.Bprev = w.Bprev;
   b.ldT = w.pmax; b.ldZ = w.capp;

@@ -136,14 +136,12 @@ struct SmallBufs {
   double* QV;     // n x pmax   (Q_V[:, :p])
   double* G;      // pmax x pmax reduced Gram
   double* R1;     // pmax x pmax
-  double* T2;     // w x pmax   (R_V^T R1^{-1})
   double* R1i;    // pmax x pmax (R1^{-1}, upper)
   double* Wz;     // pmax x ldZ  (W_r Sigma_r^{-1})
   double* Wv;     // pmax x ldZ  (W_r Sigma_r)
   double* W0;     // pmax x pmax (warm-start basis Q_V^T B_prev), null: warm start off
   double* Wfull;  // pmax x pmax (full right basis W of the core)
   double* Bprev;  // n x pmax    (Q_V W of the previous iteration)
-  double* Z;      // w x capp   (R_V^T W_r Sigma_r^{-1})
   int ldT;        // = pmax
   int ldZ;        // = capp
 };
@@ -152,9 +150,9 @@ struct SmallBufs {
 cudaError_t launch_vside(const VDesc& d, int n, const double* dmu, const double* dnu,
                          const double* omega, int k, State st, SmallBufs b, int wmax,
                          cudaStream_t s);
-// chol1: R1 = chol(G + s1 I) (escalating), T2 = T1 R1^{-1}
+// chol1: R1 = chol(G + s1 I) (escalating), R1^{-1}
 cudaError_t launch_chol1(State st, SmallBufs b, int pmax, int wmax, cudaStream_t s);
-// chol2 + SVD: R2 = chol(G + s2 I), R = R2 R1, Jacobi SVD, rank rule, Z, V'
+// chol2 + SVD: R2 = chol(G + s2 I), R = R2 R1, Jacobi SVD, rank rule, W_r Sigma_r^{-1}, V'
 cudaError_t launch_chol2_svd(State st, SmallBufs b, int pmax, int wmax, int n, double tol,
                              int cap, int rank_slot, int sigma_row, double* Vout, int ldv,
                              cudaStream_t s);

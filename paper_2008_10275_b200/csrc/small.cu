@@ -6,13 +6,13 @@
 //                the D_mu/D_nu scaling is applied on the V side only), then its
 //                Householder QR  Vcat = Q_V [R_V; 0]  (p = min(n, w)).  Writes T1 = R_V^T (w x p)
 //                and Q_V[:, :p] (n x p).  X = Ucat Vcat^T = (Ucat R_V^T) Q_V^T, so the left factor
-//                to re-orthogonalise is Y = Ucat R_V^T (M x p, formed tile by tile, never stored).
-//   chol1      : R1 = chol(G1 + s1 I), s1 = delta tr(G1) (escalated x100 on breakdown),
-//                T2 = T1 R1^{-1}  (pass 2 then forms Q1 = Ucat T2 = Y R1^{-1} tile by tile).
+//                to re-orthogonalise is Y = Ucat R_V^T (M x p, formed and stored by Gram pass 1).
+//   chol1      : R1 = chol(G1 + s1 I), s1 = delta tr(G1) (escalated x100 on breakdown), and
+//                R1^{-1} (pass 2 then forms Q1 = Y R1^{-1} tile by tile from the stored Y).
 //   chol2_svd  : R2 = chol(G2 + s2 I) (s2 = 0 first, escalated on breakdown), R = R2 R1,
 //                one-sided (Hestenes) Jacobi SVD R = P Sigma W^T, rank rule
 //                r' = min(cap, #{sigma_i > tol sigma_1}) (reading S5), and
-//                Z = R_V^T W_r Sigma_r^{-1} (so U_{k+1} = Ucat Z = Q_Y P_r),  V_{k+1} = Q_V W_r Sigma_r.
+//                Wz = W_r Sigma_r^{-1} (so U_{k+1} = Y Wz = Q_Y P_r),  V_{k+1} = Q_V W_r Sigma_r.
 #include <cmath>
 #include "lrc_internal.cuh"
 
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kT) vside_kernel(VDesc d, int n, const double*
 }
 
 // ------------------------------------------------------------------------------------------
-// chol1: R1 = chol(G1 + s1 I); T2 = T1 R1^{-1}
+// chol1: R1 = chol(G1 + s1 I); R1^{-1}
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kT) chol1_kernel(State st, SmallBufs b, int pmax) {
   extern __shared__ double sm[];
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kT) chol1_kernel(State st, SmallBufs b, int pm
     for (int j = i + tid; j < p; j += kT) s_r[i * LD + j] = s_row[j];
     __syncthreads();
   }
-  // R1^{-1} (upper) -> global; T2 = T1 R1^{-1} is a multi-CTA tiny GEMM (tiny_gemm_kernel)
+  // R1^{-1} (upper, zero outside p x p) -> global: the T matrix of Gram pass 2 (Q1 = Y R1^{-1})
   for (int e = tid; e < pmax * pmax; e += kT) {
     const int i = e / pmax, c = e - (e / pmax) * pmax;
     b.R1i[e] = (i < p && c < p && c >= i) ? s_r[i * LD + c] : 0.0;
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(kT) chol2_svd_kernel(State st, SmallBufs b, in
   if (sigma_row >= 0)
     for (int i = tid; i < kSigmaStride; i += kT)
       st.sigma[(size_t)sigma_row * kSigmaStride + i] = (i < p) ? s_sig[s_perm[i]] : 0.0;
-  // Wz = W_r Sigma_r^{-1}, Wv = W_r Sigma_r (p x ldZ) for the tiny GEMMs Z = T1 Wz, V' = Q_V Wv
+  // Wz = W_r Sigma_r^{-1} (basis pass U' = Y Wz), Wv = W_r Sigma_r (V' = Q_V Wv), p x ldZ
   for (int e = tid; e < pmax * b.ldZ; e += kT) {
     const int k = e / b.ldZ, q = e - (e / b.ldZ) * b.ldZ;
     double wz = 0.0, wv = 0.0;
