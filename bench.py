@@ -334,10 +334,10 @@ def main():
             Y5 = ctx5.apply_dense(S5)
             kms.append(ctx5.last_kernel_ms())
         avg = float(np.mean(kms))
-        byts = 52.0 * nnz + 4.0 * (M + 1) + 16.0 * M * cfg5.dense_cols
+        byts5 = 52.0 * nnz + 4.0 * (M + 1) + 16.0 * M * cfg5.dense_cols
         dense = {"workload": f"config 5: M={M} dense S M x {cfg5.dense_cols}, {cfg5.reps} repetitions",
-                 "avg_ms": avg, "achieved": byts / (avg / 1e3) / 1e9, "unit": "GB/s", "peak": hbm_peak(),
-                 "frac": byts / (avg / 1e3) / 1e9 / hbm_peak(),
+                 "avg_ms": avg, "achieved": byts5 / (avg / 1e3) / 1e9, "unit": "GB/s", "peak": hbm_peak(),
+                 "frac": byts5 / (avg / 1e3) / 1e9 / hbm_peak(),
                  "tflops": 6.0 * nnz * cfg5.dense_cols / (avg / 1e3) / 1e12,
                  "tensor_frac": 6.0 * nnz * cfg5.dense_cols / (avg / 1e3) / 1e12 / FP64_DMMA_PEAK_TFLOPS,
                  "bound": "tensor (6 nnz ncols fp64 flops at the DMMA peak outlast the bytes at the HBM peak)"}
