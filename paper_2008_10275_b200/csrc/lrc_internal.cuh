@@ -96,7 +96,7 @@ struct TsArgs {
   int u16;                  // (set by launch_ts) all Ucat blocks 16-byte aligned with even ld/offsets
   int o16;                  // (set by launch_ts) STORE rows 16-byte aligned (even ldo)
   int dbg;                  // (set by launch_ts; developer bisection, env LRCHEB_TS_DBG) 1: no copies,
-                            // 2: no Gram / store epilogue, 4: no phase-A DMMA
+                            // 2: no Gram / store epilogue, 4: no phase-A DMMA, 8: no Y stores
 };
 // mode 0 = GRAM (partial X^T X, X = Ucat T), 1 = STORE (out = Ucat T)
 cudaError_t launch_ts(int mode, const TsArgs& a, int pmax, int grid, cudaStream_t s);

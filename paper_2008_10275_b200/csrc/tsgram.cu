@@ -321,7 +321,7 @@ ts_kernel(TsArgs a) {
       }
       if (pm0 >= 0) { cp_commit(); issued = g + 2; }
     }
-    if (MODE == 0 && a.yout) {
+    if (MODE == 0 && a.yout && !(a.dbg & 8)) {
       // Y = this X tile straight from the accumulators (all PMAX columns; the ones >= p are exact
       // zeros): fire-and-forget 16-byte evict-first stores, full 32-byte sectors per quad
       const int row = m0 + warp * 8 + gid;
