@@ -182,6 +182,32 @@ __device__ __forceinline__ void cp_async16(double* smem, const double* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
 }
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
+  unsigned ok;
+  asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+               : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  while (!mbar_try(b, parity)) {}
+}
+
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
 // rows of U (r columns, ldu even, 16-byte aligned) -> s_u (row stride ust even) in 16-byte chunks
 __device__ __forceinline__ void stage_u_rows(const SpmmArgs& a, int r, const int* ids, int nu, double* su,
                                              int ust, int tid, int nthreads) {
@@ -534,7 +560,13 @@ spmm_u_kernel(SpmmArgs a, int ust) {
   __shared__ __align__(16) int s_desc[kDescInts];
   __shared__ int s_bstart[kTileBlocks + 1], s_vbase[kTileBlocks], s_lp[kTileBlocks];
   __shared__ float s_invL[kTileBlocks];
+  __shared__ __align__(8) unsigned long long ubar;   // U-row bulk copies (TMA) complete here
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool ubulk = a.u_aligned16 != 0;
+  if (tid == 0 && ubulk) {
+    mbar_init(&ubar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   const int CT = (r + 31) >> 5;
   // U tiles are stored first (tile = blockIdx.x); the value loads need only (e0, tot), fetched in
   // parallel with the descriptor, so they are issued before the descriptor arrives
@@ -558,8 +590,21 @@ spmm_u_kernel(SpmmArgs a, int ust) {
   }
   __syncthreads();
   const int nb = s_desc[2], nu = s_desc[3];
-  if (!(a.dbg & 2)) stage_u_rows(a, r, s_desc + kDescUrows, nu, s_u, ust, tid, kThreads);
-  asm volatile("cp.async.commit_group;\n" ::);
+  if (ubulk) {
+    // the tile's deduplicated U rows by TMA bulk copies (one per row, warp 0): this traffic stays off
+    // the LSU path the value loads and the contraction's shared-memory loads share
+    if (warp == 0) {
+      const unsigned ubytes = (unsigned)((r + 1) >> 1) * 16u;
+      const int nuc = (a.dbg & 2) ? 0 : nu;
+      if (lane == 0) mbar_expect_tx(&ubar, ubytes * (unsigned)nuc);
+      __syncwarp();
+      for (int u = lane; u < nuc; u += 32)
+        bulk_g2s(s_u + u * ust, a.U + (size_t)s_desc[kDescUrows + u] * a.ldu, ubytes, &ubar);
+    }
+  } else {
+    if (!(a.dbg & 2)) stage_u_rows(a, r, s_desc + kDescUrows, nu, s_u, ust, tid, kThreads);
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
   if (tid == 0) {
     int vb = 0, eb = 0;
     for (int b = 0; b < nb; ++b) {
@@ -598,7 +643,8 @@ spmm_u_kernel(SpmmArgs a, int ust) {
       if (j < ((L + 3) & ~3)) s_v[s_vbase[b] + (i >> 2) * lp + j] = 0.0;
     }
   }
-  asm volatile("cp.async.wait_all;\n" ::);
+  if (ubulk) mbar_wait(&ubar, 0);
+  else asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
   const unsigned short* lx = reinterpret_cast<const unsigned short*>(s_desc + kDescLidx);
   int cb = 0;
@@ -916,32 +962,6 @@ spmm_dense_kernel(SpmmArgs a) {
 constexpr int kTRaw = kSpmmCap + 2;                // doubles per raw value stream (alignment slack)
 constexpr int kTCompute = 256, kTThreads = kTCompute + 32;
 constexpr int kTRing = 4;                          // descriptor ring depth
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
-  unsigned ok;
-  asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-               : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
-  while (!mbar_try(b, parity)) {}
-}
-
-
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
 
 // dynamic shared memory: raw[2][6][kTRaw] | ustage[2][ustage] | sv[kValCap]
 size_t t_smem(int ustage) {
