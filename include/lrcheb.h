@@ -117,7 +117,11 @@ typedef struct {
  * Outputs: U_out M x rank_cap (ld_u >= rank_cap), V_out n x rank_cap (ld_v >= rank_cap);
  * columns >= info->rank are set to 0.  U has orthonormal columns, V = Y Sigma (reading S12).
  * where: HOST (pointers are host memory; copies are inside the call) or DEVICE.
- * info may be NULL. */
+ * info may be NULL.
+ * Device workspace (kept in ctx between calls, reallocated when a shape grows): about
+ * 8 * M * (r_B + 3 rank_cap + 3 rank_cap + pmax) bytes plus small buffers, pmax = 8 ceil(min(n,
+ * r_B + 4 rank_cap) / 8) -- B_U, the three grouped SpMM outputs, three rotating U factors and
+ * Y = Ucat R_V^T of the truncation (about 4.8 GB on BASELINE's Large config). */
 lrc_status lrc_solve(lrc_ctx *ctx,
                      const double *B_U, int64_t ld_bu, const double *B_V, int64_t ld_bv, int64_t r_B,
                      const lrc_solve_opts *opts,
