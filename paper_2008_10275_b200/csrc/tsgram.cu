@@ -35,9 +35,25 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// mbarrier helpers for the stage handshakes of the chunk ring
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mb_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(b)), "r"(count));
+}
+__device__ __forceinline__ void mb_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(b)) : "memory");
+}
+// arrives once all of this thread's earlier cp.async copies have landed
+__device__ __forceinline__ void mb_arrive_cp(unsigned long long* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(unsigned long long* b, unsigned parity) {
+  unsigned ok = 0;
+  while (!ok)
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(ok) : "r"(smem_addr(b)), "r"(parity) : "memory");
+}
 
 // column offsets of the Ucat blocks (off[nb] = w)
 __device__ __forceinline__ int ucat_offsets(const TsArgs& a, int (&off)[kMaxUBlocks + 1]) {
@@ -260,16 +276,25 @@ ts_kernel(TsArgs a) {
 
   const int nk = (w + kBK - 1) / kBK;
   // Chunks of all this CTA's tiles form one sequence g = 0, 1, ...; chunk g lives in stage g % 3.
-  // Chunk g+1 is in flight while g is computed and g+2 is issued during g's DMMA steps, except that
-  // at most the next tile's chunk 0 is prefetched across a tile boundary: the X tile of the
-  // epilogue is parked (as two 64-row halves) in the two stages that chunk does not use.
+  // Chunk g+1 is in flight while g is computed and g+2 is issued during the second half of g's DMMA
+  // steps, except that at most the next tile's chunk 0 is prefetched across a tile boundary: the X
+  // tile of the epilogue is parked (as two 64-row halves) in the two stages that chunk does not use.
+  // Stage hand-offs are mbarriers instead of CTA barriers: full[s] completes when every thread's
+  // copies of the chunk in stage s have landed (cp.async arrive-on), empty[s] when every warp has
+  // contracted it; use count u of a stage -> parity u & 1.
+  __shared__ __align__(8) unsigned long long full[3], empty[3];
+  if (tid == 0) {
+    for (int i = 0; i < 3; ++i) { mb_init(&full[i], kThreads); mb_init(&empty[i], kWarps); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  auto produce_wait = [&](int h) { if (h >= 3) mb_wait(&empty[h % 3], ((h / 3) - 1) & 1); };
   int g = 0, issued = 0;
-  __syncthreads();   // off[]
+  __syncthreads();   // off[], barriers
   {
     const ChunkPlan c0 = plan_chunk<PT>(a, sbase, blockIdx.x * kBM, 0, w, off, tid);
 #pragma unroll
     for (int part = 0; part < 8; ++part) issue_part<PT>(a, c0, part, w, tid);
-    cp_commit();
+    mb_arrive_cp(&full[0]);
   }
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int m0 = tile * kBM;
@@ -279,21 +304,22 @@ ts_kernel(TsArgs a) {
     for (int n = 0; n < PT; ++n) x0[n][0] = x0[n][1] = 0.0;
 
     for (int kc = 0; kc < nk; ++kc, ++g) {
-      if (issued > g) cp_wait<1>(); else cp_wait<0>();
-      __syncthreads();   // chunk g visible to all; every warp is done with chunk g-1 (and the X tile)
+      if (kc == 0) __syncthreads();   // tile start: the previous tile's X halves are fully consumed
       if (issued == g) {
         // (tile start without prefetch) chunk g+1 now, before computing g
         int nm0 = -1, nk0 = 0;
         if (kc + 1 < nk) { nm0 = m0; nk0 = (kc + 1) * kBK; }
         else if (has_next) { nm0 = m0 + gridDim.x * kBM; nk0 = 0; }
         if (nm0 >= 0) {
+          produce_wait(g + 1);
           const ChunkPlan c1 = plan_chunk<PT>(a, sbase + 8u * S::STAGE * ((g + 1) % 3), nm0, nk0, w, off, tid);
 #pragma unroll
           for (int part = 0; part < 8; ++part) issue_part<PT>(a, c1, part, w, tid);
-          cp_commit();
+          mb_arrive_cp(&full[(g + 1) % 3]);
           issued = g + 1;
         }
       }
+      mb_wait(&full[g % 3], (g / 3) & 1);   // chunk g has landed
       // chunk g+2 (this tile's kc+2, or the next tile's chunk 0) is issued during the DMMA steps
       int pm0 = -1, pk0 = 0;
       if (issued == g + 1) {
@@ -317,9 +343,16 @@ ts_kernel(TsArgs a) {
           mma_row_from<PT>(x0, a0, s_t + (kk + tig) * SX + gid, (k0 + kk) >> 3);
         else
           mma_row<PT>(x0, a0, s_t + (kk + tig) * SX + gid, nact);
-        if (pm0 >= 0) issue_part<PT>(a, c2, kk / 4, w, tid);
+        // second half of the chunk: the stage of chunk g-1 is (almost surely) free by now
+        if (pm0 >= 0 && kk >= kBK / 2) {
+          if (kk == kBK / 2) produce_wait(g + 2);
+          issue_part<PT>(a, c2, 2 * ((kk - kBK / 2) / 4), w, tid);
+          issue_part<PT>(a, c2, 2 * ((kk - kBK / 2) / 4) + 1, w, tid);
+        }
       }
-      if (pm0 >= 0) { cp_commit(); issued = g + 2; }
+      if (pm0 >= 0) { mb_arrive_cp(&full[(g + 2) % 3]); issued = g + 2; }
+      __syncwarp();
+      if (lane == 0) mb_arrive(&empty[g % 3]);   // this warp is done with stage g % 3
     }
     if (MODE == 0 && a.yout && !(a.dbg & 8)) {
       // Y = this X tile straight from the accumulators (all PMAX columns; the ones >= p are exact
