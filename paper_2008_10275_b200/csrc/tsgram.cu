@@ -304,7 +304,9 @@ ts_kernel(TsArgs a) {
     for (int n = 0; n < PT; ++n) x0[n][0] = x0[n][1] = 0.0;
 
     for (int kc = 0; kc < nk; ++kc, ++g) {
-      if (kc == 0) __syncthreads();   // tile start: the previous tile's X halves are fully consumed
+      // tile start: the previous tile's X halves are fully consumed (the direct-store basis pass
+      // parks no X tile)
+      if (kc == 0 && !(MODE == 1 && a.o16)) __syncthreads();
       if (issued == g) {
         // (tile start without prefetch) chunk g+1 now, before computing g
         int nm0 = -1, nk0 = 0;
