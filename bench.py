@@ -361,8 +361,7 @@ def main():
         "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded FE-like operator, DESIGN.md input recipe)",
-        "config": {"workload": f"{cfg.name}: M={M} nnz/matrix={nnz} n={n} r_B={rB} cap={r} tol={cfg.tol} "
-                               f"N={N} iterations per subset solve",
+        "config": {"workload": workload_str(cfg, op, n),
                    "step": "one full ChebyshevT solve of one parameter subset (N iterations + final residual)",
                    "subsets_per_rank": len(my_subsets), "parallelism": f"subsets round-robin over {world} GPU(s)",
                    "concurrent_subsets_per_gpu": S, "reserved_sms": reserve,
@@ -413,6 +412,12 @@ def ncu_traffic(kernel):
         return None
 
 
+def workload_str(cfg, op, n):
+    """The workload named in both arms' `config` (same string, so the driver compares like with like)."""
+    return (f"{cfg.name}: M={op.M} nnz/matrix={op.nnz} n={n} r_B={cfg.r_B} cap={cfg.rank_cap} tol={cfg.tol} "
+            f"N={cfg.n_iter} iterations per subset solve")
+
+
 def run_reference(args, rank, world):
     """The oracle as it stands, timed on host cores on a row-sampled piece of our config's workload."""
     from synth import generator as gen
@@ -435,7 +440,9 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": "ChebyshevT iterations/sec (fused-SpMM HBM GB/s in roofline_spmm)",
         "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic", "config": {"workload": f"{cfg.name} (row-sampled)"},
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_str(cfg, op, len(prob.subset(0)[0])),
+                   "sampling": "each step times one steady-state oracle iteration on a row block; see sample"},
         "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": cpu_cores(), "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
