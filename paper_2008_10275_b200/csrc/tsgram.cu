@@ -1,20 +1,23 @@
 // a3 / a4 / a6 -- tall-skinny fp64 DMMA kernels of the truncation (
 // truncation operator T of PAPER.md P:544).
 //
-// All three M-level passes of the truncation have the same shape: a row tile of the logical
-// concatenation Ucat = [A | B] (M x w, two strided blocks, widths read from device-resident ranks)
-// is multiplied by a small w x p matrix T held in L2, on the fp64 tensor pipe
-// (mma.sync.m8n8k4.f64, "DMMA"), and the p-wide tile X = Ucat_tile T is then either
+// All three M-level passes of the truncation have the same shape: a row tile of a logical
+// concatenation of strided blocks (M x w, up to five blocks, widths read from device-resident
+// ranks and padded to even) is multiplied by a small w x p matrix T held in L2, on the fp64 tensor
+// pipe (mma.sync.m8n8k4.f64, "DMMA"), and the p-wide tile X = U_tile T is then either
 //   GRAM  : contracted with itself, G += X^T X (upper 8x8 tiles in 2x2 register blocks, DMMA),
 //           accumulated in registers across the CTA's tiles and written once as a per-CTA partial
-//           (deterministic fixed-order reduction in gram_reduce_kernel), or
-//   STORE : written out (U_{k+1} = Ucat Z, row-major).
-// Gram pass 1 uses T = R_V^T, pass 2 T = R_V^T R1^{-1}, the basis GEMM T = Z.
+//           (deterministic fixed-order reduction in gram_reduce_kernel); optionally X itself is
+//           written out (pass 1 keeps Y), or
+//   STORE : written out (U_{k+1}, row-major).
+// Pass 1: U = Ucat = [B_U | W0' | W1 | W2 | U_{k-1}], T = R_V^T (lower trapezoidal), X = Y stored.
+// Pass 2: U = Y, T = R1^{-1} (upper triangular).  Basis pass: U = Y, T = W_r Sigma_r^{-1}.
 //
 // Tile: 128 rows x p, 16 warps, warp w owns rows [8w, 8w+8) (one 8-row DMMA tile) and all p
-// columns.  The K loop streams 32-column chunks of Ucat and 32-row chunks of T into a cp.async
-// double buffer (8-byte copies: the two Ucat blocks meet at an odd column; zero fill past M / w).
-// The X tile is parked in the (then idle) stage buffers for the Gram / store epilogue.
+// columns.  The K loop streams 32-column chunks of U and 32-row chunks of T through a 3-stage
+// shared-memory ring (16-byte cp.async when every block is 16-byte aligned, else 8-byte; zero fill
+// past M / w) whose hand-offs are mbarriers.  The X tile of the Gram epilogue is parked in two of
+// the (then idle) stages.
 #include <cstdlib>
 
 #include "lrc_internal.cuh"
