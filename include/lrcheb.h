@@ -29,7 +29,7 @@
  *     synchronous) unless stated otherwise.  One ctx per host thread; no internal locking.
  *
  * Limits of this build (checked, LRC_ERR_ARG otherwise): M < 2^31, nnz < 2^31,
- *   rank_cap <= 128, r_B <= 64, min(n, r_B + 4 rank_cap) <= 128, n <= 1024,
+ *   rank_cap <= 128, r_B <= 64, min(n, r_B + 4 rank_cap) <= 112, n <= 1024,
  *   lrc_apply_dense: ncols <= 256.
  */
 #ifndef LRCHEB_H

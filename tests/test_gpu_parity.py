@@ -203,6 +203,31 @@ def test_solve_small_cold_jacobi_start():
     _solve_parity("small", 1, 30, warm_start=False)
 
 
+def test_solve_wide_parameter_block():
+    """n = 111 parameters in one subset (the build limit is min(n, w) <= 112): p grows to 111, an odd
+    width with the PT = 14 instantiations of the tall-skinny kernels (Y block 111 wide + its zero pad
+    column, R1^{-1} 111 x 111) against the oracle."""
+    require_gpu()
+    prob = problem("tiny")
+    op = prob.op
+    rng = np.random.default_rng(7)
+    n, r_B, tau, cap, N = 111, 3, 1e-12, 40, 8
+    # parameter values inside the grid's range keep the tiny spectrum bounds valid (monotone in mu, nu)
+    d_mu, d_nu = 0.5 + 1.5 * rng.random(n), 0.5 + 1.5 * rng.random(n)
+    BU, BV = rng.standard_normal((op.M, r_B)), rng.standard_normal((n, r_B))
+    ctx = make_ctx(op, d_mu, d_nu)
+    U, V, info = ctx.solve(BU, BV, prob.lam_min, prob.lam_max, tau, cap, N, record_iterates=True)
+    ref = orc.chebyshevt(oracle_terms(op, d_mu, d_nu), BU, BV, prob.lam_min, prob.lam_max, tau, cap, N)
+    for k in range(1, N + 1):
+        Uk, Vk, rk = ctx.get_iterate(k, cap)
+        Uo, Vo = ref.iterates[k - 1]
+        assert rk == ref.ranks[k - 1] or near_tie(ref.sigmas[k - 1], tau, cap, ref.ranks[k - 1]), (k, rk)
+        assert lowrank_rel_diff(Uk[:, :rk], Vk[:, :rk], Uo, Vo) <= 1e-8, k
+    assert max(ref.ranks) == cap                      # the cap binds, so p really reached min(n, w)
+    assert abs(info["rel_residual"] - ref.rel_residual) <= 1e-9
+    ctx.close()
+
+
 # The opt-in SpMM variants (persistent 2-CTA register prefetch, TMA-fed pipeline) are selected by
 # environment variables read once per process, so each runs in a child process.
 _VARIANT_CODE = r"""
