@@ -794,21 +794,19 @@ spmm_p_kernel(SpmmArgs a, int ust) {
 // fp64 tensor pipe, shared-memory-U tiles.  Per tile the six value streams are combined once into
 // the three grouped streams; S is then processed in 64-column chunks: the chunk of the tile's
 // deduplicated S rows is staged (16-byte cp.async), every warp contracts one (node block, 32-column
-// half) exactly like the hot kernel (transposed m16n8k4, D = S_chunk^T Vals^T), parks its D tile in
-// its own shared-memory slab and writes Y[row][c] = D[c][3q] + d_mu[c] D[c][3q+1] + d_nu[c] D[c][3q+2]
-// with coalesced row stores.
+// half) exactly like the hot kernel (transposed m16n8k4, D = S_chunk^T Vals^T) and combines the three
+// streams of D in registers (five quad shuffles) into Y[row][c] = D[c][3q] + d_mu[c] D[c][3q+1] +
+// d_nu[c] D[c][3q+2], stored as 64-byte row segments.  No D slab: ~75 KB of shared memory per CTA.
 constexpr int kDenseChunk = 64;
 constexpr int kDenseUst = kDenseChunk + 4;          // == 4 mod 16 doubles
-constexpr int kDenseDst = 17;                       // per-warp D slab row stride (odd: conflict free)
 
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 3)
 spmm_dense_kernel(SpmmArgs a) {
   const int ncols = a.r_fixed;
   extern __shared__ __align__(16) double smem_dyn[];
   double* s_v = smem_dyn;                                     // [kValCap]
   double* s_u = s_v + kValCap;                                // [kUCap][kDenseUst] (+32 slack)
-  double* s_d = s_u + kUCap * kDenseUst + 32;                 // [8 warps][32][kDenseDst]
   __shared__ __align__(16) int s_desc[kDescInts];
   __shared__ int s_bstart[kTileBlocks + 1], s_vbase[kTileBlocks], s_lp[kTileBlocks];
   __shared__ float s_invL[kTileBlocks];
@@ -870,7 +868,6 @@ spmm_dense_kernel(SpmmArgs a) {
     }
   }
   const unsigned short* lx = reinterpret_cast<const unsigned short*>(s_desc + kDescLidx);
-  double* slab = s_d + warp * 32 * kDenseDst;
   for (int c0 = 0; c0 < ncols; c0 += kDenseChunk) {
     const int cw = min(kDenseChunk, ncols - c0);
     __syncthreads();   // previous chunk fully consumed (and the staged values visible)
@@ -920,28 +917,40 @@ spmm_dense_kernel(SpmmArgs a) {
           dmma1684(acc[1][0], a10, a11, b0);
           dmma1684(acc[1][1], a10, a11, b1);
         }
-        // D[col m][slot n] -> slab[m][n]
+        // Y[row q][c] = D[c][3q] + d_mu[c] D[c][3q+1] + d_nu[c] D[c][3q+2].  Lane (gid, t) holds, per
+        // column c = n0 + mt*16 + gid + hm*8, slots v0 = 2t, v1 = 2t+1, v2 = 8+2t, v3 = 9+2t; each of the
+        // five outputs of a quad needs exactly one slot of another lane of the quad (five shuffles):
+        //   q0 = t0 (0, 1 | 2 from t1)    q1 = t2 (3 from t1 | 4, 5)    q2 = t3 (6, 7 | 8 from t0)
+        //   q3 = t1 (9 from t0 | 10, 11)  q4 = t2 (12, 13 | 14 from t3)
+        const int base = lane & ~3;
+        const int rowq = s_desc[8 + b] + qo;
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-          for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-            for (int hm = 0; hm < 2; ++hm) {
-              const int m = mt * 16 + gid + hm * 8;
-              slab[m * kDenseDst + nt * 8 + 2 * tig] = acc[mt][nt][hm * 2];
-              slab[m * kDenseDst + nt * 8 + 2 * tig + 1] = acc[mt][nt][hm * 2 + 1];
+          for (int hm = 0; hm < 2; ++hm) {
+            const double v0 = acc[mt][0][hm * 2], v1 = acc[mt][0][hm * 2 + 1];
+            const double v2 = acc[mt][1][hm * 2], v3 = acc[mt][1][hm * 2 + 1];
+            const double x1v0 = __shfl_sync(0xffffffffu, v0, base + 1);
+            const double x1v1 = __shfl_sync(0xffffffffu, v1, base + 1);
+            const double x0v2 = __shfl_sync(0xffffffffu, v2, base + 0);
+            const double x0v3 = __shfl_sync(0xffffffffu, v3, base + 0);
+            const double x3v2 = __shfl_sync(0xffffffffu, v2, base + 3);
+            const int cl = n0 + mt * 16 + gid + hm * 8;
+            if (cl >= cw) continue;
+            const int c = c0 + cl;
+            const double dm = __ldg(a.dmu + c), dn = __ldg(a.dnu + c);
+            double* oc = a.out + a.out_off + c;
+            if (tig == 0) {
+              if (0 < gs) __stcs(oc + (size_t)(rowq + 0) * a.ldo, fma(dn, x1v0, fma(dm, v1, v0)));
+            } else if (tig == 1) {
+              if (3 < gs) __stcs(oc + (size_t)(rowq + 3) * a.ldo, fma(dn, v3, fma(dm, v2, x0v3)));
+            } else if (tig == 2) {
+              if (1 < gs) __stcs(oc + (size_t)(rowq + 1) * a.ldo, fma(dn, v1, fma(dm, v0, x1v1)));
+              if (4 < gs) __stcs(oc + (size_t)(rowq + 4) * a.ldo, fma(dn, x3v2, fma(dm, v3, v2)));
+            } else {
+              if (2 < gs) __stcs(oc + (size_t)(rowq + 2) * a.ldo, fma(dn, x0v2, fma(dm, v1, v0)));
             }
-        __syncwarp();
-        const int c = c0 + n0 + lane;
-        if (n0 + lane < cw) {
-          const double dm = __ldg(a.dmu + c), dn = __ldg(a.dnu + c);
-          const double* sr = slab + lane * kDenseDst;
-          for (int q = 0; q < gs; ++q) {
-            const double y = fma(dn, sr[3 * q + 2], fma(dm, sr[3 * q + 1], sr[3 * q]));
-            __stcs(a.out + (size_t)(s_desc[8 + b] + qo + q) * a.ldo + a.out_off + c, y);
           }
-        }
-        __syncwarp();
       }
     }
   }
@@ -1123,7 +1132,7 @@ spmm_t_kernel(SpmmArgs a, int ust, int ustage) {
 int ust_for(int rmax) { return ((rmax + 11) / 16) * 16 + 4; }   // >= rmax + 1, == 4 mod 16 (even)
 
 size_t dense_smem() {
-  return sizeof(double) * (kValCap + (size_t)kUCap * kDenseUst + 32 + (size_t)kWarps * 32 * kDenseDst);
+  return sizeof(double) * (kValCap + (size_t)kUCap * kDenseUst + 32);
 }
 
 size_t smem_for(int mode, int rmax) {
