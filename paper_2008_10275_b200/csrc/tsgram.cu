@@ -29,8 +29,11 @@ namespace {
 constexpr int kThreads = 512;   // 16 warps
 constexpr int kWarps = kThreads / 32;
 constexpr int kBM = 128;        // rows per tile
-constexpr int kBK = 32;         // k chunk
-constexpr int kSU = kBK + 4;    // smem row stride of the U chunk (== 4 mod 16 doubles: conflict free)
+// k chunk: 32 for the Gram passes, 36 for the basis pass (p = 100 -> 3 chunks instead of 4; the Gram
+// kernels run out of registers with the wider chunk plan).  The U chunk's shared-memory row stride is
+// 36 doubles in both cases (== 4 mod 16: conflict-free fragment loads).
+template <int MODE> struct BKof { static constexpr int v = MODE == 1 ? 36 : 32; };
+constexpr int kSU = 36;
 
 __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -73,11 +76,11 @@ __device__ __forceinline__ int ucat_offsets(const TsArgs& a, int (&off)[kMaxUBlo
   return o;
 }
 
-template <int PT>
+template <int PT, int BK>
 struct TsShape {
   static constexpr int PMAX = PT * 8;
   static constexpr int SX = PMAX + 4;                    // T chunk / X tile row stride
-  static constexpr int STAGE = kBM * kSU + kBK * SX;     // doubles per pipeline stage
+  static constexpr int STAGE = kBM * kSU + BK * SX;      // doubles per pipeline stage
   static constexpr int NSTAGE = 3;
   static constexpr int SMEM = NSTAGE * STAGE;
   static constexpr int XH = (kBM / 2) * SX;              // half X tile (64 rows), fits one stage
@@ -97,30 +100,40 @@ struct TsShape {
 struct ChunkPlan {
   const double* ub;   // Ucat source of this thread's column at row m0 (null: column past w)
   int ld;
+  const double* ub2;  // the thread's extra copy (columns 32..35 of the chunk), null if none
+  int ld2;
   int m0, k0;
   unsigned st;        // stage base (shared address)
 };
 
-template <int PT>
+__device__ __forceinline__ const double* col_src(const TsArgs& a, int col, int m0, int w, const int* off, int& ld) {
+  ld = 0;
+  if (col >= w) return nullptr;
+  int bi = 0;
+#pragma unroll
+  for (int q = 1; q < kMaxUBlocks; ++q) bi += (col >= off[q]);
+  ld = a.u.b[bi].ld;
+  return a.u.b[bi].p + (size_t)m0 * ld + (col - off[bi]);
+}
+
+// Chunk columns 0..31: 16-byte mode -> pair (tid & 15) of rows (tid >> 4) + 32q; 8-byte mode ->
+// column (tid & 31) of rows (tid >> 5) + 16q.  Columns 32..35: 16-byte mode -> pair 16 + (tid & 1)
+// of row tid >> 1 (threads < 256); 8-byte mode -> column 32 + (tid & 3) of row tid >> 2.
+template <int PT, int BK>
 __device__ __forceinline__ ChunkPlan plan_chunk(const TsArgs& a, unsigned stage, int m0, int k0, int w,
                                                 const int* off, int tid) {
   ChunkPlan c;
   c.m0 = m0; c.k0 = k0; c.st = stage;
-  const int col = k0 + (a.u16 ? (tid & 15) * 2 : (tid & 31));
-  c.ub = nullptr; c.ld = 0;
-  if (col < w) {
-    int bi = 0;
-#pragma unroll
-    for (int q = 1; q < kMaxUBlocks; ++q) bi += (col >= off[q]);
-    c.ld = a.u.b[bi].ld;
-    c.ub = a.u.b[bi].p + (size_t)m0 * c.ld + (col - off[bi]);
-  }
+  c.ub = col_src(a, k0 + (a.u16 ? (tid & 15) * 2 : (tid & 31)), m0, w, off, c.ld);
+  c.ub2 = nullptr; c.ld2 = 0;
+  if (BK > 32 && (!a.u16 || tid < 256))
+    c.ub2 = col_src(a, k0 + 32 + (a.u16 ? (tid & 1) * 2 : (tid & 3)), m0, w, off, c.ld2);
   return c;
 }
 
-template <int PT>
+template <int PT, int BK>
 __device__ __forceinline__ void issue_part(const TsArgs& a, const ChunkPlan& c, int part, int w, int tid) {
-  using S = TsShape<PT>;
+  using S = TsShape<PT, BK>;
   if (a.dbg & 1) return;
   if (a.u16) {
     if (part < 4) {
@@ -137,10 +150,37 @@ __device__ __forceinline__ void issue_part(const TsArgs& a, const ChunkPlan& c, 
     const unsigned sa = c.st + 8u * (i * kSU + j);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src), "r"(ok ? 8 : 0));
   }
-  if (part >= 4) {
+  if (BK > 32 && part == 4) {   // U chunk columns 32..35
+    if (a.u16) {
+      if (tid < 256) {
+        const int i = tid >> 1, j = 32 + (tid & 1) * 2;
+        const bool ok = c.ub2 != nullptr && (c.m0 + i < a.M);
+        const double* src = ok ? c.ub2 + (size_t)i * c.ld2 : a.u.b[0].p;
+        const unsigned sa = c.st + 8u * (i * kSU + j);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(ok ? 16 : 0));
+      }
+    } else {
+      const int i = tid >> 2, j = 32 + (tid & 3);
+      const bool ok = c.ub2 != nullptr && (c.m0 + i < a.M);
+      const double* src = ok ? c.ub2 + (size_t)i * c.ld2 : a.u.b[0].p;
+      const unsigned sa = c.st + 8u * (i * kSU + j);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src), "r"(ok ? 8 : 0));
+    }
+  }
+  if (part >= 4) {   // T chunk rows 0..31 (warp wp: rows 2wp, 2wp+1)
     const int q = part - 4;
     const int wp = tid >> 5, lane = tid & 31;
     const int row = 2 * wp + (q >> 1), piece = lane + 32 * (q & 1);
+    if (piece < S::HP) {
+      const int cr = c.k0 + row;
+      const bool ok = cr < w;
+      const double* g = ok ? a.T + (size_t)cr * a.ldt + 2 * piece : a.T;
+      const unsigned sa = c.st + 8u * (kBM * kSU + row * S::SX + 2 * piece);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 16 : 0));
+    }
+  }
+  if (BK > 32 && part == 5 && tid < 4 * 64) {   // T chunk rows 32..35
+    const int row = 32 + (tid >> 6), piece = tid & 63;
     if (piece < S::HP) {
       const int cr = c.k0 + row;
       const bool ok = cr < w;
@@ -236,7 +276,8 @@ __device__ __forceinline__ void gram_tile(double (&acc)[4][2], const double* xh0
 template <int PT, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 ts_kernel(TsArgs a) {
-  using S = TsShape<PT>;
+  constexpr int kBK = BKof<MODE>::v;
+  using S = TsShape<PT, kBK>;
   constexpr int PMAX = S::PMAX, SX = S::SX;
 
   // block column offsets in shared memory (keeps them out of the register budget)
@@ -294,9 +335,9 @@ ts_kernel(TsArgs a) {
   int g = 0, issued = 0;
   __syncthreads();   // off[], barriers
   {
-    const ChunkPlan c0 = plan_chunk<PT>(a, sbase, blockIdx.x * kBM, 0, w, off, tid);
+    const ChunkPlan c0 = plan_chunk<PT, kBK>(a, sbase, blockIdx.x * kBM, 0, w, off, tid);
 #pragma unroll
-    for (int part = 0; part < 8; ++part) issue_part<PT>(a, c0, part, w, tid);
+    for (int part = 0; part < 8; ++part) issue_part<PT, kBK>(a, c0, part, w, tid);
     mb_arrive_cp(&full[0]);
   }
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -317,9 +358,9 @@ ts_kernel(TsArgs a) {
         else if (has_next) { nm0 = m0 + gridDim.x * kBM; nk0 = 0; }
         if (nm0 >= 0) {
           produce_wait(g + 1);
-          const ChunkPlan c1 = plan_chunk<PT>(a, sbase + 8u * S::STAGE * ((g + 1) % 3), nm0, nk0, w, off, tid);
+          const ChunkPlan c1 = plan_chunk<PT, kBK>(a, sbase + 8u * S::STAGE * ((g + 1) % 3), nm0, nk0, w, off, tid);
 #pragma unroll
-          for (int part = 0; part < 8; ++part) issue_part<PT>(a, c1, part, w, tid);
+          for (int part = 0; part < 8; ++part) issue_part<PT, kBK>(a, c1, part, w, tid);
           mb_arrive_cp(&full[(g + 1) % 3]);
           issued = g + 1;
         }
@@ -332,7 +373,7 @@ ts_kernel(TsArgs a) {
         else if (kc + 2 == nk && has_next) { pm0 = m0 + gridDim.x * kBM; pk0 = 0; }
       }
       ChunkPlan c2;
-      if (pm0 >= 0) c2 = plan_chunk<PT>(a, sbase + 8u * S::STAGE * ((g + 2) % 3), pm0, pk0, w, off, tid);
+      if (pm0 >= 0) c2 = plan_chunk<PT, kBK>(a, sbase + 8u * S::STAGE * ((g + 2) % 3), pm0, pk0, w, off, tid);
       const double* s_u = sm + (g % 3) * S::STAGE;
       const double* s_t = s_u + kBM * kSU;
       const int k0 = kc * kBK;
@@ -349,10 +390,11 @@ ts_kernel(TsArgs a) {
         else
           mma_row<PT>(x0, a0, s_t + (kk + tig) * SX + gid, nact);
         // second half of the chunk: the stage of chunk g-1 is (almost surely) free by now
-        if (pm0 >= 0 && kk >= kBK / 2) {
-          if (kk == kBK / 2) produce_wait(g + 2);
-          issue_part<PT>(a, c2, 2 * ((kk - kBK / 2) / 4), w, tid);
-          issue_part<PT>(a, c2, 2 * ((kk - kBK / 2) / 4) + 1, w, tid);
+        constexpr int kIssue0 = kBK - 16;   // the last four k4 steps issue two parts each
+        if (pm0 >= 0 && kk >= kIssue0) {
+          if (kk == kIssue0) produce_wait(g + 2);
+          issue_part<PT, kBK>(a, c2, 2 * ((kk - kIssue0) / 4), w, tid);
+          issue_part<PT, kBK>(a, c2, 2 * ((kk - kIssue0) / 4) + 1, w, tid);
         }
       }
       if (pm0 >= 0) { mb_arrive_cp(&full[(g + 2) % 3]); issued = g + 2; }
@@ -461,14 +503,14 @@ ts_kernel(TsArgs a) {
 
 template <int PT, int MODE>
 cudaError_t launch_pt(const TsArgs& a, int grid, cudaStream_t s) {
-  ts_kernel<PT, MODE><<<grid, kThreads, sizeof(double) * TsShape<PT>::SMEM, s>>>(a);
+  ts_kernel<PT, MODE><<<grid, kThreads, sizeof(double) * TsShape<PT, BKof<MODE>::v>::SMEM, s>>>(a);
   return cudaGetLastError();
 }
 
 template <int PT, int MODE>
 cudaError_t prep_pt() {
   return cudaFuncSetAttribute(ts_kernel<PT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(sizeof(double) * TsShape<PT>::SMEM));
+                              (int)(sizeof(double) * TsShape<PT, BKof<MODE>::v>::SMEM));
 }
 
 template <int MODE, int PT>
