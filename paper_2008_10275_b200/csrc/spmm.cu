@@ -9,13 +9,15 @@
 //
 // Mapping: rows come in node blocks -- runs of <= 8 consecutive rows with
 // identical column lists (the 5 field rows of an FE node share one list), detected at
-// set_operator -- packed into CTA tiles of <= 8 blocks / kSpmmCap nnz.  A 16-warp CTA streams the
-// tile's contiguous CSR segment (six value arrays, coalesced, evict-first so U keeps L1/L2) into
-// shared memory, combining the six arrays into the three grouped streams and interleaving them
-// per column-list entry ([j][row][stream], 16-byte aligned rows) on the way; the column list of a
-// block is read from its first row only.  Each warp then owns one (node block, 32-column slice):
-// every gathered U element (a 4-deep register prefetch ring hides the L2 latency) feeds
-// 3 x (rows of the block) FMAs.
+// set_operator -- packed into CTA tiles of <= 4 blocks / kSpmmCap nnz / kUCap deduplicated U rows,
+// each described by a 1 KB host-built descriptor (U-path tiles stored first).  The hot kernel
+// (spmm_u_kernel, 8 warps, 3 CTAs/SM) loads the tile's six contiguous value segments into
+// registers (evict-first), stages the tile's deduplicated U rows in shared memory (TMA bulk copies
+// behind an mbarrier), combines the six arrays into the three grouped streams in a conflict-free
+// [slot][j] layout, and gives each warp one (node block, 32-column slice) contraction on the fp64
+// tensor pipe (m16n8k4 DMMA, computed transposed so stores are full sectors).  Tiles whose rows do
+// not fit the U-path bounds take the general spmm_kernel (L2 gather).  spmm_dense_kernel is the
+// config-5 dense variant; spmm_p_kernel / spmm_t_kernel are opt-in pipelined experiments.
 #include <cstdlib>
 #include "lrc_internal.cuh"
 
