@@ -167,166 +167,278 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------------------------
-def main():
-    args = parse()
-    rank, world, local = dist_env()
-    from synth import generator as gen
+# launch: `--gpus N` without a torchrun environment re-executes this file under torchrun
+# ----------------------------------------------------------------------------------------------
+def free_port():
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
 
-    if args.impl == "reference":
-        return run_reference(args, rank, world)
 
-    import torch
-    import torch.distributed as dist
-    from paper_2008_10275_b200 import lrcheb
+def relaunch_under_torchrun(args):
+    """One process per GPU (the contract's launch): python -m torch.distributed.run ... bench.py."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    prob = gen.make_problem(args.config)
-    cfg, op = prob.cfg, prob.op
-    N = cfg.n_iter
-    # S concurrent subset solves (subsets are independent): one lrc context,
-    # CUDA stream and host thread each, all sharing the borrowed operator.  The persistent M-level
-    # kernels leave `reserve` SMs free so one solve's single-CTA core steps overlap the other's
-    # M-level work.  Steps are dealt round-robin to the streams.
-    S = max(1, args.streams)
-    reserve = args.reserve_sms if S > 1 else 0
-    rp_d, ci_d = torch.from_numpy(op.row_ptr).to(dev), torch.from_numpy(op.col_idx).to(dev)
-    vals_d = [torch.from_numpy(v).to(dev) for v in op.vals]
-    ctxs = []
-    for _ in range(S):
-        c = lrcheb.Context(local)
-        c.set_reserved_sms(reserve)
-        c.set_operator(rp_d, ci_d, vals_d, op.rho_f, op.lambda_s, borrow=True)
-        ctxs.append(c)
-    ctx = ctxs[0]
-    my_subsets = shard_subsets(cfg.K, rank, world)
-    inputs = []
-    for k in my_subsets:
-        d_mu, d_nu, BU, BV = prob.subset(k)
-        inputs.append((d_mu, d_nu, torch.from_numpy(BU).to(dev), torch.from_numpy(BV).to(dev),
-                       torch.from_numpy(BU).pin_memory(), torch.from_numpy(BV).pin_memory()))
-    n = len(inputs[0][0])
-    outs = [(torch.empty((op.M, cfg.rank_cap), dtype=torch.float64, device=dev),
-             torch.empty((n, cfg.rank_cap), dtype=torch.float64, device=dev),
-             torch.empty((op.M, cfg.rank_cap), dtype=torch.float64).pin_memory(),
-             torch.empty((n, cfg.rank_cap), dtype=torch.float64).pin_memory()) for _ in range(S)]
 
-    def step(i, host=False, c=None):
-        si = (i % S) if c is None else c
-        cx = ctxs[si]
-        Uo, Vo, Uh, Vh = outs[si]
-        d_mu, d_nu, bu, bv, bu_h, bv_h = inputs[i % len(inputs)]
+# ----------------------------------------------------------------------------------------------
+# the distributed skeleton (backend-agnostic: NCCL on the GPU box, gloo in tests/test_multirank.py)
+# ----------------------------------------------------------------------------------------------
+def run_distributed(args, leg, rank, world, dist=None, device=None, emit=print):
+    """Shard the subsets over the ranks (no data-path collective), run W untimed warm-up
+    steps, time exactly K steps between barriers (device time from the leg), take the max over
+    ranks, and have rank 0 emit the JSON line.  `leg` does the work: prepare(subsets), steps(n, host)
+    -> (device ms, infos, launches), extras(value) -> dict of extra keys."""
+    cfg = leg.cfg
+    mine = shard_subsets(cfg.K, rank, world)
+    leg.prepare(mine)
+    leg.warmup(args.warmup)
+
+    def timed(host):
+        if dist is not None and world > 1:
+            dist.barrier()
+        ms, infos, launches = leg.steps(args.steps, host)
+        ms = max_over_ranks(ms, dist if world > 1 else None, device)
+        if dist is not None and world > 1:
+            dist.barrier()
+        return ms, infos, launches
+
+    leg.clock_start()
+    ms, infos, launches = timed(False)
+    clocks = leg.clock_stop()
+    ms_e2e, _, _ = timed(True)
+    iters = args.steps * cfg.n_iter * world
+    value = iters / (ms / 1e3)
+    e2e_value = iters / (ms_e2e / 1e3)
+    result = {
+        "metric": "ChebyshevT iterations/sec (fused-SpMM HBM GB/s in roofline_spmm)",
+        "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded FE-like operator, DESIGN.md input recipe)",
+        "config": dict(leg.config(), subsets_per_rank=len(mine),
+                       parallelism=f"subsets round-robin over {world} GPU(s), no data-path collective"),
+        "e2e": {"value": e2e_value, "unit": "iterations/s", "h2d_bytes_per_step": int(leg.h2d_bytes()),
+                "d2h_bytes_per_step": int(leg.d2h_bytes())},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    result.update(leg.extras(value, rank, world))
+    if infos and infos[-1] is not None:
+        result["final_rel_residual"] = infos[-1]["rel_residual"]
+        result["ranks_final"] = infos[-1]["rank"]
+    if rank == 0:
+        emit(json.dumps(result))
+    return result
+
+
+class GpuLeg:
+    """The product path: S concurrent subset solves per GPU (one lrc context, CUDA stream and host
+    thread each, all borrowing one device copy of the operator)."""
+
+    def __init__(self, args, local):
+        import torch
+        from paper_2008_10275_b200 import lrcheb
+        from synth import generator as gen
+        self.args, self.local, self.torch, self.lrcheb, self.gen = args, local, torch, lrcheb, gen
+        self.dev = torch.device("cuda", local)
+        self.prob = gen.make_problem(args.config)
+        self.cfg, self.op = self.prob.cfg, self.prob.op
+        self.S = max(1, args.streams)
+        self.reserve = args.reserve_sms if self.S > 1 else 0
+        op, dev = self.op, self.dev
+        self.rp_d, self.ci_d = torch.from_numpy(op.row_ptr).to(dev), torch.from_numpy(op.col_idx).to(dev)
+        self.vals_d = [torch.from_numpy(v).to(dev) for v in op.vals]
+        self.ctxs = []
+        for _ in range(self.S):
+            c = lrcheb.Context(local)
+            c.set_reserved_sms(self.reserve)
+            c.set_operator(self.rp_d, self.ci_d, self.vals_d, op.rho_f, op.lambda_s, borrow=True)
+            self.ctxs.append(c)
+        self.main_s = torch.cuda.Stream(device=dev)
+        self.clk = ClockSampler(local)
+
+    def prepare(self, subsets):
+        torch, cfg, op, dev = self.torch, self.cfg, self.op, self.dev
+        self.subsets = subsets
+        self.inputs = []
+        for k in subsets:
+            d_mu, d_nu, BU, BV = self.prob.subset(k)
+            self.inputs.append((d_mu, d_nu, torch.from_numpy(BU).to(dev), torch.from_numpy(BV).to(dev),
+                                torch.from_numpy(BU).pin_memory(), torch.from_numpy(BV).pin_memory()))
+        self.n = len(self.inputs[0][0])
+        self.outs = [(torch.empty((op.M, cfg.rank_cap), dtype=torch.float64, device=dev),
+                      torch.empty((self.n, cfg.rank_cap), dtype=torch.float64, device=dev),
+                      torch.empty((op.M, cfg.rank_cap), dtype=torch.float64).pin_memory(),
+                      torch.empty((self.n, cfg.rank_cap), dtype=torch.float64).pin_memory())
+                     for _ in range(self.S)]
+
+    def step(self, i, host=False, c=None):
+        si = (i % self.S) if c is None else c
+        cx = self.ctxs[si]
+        Uo, Vo, Uh, Vh = self.outs[si]
+        d_mu, d_nu, bu, bv, bu_h, bv_h = self.inputs[i % len(self.inputs)]
         cx.set_params(d_mu, d_nu)
+        p, cfg = self.prob, self.cfg
         if host:
-            return cx.solve(bu_h, bv_h, prob.lam_min, prob.lam_max, cfg.tol, cfg.rank_cap, N, out=(Uh, Vh))[2]
-        return cx.solve(bu, bv, prob.lam_min, prob.lam_max, cfg.tol, cfg.rank_cap, N, out=(Uo, Vo))[2]
+            return cx.solve(bu_h, bv_h, p.lam_min, p.lam_max, cfg.tol, cfg.rank_cap, cfg.n_iter, out=(Uh, Vh))[2]
+        return cx.solve(bu, bv, p.lam_min, p.lam_max, cfg.tol, cfg.rank_cap, cfg.n_iter, out=(Uo, Vo))[2]
 
-    def run_steps(nsteps, host):
+    def run_steps(self, nsteps, host):
         """nsteps solves dealt round-robin to the S streams, one host thread per stream."""
         infos = [None] * nsteps
+        errs = []
+
         def worker(si):
-            for i in range(si, nsteps, S):
-                infos[i] = step(i, host, si)
-        ths = [threading.Thread(target=worker, args=(si,)) for si in range(S)]
+            try:
+                for i in range(si, nsteps, self.S):
+                    infos[i] = self.step(i, host, si)
+            except Exception as e:   # surfaced below: a failing solve must fail the bench
+                errs.append(e)
+        ths = [threading.Thread(target=worker, args=(si,)) for si in range(self.S)]
         for t in ths:
             t.start()
         for t in ths:
             t.join()
+        if errs:
+            raise errs[0]
         return infos
 
-    run_steps(max(args.warmup, S), False)           # >= 1 warm-up per stream (graph capture)
-    main_s = torch.cuda.Stream(device=dev)
+    def warmup(self, w):
+        self.run_steps(max(w, self.S), False)           # >= 1 warm-up per stream (graph capture)
 
-    def timed(host):
-        if world > 1:
-            dist.barrier()
+    def steps(self, nsteps, host):
+        torch = self.torch
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        launches0 = sum(c.kernel_launches() for c in ctxs)
-        e0.record(main_s)
-        for c in ctxs:
+        launches0 = sum(c.kernel_launches() for c in self.ctxs)
+        e0.record(self.main_s)
+        for c in self.ctxs:
             c.stream.wait_event(e0)
-        infos = run_steps(args.steps, host)
-        for c in ctxs:
+        infos = self.run_steps(nsteps, host)
+        for c in self.ctxs:
             ev = torch.cuda.Event()
             ev.record(c.stream)
-            main_s.wait_event(ev)
-        e1.record(main_s)
+            self.main_s.wait_event(ev)
+        e1.record(self.main_s)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), infos, sum(c.kernel_launches() for c in self.ctxs) - launches0
+
+    def clock_start(self):
+        self.clk.start()
+
+    def clock_stop(self):
+        return self.clk.stop()
+
+    def h2d_bytes(self):
+        a = self.args
+        return sum(self.inputs[i % len(self.inputs)][4].numel() * 8 + self.inputs[i % len(self.inputs)][5].numel() * 8
+                   for i in range(a.steps)) / a.steps
+
+    def d2h_bytes(self):
+        return (self.outs[0][2].numel() + self.outs[0][3].numel()) * 8 + 64
+
+    def config(self):
+        return {"workload": workload_str(self.cfg, self.op, self.n),
+                "step": "one full ChebyshevT solve of one parameter subset (N iterations + final residual)",
+                "concurrent_subsets_per_gpu": self.S, "reserved_sms": self.reserve,
+                "l2": f"inputs larger than L2 (operator {operator_bytes(self.op) / 1e9:.2f} GB vs 126 MB)"
+                      if operator_bytes(self.op) > L2_BYTES else "operator fits in L2 (latency-bound config)"}
+
+    def single_stream(self, steps=2):
+        """Per-subset latency: the same solve on one context alone (graph replay)."""
+        torch = self.torch
+        self.step(0, c=0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s = self.ctxs[0].stream
+        e0.record(s)
+        for i in range(steps):
+            self.step(i * self.S, c=0)
+        e1.record(s)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
-        launches = sum(c.kernel_launches() for c in ctxs) - launches0
-        ms = max_over_ranks(ms, dist if world > 1 else None, dev)
-        if world > 1:
-            dist.barrier()
-        return ms, infos, launches
+        return {"value": steps * self.cfg.n_iter / (ms / 1e3), "unit": "iterations/s",
+                "ms_per_iteration": ms / (steps * self.cfg.n_iter), "steps": steps,
+                "note": "one subset at a time on one stream (latency view); reserved SMs as in the headline"}
 
-    clk = ClockSampler(local)
-    clk.start()
-    ms, infos, launches = timed(False)
-    clocks = clk.stop()
-    ms_e2e, _, _ = timed(True)
-    iters = args.steps * N * world
-    value = iters / (ms / 1e3)
-    e2e_value = iters / (ms_e2e / 1e3)
-    h2d = sum(inputs[i % len(inputs)][4].numel() * 8 + inputs[i % len(inputs)][5].numel() * 8
-              for i in range(args.steps)) / args.steps
-    d2h = (outs[0][2].numel() + outs[0][3].numel()) * 8 + 64
+    def extras(self, value, rank, world):
+        args, cfg, op = self.args, self.cfg, self.op
+        out = {"single_stream": self.single_stream()}
+        ctx = self.ctxs[0]
+        # ---- roofline pass: per-kernel CUDA events on the launching streams (same workload, no graph)
+        ctx.set_profiling(True)
+        self.step(0, c=0)
+        prof = ctx.profile()
+        ctx.set_profiling(False)
+        g1, g2 = prof.get("ts_gram", (0.0, 0)), prof.get("ts_gram2", (0.0, 0))
+        step_ms = sum(v[0] for v in prof.values())
+        M, nnz, r, rB, n = op.M, op.nnz, cfg.rank_cap, cfg.r_B, self.n
+        w = rB + 4 * r
+        p = min(n, w)
+        flops, byts = algorithmic_work(M, nnz, r, rB, n)
 
-    # ---- roofline pass: per-kernel CUDA events on the launching streams (same workload, no graph)
-    ctx.set_profiling(True)
-    step(0, c=0)
-    prof = ctx.profile()
-    ctx.set_profiling(False)
-    g1, g2 = prof.get("ts_gram", (0.0, 0)), prof.get("ts_gram2", (0.0, 0))
-    gram_split = {"pass1_avg_ms": g1[0] / max(g1[1], 1), "pass2_avg_ms": g2[0] / max(g2[1], 1)}
-    step_ms = sum(v[0] for v in prof.values())
-    M, nnz, r, rB = op.M, op.nnz, cfg.rank_cap, cfg.r_B
-    w = rB + 4 * r
-    p = min(n, w)
-    # algorithmic (structurally necessary) work per launch at steady state (DESIGN.md "Roofline"):
-    #   pass 1  Y = Ucat R_V^T (R_V^T lower trapezoidal) + G1 = Y^T Y (symmetric)
-    #   pass 2  Q1 = Y R1^{-1} (upper triangular) + G2 = Q1^T Q1
-    #   basis   U' = Y W_r Sigma_r^{-1}
-    flops = {"spmm": 6.0 * nnz * r,
-             "ts_gram": 2.0 * M * (w * p - p * (p - 1) / 2.0) + 1.0 * M * p * (p + 1),
-             "ts_gram2": 1.0 * M * p * (p + 1) + 1.0 * M * p * (p + 1),
-             "ts_store": 2.0 * M * p * r}
-    byts = {"spmm": 52.0 * nnz + 4.0 * (M + 1) + 32.0 * M * r,
-            "ts_gram": 8.0 * M * w + 8.0 * M * p, "ts_gram2": 8.0 * M * p, "ts_store": 8.0 * M * p + 8.0 * M * r}
-    bytes_spmm = byts["spmm"]
+        def kernel_entry(name):
+            ms_tot, cnt = prof[name]
+            avg = ms_tot / max(cnt, 1)
+            if name == "spmm":
+                ach = byts["spmm"] / (avg / 1e3) / 1e9
+                return {"bound": "hbm", "achieved": ach, "peak": hbm_peak(), "unit": "GB/s",
+                        "frac": ach / hbm_peak(), "avg_ms": avg, "launches": cnt, "share": ms_tot / step_ms,
+                        "traffic": ncu_traffic(name, args.config)}
+            ach = flops[name] / (avg / 1e3) / 1e12
+            return {"bound": "tensor", "achieved": ach, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": ach / FP64_DMMA_PEAK_TFLOPS, "avg_ms": avg, "launches": cnt, "share": ms_tot / step_ms,
+                    "traffic": ncu_traffic(name, args.config)}
+        cand = {k: v for k, v in prof.items() if k in flops}
+        dom = max(cand.items(), key=lambda kv: kv[1][0])
+        roof = kernel_entry(dom[0])
+        roof["kernel"] = dom[0]
+        roof["peak_source"] = ("MEASURED_PEAKS.json hbm_gbs" if roof["unit"] == "GB/s" else
+                               "measured DMMA m8n8k4 fp64 (profiles/r01_phase0_fp64_peaks.jsonl); "
+                               "MEASURED_PEAKS.json has no fp64 entry")
+        kernels = {k: kernel_entry(k) for k in cand}
+        out.update({"roofline": roof, "roofline_spmm": kernel_entry("spmm"), "roofline_kernels": kernels,
+                    "kernel_ms_per_step": {k: v[0] for k, v in prof.items()},
+                    "ts_gram_passes": {"pass1_avg_ms": g1[0] / max(g1[1], 1), "pass2_avg_ms": g2[0] / max(g2[1], 1)}})
+        # ---- the whole iteration against its roofline: per kernel max(flops / fp64 peak, bytes / HBM
+        #      peak), summed over the M-level kernels of one steady-state iteration (DESIGN.md §8)
+        it_parts = {k: (flops[k], byts[k]) for k in flops}
+        t_roof = sum(max(f / (FP64_DMMA_PEAK_TFLOPS * 1e12), b / (hbm_peak() * 1e9)) for f, b in it_parts.values())
+        t_meas = world / value                       # one GPU's time per iteration
+        out["iteration_roofline"] = {
+            "flops": sum(f for f, _ in it_parts.values()), "bytes": sum(b for _, b in it_parts.values()),
+            "roofline_ms": t_roof * 1e3, "measured_ms_per_iteration": t_meas * 1e3, "frac": t_roof / t_meas,
+            "hbm_only_ms": sum(b for _, b in it_parts.values()) / (hbm_peak() * 1e9) * 1e3,
+            "per_kernel_ms": {k: max(f / (FP64_DMMA_PEAK_TFLOPS * 1e9), b / (hbm_peak() * 1e6))
+                              for k, (f, b) in it_parts.items()},
+            "bound": "fp64 tensor (the Gram / basis passes); the SpMM alone is HBM-bound"}
+        if args.dense and rank == 0 and args.config == "large":
+            out["config5_dense_spmm"] = self.dense_config5()
+        if rank == 0 and not args.no_cpu_baseline:
+            rows = cpu_calibrate(self.prob, args.cpu_seconds)
+            t = cpu_sample(self.prob, rows)
+            out["cpu_baseline"] = {"value": (rows / M) / t, "unit": "iterations/s", "cores": cpu_cores(),
+                                   "kind": "oracle",
+                                   "sample": f"one steady-state oracle iteration (six-term scipy SpMM, single-"
+                                             f"threaded; Householder QR + SVD truncation, BLAS threads = cores) on "
+                                             f"rows [0,{rows}) of {M}; {t:.1f}s, scaled by rows/M"}
+        return out
 
-    def kernel_entry(name):
-        ms_tot, cnt = prof[name]
-        avg = ms_tot / max(cnt, 1)
-        if name == "spmm":
-            ach = bytes_spmm / (avg / 1e3) / 1e9
-            return {"bound": "hbm", "achieved": ach, "peak": hbm_peak(), "unit": "GB/s",
-                    "frac": ach / hbm_peak(), "avg_ms": avg, "launches": cnt, "share": ms_tot / step_ms}
-        ach = flops[name] / (avg / 1e3) / 1e12
-        return {"bound": "tensor", "achieved": ach, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": ach / FP64_DMMA_PEAK_TFLOPS, "avg_ms": avg, "launches": cnt, "share": ms_tot / step_ms}
-    cand = {k: v for k, v in prof.items() if k in flops}
-    dom = max(cand.items(), key=lambda kv: kv[1][0])
-    roof = kernel_entry(dom[0])
-    roof["kernel"] = dom[0]
-    roof["traffic"] = ncu_traffic(dom[0])
-    roof["peak_source"] = ("MEASURED_PEAKS.json hbm_gbs" if roof["unit"] == "GB/s" else
-                           "measured DMMA m8n8k4 fp64 (profiles/r01_phase0_fp64_peaks.jsonl)")
-    kernels = {k: kernel_entry(k) for k in cand}
-
-    # ---- BASELINE config 5 (full-rank direct approach): fused six-term operator on a dense M x 256 S,
-    #      D_mu / D_nu from a 16 x 16 parameter grid, 20 repetitions, HBM GB/s vs the same roofline
-    dense = None
-    if args.dense and rank == 0:
+    def dense_config5(self):
+        """BASELINE config 5 (full-rank direct approach): fused six-term operator on a dense M x 256 S,
+        D_mu / D_nu from a 16 x 16 parameter grid, 20 repetitions, HBM GB/s vs the same roofline."""
+        torch, gen, op, nnz, M = self.torch, self.gen, self.op, self.op.nnz, self.op.M
         cfg5 = gen.config_by_name("fullrank")
         mu5, nu5 = gen.parameter_grid(cfg5)
-        ctx5 = lrcheb.Context(local)
-        ctx5.set_operator(rp_d, ci_d, vals_d, op.rho_f, op.lambda_s, borrow=True)
+        ctx5 = self.lrcheb.Context(self.local)
+        ctx5.set_operator(self.rp_d, self.ci_d, self.vals_d, op.rho_f, op.lambda_s, borrow=True)
         ctx5.set_params(mu5, nu5)
-        g = torch.Generator(device=dev).manual_seed(cfg5.seed)
-        S5 = torch.randn((op.M, cfg5.dense_cols), dtype=torch.float64, device=dev, generator=g)
+        g = torch.Generator(device=self.dev).manual_seed(cfg5.seed)
+        S5 = torch.randn((M, cfg5.dense_cols), dtype=torch.float64, device=self.dev, generator=g)
         for _ in range(3):
             Y5 = ctx5.apply_dense(S5)
         kms = []
@@ -335,61 +447,55 @@ def main():
             kms.append(ctx5.last_kernel_ms())
         avg = float(np.mean(kms))
         byts5 = 52.0 * nnz + 4.0 * (M + 1) + 16.0 * M * cfg5.dense_cols
-        dense = {"workload": f"config 5: M={M} dense S M x {cfg5.dense_cols}, {cfg5.reps} repetitions",
-                 "avg_ms": avg, "achieved": byts5 / (avg / 1e3) / 1e9, "unit": "GB/s", "peak": hbm_peak(),
-                 "frac": byts5 / (avg / 1e3) / 1e9 / hbm_peak(),
-                 "tflops": 6.0 * nnz * cfg5.dense_cols / (avg / 1e3) / 1e12,
-                 "tensor_frac": 6.0 * nnz * cfg5.dense_cols / (avg / 1e3) / 1e12 / FP64_DMMA_PEAK_TFLOPS,
-                 "bound": "tensor (6 nnz ncols fp64 flops at the DMMA peak outlast the bytes at the HBM peak)"}
+        fl5 = 6.0 * nnz * cfg5.dense_cols
         del S5, Y5
         ctx5.close()
+        return {"workload": f"config 5: M={M} dense S M x {cfg5.dense_cols}, {cfg5.reps} repetitions",
+                "avg_ms": avg, "achieved": byts5 / (avg / 1e3) / 1e9, "unit": "GB/s", "peak": hbm_peak(),
+                "frac": byts5 / (avg / 1e3) / 1e9 / hbm_peak(),
+                "tflops": fl5 / (avg / 1e3) / 1e12, "tensor_frac": fl5 / (avg / 1e3) / 1e12 / FP64_DMMA_PEAK_TFLOPS,
+                "bound": "tensor (6 nnz ncols fp64 flops at the DMMA peak outlast the bytes at the HBM peak)",
+                "traffic": ncu_traffic("dense", "large")}
 
-    # ---- the whole iteration against its roofline: per kernel max(flops / fp64 peak, bytes / HBM peak),
-    #      summed over the M-level kernels of one steady-state iteration
-    it_parts = {k: (flops[k], byts[k]) for k in flops}
-    t_roof = sum(max(f / (FP64_DMMA_PEAK_TFLOPS * 1e12), b / (hbm_peak() * 1e9)) for f, b in it_parts.values())
-    t_meas = 1.0 / value
-    iteration_roofline = {"flops": sum(f for f, _ in it_parts.values()), "bytes": sum(b for _, b in it_parts.values()),
-                          "roofline_ms": t_roof * 1e3, "measured_ms_per_iteration": t_meas * 1e3,
-                          "frac": t_roof / t_meas,
-                          "per_kernel_ms": {k: max(f / (FP64_DMMA_PEAK_TFLOPS * 1e9), b / (hbm_peak() * 1e6))
-                                            for k, (f, b) in it_parts.items()},
-                          "bound": "fp64 tensor (the Gram / basis passes); the SpMM alone is HBM-bound"}
 
-    result = {
-        "metric": "ChebyshevT iterations/sec (fused-SpMM HBM GB/s in roofline_spmm)",
-        "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded FE-like operator, DESIGN.md input recipe)",
-        "config": {"workload": workload_str(cfg, op, n),
-                   "step": "one full ChebyshevT solve of one parameter subset (N iterations + final residual)",
-                   "subsets_per_rank": len(my_subsets), "parallelism": f"subsets round-robin over {world} GPU(s)",
-                   "concurrent_subsets_per_gpu": S, "reserved_sms": reserve,
-                   "l2": "inputs larger than L2 (operator 3.06 GB >> 126 MB)"},
-        "e2e": {"value": e2e_value, "unit": "iterations/s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h)},
-        "gpu_launches": int(launches),
-        "clocks": clocks,
-        "roofline": roof,
-        "roofline_spmm": kernel_entry("spmm"),
-        "roofline_kernels": kernels,
-        "iteration_roofline": iteration_roofline,
-        "config5_dense_spmm": dense,
-        "kernel_ms_per_step": {k: v[0] for k, v in prof.items()},
-        "ts_gram_passes": gram_split,
-        "final_rel_residual": infos[-1]["rel_residual"],
-        "ranks_final": infos[-1]["rank"],
-    }
-    if rank == 0 and not args.no_cpu_baseline:
-        rows = cpu_calibrate(prob, args.cpu_seconds)
-        t = cpu_sample(prob, rows)
-        result["cpu_baseline"] = {"value": (rows / M) / t, "unit": "iterations/s", "cores": cpu_cores(),
-                                  "kind": "oracle",
-                                  "sample": f"one steady-state oracle iteration (six-term scipy SpMM, single-"
-                                            f"threaded; Householder QR + SVD truncation, BLAS threads = cores) on "
-                                            f"rows [0,{rows}) of {M}; {t:.1f}s, scaled by rows/M"}
-    if rank == 0:
-        print(json.dumps(result))
+def algorithmic_work(M, nnz, r, rB, n):
+    """Structurally necessary flops / bytes per launch at steady state (DESIGN.md §2 table):
+    pass 1  Y = Ucat R_V^T (R_V^T lower trapezoidal) + G1 = Y^T Y (symmetric);
+    pass 2  Q1 = Y R1^{-1} (upper triangular) + G2 = Q1^T Q1;  basis  U' = Y W_r Sigma_r^{-1}."""
+    w = rB + 4 * r
+    p = min(n, w)
+    flops = {"spmm": 6.0 * nnz * r,
+             "ts_gram": 2.0 * M * (w * p - p * (p - 1) / 2.0) + 1.0 * M * p * (p + 1),
+             "ts_gram2": 1.0 * M * p * (p + 1) + 1.0 * M * p * (p + 1),
+             "ts_store": 2.0 * M * p * r}
+    byts = {"spmm": 52.0 * nnz + 4.0 * (M + 1) + 32.0 * M * r,
+            "ts_gram": 8.0 * M * w + 8.0 * M * p, "ts_gram2": 8.0 * M * p, "ts_store": 8.0 * M * p + 8.0 * M * r}
+    return flops, byts
+
+
+def operator_bytes(op):
+    return 52 * op.nnz + 4 * (op.M + 1)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        rank, world, _ = dist_env()
+        return run_reference(args, rank, world)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
+    rank, world, local = dist_env()
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    leg = GpuLeg(args, local)
+    run_distributed(args, leg, rank, world, dist if world > 1 else None, dev)
     if world > 1:
         dist.destroy_process_group()
 
@@ -402,12 +508,15 @@ def hbm_peak():
         return 6650.0   # B200_PROFILING.md fallback
 
 
-def ncu_traffic(kernel):
-    """dram bytes per launch of `kernel` from the committed ncu --set full summary, else None."""
+def ncu_traffic(kernel, config="large"):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary (profiles/
+    ncu_traffic.json, keyed by config), else None."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(kernel)
+            d = json.load(f)
+        d = d.get(config, d if config == "large" else {})
+        return d.get(kernel)
     except Exception:
         return None
 

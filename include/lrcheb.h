@@ -24,7 +24,9 @@
  *     only: the library keeps the caller's device pointers; the caller keeps them alive and
  *     unchanged until the next set_operator or lrc_destroy).
  *   - Every call returns an lrc_status; nothing throws or exits.  On error the outputs are
- *     untouched and lrc_last_error(ctx) holds a one-line message.
+ *     untouched and lrc_last_error(ctx) holds a one-line message.  (lrc_solve: an error found on
+ *     the device -- LRC_ERR_NUMERIC -- still fills *info for diagnosis; U_out / V_out are not
+ *     written.  SPEC S:508's "best iterate" of a diverging run is the OK case info->diverged = 1.)
  *   - All work is ordered on ctx's stream; calls return after the work completed (host
  *     synchronous) unless stated otherwise.  One ctx per host thread; no internal locking.
  *
@@ -35,6 +37,7 @@
 #ifndef LRCHEB_H
 #define LRCHEB_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -61,6 +64,8 @@ typedef enum { LRC_MEM_HOST = 0, LRC_MEM_DEVICE = 1, LRC_MEM_DEVICE_BORROW = 2 }
 #define LRC_NO_GRAPH             4u  /* launch the iteration kernels directly instead of a CUDA graph */
 #define LRC_NO_WARM_START        8u  /* start every core Jacobi SVD from W = I (default: warm start from the
                                         previous iteration's right singular basis when p == n) */
+#define LRC_ASYNC               16u  /* DEVICE inputs/outputs only: lrc_solve returns once the work is
+                                        enqueued on ctx's stream; lrc_solve_wait completes the call */
 
 /* lrc_apply_lowrank modes */
 #define LRC_APPLY_PLAIN3  0u  /* W = [W0 | W1 | W2], W0 = (A0+rho Jrho+lam Jlam)U, W1 = (A1+Jmu)U, W2 = rho A2 U */
@@ -127,6 +132,23 @@ lrc_status lrc_solve(lrc_ctx *ctx,
                      const lrc_solve_opts *opts,
                      double *U_out, int64_t ld_u, double *V_out, int64_t ld_v,
                      lrc_mem where, lrc_solve_info *info);
+
+/* Completes a solve started with LRC_ASYNC: waits for ctx's stream, fills *info (may be NULL) and
+ * returns the solve's status (LRC_ERR_STATE if no solve is pending).  The caller keeps B_U, B_V,
+ * U_out and V_out alive until then.  A pending solve is also completed (info discarded) by the
+ * next lrc_solve / lrc_set_workspace on ctx. */
+lrc_status lrc_solve_wait(lrc_ctx *ctx, lrc_solve_info *info);
+
+/* Workspace ownership.  By default ctx allocates its solve workspace (cudaMalloc) and keeps it
+ * between calls.  lrc_workspace_bytes returns the bytes a solve with (r_B, rank_cap, n_iter,
+ * flags & LRC_RECORD_ITERATES) needs for the current operator / params; lrc_set_workspace hands ctx
+ * a caller-owned device buffer (256-byte aligned, on ctx's device; the caller keeps it alive until
+ * the next lrc_set_workspace or lrc_destroy) that all later workspaces are carved from (NULL: back
+ * to library-owned memory).  A solve that does not fit the buffer fails with LRC_ERR_NOMEM.  The
+ * test hooks (lrc_apply_*, lrc_truncate) keep their own library-owned scratch. */
+lrc_status lrc_workspace_bytes(lrc_ctx *ctx, int64_t r_B, int64_t rank_cap, int64_t n_iter, uint32_t flags,
+                               size_t *bytes);
+lrc_status lrc_set_workspace(lrc_ctx *ctx, void *dev_ptr, size_t bytes);
 
 /* Test / bench hooks (same ctx state; where = HOST or DEVICE for all pointers of the call). */
 

@@ -195,9 +195,11 @@ def residual(terms, BU, BV, U, V) -> float:
 
 def chebyshevt(terms, BU, BV, lam_min: float, lam_max: float, tau: float, R: int, N: int,
                record_iterates: bool = True, final_residual: bool = True,
-               restart_every: Optional[int] = None) -> Result:
+               restart_every: Optional[int] = None, on_iterate=None) -> Result:
     """N updates X_1..X_N from X_0 = X_{-1} = 0 (readings S6, S7).  Optional restart (S8,
-    P:546 'restarted once after 6 iterations'): the w sequence restarts with X_{-1} := X_k."""
+    P:546 'restarted once after 6 iterations'): the w sequence restarts with X_{-1} := X_k.
+    on_iterate(k, U_k, V_k, sigma) (optional, no arithmetic) sees every X_k as it is produced,
+    so a caller can keep selected iterates of a long solve without recording all of them."""
     M, n = BU.shape[0], BV.shape[0]
     c, d = chebyshev_cd(lam_min, lam_max)
     gamma = 1.0 / d
@@ -215,6 +217,8 @@ def chebyshevt(terms, BU, BV, lam_min: float, lam_max: float, tau: float, R: int
         Ukm1, Vkm1, Uk, Vk = Uk, Vk, Un, Vn
         ranks.append(Un.shape[1])
         sigmas.append(s)
+        if on_iterate is not None:
+            on_iterate(k + 1, Un, Vn, s)
         if record_iterates:
             iterates.append((Un, Vn))
     rho = residual(terms, BU, BV, Uk, Vk) if final_residual else float("nan")

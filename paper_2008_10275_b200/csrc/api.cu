@@ -54,15 +54,25 @@ struct Workspace {
   double* partials = nullptr;
   double* Y = nullptr;                          // M x pmax: Y = Ucat R_V^T of the current truncation
   double* Uh = nullptr; double* Vh = nullptr;   // iterate history
-  double* tmpA = nullptr; size_t tmpA_sz = 0;   // hook scratch
-  double* tmpB = nullptr; size_t tmpB_sz = 0;
-  double* tmpC = nullptr; size_t tmpC_sz = 0;
+  bool arena = false;                           // carved from the caller's lrc_set_workspace buffer
 };
 
 enum ProfClass { P_SPMM = 0, P_VSIDE, P_TS_GRAM, P_REDUCE, P_CHOL1, P_CHOL2, P_TS_STORE, P_TRACE,
                  P_MISC, P_TINY, P_TS_GRAM2, P_NCLASS };
 const char* const kProfNames[P_NCLASS] = {"spmm", "vside_qr", "ts_gram", "gram_reduce", "chol1",
                                           "chol2_svd", "ts_store", "trace", "misc", "tiny_gemm", "ts_gram2"};
+
+struct Pending {             // a solve enqueued by lrc_solve (completed by finish_solve)
+  bool active = false;
+  int N = 0, rb = 0, cap = 0;
+  int64_t M = 0, n = 0;
+  uint32_t opt_flags = 0;
+  bool record = false;
+  lrc_mem where = LRC_MEM_HOST;
+  double* U_out = nullptr; double* V_out = nullptr;
+  int64_t ld_u = 0, ld_v = 0;
+  const double* UN = nullptr; const double* VN = nullptr;
+};
 
 struct GraphKey {
   int64_t gen = -1, N = 0; int rb = 0, cap = 0; double gamma = 0, tol = 0; uint32_t flags = 0;
@@ -96,12 +106,19 @@ struct lrc_ctx {
   int64_t n = 0;
   double* dmu = nullptr; double* dnu = nullptr;
   Workspace ws;
+  void* user_ws = nullptr;  // caller-owned device arena for the workspace (lrc_set_workspace)
+  size_t user_ws_bytes = 0;
+  double* tmpA = nullptr; size_t tmpA_sz = 0;   // hook scratch (library-owned)
+  double* tmpB = nullptr; size_t tmpB_sz = 0;
+  double* tmpC = nullptr; size_t tmpC_sz = 0;
   int64_t gen = 0;
   // graph
   cudaGraphExec_t gexec = nullptr;
   GraphKey gkey;
   // last solve
   int64_t last_N = 0; bool last_record = false; int last_cap = 0;
+  Pending pending;                                   // enqueued solve awaiting finish_solve
+  int* h_ints = nullptr; double* h_scal = nullptr; double* h_sigma = nullptr; int h_cap = 0;   // pinned
   float last_kernel_ms = 0.f;
   bool warm_start = true;   // LRC_NO_WARM_START clears it per solve
   int reserved_sms = 0;     // SMs the persistent kernels leave free (concurrent subset solves)
@@ -175,12 +192,14 @@ cudaMemcpyKind kind_out(lrc_mem where) {
 }
 
 void free_ws(Workspace& w) {
-  dfree(w.BUb); dfree(w.W3);
-  for (int i = 0; i < 3; ++i) { dfree(w.Ubuf[i]); dfree(w.Vbuf[i]); }
-  dfree(w.BV); dfree(w.omega); dfree(w.ints); dfree(w.sigma); dfree(w.scal);
-  dfree(w.T1); dfree(w.QV); dfree(w.G); dfree(w.R1); dfree(w.Y);
-  dfree(w.R1i); dfree(w.Wz); dfree(w.Wv); dfree(w.W0); dfree(w.Wfull); dfree(w.Bprev);
-  dfree(w.partials); dfree(w.Uh); dfree(w.Vh); dfree(w.tmpA); dfree(w.tmpB); dfree(w.tmpC);
+  if (!w.arena) {
+    dfree(w.BUb); dfree(w.W3);
+    for (int i = 0; i < 3; ++i) { dfree(w.Ubuf[i]); dfree(w.Vbuf[i]); }
+    dfree(w.BV); dfree(w.omega); dfree(w.ints); dfree(w.sigma); dfree(w.scal);
+    dfree(w.T1); dfree(w.QV); dfree(w.G); dfree(w.R1); dfree(w.Y);
+    dfree(w.R1i); dfree(w.Wz); dfree(w.Wv); dfree(w.W0); dfree(w.Wfull); dfree(w.Bprev);
+    dfree(w.partials); dfree(w.Uh); dfree(w.Vh);
+  }
   w = Workspace();
 }
 
@@ -195,12 +214,83 @@ cudaError_t dalloc(T** p, size_t count) {
   return cudaMalloc((void**)p, sizeof(T) * (count ? count : 1));
 }
 
-// Ensure a workspace for (M, n, r_B <= rb, rank cap, N iterations, wmax).
+// Hands out the workspace buffers: cudaMalloc (library-owned), a caller arena (lrc_set_workspace,
+// 256-byte aligned carving) or a dry run that only counts bytes (lrc_workspace_bytes).
+struct Carver {
+  char* base = nullptr;     // arena, or null
+  size_t cap = 0, used = 0;
+  bool dry = false;
+  template <typename T>
+  cudaError_t get(T** p, size_t count) {
+    const size_t bytes = (sizeof(T) * (count ? count : 1) + 255) & ~(size_t)255;
+    if (dry) { *p = nullptr; used += bytes; return cudaSuccess; }
+    if (base) {
+      if (used + bytes > cap) return cudaErrorMemoryAllocation;
+      *p = reinterpret_cast<T*>(base + used);
+      used += bytes;
+      return cudaSuccess;
+    }
+    used += bytes;
+    return dalloc(p, count);
+  }
+};
+
+// The shape of a workspace for (M, n, r_B <= rb, rank cap, N iterations, wmax).
+void ws_shape(const lrc_ctx* ctx, Workspace& w, int rb, int cap, int N, int wmax, bool record) {
+  const int p_need = (int)std::min<int64_t>(ctx->n, wmax);
+  w.M = ctx->M; w.n = ctx->n; w.rb = rb; w.cap = cap; w.N = N;
+  w.pmax = ts_pmax_for(p_need < 1 ? 1 : p_need);
+  w.wmax = wmax;
+  w.capp = ts_pmax_for(cap);
+  w.record = record;
+  w.LDB = rb + (rb & 1);
+  w.LDU = cap + (cap & 1);
+  w.grid = ts_grid_for((int)ctx->M, ctx->reserved_sms);
+}
+
+// Every device buffer of a workspace whose shape fields are set.
+cudaError_t ws_carve(Workspace& w, Carver& c) {
+  const size_t M = (size_t)w.M, n = (size_t)w.n, N = (size_t)w.N, pmax = (size_t)w.pmax;
+  cudaError_t e = cudaSuccess;
+#define CV(ptr, count) do { if ((e = c.get(ptr, count)) != cudaSuccess) return e; } while (0)
+  CV(&w.BUb, M * w.LDB);
+  CV(&w.W3, 3 * M * w.LDU);
+  for (int i = 0; i < 3; ++i) {
+    CV(&w.Ubuf[i], M * w.LDU);
+    CV(&w.Vbuf[i], n * w.cap);
+  }
+  CV(&w.BV, n * (w.rb > 0 ? w.rb : 1));
+  CV(&w.omega, N + 1);
+  CV(&w.ints, N + 16);
+  CV(&w.sigma, (N + 4) * kSigmaStride);
+  CV(&w.scal, 8);
+  CV(&w.T1, (size_t)w.wmax * pmax);
+  CV(&w.QV, n * pmax);
+  CV(&w.G, pmax * pmax);
+  CV(&w.R1, pmax * pmax);
+  CV(&w.R1i, pmax * pmax);
+  CV(&w.Wz, pmax * w.capp);
+  CV(&w.Wv, pmax * w.capp);
+  CV(&w.W0, pmax * pmax);
+  CV(&w.Wfull, pmax * pmax);
+  CV(&w.Bprev, n * pmax);
+  CV(&w.partials, (size_t)w.grid * pmax * pmax);
+  CV(&w.Y, M * pmax);
+  if (w.record) {
+    CV(&w.Uh, N * M * w.LDU);
+    CV(&w.Vh, N * n * w.cap);
+  }
+#undef CV
+  return e;
+}
+
+// Ensure a workspace for (M, n, r_B <= rb, rank cap, N iterations, wmax).  All or nothing: on an
+// allocation failure everything allocated so far is released and the workspace is left empty.
 lrc_status ensure_ws(lrc_ctx* ctx, int rb, int cap, int N, int wmax, bool record) {
   Workspace& w = ctx->ws;
   const int p_need = (int)std::min<int64_t>(ctx->n, wmax);
   const int pmax = ts_pmax_for(p_need < 1 ? 1 : p_need);
-  const int capp = ts_pmax_for(cap);
+  if (pmax < 0) return fail(ctx, LRC_ERR_ARG, "Gram width out of range");
   if (w.W3 && w.M == ctx->M && w.n == ctx->n && w.rb >= rb && w.cap == cap && w.N >= N &&
       w.wmax >= wmax && w.pmax == pmax && (!record || w.record))
     return LRC_OK;
@@ -208,44 +298,43 @@ lrc_status ensure_ws(lrc_ctx* ctx, int rb, int cap, int N, int wmax, bool record
   drop_graph(ctx);
   free_ws(w);
   ++ctx->gen;
+  Workspace nw;
+  ws_shape(ctx, nw, rb, cap, N, wmax, record);
+  Carver c;
+  c.base = static_cast<char*>(ctx->user_ws);
+  c.cap = ctx->user_ws_bytes;
+  nw.arena = c.base != nullptr;
+  const cudaError_t e = ws_carve(nw, c);
+  if (e != cudaSuccess) {
+    free_ws(nw);                          // releases the partial allocation (no-op for an arena)
+    cudaGetLastError();
+    return fail(ctx, LRC_ERR_NOMEM, nw.arena ? "workspace arena too small (see lrc_workspace_bytes)"
+                                              : std::string("workspace allocation: ") + cudaGetErrorString(e));
+  }
+  w = nw;
   const size_t M = (size_t)ctx->M, n = (size_t)ctx->n;
-  w.M = ctx->M; w.n = ctx->n; w.rb = rb; w.cap = cap; w.N = N; w.pmax = pmax; w.wmax = wmax;
-  w.capp = capp; w.record = record;
-  w.LDB = rb + (rb & 1);
-  w.LDU = cap + (cap & 1);
-  w.grid = ts_grid_for((int)ctx->M, ctx->reserved_sms);
-  CK(dalloc(&w.BUb, M * w.LDB));
-  CK(dalloc(&w.W3, 3 * M * w.LDU));
-  for (int i = 0; i < 3; ++i) {
-    CK(dalloc(&w.Ubuf[i], M * w.LDU));
-    CK(dalloc(&w.Vbuf[i], n * cap));
-  }
-  CK(dalloc(&w.BV, n * (rb > 0 ? rb : 1)));
-  CK(dalloc(&w.omega, (size_t)N + 1));
-  CK(dalloc(&w.ints, (size_t)N + 16));
-  CK(dalloc(&w.sigma, ((size_t)N + 4) * kSigmaStride));
-  CK(dalloc(&w.scal, 8));
-  CK(dalloc(&w.T1, (size_t)wmax * pmax));
-  CK(dalloc(&w.QV, n * pmax));
-  CK(dalloc(&w.G, (size_t)pmax * pmax));
-  CK(dalloc(&w.R1, (size_t)pmax * pmax));
-  CK(dalloc(&w.R1i, (size_t)pmax * pmax));
-  CK(dalloc(&w.Wz, (size_t)pmax * capp));
-  CK(dalloc(&w.Wv, (size_t)pmax * capp));
-  CK(dalloc(&w.W0, (size_t)pmax * pmax));
-  CK(dalloc(&w.Wfull, (size_t)pmax * pmax));
-  CK(dalloc(&w.Bprev, n * pmax));
-  CK(dalloc(&w.partials, (size_t)w.grid * pmax * pmax));
-  CK(dalloc(&w.Y, M * pmax));
-  if (record) {
-    CK(dalloc(&w.Uh, (size_t)N * M * w.LDU));
-    CK(dalloc(&w.Vh, (size_t)N * n * cap));
-  }
   CK(cudaMemsetAsync(w.BUb, 0, sizeof(double) * M * w.LDB, ctx->stream));
   CK(cudaMemsetAsync(w.W3, 0, sizeof(double) * 3 * M * w.LDU, ctx->stream));
   for (int i = 0; i < 3; ++i) {
     CK(cudaMemsetAsync(w.Ubuf[i], 0, sizeof(double) * M * w.LDU, ctx->stream));
     CK(cudaMemsetAsync(w.Vbuf[i], 0, sizeof(double) * n * cap, ctx->stream));
+  }
+  return LRC_OK;
+}
+
+// ensure_ws, and make sure the (possibly reused, wider) workspace still fits the single-CTA V-side
+// kernel's shared memory at the wmax / pmax its launches will use
+lrc_status ensure_ws_fit(lrc_ctx* ctx, int rb, int cap, int N, int wmax, bool record) {
+  lrc_status st = ensure_ws(ctx, rb, cap, N, wmax, record);
+  if (st != LRC_OK) return st;
+  if (lrc::vside_smem_bytes((int)ctx->n, ctx->ws.wmax, ctx->ws.pmax) > kSmemLimit) {
+    cudaStreamSynchronize(ctx->stream);
+    drop_graph(ctx);
+    free_ws(ctx->ws);
+    st = ensure_ws(ctx, rb, cap, N, wmax, record);
+    if (st != LRC_OK) return st;
+    if (lrc::vside_smem_bytes((int)ctx->n, ctx->ws.wmax, ctx->ws.pmax) > kSmemLimit)
+      return fail(ctx, LRC_ERR_ARG, "n x w too large for the single-CTA V-side QR");
   }
   return LRC_OK;
 }
@@ -497,6 +586,68 @@ std::vector<double> omega_schedule(double lmin, double lmax, int N, int restart)
 
 bool valid_mem(lrc_mem m) { return m == LRC_MEM_HOST || m == LRC_MEM_DEVICE; }
 
+cudaError_t ensure_pinned(lrc_ctx* ctx, int N) {
+  if (ctx->h_cap >= N && ctx->h_ints) return cudaSuccess;
+  if (ctx->h_ints) cudaFreeHost(ctx->h_ints);
+  if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
+  if (ctx->h_sigma) cudaFreeHost(ctx->h_sigma);
+  ctx->h_ints = nullptr; ctx->h_scal = nullptr; ctx->h_sigma = nullptr; ctx->h_cap = 0;
+  cudaError_t e;
+  if ((e = cudaMallocHost((void**)&ctx->h_ints, sizeof(int) * ((size_t)N + 16))) != cudaSuccess) return e;
+  if ((e = cudaMallocHost((void**)&ctx->h_scal, sizeof(double) * 8)) != cudaSuccess) return e;
+  if ((e = cudaMallocHost((void**)&ctx->h_sigma, sizeof(double) * (size_t)N * kSigmaStride)) != cudaSuccess) return e;
+  ctx->h_cap = N;
+  return cudaSuccess;
+}
+
+lrc_status finish_solve(lrc_ctx* ctx, lrc_solve_info* info) {
+  Pending pd = ctx->pending;
+  ctx->pending.active = false;
+  cudaStream_t s = ctx->stream;
+  CK(cudaStreamSynchronize(s));
+  prof_collect(ctx);
+  Workspace& w = ctx->ws;
+  const int N = pd.N;
+  const int* ints = ctx->h_ints;
+  const double* scal = ctx->h_scal;
+  ctx->last_N = N;
+  ctx->last_record = pd.record;
+  ctx->last_cap = pd.cap;
+  const int flags = pd.rb > 0 ? ints[w.N + 6] : 0;
+  if (info) {
+    float ms_it = 0.f, ms_tot = 0.f;
+    cudaEventElapsedTime(&ms_it, ctx->ev[1], ctx->ev[2]);
+    cudaEventElapsedTime(&ms_tot, ctx->ev[0], ctx->ev[3]);
+    info->rank = pd.rb > 0 ? ints[N + 1] : 0;
+    const double b2 = pd.rb > 0 ? scal[0] : 0.0;
+    info->b_norm = std::sqrt(b2);
+    if (pd.opt_flags & LRC_SKIP_FINAL_RESIDUAL) info->rel_residual = NAN;
+    else info->rel_residual = (b2 > 0.0) ? std::sqrt(scal[1] / b2) : 0.0;
+    info->diverged = (info->rel_residual > 1.0) ? 1 : 0;
+    info->shift_escalations = pd.rb > 0 ? ints[w.N + 7] : 0;
+    info->ms_iterations = ms_it;
+    info->ms_total = ms_tot;
+    if (info->rank_history)
+      for (int k = 0; k < N; ++k) info->rank_history[k] = pd.rb > 0 ? ints[k + 2] : 0;
+    if (info->sigma_history) {
+      if (pd.rb > 0) std::memcpy(info->sigma_history, ctx->h_sigma, sizeof(double) * (size_t)N * kSigmaStride);
+      else std::memset(info->sigma_history, 0, sizeof(double) * (size_t)N * kSigmaStride);
+    }
+    info->jacobi_sweeps = pd.rb > 0 ? ints[w.N + 8] : 0;
+    for (int i = 0; i < 3; ++i) info->chol2_cycles[i] = pd.rb > 0 ? scal[4 + i] : 0.0;
+  }
+  if (flags & 1) return fail(ctx, LRC_ERR_NUMERIC, "shifted Cholesky failed after all escalations");
+  if (flags & 2) return fail(ctx, LRC_ERR_NUMERIC, "non-finite singular value in the core SVD");
+  if (pd.rb > 0 && pd.where == LRC_MEM_HOST) {   // HOST outputs only now: untouched on error
+    CK(cudaMemcpy2DAsync(pd.U_out, sizeof(double) * pd.ld_u, pd.UN, sizeof(double) * w.LDU,
+                         sizeof(double) * pd.cap, pd.M, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpy2DAsync(pd.V_out, sizeof(double) * pd.ld_v, pd.VN, sizeof(double) * pd.cap,
+                         sizeof(double) * pd.cap, pd.n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  return LRC_OK;
+}
+
 }  // namespace
 
 // =============================================================================================
@@ -551,12 +702,16 @@ void lrc_destroy(lrc_ctx* ctx) {
     dfree(ctx->row_ptr); dfree(ctx->col_idx);
     for (int t = 0; t < 6; ++t) dfree(ctx->vals[t]);
   }
+  dfree(ctx->tmpA); dfree(ctx->tmpB); dfree(ctx->tmpC);
   dfree(ctx->group_ptr); dfree(ctx->tdesc); dfree(ctx->tlist_u); dfree(ctx->tlist_g); dfree(ctx->tile_ev); dfree(ctx->dmu); dfree(ctx->dnu);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   for (int i = 0; i < 4; ++i) if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
   for (cudaEvent_t e : ctx->evpool) cudaEventDestroy(e);
+  if (ctx->h_ints) cudaFreeHost(ctx->h_ints);
+  if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
+  if (ctx->h_sigma) cudaFreeHost(ctx->h_sigma);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -566,6 +721,44 @@ const char* lrc_last_error(const lrc_ctx* ctx) { return ctx ? ctx->err.c_str() :
 float lrc_last_kernel_ms(const lrc_ctx* ctx) { return ctx ? ctx->last_kernel_ms : 0.f; }
 
 int64_t lrc_kernel_launches(const lrc_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+lrc_status lrc_workspace_bytes(lrc_ctx* ctx, int64_t r_B, int64_t rank_cap, int64_t n_iter, uint32_t flags,
+                               size_t* bytes) {
+  if (!ctx || !bytes) return LRC_ERR_ARG;
+  ctx->err.clear();
+  if (!ctx->op_set || !ctx->par_set) return fail(ctx, LRC_ERR_STATE, "lrc_workspace_bytes before set_operator + set_params");
+  if (r_B < 0 || r_B > 64 || rank_cap < 1 || rank_cap > kMaxRank || n_iter < 1 || n_iter > 100000)
+    return fail(ctx, LRC_ERR_ARG, "r_B / rank_cap / n_iter out of range");
+  const int rb = std::max((int)r_B, 1), cap = (int)rank_cap;
+  const int wmax = (rb + (rb & 1)) + 4 * (cap + (cap & 1));
+  if (ts_pmax_for((int)std::min<int64_t>(ctx->n, wmax)) < 0) return fail(ctx, LRC_ERR_ARG, "Gram width out of range");
+  Workspace w;
+  ws_shape(ctx, w, rb, cap, (int)n_iter, wmax, (flags & LRC_RECORD_ITERATES) != 0);
+  Carver c;
+  c.dry = true;
+  ws_carve(w, c);
+  *bytes = c.used;
+  return LRC_OK;
+}
+
+lrc_status lrc_set_workspace(lrc_ctx* ctx, void* dev_ptr, size_t bytes) {
+  if (!ctx) return LRC_ERR_ARG;
+  ctx->err.clear();
+  if (dev_ptr && (reinterpret_cast<uintptr_t>(dev_ptr) & 255)) return fail(ctx, LRC_ERR_ARG, "workspace must be 256-byte aligned");
+  if (ctx->pending.active) {
+    lrc_status ps = finish_solve(ctx, nullptr);
+    if (ps != LRC_OK) return ps;
+  }
+  CK(cudaSetDevice(ctx->device));
+  cudaStreamSynchronize(ctx->stream);
+  drop_graph(ctx);
+  free_ws(ctx->ws);
+  ++ctx->gen;
+  ctx->user_ws = dev_ptr;
+  ctx->user_ws_bytes = dev_ptr ? bytes : 0;
+  ctx->last_record = false;
+  return LRC_OK;
+}
 
 lrc_status lrc_set_reserved_sms(lrc_ctx* ctx, int n) {
   if (!ctx) return LRC_ERR_ARG;
@@ -666,6 +859,7 @@ lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t*
       d[3] = ushared ? (int)uni.size() : 0;
       d[4] = r0;
       d[5] = r1;
+      d[6] = 0;                            // staged doubles (three grouped streams, padded rows)
       uint16_t* lx = reinterpret_cast<uint16_t*>(d.data() + kDescLidx);
       int lo = 0;
       for (size_t b = 0; b < tb.size(); ++b) {
@@ -675,6 +869,7 @@ lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t*
         d[8 + b] = groups[gi];
         d[12 + b] = groups[gi + 1] - groups[gi];
         d[16 + b] = L;
+        d[6] += 3 * (groups[gi + 1] - groups[gi]) * (L + ((20 - (L & 15)) & 15));
         d[20 + b] = -1;                    // local row of the block's first row in the staged U rows
         if (ushared) {
           auto it = std::lower_bound(uni.begin(), uni.end(), (int32_t)groups[gi]);
@@ -855,11 +1050,17 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
   if (p_need > 112) return fail(ctx, LRC_ERR_ARG, "min(n, r_B + 4 rank_cap) must be <= 112 in this build");
   if (lrc::vside_smem_bytes((int)n, wmax, ts_pmax_for(p_need)) > kSmemLimit)
     return fail(ctx, LRC_ERR_ARG, "n x (r_B + 4 rank_cap) too large for the single-CTA V-side QR");
+  if ((opts->flags & LRC_ASYNC) && where != LRC_MEM_DEVICE)
+    return fail(ctx, LRC_ERR_ARG, "LRC_ASYNC needs DEVICE inputs and outputs");
+  if (ctx->pending.active) {                         // an LRC_ASYNC solve never waited for
+    lrc_status ps = finish_solve(ctx, nullptr);
+    if (ps != LRC_OK) return ps;
+  }
   const bool record = (opts->flags & LRC_RECORD_ITERATES) != 0;
   const bool use_graph = (opts->flags & LRC_NO_GRAPH) == 0 && !ctx->profiling;
   ctx->warm_start = (opts->flags & LRC_NO_WARM_START) == 0;
   CK(cudaSetDevice(ctx->device));
-  lrc_status st = ensure_ws(ctx, std::max(rb, 1), cap, N, wmax, record);
+  lrc_status st = ensure_ws_fit(ctx, std::max(rb, 1), cap, N, wmax, record);
   if (st != LRC_OK) return st;
   Workspace& w = ctx->ws;
   cudaStream_t s = ctx->stream;
@@ -946,11 +1147,16 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
       st = enqueue_norm2(ctx, ur, vr, 1, s);
       if (st != LRC_OK) return st;
     }
-    // outputs (zero the columns >= rank)
-    KL(P_MISC, s, launch_zero_cols(UN, (int)M, w.LDU, sd.rk + slotN, 0, cap, s));
-    KL(P_MISC, s, launch_zero_cols(VN, (int)n, cap, sd.rk + slotN, 0, cap, s));
-    CK(cudaMemcpy2DAsync(U_out, sizeof(double) * ld_u, UN, sizeof(double) * w.LDU, sizeof(double) * cap, M, kind_out(where), s));
-    CK(cudaMemcpy2DAsync(V_out, sizeof(double) * ld_v, VN, sizeof(double) * cap, sizeof(double) * cap, n, kind_out(where), s));
+    // outputs: DEVICE outputs by a guarded copy kernel (columns >= rank zeroed; nothing is written
+    // when the device flags an error, so the outputs stay untouched on LRC_ERR_NUMERIC); HOST
+    // outputs are copied in finish_solve after the flags were checked
+    if (where == LRC_MEM_DEVICE) {
+      KL(P_MISC, s, launch_copy_out(UN, w.LDU, U_out, (int)ld_u, (int)M, cap, sd.rk + slotN, sd.flags, s));
+      KL(P_MISC, s, launch_copy_out(VN, cap, V_out, (int)ld_v, (int)n, cap, sd.rk + slotN, sd.flags, s));
+    } else {
+      KL(P_MISC, s, launch_zero_cols(UN, (int)M, w.LDU, sd.rk + slotN, 0, cap, s));
+      KL(P_MISC, s, launch_zero_cols(VN, (int)n, cap, sd.rk + slotN, 0, cap, s));
+    }
   } else {
     CK(cudaEventRecord(ctx->ev[1], s));
     CK(cudaEventRecord(ctx->ev[2], s));
@@ -963,44 +1169,27 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
     }
   }
   CK(cudaEventRecord(ctx->ev[3], s));
-  // results
-  std::vector<int> ints(w.N + 16, 0);
-  std::vector<double> scal(8, 0.0);
-  CK(cudaMemcpyAsync(ints.data(), w.ints, sizeof(int) * (w.N + 16), cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(scal.data(), w.scal, sizeof(double) * 8, cudaMemcpyDeviceToHost, s));
-  std::vector<double> sig;
-  if (info && info->sigma_history) {
-    sig.resize((size_t)N * kSigmaStride);
-    CK(cudaMemcpyAsync(sig.data(), w.sigma, sizeof(double) * sig.size(), cudaMemcpyDeviceToHost, s));
-  }
-  CK(cudaStreamSynchronize(s));
-  prof_collect(ctx);
-  ctx->last_N = N;
-  ctx->last_record = record;
-  ctx->last_cap = cap;
-  const int flags = ints[w.N + 6];
-  if (info) {
-    float ms_it = 0.f, ms_tot = 0.f;
-    cudaEventElapsedTime(&ms_it, ctx->ev[1], ctx->ev[2]);
-    cudaEventElapsedTime(&ms_tot, ctx->ev[0], ctx->ev[3]);
-    info->rank = rb > 0 ? ints[N + 1] : 0;
-    const double b2 = scal[0];
-    info->b_norm = std::sqrt(b2);
-    if (opts->flags & LRC_SKIP_FINAL_RESIDUAL) info->rel_residual = NAN;
-    else info->rel_residual = (b2 > 0.0) ? std::sqrt(scal[1] / b2) : 0.0;
-    info->diverged = (info->rel_residual > 1.0) ? 1 : 0;
-    info->shift_escalations = ints[w.N + 7];
-    info->ms_iterations = ms_it;
-    info->ms_total = ms_tot;
-    if (info->rank_history)
-      for (int k = 0; k < N; ++k) info->rank_history[k] = rb > 0 ? ints[k + 2] : 0;
-    if (info->sigma_history) std::memcpy(info->sigma_history, sig.data(), sizeof(double) * sig.size());
-    info->jacobi_sweeps = ints[w.N + 8];
-    info->chol2_cycles[0] = scal[4]; info->chol2_cycles[1] = scal[5]; info->chol2_cycles[2] = scal[6];
-  }
-  if (flags & 1) return fail(ctx, LRC_ERR_NUMERIC, "shifted Cholesky failed after all escalations");
-  if (flags & 2) return fail(ctx, LRC_ERR_NUMERIC, "non-finite singular value in the core SVD");
-  return LRC_OK;
+  // results -> pinned host mirrors (read by finish_solve after the stream synchronises)
+  CK(ensure_pinned(ctx, w.N));
+  CK(cudaMemcpyAsync(ctx->h_ints, w.ints, sizeof(int) * (w.N + 16), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(ctx->h_scal, w.scal, sizeof(double) * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(ctx->h_sigma, w.sigma, sizeof(double) * (size_t)N * kSigmaStride, cudaMemcpyDeviceToHost, s));
+  Pending& pd = ctx->pending;
+  pd.active = true;
+  pd.N = N; pd.rb = rb; pd.cap = cap; pd.M = M; pd.n = n; pd.opt_flags = opts->flags; pd.record = record;
+  pd.where = where; pd.U_out = U_out; pd.V_out = V_out; pd.ld_u = ld_u; pd.ld_v = ld_v;
+  pd.UN = w.Ubuf[(N + 1) % 3]; pd.VN = w.Vbuf[(N + 1) % 3];
+  if (opts->flags & LRC_ASYNC) return LRC_OK;     // lrc_solve_wait completes the call
+  return finish_solve(ctx, info);
+}
+
+// Wait for the solve enqueued last on ctx, fill info, copy HOST outputs (only when no error was
+// flagged on the device) and return the call's status.
+lrc_status lrc_solve_wait(lrc_ctx* ctx, lrc_solve_info* info) {
+  if (!ctx) return LRC_ERR_ARG;
+  if (!ctx->pending.active) return fail(ctx, LRC_ERR_STATE, "no solve pending on this context");
+  CK(cudaSetDevice(ctx->device));
+  return finish_solve(ctx, info);
 }
 
 lrc_status lrc_apply_lowrank(lrc_ctx* ctx, const double* U, int64_t ld_u, int64_t r, double* W,
@@ -1021,13 +1210,13 @@ lrc_status lrc_apply_lowrank(lrc_ctx* ctx, const double* U, int64_t ld_u, int64_
   double* Wd = W;
   int ldu = (int)ld_u, ldw = (int)ld_w;
   if (where == LRC_MEM_HOST) {
-    lrc_status st = ensure_tmp(ctx, &ctx->ws.tmpA, &ctx->ws.tmpA_sz, (size_t)M * r);
+    lrc_status st = ensure_tmp(ctx, &ctx->tmpA, &ctx->tmpA_sz, (size_t)M * r);
     if (st != LRC_OK) return st;
-    st = ensure_tmp(ctx, &ctx->ws.tmpB, &ctx->ws.tmpB_sz, (size_t)M * nout * r);
+    st = ensure_tmp(ctx, &ctx->tmpB, &ctx->tmpB_sz, (size_t)M * nout * r);
     if (st != LRC_OK) return st;
-    CK(cudaMemcpy2DAsync(ctx->ws.tmpA, sizeof(double) * r, U, sizeof(double) * ld_u, sizeof(double) * r, M, cudaMemcpyHostToDevice, s));
-    Ud = ctx->ws.tmpA; ldu = (int)r;
-    Wd = ctx->ws.tmpB; ldw = nout * (int)r;
+    CK(cudaMemcpy2DAsync(ctx->tmpA, sizeof(double) * r, U, sizeof(double) * ld_u, sizeof(double) * r, M, cudaMemcpyHostToDevice, s));
+    Ud = ctx->tmpA; ldu = (int)r;
+    Wd = ctx->tmpB; ldw = nout * (int)r;
   }
   SpmmArgs a = spmm_base(ctx);
   a.U = Ud; a.ldu = ldu; a.d_r = nullptr; a.r_fixed = (int)r; a.out = Wd; a.ldo = ldw; a.out_off = 0;
@@ -1068,13 +1257,13 @@ lrc_status lrc_apply_dense(lrc_ctx* ctx, const double* S, int64_t ld_s, int64_t 
   double* Yd = Y;
   int lds = (int)ld_s, ldy = (int)ld_y;
   if (where == LRC_MEM_HOST) {
-    lrc_status st = ensure_tmp(ctx, &ctx->ws.tmpA, &ctx->ws.tmpA_sz, (size_t)M * ncols);
+    lrc_status st = ensure_tmp(ctx, &ctx->tmpA, &ctx->tmpA_sz, (size_t)M * ncols);
     if (st != LRC_OK) return st;
-    st = ensure_tmp(ctx, &ctx->ws.tmpB, &ctx->ws.tmpB_sz, (size_t)M * ncols);
+    st = ensure_tmp(ctx, &ctx->tmpB, &ctx->tmpB_sz, (size_t)M * ncols);
     if (st != LRC_OK) return st;
-    CK(cudaMemcpy2DAsync(ctx->ws.tmpA, sizeof(double) * ncols, S, sizeof(double) * ld_s, sizeof(double) * ncols, M, cudaMemcpyHostToDevice, s));
-    Sd = ctx->ws.tmpA; lds = (int)ncols;
-    Yd = ctx->ws.tmpB; ldy = (int)ncols;
+    CK(cudaMemcpy2DAsync(ctx->tmpA, sizeof(double) * ncols, S, sizeof(double) * ld_s, sizeof(double) * ncols, M, cudaMemcpyHostToDevice, s));
+    Sd = ctx->tmpA; lds = (int)ncols;
+    Yd = ctx->tmpB; ldy = (int)ncols;
   }
   SpmmArgs a = spmm_base(ctx);
   a.U = Sd; a.ldu = lds; a.d_r = nullptr; a.r_fixed = (int)ncols; a.out = Yd; a.ldo = ldy;
@@ -1106,40 +1295,37 @@ lrc_status lrc_truncate(lrc_ctx* ctx, const double* U, int64_t ld_u, const doubl
   const int w = (int)wdt, capi = (int)cap;
   const int p_need = (int)std::min<int64_t>(n, w);
   if (p_need > 112) return fail(ctx, LRC_ERR_ARG, "min(n, w) must be <= 112 in this build");
-  const int wmax = std::max(w, 4 * capi + 1);
-  if (lrc::vside_smem_bytes((int)n, std::max(w, 1), ts_pmax_for(p_need)) > kSmemLimit)
+  if (lrc::vside_smem_bytes((int)n, w, ts_pmax_for(p_need)) > kSmemLimit)
     return fail(ctx, LRC_ERR_ARG, "n x w too large for the single-CTA V-side QR");
   CK(cudaSetDevice(ctx->device));
-  lrc_status st = ensure_ws(ctx, std::max(ctx->ws.rb, 1), capi, std::max(ctx->ws.N, 1),
-                            std::max(wmax, ctx->ws.wmax), ctx->ws.record);
+  // a workspace for this call's width (an existing one is reused when it is compatible)
+  lrc_status st = ensure_ws_fit(ctx, std::max(ctx->ws.rb, 1), capi, std::max(ctx->ws.N, 1), w, false);
   if (st != LRC_OK) return st;
   Workspace& ws = ctx->ws;
   cudaStream_t s = ctx->stream;
   // inputs
-  st = ensure_tmp(ctx, &ws.tmpA, &ws.tmpA_sz, (size_t)M * w);
+  st = ensure_tmp(ctx, &ctx->tmpA, &ctx->tmpA_sz, (size_t)M * w);
   if (st != LRC_OK) return st;
-  st = ensure_tmp(ctx, &ws.tmpB, &ws.tmpB_sz, (size_t)n * w + (size_t)n * capi);
+  st = ensure_tmp(ctx, &ctx->tmpB, &ctx->tmpB_sz, (size_t)n * w + (size_t)n * capi);
   if (st != LRC_OK) return st;
-  st = ensure_tmp(ctx, &ws.tmpC, &ws.tmpC_sz, (size_t)M * capi);
+  st = ensure_tmp(ctx, &ctx->tmpC, &ctx->tmpC_sz, (size_t)M * capi);
   if (st != LRC_OK) return st;
-  CK(cudaMemcpy2DAsync(ws.tmpA, sizeof(double) * w, U, sizeof(double) * ld_u, sizeof(double) * w, M, kind_in(where), s));
-  CK(cudaMemcpy2DAsync(ws.tmpB, sizeof(double) * w, V, sizeof(double) * ld_v, sizeof(double) * w, n, kind_in(where), s));
+  CK(cudaMemcpy2DAsync(ctx->tmpA, sizeof(double) * w, U, sizeof(double) * ld_u, sizeof(double) * w, M, kind_in(where), s));
+  CK(cudaMemcpy2DAsync(ctx->tmpB, sizeof(double) * w, V, sizeof(double) * ld_v, sizeof(double) * w, n, kind_in(where), s));
   State sd = make_state(ws);
   const int slot = ws.N + 2;
   CK(cudaMemsetAsync(ws.ints, 0, sizeof(int) * (ws.N + 16), s));
   CK(cudaMemsetAsync(ws.sigma, 0, sizeof(double) * (size_t)(ws.N + 4) * kSigmaStride, s));
   UDesc ud{};
   ud.nb = 1;
-  ud.b[0] = ublock(ws.tmpA, w, w, -1);
+  ud.b[0] = ublock(ctx->tmpA, w, w, -1);
   VDesc vd{};
   vd.nb = 1;
-  vd.b[0] = vblock(ws.tmpB, w, w, -1, 1.0, 0, 0);
-  double* Vnew = ws.tmpB + (size_t)n * w;
-  st = enqueue_truncation(ctx, ud, vd, nullptr, 0, tol, capi, slot, ws.N, ws.tmpC, capi, Vnew, capi, s, false);
+  vd.b[0] = vblock(ctx->tmpB, w, w, -1, 1.0, 0, 0);
+  double* Vnew = ctx->tmpB + (size_t)n * w;
+  st = enqueue_truncation(ctx, ud, vd, nullptr, 0, tol, capi, slot, ws.N, ctx->tmpC, capi, Vnew, capi, s, false);
   if (st != LRC_OK) return st;
-  KL(P_MISC, s, launch_zero_cols(ws.tmpC, (int)M, capi, sd.rk + slot, 0, capi, s));
-  CK(cudaMemcpyAsync(U_out, ws.tmpC, sizeof(double) * M * capi, kind_out(where), s));
-  CK(cudaMemcpyAsync(V_out, Vnew, sizeof(double) * n * capi, kind_out(where), s));
+  KL(P_MISC, s, launch_zero_cols(ctx->tmpC, (int)M, capi, sd.rk + slot, 0, capi, s));
   int hr = 0, flags = 0;
   CK(cudaMemcpyAsync(&hr, sd.rk + slot, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(&flags, sd.flags, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1147,11 +1333,14 @@ lrc_status lrc_truncate(lrc_ctx* ctx, const double* U, int64_t ld_u, const doubl
   CK(cudaMemcpyAsync(sg.data(), ws.sigma + (size_t)ws.N * kSigmaStride, sizeof(double) * kSigmaStride, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   prof_collect(ctx);
-  *rank = hr;
-  if (sigma) std::memcpy(sigma, sg.data(), sizeof(double) * p_need);
   ctx->last_record = false;   // tmp state overwrote the iterate bookkeeping slots
   if (flags & 1) return fail(ctx, LRC_ERR_NUMERIC, "shifted Cholesky failed after all escalations");
   if (flags & 2) return fail(ctx, LRC_ERR_NUMERIC, "non-finite singular value in the core SVD");
+  CK(cudaMemcpyAsync(U_out, ctx->tmpC, sizeof(double) * M * capi, kind_out(where), s));   // outputs only on success
+  CK(cudaMemcpyAsync(V_out, Vnew, sizeof(double) * n * capi, kind_out(where), s));
+  CK(cudaStreamSynchronize(s));
+  *rank = hr;
+  if (sigma) std::memcpy(sigma, sg.data(), sizeof(double) * p_need);
   return LRC_OK;
 }
 

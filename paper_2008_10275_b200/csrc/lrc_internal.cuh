@@ -15,7 +15,7 @@ constexpr int kValCap = 3200;    // staged (combined, row-padded) doubles per Sp
 constexpr int kTileBlocks = 4;   // node blocks per SpMM tile
 constexpr int kUCap = 90;        // deduplicated U rows staged in shared memory per SpMM tile
 // SpMM tile descriptor (int32 words): [0] e0 (first nnz) [1] tot (nnz) [2] nb (blocks) [3] nu (U rows
-// staged; 0 = L2-gather tile) [4] rbeg [5] rend [6..7] pad, [8+b] row0, [12+b] g, [16+b] L, [20+b] local U row of the block's
+// staged; 0 = L2-gather tile) [4] rbeg [5] rend [6] staged doubles (3 streams, padded rows) [7] pad, [8+b] row0, [12+b] g, [16+b] L, [20+b] local U row of the block's
 // first row (-1: not staged)
 // (b < 4); [24 .. 24+kUCap) U row ids; [kDescLidx ..) uint16 local column indices of the blocks'
 // column lists, concatenated (<= kLidxCap entries).
@@ -43,9 +43,6 @@ struct SpmmArgs {
   int ntl_g;
   const int* tlist;         // (set by the launcher) tile list, or null for all tiles
   int u_aligned16;          // (set by the launcher) U rows may be copied in 16-byte chunks
-  int dbg;                  // (developer bisection, env LRCHEB_SPMM_DBG) 1: no DMMA, 2: no U staging,
-                            // 4: no value loads, 8: no output stores; 32 (env LRCHEB_SPMM_TMA): use
-                            // the experimental persistent TMA pipeline kernel
   const int* row_ptr;
   const int* col_idx;
   const double* v[6];       // A0, A1, A2, Jrho, Jmu, Jlam
@@ -95,8 +92,6 @@ struct TsArgs {
   int ldy;
   int u16;                  // (set by launch_ts) all Ucat blocks 16-byte aligned with even ld/offsets
   int o16;                  // (set by launch_ts) STORE rows 16-byte aligned (even ldo)
-  int dbg;                  // (set by launch_ts; developer bisection, env LRCHEB_TS_DBG) 1: no copies,
-                            // 2: no Gram / store epilogue, 4: no phase-A DMMA, 8: no Y stores
 };
 // mode 0 = GRAM (partial X^T X, X = Ucat T), 1 = STORE (out = Ucat T)
 cudaError_t launch_ts(int mode, const TsArgs& a, int pmax, int grid, cudaStream_t s);
@@ -165,6 +160,8 @@ cudaError_t launch_trace(State st, const double* G, int pmax, int slot, cudaStre
 
 // misc
 cudaError_t launch_fill_int(int* p, int v, int n, cudaStream_t s);
+cudaError_t launch_copy_out(const double* src, int ld_src, double* dst, int ld_dst, int rows, int cols,
+                            const int* d_rank, const int* flags, cudaStream_t s);
 cudaError_t launch_zero_cols(double* X, int rows, int ld, const int* d_r, int r_fixed, int cols,
                              cudaStream_t s);
 

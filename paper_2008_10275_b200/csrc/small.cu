@@ -599,6 +599,18 @@ __global__ void zero_cols_kernel(double* X, int rows, int ld, const int* d_r, in
   if (c >= r) X[(size_t)i * ld + c] = 0.0;
 }
 
+// dst (rows x cols, ld_dst) = src with the columns >= *d_rank zeroed -- unless *flags != 0 (an
+// error was flagged on the device), in which case dst is left untouched
+__global__ void copy_out_kernel(const double* __restrict__ src, int ld_src, double* __restrict__ dst,
+                                int ld_dst, int rows, int cols, const int* d_rank, const int* flags) {
+  if (*flags) return;
+  const int r = *d_rank;
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)rows * cols) return;
+  const int i = (int)(e / cols), c = (int)(e % cols);
+  dst[(size_t)i * ld_dst + c] = (c < r) ? src[(size_t)i * ld_src + c] : 0.0;
+}
+
 template <typename K>
 cudaError_t set_smem(K kern, size_t bytes) {
   cudaFuncAttributes fa;
@@ -666,6 +678,14 @@ cudaError_t launch_trace(State st, const double* G, int pmax, int slot, cudaStre
 cudaError_t launch_fill_int(int* p, int v, int n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   fill_int_kernel<<<(n + 255) / 256, 256, 0, s>>>(p, v, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_out(const double* src, int ld_src, double* dst, int ld_dst, int rows, int cols,
+                            const int* d_rank, const int* flags, cudaStream_t s) {
+  const size_t tot = (size_t)rows * cols;
+  if (tot == 0) return cudaSuccess;
+  copy_out_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(src, ld_src, dst, ld_dst, rows, cols, d_rank, flags);
   return cudaGetLastError();
 }
 

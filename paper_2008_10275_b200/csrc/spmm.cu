@@ -17,8 +17,7 @@
 // [slot][j] layout, and gives each warp one (node block, 32-column slice) contraction on the fp64
 // tensor pipe (m16n8k4 DMMA, computed transposed so stores are full sectors).  Tiles whose rows do
 // not fit the U-path bounds take the general spmm_kernel (L2 gather).  spmm_dense_kernel is the
-// config-5 dense variant; spmm_p_kernel / spmm_t_kernel are opt-in pipelined experiments.
-#include <cstdlib>
+// config-5 dense variant.
 #include "lrc_internal.cuh"
 
 namespace lrc {
@@ -188,9 +187,6 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)_
 __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
 }
-__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
-}
 __device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
   unsigned ok;
   asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
@@ -246,7 +242,7 @@ __device__ __forceinline__ void block_task_mma_smem(const SpmmArgs& a, int r, in
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.0;
-  for (int k0 = 0; k0 < ((a.dbg & 1) ? 0 : L); k0 += 4) {
+  for (int k0 = 0; k0 < L; k0 += 4) {
     const int j = k0 + tig;
     const bool jv = j < L;
     const double* vj = vals + qo * 3 * lp + j;
@@ -281,7 +277,7 @@ __device__ __forceinline__ void block_task_mma_smem(const SpmmArgs& a, int r, in
           if (c < r) {
             double v = acc[mt][nt][hm * 2 + e];
             if (MODE == SPMM_S2STEP && st == 0) v = fma(-a.gamma, v, urow_self[c]);
-            if (!(a.dbg & 8)) __stcs(orow + c, v);
+            __stcs(orow + c, v);
           } else if (c == r && (r & 1) && a.out_sstride) {
             __stcs(orow + c, 0.0);        // zero pad column of the (even-padded) Ucat block
           }
@@ -306,7 +302,7 @@ __device__ __forceinline__ void block_task_mma_fast(const SpmmArgs& a, int r, in
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.0;
-  const int L4 = (a.dbg & 1) ? 0 : ((L + 3) & ~3);
+  const int L4 = (L + 3) & ~3;
   const double* vb = vals + (qo * 3 + gid) * lp + tig;
   const double* ub = s_u + n0 + gid;
   const unsigned short* lc = lcols + tig;
@@ -337,7 +333,6 @@ __device__ __forceinline__ void block_task_mma_fast(const SpmmArgs& a, int r, in
       const bool s2 = (MODE == SPMM_S2STEP) && st == 0;
       const double alpha = s2 ? -a.gamma : 1.0, beta = s2 ? 1.0 : 0.0;
       const double* us = s_u + (MODE == SPMM_S2STEP ? (lrow0 + qo + q) * ust : 0) + n0 + gid;
-      if (a.dbg & 8) continue;
       if (full) {
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
@@ -432,7 +427,9 @@ spmm_kernel(SpmmArgs a, int ust) {
   const int rbeg = s_desc[4], rend = s_desc[5];
   const unsigned short* s_lx = reinterpret_cast<const unsigned short*>(s_desc + kDescLidx);
 
-  if (tot <= kSpmmCap) {
+  // staged path only if the whole tile fits the value stage (s_desc[6] = staged doubles at NV = 3);
+  // a single block longer or taller than that takes the chunked long path below
+  if (tot <= kSpmmCap && s_desc[6] <= kValCap) {
     if (tid == 0) {
       int vb = 0, cb = 0, eb = 0;
       for (int b = 0; b < nb; ++b) {
@@ -582,7 +579,7 @@ spmm_u_kernel(SpmmArgs a, int ust) {
 #pragma unroll
   for (int k = 0; k < kStg; ++k) {
     const int e = tid + k * kThreads;
-    if (e < tot && !(a.dbg & 4)) {
+    if (e < tot) {
 #pragma unroll
       for (int v = 0; v < 6; ++v) raw[k][v] = __ldcs(a.v[v] + e0 + e);
     } else {
@@ -597,14 +594,14 @@ spmm_u_kernel(SpmmArgs a, int ust) {
     // the LSU path the value loads and the contraction's shared-memory loads share
     if (warp == 0) {
       const unsigned ubytes = (unsigned)((r + 1) >> 1) * 16u;
-      const int nuc = (a.dbg & 2) ? 0 : nu;
+      const int nuc = nu;
       if (lane == 0) mbar_expect_tx(&ubar, ubytes * (unsigned)nuc);
       __syncwarp();
       for (int u = lane; u < nuc; u += 32)
         bulk_g2s(s_u + u * ust, a.U + (size_t)s_desc[kDescUrows + u] * a.ldu, ubytes, &ubar);
     }
   } else {
-    if (!(a.dbg & 2)) stage_u_rows(a, r, s_desc + kDescUrows, nu, s_u, ust, tid, kThreads);
+    stage_u_rows(a, r, s_desc + kDescUrows, nu, s_u, ust, tid, kThreads);
     asm volatile("cp.async.commit_group;\n" ::);
   }
   if (tid == 0) {
@@ -665,130 +662,6 @@ spmm_u_kernel(SpmmArgs a, int ust) {
       }
     }
     cb += L;
-  }
-}
-
-// Persistent variant of spmm_u_kernel (2 CTAs / SM, 128 registers): while tile i is contracted, the
-// six value streams, the (e0, nnz) pair and the descriptor of tile i + G are already in flight in
-// registers, so a tile's HBM latency overlaps the previous tile's DMMA work.  Opt-in
-// (LRCHEB_SPMM_PERSIST=1) until it measures faster than spmm_u_kernel.
-template <int MODE>
-__global__ void __launch_bounds__(kThreads, 2)
-spmm_p_kernel(SpmmArgs a, int ust) {
-  const int r = a.d_r ? *a.d_r : a.r_fixed;
-  if (r <= 0) return;
-  extern __shared__ double smem_dyn[];
-  double* s_v = smem_dyn;                        // [kValCap]
-  double* s_u = smem_dyn + kValCap;              // [kUCap][ust]
-  __shared__ __align__(16) int s_descb[2][kDescInts];
-  __shared__ int s_bstart[kTileBlocks + 1], s_vbase[kTileBlocks], s_lp[kTileBlocks];
-  __shared__ float s_invL[kTileBlocks];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int CT = (r + 31) >> 5;
-  const int G = gridDim.x, ntl = a.ntl_u;
-  constexpr int kStg = (kSpmmCap + kThreads - 1) / kThreads;
-  int idx = blockIdx.x;
-  if (idx >= ntl) return;
-  // prologue: tile idx in flight
-  int2 et = __ldg(reinterpret_cast<const int2*>(a.tile_ev) + idx);
-  int4 dq = make_int4(0, 0, 0, 0);
-  if (tid < kDescInts / 4) dq = __ldg(reinterpret_cast<const int4*>(a.tdesc + (size_t)idx * kDescInts) + tid);
-  double raw[kStg][6];
-#pragma unroll
-  for (int k = 0; k < kStg; ++k) {
-    const int e = tid + k * kThreads;
-    if (e < et.y && !(a.dbg & 4)) {
-#pragma unroll
-      for (int v = 0; v < 6; ++v) raw[k][v] = __ldcs(a.v[v] + et.x + e);
-    } else {
-#pragma unroll
-      for (int v = 0; v < 6; ++v) raw[k][v] = 0.0;
-    }
-  }
-  if (tid < kDescInts / 4) *reinterpret_cast<int4*>(&s_descb[0][4 * tid]) = dq;
-  __syncthreads();
-  for (int buf = 0; idx < ntl; idx += G, buf ^= 1) {
-    const int* s_desc = s_descb[buf];
-    const int tot = et.y, nb = s_desc[2], nu = s_desc[3];
-    // ---- (A) stage this tile: U rows, block table, grouped values
-    if (!(a.dbg & 2)) stage_u_rows(a, r, s_desc + kDescUrows, nu, s_u, ust, tid, kThreads);
-    asm volatile("cp.async.commit_group;\n" ::);
-    if (tid == 0) {
-      int vb = 0, eb = 0;
-      for (int b = 0; b < nb; ++b) {
-        const int g = s_desc[12 + b], L = s_desc[16 + b];
-        s_bstart[b] = eb; s_lp[b] = row_pitch(L); s_vbase[b] = vb; s_invL[b] = 1.0f / (float)L;
-        vb += g * 3 * s_lp[b];
-        eb += g * L;
-      }
-      s_bstart[nb] = tot;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kStg; ++k) {
-      const int e = tid + k * kThreads;
-      if (e < tot) {
-        int b = 0;
-#pragma unroll
-        for (int kk = 1; kk < kTileBlocks; ++kk) b += (kk < nb && e >= s_bstart[kk]);
-        const int L = s_desc[16 + b];
-        const int rel = e - s_bstart[b];
-        const int q = __float2int_rz(((float)rel + 0.5f) * s_invL[b]), j = rel - q * L;
-        const int lp = s_lp[b];
-        double* dst = s_v + s_vbase[b] + q * 3 * lp + j;
-        dst[0] = fma(a.lam, raw[k][5], fma(a.rho, raw[k][3], raw[k][0]));   // A0 + rho Jrho + lam Jlam
-        dst[lp] = raw[k][1] + raw[k][4];                                   // A1 + Jmu
-        dst[2 * lp] = a.rho * raw[k][2];                                    // rho A2
-      }
-    }
-    for (int b = 0; b < nb; ++b) {
-      const int g = s_desc[12 + b], L = s_desc[16 + b], lp = s_lp[b];
-      for (int i = tid; i < g * 3 * 4; i += kThreads) {
-        const int j = L + (i & 3);
-        if (j < ((L + 3) & ~3)) s_v[s_vbase[b] + (i >> 2) * lp + j] = 0.0;
-      }
-    }
-    asm volatile("cp.async.wait_all;\n" ::);
-    __syncthreads();
-    // ---- (B) next tile in flight (registers)
-    const int in = idx + G;
-    if (in < ntl) {
-      et = __ldg(reinterpret_cast<const int2*>(a.tile_ev) + in);
-      if (tid < kDescInts / 4) dq = __ldg(reinterpret_cast<const int4*>(a.tdesc + (size_t)in * kDescInts) + tid);
-#pragma unroll
-      for (int k = 0; k < kStg; ++k) {
-        const int e = tid + k * kThreads;
-        if (e < et.y && !(a.dbg & 4)) {
-#pragma unroll
-          for (int v = 0; v < 6; ++v) raw[k][v] = __ldcs(a.v[v] + et.x + e);
-        } else {
-#pragma unroll
-          for (int v = 0; v < 6; ++v) raw[k][v] = 0.0;
-        }
-      }
-    }
-    // ---- (C) contract this tile
-    const unsigned short* lx = reinterpret_cast<const unsigned short*>(s_desc + kDescLidx);
-    int cb = 0;
-    for (int b = 0, task0 = 0; b < nb; ++b) {
-      const int g = s_desc[12 + b], L = s_desc[16 + b];
-      for (int ct = 0; ct < CT; ++ct, ++task0) {
-        if ((task0 % kWarps) != warp) continue;
-        const int lrow0 = s_desc[20 + b];
-        for (int qo = 0; qo < g; qo += 5) {
-          if (MODE == SPMM_S2STEP && lrow0 < 0)
-            block_task_mma_smem<MODE>(a, r, ct * 32, s_desc[8 + b] + qo, min(5, g - qo), qo, L, s_lp[b],
-                                      s_v + s_vbase[b], lx + cb, s_u, ust, lrow0, lane);
-          else
-            block_task_mma_fast<MODE>(a, r, ct * 32, s_desc[8 + b] + qo, min(5, g - qo), qo, L, s_lp[b],
-                                      s_v + s_vbase[b], lx + cb, s_u, ust, lrow0, lane);
-        }
-      }
-      cb += L;
-    }
-    // ---- (D) publish the next descriptor; every warp is done with s_u / s_v / this descriptor
-    if (in < ntl && tid < kDescInts / 4) *reinterpret_cast<int4*>(&s_descb[buf ^ 1][4 * tid]) = dq;
-    __syncthreads();
   }
 }
 
@@ -958,179 +831,6 @@ spmm_dense_kernel(SpmmArgs a) {
   }
 }
 
-// ---------------------------------------------------------------------------------------------
-// Persistent TMA-fed pipeline (S2STEP / PLAIN3, shared-memory-U tiles), one CTA per SM; opt-in
-// (env LRCHEB_SPMM_TMA=1), slower than spmm_u_kernel on B200 so far.
-//   producer warp (8): per tile, the descriptor (loaded one tile ahead into registers, written to a
-//       4-deep ring), then TMA bulk copies (cp.async.bulk + mbarrier complete_tx) of the six raw value
-//       segments and of the tile's deduplicated U rows into double-buffered stages;
-//   compute warps (0-7): combine the raw six streams into the grouped [slot][j] values, contract on
-//       the fp64 tensor pipe, store.
-// Tile k+1's copies overlap tile k's combine and contraction; hand-offs are mbarriers (parity = use
-// count & 1).  With a single CTA per SM the per-tile critical path (combine, two barriers, one task
-// per warp) is ~2.3 us, which bounds it above the 3-CTA lean kernel.
-// ---------------------------------------------------------------------------------------------
-constexpr int kTRaw = kSpmmCap + 2;                // doubles per raw value stream (alignment slack)
-constexpr int kTCompute = 256, kTThreads = kTCompute + 32;
-constexpr int kTRing = 4;                          // descriptor ring depth
-
-// dynamic shared memory: raw[2][6][kTRaw] | ustage[2][ustage] | sv[kValCap]
-size_t t_smem(int ustage) {
-  return sizeof(double) * (2 * 6 * (size_t)kTRaw + 2 * (size_t)ustage + kValCap);
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(kTThreads, 1)
-spmm_t_kernel(SpmmArgs a, int ust, int ustage) {
-  const int r = a.d_r ? *a.d_r : a.r_fixed;
-  if (r <= 0) return;
-  extern __shared__ __align__(16) double smem_dyn[];
-  double* s_raw = smem_dyn;
-  double* s_ust = s_raw + 2 * 6 * kTRaw;
-  double* s_v = s_ust + 2 * ustage;
-  __shared__ __align__(16) int s_ring[kTRing][kDescInts];
-  __shared__ __align__(8) unsigned long long raw_full[2], raw_empty[2], u_full[2], u_empty[2];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&raw_full[i], 1); mbar_init(&raw_empty[i], 1);
-      mbar_init(&u_full[i], 1); mbar_init(&u_empty[i], kTCompute / 32);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  const int G = gridDim.x, ntl = a.ntl_u;
-  const int CT = (r + 31) >> 5;
-  const int2* ev = reinterpret_cast<const int2*>(a.tile_ev);
-
-  if (warp == kTCompute / 32) {
-    // ------------------------------------------------------------------------------ producer
-    const unsigned ubytes = (unsigned)((r + 1) >> 1) * 16u;
-    // the descriptor words and (e0, nnz) of the next tile are loaded one tile ahead (registers), so
-    // no DRAM latency sits on the producer's per-tile path
-    int4 dq[kDescInts / 128];
-    int2 e;
-    {
-      const int4* gd = reinterpret_cast<const int4*>(a.tdesc + (size_t)blockIdx.x * kDescInts);
-#pragma unroll
-      for (int i = 0; i < kDescInts / 128; ++i) dq[i] = __ldg(gd + lane + 32 * i);
-      e = __ldg(ev + blockIdx.x);
-    }
-    for (int k = 0;; ++k) {
-      const int idx = blockIdx.x + k * G;
-      if (idx >= ntl) break;
-      int4 nq[kDescInts / 128];
-      int2 ne = make_int2(0, 0);
-      if (idx + G < ntl) {
-        const int4* gd = reinterpret_cast<const int4*>(a.tdesc + (size_t)(idx + G) * kDescInts);
-#pragma unroll
-        for (int i = 0; i < kDescInts / 128; ++i) nq[i] = __ldg(gd + lane + 32 * i);
-        ne = __ldg(ev + idx + G);
-      }
-      const int st = k & 1;
-      // descriptor of tile k first (ring slot of tile k-4, free once tile k-2 is contracted): the
-      // combiners read it as soon as the raw values land
-      if (k >= 2) mbar_wait(&u_empty[st], ((k >> 1) - 1) & 1);
-      int* d = s_ring[k % kTRing];
-#pragma unroll
-      for (int i = 0; i < kDescInts / 128; ++i) *reinterpret_cast<int4*>(d + 4 * (lane + 32 * i)) = dq[i];
-      __syncwarp();
-      // raw value segments of tile k (buffer st, free once the combiners are done with tile k-2)
-      if (k >= 2) mbar_wait(&raw_empty[st], ((k >> 1) - 1) & 1);
-      const int e0a = e.x & ~1, end = e.x + e.y, enda = end & ~1;
-      double* raw = s_raw + st * 6 * kTRaw;
-      if (lane == 0) {
-        if ((end & 1) && !(a.dbg & 4))   // odd tail element: plain load (never read past the array)
-          for (int v = 0; v < 6; ++v) raw[v * kTRaw + (end - 1 - e0a)] = __ldg(a.v[v] + end - 1);
-        mbar_expect_tx(&raw_full[st], (a.dbg & 4) ? 0u : 6u * 8u * (unsigned)(enda - e0a));
-      }
-      __syncwarp();
-      if (lane < 6 && enda > e0a && !(a.dbg & 4))
-        bulk_g2s(raw + lane * kTRaw, a.v[lane] + e0a, 8u * (unsigned)(enda - e0a), &raw_full[st]);
-      // U rows of tile k (buffer st)
-      const int nu = (a.dbg & 2) ? 0 : d[3];
-      double* su = s_ust + st * ustage;
-      if (lane == 0) mbar_expect_tx(&u_full[st], ubytes * (unsigned)nu);
-      __syncwarp();
-      for (int u = lane; u < nu; u += 32)
-        bulk_g2s(su + u * ust, a.U + (size_t)d[kDescUrows + u] * a.ldu, ubytes, &u_full[st]);
-#pragma unroll
-      for (int i = 0; i < kDescInts / 128; ++i) dq[i] = nq[i];
-      e = ne;
-    }
-    return;
-  }
-
-  // ------------------------------------------------------------------- compute (combine + contract)
-  const int c = tid;
-  for (int k = 0;; ++k) {
-    const int idx = blockIdx.x + k * G;
-    if (idx >= ntl) break;
-    const int st = k & 1;
-    mbar_wait(&raw_full[st], (k >> 1) & 1);
-    asm volatile("bar.sync 1, %0;\n" ::"n"(kTCompute) : "memory");   // s_v of tile k-1 fully consumed
-    const int* d = s_ring[k % kTRing];
-    const double* raw = s_raw + st * 6 * kTRaw;
-    const int e0 = d[0], tot = d[1], nb = d[2];
-    const int off = e0 - (e0 & ~1);
-    int bs[kTileBlocks], vbs[kTileBlocks];
-    {
-      int eb = 0, vb = 0;
-#pragma unroll
-      for (int b = 0; b < kTileBlocks; ++b) {
-        bs[b] = b < nb ? eb : 0x7fffffff;
-        vbs[b] = vb;
-        if (b < nb) { const int g = d[12 + b], L = d[16 + b]; eb += g * L; vb += 3 * g * row_pitch(L); }
-      }
-    }
-    for (int e = c; e < tot; e += kTCompute) {
-      int b = 0;
-#pragma unroll
-      for (int kk = 1; kk < kTileBlocks; ++kk) b += (e >= bs[kk]);
-      int eb = bs[0], vb = vbs[0];
-#pragma unroll
-      for (int kk = 1; kk < kTileBlocks; ++kk) if (b == kk) { eb = bs[kk]; vb = vbs[kk]; }
-      const int L = d[16 + b];
-      const int rel = e - eb;
-      const int q = __float2int_rz(((float)rel + 0.5f) / (float)L), j = rel - q * L;
-      const int lp = row_pitch(L);
-      const double* rv = raw + off + e;
-      double* dst = s_v + vb + q * 3 * lp + j;
-      dst[0] = fma(a.lam, rv[5 * kTRaw], fma(a.rho, rv[3 * kTRaw], rv[0]));   // A0 + rho Jrho + lam Jlam
-      dst[lp] = rv[1 * kTRaw] + rv[4 * kTRaw];                             // A1 + Jmu
-      dst[2 * lp] = a.rho * rv[2 * kTRaw];                                  // rho A2
-    }
-    for (int b = 0; b < nb; ++b) {
-      const int g = d[12 + b], L = d[16 + b], lp = row_pitch(L);
-      for (int i = c; i < g * 3 * 4; i += kTCompute) {
-        const int j = L + (i & 3);
-        if (j < ((L + 3) & ~3)) s_v[vbs[b] + (i >> 2) * lp + j] = 0.0;
-      }
-    }
-    asm volatile("bar.sync 1, %0;\n" ::"n"(kTCompute) : "memory");   // grouped values ready
-    if (c == 0) mbar_arrive(&raw_empty[st]);
-    mbar_wait(&u_full[st], (k >> 1) & 1);
-    const double* s_u = s_ust + st * ustage;
-    const unsigned short* lx = reinterpret_cast<const unsigned short*>(d + kDescLidx);
-    for (int task = warp; task < nb * CT; task += kTCompute / 32) {
-      const int b = task / CT, ct = task - (task / CT) * CT;
-      int cb = 0;
-      for (int bb = 0; bb < b; ++bb) cb += d[16 + bb];
-      const int g = d[12 + b], L = d[16 + b], lrow0 = d[20 + b];
-      for (int qo = 0; qo < g; qo += 5) {
-        if (MODE == SPMM_S2STEP && lrow0 < 0)
-          block_task_mma_smem<MODE>(a, r, ct * 32, d[8 + b] + qo, min(5, g - qo), qo, L, row_pitch(L),
-                                    s_v + vbs[b], lx + cb, s_u, ust, lrow0, lane);
-        else
-          block_task_mma_fast<MODE>(a, r, ct * 32, d[8 + b] + qo, min(5, g - qo), qo, L, row_pitch(L),
-                                    s_v + vbs[b], lx + cb, s_u, ust, lrow0, lane);
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&u_empty[st]);
-  }
-}
-
 int ust_for(int rmax) { return ((rmax + 11) / 16) * 16 + 4; }   // >= rmax + 1, == 4 mod 16 (even)
 
 size_t dense_smem() {
@@ -1142,67 +842,17 @@ size_t smem_for(int mode, int rmax) {
   return sizeof(double) * (kValCap + (hot ? (size_t)kUCap * ust_for(rmax) : 0)) + sizeof(int) * kSpmmCap;
 }
 
-int sm_count() {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
-}
 
 template <int MODE>
 cudaError_t launch_m(const SpmmArgs& a0, int rmax, cudaStream_t s) {
   SpmmArgs a = a0;
-  {
-    static int dbg = -1;
-    if (dbg < 0) {
-      const char* e = getenv("LRCHEB_SPMM_DBG");
-      dbg = e ? atoi(e) : 0;
-      if (getenv("LRCHEB_SPMM_TMA")) dbg |= 32;
-      if (getenv("LRCHEB_SPMM_PERSIST")) dbg |= 64;
-    }
-    a.dbg = dbg;
-  }
   // 16-byte U row copies need 16-byte aligned rows and room for the padding element of an odd r
   a.u_aligned16 = ((reinterpret_cast<uintptr_t>(a.U) & 15) == 0) && (a.ldu % 2 == 0) && (rmax < a.ldu || rmax % 2 == 0);
   constexpr bool HOT = (MODE == SPMM_S2STEP || MODE == SPMM_PLAIN3);
   if constexpr (HOT) {
     // slack: the predicate-free contraction reads up to 32*CT - 1 columns of the last staged U row
     const int ust = ust_for(rmax), slack = max(0, 32 * ((rmax + 31) / 32) - ust);
-    // three-role TMA pipeline (dbg bit 32 = env LRCHEB_SPMM_TMA selects it)
-    const int ustage = (kUCap * ust + slack + 1) & ~1;
-    bool al = a.u_aligned16;
-    for (int v = 0; v < 6; ++v) al = al && ((reinterpret_cast<uintptr_t>(a.v[v]) & 15) == 0);
-    if ((a.dbg & 32) && al && t_smem(ustage) <= 232448 - 8192) {
-      if (a.ntl_u > 0) {
-        const int grid = min(a.ntl_u, max(1, sm_count() - max(0, a.reserved_sms)));
-        spmm_t_kernel<MODE><<<grid, kTThreads, t_smem(ustage), s>>>(a, ust, ustage);
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-      }
-      if (a.ntl_g > 0) {
-        a.tlist = a.tlist_g;
-        spmm_kernel<MODE, 5><<<a.ntl_g, kThreads, smem_for(MODE, rmax), s>>>(a, ust_for(rmax));
-      }
-      return cudaGetLastError();
-    }
     const size_t sm_u = sizeof(double) * (kValCap + (size_t)kUCap * ust + slack);
-    if (sm_u <= 75 * 1024 && (a.dbg & 64)) {       // persistent, 2 CTAs / SM (opt-in)
-      if (a.ntl_u > 0) {
-        const int grid = min(a.ntl_u, 2 * max(1, sm_count() - max(0, a.reserved_sms)));
-        spmm_p_kernel<MODE><<<grid, kThreads, sm_u, s>>>(a, ust);
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-      }
-      if (a.ntl_g > 0) {
-        a.tlist = a.tlist_g;
-        spmm_kernel<MODE, 5><<<a.ntl_g, kThreads, smem_for(MODE, rmax), s>>>(a, ust_for(rmax));
-      }
-      return cudaGetLastError();
-    }
     if (sm_u <= 75 * 1024) {                       // 3 CTAs / SM
       if (a.ntl_u > 0) {
         spmm_u_kernel<MODE><<<a.ntl_u, kThreads, sm_u, s>>>(a, ust);
@@ -1248,13 +898,6 @@ cudaError_t prep_m() {
   if constexpr (MODE == SPMM_S2STEP || MODE == SPMM_PLAIN3) {
     e = cudaFuncSetAttribute(spmm_u_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 75 * 1024);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(spmm_p_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 75 * 1024);
-    if (e != cudaSuccess) return e;
-    cudaFuncAttributes fa;
-    e = cudaFuncGetAttributes(&fa, spmm_t_kernel<MODE>);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(spmm_t_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(232448 - fa.sharedSizeBytes));
   }
   return e;
 }

@@ -18,8 +18,6 @@
 // shared-memory ring (16-byte cp.async when every block is 16-byte aligned, else 8-byte; zero fill
 // past M / w) whose hand-offs are mbarriers.  The X tile of the Gram epilogue is parked in two of
 // the (then idle) stages.
-#include <cstdlib>
-
 #include "lrc_internal.cuh"
 
 namespace lrc {
@@ -134,7 +132,6 @@ __device__ __forceinline__ ChunkPlan plan_chunk(const TsArgs& a, unsigned stage,
 template <int PT, int BK>
 __device__ __forceinline__ void issue_part(const TsArgs& a, const ChunkPlan& c, int part, int w, int tid) {
   using S = TsShape<PT, BK>;
-  if (a.dbg & 1) return;
   if (a.u16) {
     if (part < 4) {
       const int i = (tid >> 4) + 32 * part, j = (tid & 15) * 2;
@@ -383,7 +380,6 @@ ts_kernel(TsArgs a) {
         // trapezoidal) the tiles with all i > c are zero
         int nact = (k0 + kk < w) ? PT : 0;
         if (a.t_lower) nact = min(nact, (k0 + kk + 3) / 8 + 1);
-        if (a.dbg & 4) nact = 0;
         const double a0 = s_u[(warp * 8 + gid) * kSU + kk + tig];
         if (a.t_upper && nact > 0 && k0 + kk >= 8)   // T = R1^{-1}: tiles with all i < c are zero
           mma_row_from<PT>(x0, a0, s_t + (kk + tig) * SX + gid, (k0 + kk) >> 3);
@@ -401,7 +397,7 @@ ts_kernel(TsArgs a) {
       __syncwarp();
       if (lane == 0) mb_arrive(&empty[g % 3]);   // this warp is done with stage g % 3
     }
-    if (MODE == 0 && a.yout && !(a.dbg & 8)) {
+    if (MODE == 0 && a.yout) {
       // Y = this X tile straight from the accumulators (all PMAX columns; the ones >= p are exact
       // zeros): fire-and-forget 16-byte evict-first stores, full 32-byte sectors per quad
       const int row = m0 + warp * 8 + gid;
@@ -414,7 +410,7 @@ ts_kernel(TsArgs a) {
     if (MODE == 1 && a.o16) {
       // rows of U_{k+1} straight from the accumulators (16-byte evict-first stores, full sectors);
       // the padded (solver) mode also writes the zero pad column of an odd rank
-      const int pw = (a.dbg & 2) ? 0 : p + (a.u.pad_even ? (p & 1) : 0);
+      const int pw = p + (a.u.pad_even ? (p & 1) : 0);
       const int row = m0 + warp * 8 + gid;
       if (row < a.M) {
         double* orow = a.out + (size_t)row * a.ldo;
@@ -441,7 +437,7 @@ ts_kernel(TsArgs a) {
     if constexpr (MODE == 0) {
 #pragma unroll
       for (int s = 0; s < S::SPW; ++s) {
-        if (sI[s] < 0 || (a.dbg & 2)) continue;
+        if (sI[s] < 0) continue;
         const int I0 = 2 * sI[s], J0 = 2 * sJ[s];
         // odd PT: the last super row/column is half; the kind is warp-uniform and fixed, so each
         // kind runs its own loop (no predicated-off DMMAs)
@@ -454,7 +450,7 @@ ts_kernel(TsArgs a) {
       }
     } else {
       // rows of U_{k+1}: 16-byte stores when the output rows are 16-byte aligned
-      const int pw = (a.dbg & 2) ? 0 : p + (a.u.pad_even ? (p & 1) : 0);   // padded (solver) mode also writes the zero pad column
+      const int pw = p + (a.u.pad_even ? (p & 1) : 0);   // padded (solver) mode also writes the zero pad column
       if (a.o16) {
         constexpr int HP = S::HP;
         for (int e = tid; e < kBM * HP; e += kThreads) {
@@ -577,11 +573,6 @@ cudaError_t launch_ts(int mode, const TsArgs& a0, int pmax, int grid, cudaStream
     u16 = u16 && (a.u.b[bi].ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(a.u.b[bi].p) & 15) == 0);
   a.u16 = u16 ? 1 : 0;
   a.o16 = (mode == 1 && a.out && a.ldo % 2 == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0) ? 1 : 0;
-  {
-    static int dbg = -1;
-    if (dbg < 0) { const char* e = getenv("LRCHEB_TS_DBG"); dbg = e ? atoi(e) : 0; }
-    a.dbg = dbg;
-  }
   return mode == 0 ? Dispatch<0, 16>::launch(a, pmax / 8, grid, s)
                    : Dispatch<1, 16>::launch(a, pmax / 8, grid, s);
 }

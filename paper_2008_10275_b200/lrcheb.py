@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(_HERE, "liblrcheb.so")
 
 LRC_OK, LRC_ERR_ARG, LRC_ERR_SHAPE, LRC_ERR_STATE, LRC_ERR_NOMEM, LRC_ERR_CUDA, LRC_ERR_NUMERIC = range(7)
 LRC_MEM_HOST, LRC_MEM_DEVICE, LRC_MEM_DEVICE_BORROW = 0, 1, 2
-LRC_RECORD_ITERATES, LRC_SKIP_FINAL_RESIDUAL, LRC_NO_GRAPH, LRC_NO_WARM_START = 1, 2, 4, 8
+LRC_RECORD_ITERATES, LRC_SKIP_FINAL_RESIDUAL, LRC_NO_GRAPH, LRC_NO_WARM_START, LRC_ASYNC = 1, 2, 4, 8, 16
 LRC_APPLY_PLAIN3, LRC_APPLY_SIX, LRC_APPLY_S2STEP = 0, 1, 2
 SIGMA_STRIDE = 128
 
@@ -31,7 +31,7 @@ EXPORTS = (
     "lrc_create", "lrc_destroy", "lrc_last_error", "lrc_version", "lrc_set_operator",
     "lrc_set_params", "lrc_solve", "lrc_apply_lowrank", "lrc_apply_dense", "lrc_truncate",
     "lrc_get_iterate", "lrc_last_kernel_ms", "lrc_kernel_launches", "lrc_set_profiling", "lrc_get_profile",
-    "lrc_set_reserved_sms",
+    "lrc_set_reserved_sms", "lrc_solve_wait", "lrc_workspace_bytes", "lrc_set_workspace",
 )
 
 
@@ -78,6 +78,9 @@ def load_library(path: str = None) -> ctypes.CDLL:
     lib.lrc_get_iterate.argtypes = [P, I64, P, P, ctypes.POINTER(I64), I32]
     lib.lrc_last_kernel_ms.argtypes = [P]
     lib.lrc_last_kernel_ms.restype = ctypes.c_float
+    lib.lrc_solve_wait.argtypes = [P, ctypes.POINTER(SolveInfo)]
+    lib.lrc_workspace_bytes.argtypes = [P, I64, I64, I64, U32, ctypes.POINTER(ctypes.c_size_t)]
+    lib.lrc_set_workspace.argtypes = [P, P, ctypes.c_size_t]
     lib.lrc_set_reserved_sms.argtypes = [P, I32]
     lib.lrc_set_reserved_sms.restype = I32
     lib.lrc_kernel_launches.argtypes = [P]
@@ -87,7 +90,8 @@ def load_library(path: str = None) -> ctypes.CDLL:
     lib.lrc_get_profile.argtypes = [P, I32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(D), ctypes.POINTER(I64)]
     lib.lrc_get_profile.restype = I32
     for name in ("lrc_create", "lrc_set_operator", "lrc_set_params", "lrc_solve", "lrc_apply_lowrank",
-                 "lrc_apply_dense", "lrc_truncate", "lrc_get_iterate"):
+                 "lrc_apply_dense", "lrc_truncate", "lrc_get_iterate", "lrc_solve_wait", "lrc_workspace_bytes",
+                 "lrc_set_workspace"):
         getattr(lib, name).restype = I32
     return lib
 
@@ -110,7 +114,8 @@ def _mat(x, rows: int = None, cols: int = None):
     """(pointer, ld, where, keepalive) of a 2-D row-major fp64 array (torch or numpy)."""
     if _is_torch(x):
         import torch
-        assert x.dtype == torch.float64, "fp64 required"
+        if x.dtype != torch.float64:
+            raise TypeError(f"fp64 tensor required, got {x.dtype}")
         if x.dim() == 1:
             x = x.reshape(-1, 1)
         assert x.stride(1) == 1 or x.shape[1] <= 1, "rows must be contiguous (row-major)"
@@ -123,7 +128,12 @@ def _mat(x, rows: int = None, cols: int = None):
 
 
 def _vec(x, dtype):
+    """(pointer, where, keepalive) of a 1-D array of `dtype` (np.int32 or np.float64)."""
     if _is_torch(x):
+        import torch
+        want = torch.int32 if np.dtype(dtype) == np.int32 else torch.float64
+        if x.dtype != want:
+            raise TypeError(f"{want} tensor required, got {x.dtype}")
         x = x.contiguous()
         return x.data_ptr(), (LRC_MEM_DEVICE if x.is_cuda else LRC_MEM_HOST), x
     a = np.ascontiguousarray(x, dtype=dtype)
@@ -167,6 +177,13 @@ class Context:
         if any(_is_torch(x) and x.is_cuda for x in xs if x is not None):
             self.stream.wait_stream(torch.cuda.current_stream(self.device))
 
+    def _settle(self, *xs):
+        """set_operator / set_params read device inputs with blocking copies outside any torch
+        stream: let the producing (current) torch stream finish first."""
+        import torch
+        if any(_is_torch(x) and x.is_cuda for x in xs if x is not None):
+            torch.cuda.current_stream(self.device).synchronize()
+
     # ------------------------------------------------------------------------------------
     def set_operator(self, row_ptr, col_idx, vals: Sequence, rho_f: float, lambda_s: float,
                      borrow: bool = False):
@@ -180,7 +197,7 @@ class Context:
         if borrow:
             assert where == LRC_MEM_DEVICE
             where = LRC_MEM_DEVICE_BORROW
-        self._order(*( [k1, k2] + [v[2] for v in vs]))
+        self._settle(*([k1, k2] + [v[2] for v in vs]))
         M = (k1.shape[0] if hasattr(k1, "shape") else len(k1)) - 1
         nnz = k2.shape[0]
         arr = (ctypes.c_void_p * 6)(*[v[0] for v in vs])
@@ -192,7 +209,7 @@ class Context:
         pm, w1, k1 = _vec(d_mu, np.float64)
         pn, w2, k2 = _vec(d_nu, np.float64)
         assert w1 == w2
-        self._order(k1, k2)
+        self._settle(k1, k2)
         n = k1.shape[0]
         self._check(self._lib.lrc_set_params(self._h, n, pm, pn, w1))
         self.n = n
@@ -237,6 +254,52 @@ class Context:
                    ms_total=info.ms_total, rank_history=list(rh), jacobi_sweeps=info.jacobi_sweeps, chol2_cycles=list(info.chol2_cycles),
                    sigma_history=np.frombuffer(sh, dtype=np.float64).reshape(n_iter, SIGMA_STRIDE).copy())
         return Uo, Vo, res
+
+    def solve_async(self, B_U, B_V, lambda_min: float, lambda_max: float, tol: float, rank_cap: int,
+                    n_iter: int, out, restart_every: int = 0, warm_start: bool = True):
+        """LRC_ASYNC solve (device tensors only): enqueues the whole solve on the context stream and
+        returns; wait() completes it and returns the info dict."""
+        pu, ldbu, w1, ku = _mat(B_U)
+        pv, ldbv, w2, kv = _mat(B_V)
+        Uo, Vo = out
+        pUo, lduo, w3, _ = _mat(Uo)
+        pVo, ldvo, w4, _ = _mat(Vo)
+        assert w1 == w2 == w3 == w4 == LRC_MEM_DEVICE
+        self._order(ku, kv)
+        flags = LRC_ASYNC | (0 if warm_start else LRC_NO_WARM_START)
+        opts = SolveOpts(float(lambda_min), float(lambda_max), float(tol), int(rank_cap), int(n_iter),
+                         int(restart_every), flags)
+        self._pending = (ku, kv, Uo, Vo, int(n_iter))
+        self._check(self._lib.lrc_solve(self._h, pu, ldbu, pv, ldbv, ku.shape[1], ctypes.byref(opts), pUo, lduo,
+                                        pVo, ldvo, LRC_MEM_DEVICE, None))
+
+    def wait(self):
+        n_iter = self._pending[4] if getattr(self, "_pending", None) else 1
+        rh = (ctypes.c_int64 * n_iter)()
+        info = SolveInfo()
+        info.rank_history = ctypes.cast(rh, ctypes.POINTER(ctypes.c_int64))
+        st = self._lib.lrc_solve_wait(self._h, ctypes.byref(info))
+        self._pending = None
+        self._check(st)
+        return dict(rank=info.rank, rel_residual=info.rel_residual, b_norm=info.b_norm, diverged=bool(info.diverged),
+                    ms_iterations=info.ms_iterations, ms_total=info.ms_total, rank_history=list(rh))
+
+    def workspace_bytes(self, r_B: int, rank_cap: int, n_iter: int, record_iterates: bool = False) -> int:
+        b = ctypes.c_size_t()
+        self._check(self._lib.lrc_workspace_bytes(self._h, int(r_B), int(rank_cap), int(n_iter),
+                                                  LRC_RECORD_ITERATES if record_iterates else 0, ctypes.byref(b)))
+        return int(b.value)
+
+    def set_workspace(self, buf):
+        """Hand the context a caller-owned device buffer (e.g. a torch uint8 CUDA tensor) to carve its
+        workspace from; None returns to library-owned memory."""
+        if buf is None:
+            self._check(self._lib.lrc_set_workspace(self._h, None, 0))
+            self._ws_keep = None
+            return
+        self._check(self._lib.lrc_set_workspace(self._h, ctypes.c_void_p(buf.data_ptr()),
+                                                buf.numel() * buf.element_size()))
+        self._ws_keep = buf
 
     def apply_lowrank(self, U, mode: int = LRC_APPLY_PLAIN3, gamma: float = 0.0):
         pu, ldu, w, ku = _mat(U)
