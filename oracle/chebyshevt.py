@@ -63,8 +63,9 @@ def term_list(mats, rho_f: float, lambda_s: float, d_mu, d_nu):
 
 
 def apply_dense(terms, S: np.ndarray) -> np.ndarray:
-    """L(S) for a dense M x n S, term by term: sum_t c_t (A_t S) diag(e_t)."""
-    Y = np.zeros_like(S, dtype=np.float64)
+    """L(S) for a dense M x n S, term by term: sum_t c_t (A_t S) diag(e_t).  The A_t may
+    be row blocks A_t[R, :] of the operator (then the result is L(S)[R, :])."""
+    Y = np.zeros((terms[0][1].shape[0], S.shape[1]), dtype=np.float64)
     for c, A, e in terms:
         Y += c * (A @ S) * e[None, :]
     return Y

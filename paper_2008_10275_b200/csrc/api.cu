@@ -99,6 +99,8 @@ struct lrc_ctx {
   int* tdesc = nullptr; int ntiles = 0;
   int* tlist_u = nullptr; int ntl_u = 0; int* tlist_g = nullptr; int ntl_g = 0;
   int* tile_ev = nullptr;   // [ntiles][2] (first nnz, nnz count) of each tile (U tiles first)
+  int* trec = nullptr;      // [ntl_u][kRecInts] tile records of the persistent TMA SpMM
+  int* trun = nullptr;      // [ntl_u][kRunInts] their U row runs
   size_t meta_bytes = 0;
   double rho = 0, lam = 0;
   // params
@@ -381,6 +383,8 @@ SpmmArgs spmm_base(lrc_ctx* ctx) {
   a.tdesc = ctx->tdesc;
   a.tlist_u = ctx->tlist_u; a.ntl_u = ctx->ntl_u;
   a.tile_ev = ctx->tile_ev;
+  a.trec = ctx->trec;
+  a.trun = ctx->trun;
   a.reserved_sms = ctx->reserved_sms;
   a.tlist_g = ctx->tlist_g; a.ntl_g = ctx->ntl_g;
   a.tlist = nullptr;
@@ -703,7 +707,7 @@ void lrc_destroy(lrc_ctx* ctx) {
     for (int t = 0; t < 6; ++t) dfree(ctx->vals[t]);
   }
   dfree(ctx->tmpA); dfree(ctx->tmpB); dfree(ctx->tmpC);
-  dfree(ctx->group_ptr); dfree(ctx->tdesc); dfree(ctx->tlist_u); dfree(ctx->tlist_g); dfree(ctx->tile_ev); dfree(ctx->dmu); dfree(ctx->dnu);
+  dfree(ctx->group_ptr); dfree(ctx->tdesc); dfree(ctx->tlist_u); dfree(ctx->tlist_g); dfree(ctx->tile_ev); dfree(ctx->trec); dfree(ctx->trun); dfree(ctx->dmu); dfree(ctx->dnu);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
@@ -924,8 +928,8 @@ lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t*
     for (int t = 0; t < 6; ++t) dfree(ctx->vals[t]);
   }
   dfree(ctx->group_ptr);
-  dfree(ctx->tdesc); dfree(ctx->tlist_u); dfree(ctx->tlist_g); dfree(ctx->tile_ev);
-  ctx->tlist_u = ctx->tlist_g = nullptr; ctx->tile_ev = nullptr;
+  dfree(ctx->tdesc); dfree(ctx->tlist_u); dfree(ctx->tlist_g); dfree(ctx->tile_ev); dfree(ctx->trec); dfree(ctx->trun);
+  ctx->tlist_u = ctx->tlist_g = nullptr; ctx->tile_ev = nullptr; ctx->trec = nullptr; ctx->trun = nullptr;
   ctx->row_ptr = nullptr; ctx->col_idx = nullptr; ctx->group_ptr = nullptr; ctx->tdesc = nullptr;
   for (int t = 0; t < 6; ++t) ctx->vals[t] = nullptr;
   ctx->op_set = false;
@@ -971,6 +975,50 @@ lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t*
   }
   CK(dalloc(&ctx->tdesc, tdesc.size()));
   CK(cudaMemcpy(ctx->tdesc, tdesc.data(), sizeof(int32_t) * tdesc.size(), cudaMemcpyHostToDevice));
+  {
+    // tile records + U row runs of the persistent TMA SpMM (lrc_internal.cuh) for the shared-memory-U
+    // tiles (stored first); not built when some tile exceeds the kernel's bounds (then the launcher
+    // keeps the 3-CTA kernel)
+    std::vector<int32_t> rec, runs;
+    bool ok = true;
+    for (int t = 0; t < ctx->ntiles && ok; ++t) {
+      const int32_t* d = tdesc.data() + (size_t)t * kDescInts;
+      if (d[3] <= 0) break;
+      if (d[1] > 900 || d[3] > 90) { ok = false; break; }
+      std::vector<int32_t> R(kRecInts, 0), Q(kRunInts, 0);
+      R[0] = d[0]; R[1] = d[1]; R[2] = d[2]; R[3] = d[3];
+      const uint16_t* lx = reinterpret_cast<const uint16_t*>(d + kDescLidx);
+      int lo = 0, eb = 0;
+      for (int b = 0; b < d[2]; ++b) {
+        const int g = d[12 + b], L = d[16 + b];
+        if (lo + L > kRecCols) { ok = false; break; }
+        R[4 + b] = d[8 + b]; R[8 + b] = g; R[12 + b] = L; R[16 + b] = lo; R[20 + b] = eb; R[24 + b] = d[20 + b];
+        for (int j = 0; j < L; ++j) R[kRecHdr + lo + j] = lx[lo + j];
+        lo += L;
+        eb += g * L;
+      }
+      int nr = 0;
+      for (int u = 0; u < d[3] && ok; ) {
+        int v = u + 1;
+        while (v < d[3] && d[kDescUrows + v] == d[kDescUrows + v - 1] + 1) ++v;
+        if (nr == kRunMax) { ok = false; break; }
+        Q[1 + 3 * nr] = d[kDescUrows + u]; Q[2 + 3 * nr] = v - u; Q[3 + 3 * nr] = u;
+        ++nr;
+        u = v;
+      }
+      Q[0] = nr;
+      rec.insert(rec.end(), R.begin(), R.end());
+      runs.insert(runs.end(), Q.begin(), Q.end());
+    }
+    dfree(ctx->trec); dfree(ctx->trun);
+    ctx->trec = nullptr; ctx->trun = nullptr;
+    if (ok && !rec.empty()) {
+      CK(dalloc(&ctx->trec, rec.size()));
+      CK(cudaMemcpy(ctx->trec, rec.data(), sizeof(int32_t) * rec.size(), cudaMemcpyHostToDevice));
+      CK(dalloc(&ctx->trun, runs.size()));
+      CK(cudaMemcpy(ctx->trun, runs.data(), sizeof(int32_t) * runs.size(), cudaMemcpyHostToDevice));
+    }
+  }
   {
     std::vector<int32_t> lu, lg;
     for (int t = 0; t < ctx->ntiles; ++t) (tdesc[(size_t)t * kDescInts + 3] > 0 ? lu : lg).push_back(t);

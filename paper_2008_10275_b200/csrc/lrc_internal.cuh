@@ -24,6 +24,17 @@ constexpr int kDescUrows = 24;
 constexpr int kDescLidx = kDescUrows + kUCap;                 // 114
 constexpr int kLidxCap = 2 * (kDescInts - kDescLidx);         // 284
 constexpr int kSigmaStride = 128;
+// Tile record of the persistent TMA SpMM (int32 words, 1 KB, one per shared-memory-U tile, same order):
+// [0] e0 [1] tot [2] nb [3] staged U rows, [4+b] row0, [8+b] g, [12+b] L, [16+b] offset of block b's
+// column list in [kRecHdr ..), [20+b] first nnz of block b relative to e0, [24+b] local row of the
+// block's first row among the staged U rows (-1: not staged) (b < 4); [kRecHdr ..) the blocks' column
+// lists as local (staged) U row indices.  U-row runs (kRunInts words per tile): [0] count, then
+// (global first row, rows, local first row) per run of consecutive staged rows.
+constexpr int kRecInts = 256;
+constexpr int kRecHdr = 32;
+constexpr int kRecCols = kRecInts - kRecHdr;
+constexpr int kRunInts = 64;
+constexpr int kRunMax = (kRunInts - 1) / 3;
 
 // ------------------------------------------------------------------------------------------
 // a1: fused six-array CSR SpMM
@@ -39,6 +50,8 @@ struct SpmmArgs {
   const int* tlist_u;       // tiles with shared-memory U rows (nu > 0): 0 .. ntl_u-1 (stored first)
   int ntl_u;
   const int* tile_ev;       // [ntiles][2] first nnz and nnz count of each tile
+  const int* trec;          // [ntl_u][kRecInts] tile records of the TMA kernel (null: not available)
+  const int* trun;          // [ntl_u][kRunInts] U row runs of the TMA kernel's tiles
   const int* tlist_g;       // L2-gather tiles (nu = 0)
   int ntl_g;
   const int* tlist;         // (set by the launcher) tile list, or null for all tiles

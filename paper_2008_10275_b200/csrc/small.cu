@@ -34,9 +34,12 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // In-place upper Cholesky of the p x p row-major matrix a (stride ld) after adding `shift` to the
-// diagonal.  Returns true on success.  Called by all threads of the CTA.
+// diagonal.  Returns true on success.  Called by all threads of the CTA.  One barrier per column: the
+// trailing update of step j uses the unscaled row j (a[i][c] -= a[j][i] a[j][c] / a[j][j]), and the
+// rows are scaled by 1/sqrt(a[j][j]) once at the end.  Threads form a 32 x (blockDim/32) grid over the
+// trailing triangle (no integer division in the update).
 __device__ bool chol_upper(double* a, int ld, int p, double shift, int* s_fail) {
-  if (threadIdx.x == 0) *s_fail = 0;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, ny = blockDim.x >> 5;
   for (int i = threadIdx.x; i < p; i += blockDim.x) a[i * ld + i] += shift;
   __syncthreads();
   for (int j = 0; j < p; ++j) {
@@ -46,20 +49,54 @@ __device__ bool chol_upper(double* a, int ld, int p, double shift, int* s_fail) 
       __syncthreads();
       return false;
     }
-    const double rjj = sqrt(d);
-    const double inv = 1.0 / rjj;
-    __syncthreads();                        // everyone has read a[j][j]
-    for (int c = j + 1 + threadIdx.x; c < p; c += blockDim.x) a[j * ld + c] *= inv;
-    if (threadIdx.x == 0) a[j * ld + j] = rjj;
-    __syncthreads();
-    const int m = p - j - 1;                // trailing upper triangle update
-    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-      const int i = j + 1 + e / m, c = j + 1 + e % m;
-      if (c >= i) a[i * ld + c] -= a[j * ld + i] * a[j * ld + c];
+    const double invd = 1.0 / d;
+    const double* rj = a + j * ld;
+    for (int i = j + 1 + ty; i < p; i += ny) {
+      const double f = rj[i] * invd;
+      double* ri = a + i * ld;
+      for (int c = i + tx; c < p; c += 32) ri[c] = fma(-f, rj[c], ri[c]);
     }
     __syncthreads();
   }
+  // scale: R[j][c] = a[j][c] / sqrt(a[j][j]) (c > j), R[j][j] = sqrt(a[j][j])
+  for (int j = ty; j < p; j += ny) {
+    const double d = a[j * ld + j], r = sqrt(d), inv = 1.0 / r;
+    for (int c = j + 1 + tx; c < p; c += 32) a[j * ld + c] *= inv;
+    if (tx == 0) a[j * ld + j] = r;
+  }
+  if (threadIdx.x == 0) *s_fail = 0;
+  __syncthreads();
   return true;
+}
+
+// X = R^{-1} (R upper triangular p x p, row-major stride ld; X the same layout, upper), bottom-up with
+// one barrier per row: row k of X is final once every row below it has been folded into the running
+// sums acc[k][j] = sum_{l > k} R[k][l] X[l][j]; X[k][j] = (delta_kj - acc[k][j]) / R[k][k].
+__device__ void tri_inv_upper(const double* R, int ld, double* X, int p) {
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, ny = blockDim.x >> 5;
+  for (int e = threadIdx.x; e < p * ld; e += blockDim.x) X[e] = 0.0;
+  __syncthreads();
+  // k = p - 1: row p-1 final right away
+  if (threadIdx.x == 0) X[(p - 1) * ld + (p - 1)] = 1.0 / R[(p - 1) * ld + (p - 1)];
+  __syncthreads();
+  for (int k = p - 1; k >= 1; --k) {
+    // fold row k into the rows i < k; the threads owning row k - 1 finish it in the same pass
+    const double* xk = X + k * ld;
+    for (int i = ty; i < k; i += ny) {
+      const double rik = R[i * ld + k];
+      double* xi = X + i * ld;
+      if (i == k - 1) {
+        const double inv = 1.0 / R[i * ld + i];
+        for (int j = i + tx; j < p; j += 32) {
+          const double acc = (j >= k) ? fma(rik, xk[j], xi[j]) : xi[j];
+          xi[j] = ((j == i) ? 1.0 - acc : -acc) * inv;
+        }
+      } else {
+        for (int j = k + tx; j < p; j += 32) xi[j] = fma(rik, xk[j], xi[j]);
+      }
+    }
+    __syncthreads();
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -203,7 +240,6 @@ __global__ void __launch_bounds__(kT) chol1_kernel(State st, SmallBufs b, int pm
   extern __shared__ double sm[];
   const int LD = pmax + 1;
   double* s_r = sm;                               // row-major [pmax][LD]
-  __shared__ double s_row[kMaxP];
   __shared__ int s_fail;
   __shared__ double s_tr;
   const int tid = threadIdx.x;
@@ -246,28 +282,12 @@ __global__ void __launch_bounds__(kT) chol1_kernel(State st, SmallBufs b, int pm
   }
   if (tid == 0) st.scal[2] = ok ? shift : 0.0;
   __syncthreads();
-  // in-place inverse: rows from the bottom, X[i][j] = -(sum_{k=i+1..j} R[i][k] X[k][j]) / R[i][i]
-  for (int i = p - 1; i >= 0; --i) {
-    const double rii = s_r[i * LD + i];
-    for (int jb = i + (tid >> 5) * 4; jb < p; jb += kT / 8) {   // 8 lanes per j, warp-uniform bound
-      const int j = jb + ((tid >> 3) & 3);
-      const int part = tid & 7;
-      double acc = 0.0;
-      if (j < p)
-        for (int kk = i + 1 + part; kk <= j; kk += 8) acc += s_r[i * LD + kk] * s_r[kk * LD + j];
-      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-      if (part == 0 && j < p) s_row[j] = (j == i) ? 1.0 / rii : -acc / rii;
-    }
-    __syncthreads();
-    for (int j = i + tid; j < p; j += kT) s_r[i * LD + j] = s_row[j];
-    __syncthreads();
-  }
+  double* s_x = sm + pmax * LD;                  // R1^{-1}
+  tri_inv_upper(s_r, LD, s_x, p);
   // R1^{-1} (upper, zero outside p x p) -> global: the T matrix of Gram pass 2 (Q1 = Y R1^{-1})
   for (int e = tid; e < pmax * pmax; e += kT) {
     const int i = e / pmax, c = e - (e / pmax) * pmax;
-    b.R1i[e] = (i < p && c < p && c >= i) ? s_r[i * LD + c] : 0.0;
+    b.R1i[e] = (i < p && c < p && c >= i) ? s_x[i * LD + c] : 0.0;
   }
 }
 
@@ -656,7 +676,7 @@ cudaError_t launch_vside(const VDesc& d, int n, const double* dmu, const double*
 
 cudaError_t launch_chol1(State st, SmallBufs b, int pmax, int wmax, cudaStream_t s) {
   (void)wmax;
-  const size_t smem = sizeof(double) * (size_t)pmax * (pmax + 1);
+  const size_t smem = sizeof(double) * 2 * (size_t)pmax * (pmax + 1);
   chol1_kernel<<<1, kT, smem, s>>>(st, b, pmax);
   return cudaGetLastError();
 }

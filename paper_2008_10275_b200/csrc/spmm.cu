@@ -187,6 +187,9 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)_
 __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
 }
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
 __device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
   unsigned ok;
   asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
@@ -665,6 +668,204 @@ spmm_u_kernel(SpmmArgs a, int ust) {
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Persistent TMA-fed hot kernel (S2STEP / PLAIN3), one CTA per SM, warp-specialised:
+//   producer warp : per tile, by cp.async.bulk (completion on the stage's mbarrier): the 1 KB tile
+//                   record (block geometry + local U-row index per column-list entry), the six raw
+//                   value segments (a 3-deep ring: up to two tiles ahead) and the tile's deduplicated
+//                   U rows as a few contiguous row runs (a 2-deep ring);
+//   consumer warps: NG groups of kTCons warps; group g takes every NG-th tile of the CTA.  A warp
+//                   owns (node block, 32-column slice) tasks; the 6 -> 3 value combination happens in
+//                   the B-fragment loads (three LDS + two FMA per element, branch-free), the U
+//                   fragments come from the staged rows, and the contraction runs on the fp64 tensor
+//                   pipe (m16n8k4, transposed so the stores are full sectors).  A warp signals the
+//                   stages' empty barriers when it is done with the tile; no CTA-wide barrier.
+// ---------------------------------------------------------------------------------------------
+constexpr int kTStages = 3;               // raw value / record stages
+constexpr int kUStages = 2;               // U row stages
+constexpr int kTCons = 12;                // consumer warps
+constexpr int kTileNnz = 900;             // nnz per tile of this kernel (4 interior FE node blocks)
+constexpr int kRawStride = 908;           // doubles per raw array per stage (>= kTileNnz + 3, == 12 mod 16)
+constexpr int kTUrowMax = 90;             // staged U rows per tile
+constexpr int kTLdMax = 64;               // U leading dimension supported (r <= 64)
+
+size_t tma_smem() {
+  return sizeof(double) * ((size_t)kTStages * 6 * kRawStride + (size_t)kUStages * kTUrowMax * kTLdMax) +
+         sizeof(int) * (size_t)kTStages * kRecInts;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__((kTCons + 1) * 32, 1)
+spmm_tma_kernel(SpmmArgs a) {
+  const int r = a.d_r ? *a.d_r : a.r_fixed;
+  if (r <= 0) return;
+  extern __shared__ __align__(16) double smem_dyn[];
+  double* s_raw = smem_dyn;                                                   // [stage][6][kRawStride]
+  double* s_ub = s_raw + (size_t)kTStages * 6 * kRawStride;                   // [ustage][kTUrowMax * ldu]
+  int* s_rec = reinterpret_cast<int*>(s_ub + (size_t)kUStages * kTUrowMax * kTLdMax);   // [stage][kRecInts]
+  __shared__ __align__(8) unsigned long long full[kTStages], empty[kTStages], uempty[kUStages];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int NCW = kTCons;
+  const int ldu = a.ldu;
+  const int CT = (r + 31) >> 5;
+  const int tpt = 4 * CT;                        // (virtual) tasks per tile: every one arrives once
+  if (tid == 0) {
+    for (int s = 0; s < kTStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], tpt); }
+    for (int s = 0; s < kUStages; ++s) mbar_init(&uempty[s], tpt);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int G = gridDim.x, ntl = a.ntl_u;
+  const int nmine = ((int)blockIdx.x < ntl) ? (ntl - (int)blockIdx.x + G - 1) / G : 0;
+
+  if (warp == NCW) {
+    // ------------------------------------------------------------------------------- producer
+    const int2* ev = reinterpret_cast<const int2*>(a.tile_ev);
+    // (first nnz, nnz) and the U row runs (lane l: run l - 8) of the next tile, one tile ahead
+    auto fetch = [&](int t, int2& e, int3& run, int& nrun) {
+      e = __ldg(ev + t);
+      const int* R = a.trun + (size_t)t * kRunInts;
+      nrun = __ldg(R);
+      const int ri = lane - 8;
+      run = (ri >= 0 && ri < nrun) ? make_int3(__ldg(R + 1 + 3 * ri), __ldg(R + 2 + 3 * ri), __ldg(R + 3 + 3 * ri))
+                                   : make_int3(0, 0, 0);
+    };
+    int2 e = make_int2(0, 0);
+    int3 run = make_int3(0, 0, 0);
+    int nrun = 0;
+    if (nmine > 0) fetch(blockIdx.x, e, run, nrun);
+    for (int i = 0; i < nmine; ++i) {
+      const int t = blockIdx.x + i * G, s = i % kTStages, us = i % kUStages;
+      int2 ne = make_int2(0, 0);
+      int3 nrunv = make_int3(0, 0, 0);
+      int nnrun = 0;
+      if (i + 1 < nmine) fetch(t + G, ne, nrunv, nnrun);
+      if (i >= kTStages) mbar_wait(&empty[s], ((i / kTStages) - 1) & 1);
+      if (i >= kUStages) mbar_wait(&uempty[us], ((i / kUStages) - 1) & 1);
+      const int e0a = e.x & ~1, end = e.x + e.y, endc = end & ~1;
+      double* raw = s_raw + (size_t)s * 6 * kRawStride;
+      unsigned ub = (unsigned)run.y * (unsigned)ldu * 8u;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ub += __shfl_xor_sync(0xffffffffu, ub, o);
+      if (lane == 0) {
+        if (end & 1)   // odd tail element: plain load (a bulk copy never reads past the tile)
+          for (int v = 0; v < 6; ++v) raw[v * kRawStride + (end - 1 - e0a)] = __ldg(a.v[v] + end - 1);
+        mbar_expect_tx(&full[s], 6u * 8u * (unsigned)(endc - e0a) + 4u * kRecInts + ub);
+      }
+      __syncwarp();
+      if (lane < 6) {
+        if (endc > e0a) bulk_g2s(raw + lane * kRawStride, a.v[lane] + e0a, 8u * (unsigned)(endc - e0a), &full[s]);
+      } else if (lane == 6) {
+        bulk_g2s(s_rec + s * kRecInts, a.trec + (size_t)t * kRecInts, 4u * kRecInts, &full[s]);
+      } else if (lane >= 8 && lane - 8 < nrun && run.y > 0) {
+        bulk_g2s(s_ub + (size_t)us * kTUrowMax * kTLdMax + (size_t)run.z * ldu, a.U + (size_t)run.x * ldu,
+                 (unsigned)run.y * (unsigned)ldu * 8u, &full[s]);
+      }
+      e = ne; run = nrunv; nrun = nnrun;
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------------------- consumers
+  // the CTA's tasks form one sequence (tile i, task) = i * tpt + task, dealt round-robin to the
+  // consumer warps; a task is one (node block, 32-column slice) of a tile; the virtual tasks of a
+  // tile with fewer than 4 blocks only arrive on the stage barriers
+  const int gid = lane >> 2, tig = lane & 3;
+  const long long sst = a.out_sstride ? a.out_sstride : r;
+  const int ntask = nmine * tpt;
+  for (int T = warp; T < ntask; T += NCW) {
+    const int i = T / tpt, task = T - i * tpt;
+    const int s = i % kTStages, us = i % kUStages;
+    mbar_wait(&full[s], (i / kTStages) & 1);
+    const int* R = s_rec + s * kRecInts;
+    const double* raw = s_raw + (size_t)s * 6 * kRawStride;
+    const double* su = s_ub + (size_t)us * kTUrowMax * kTLdMax;
+    const int nb = R[2];
+    const int off = R[0] & 1;                      // the stage starts at the even element before e0
+    const int b = task / CT, n0 = (task - b * CT) * 32;
+    if (b < nb) {
+      const int row0 = R[4 + b], g = R[8 + b], L = R[12 + b], cb = kRecHdr + R[16 + b], nbase = R[20 + b];
+      const int lrow0 = R[24 + b];
+      // B operand (staged values, combined in the load): slot = nt*8 + gid -> (row q, stream st)
+      int po[2][3];
+      double co[2][3];
+      bool sv[2];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int slot = nt * 8 + gid, q = slot / 3, st = slot - q * 3;
+        sv[nt] = q < g;
+        const int o = off + nbase + (sv[nt] ? q * L : 0) + tig;
+        const int a0 = st == 0 ? 0 : (st == 1 ? 1 : 2);
+        const int a1 = st == 0 ? 3 : (st == 1 ? 4 : 2);
+        const int a2 = st == 0 ? 5 : (st == 1 ? 4 : 2);
+        po[nt][0] = a0 * kRawStride + o; po[nt][1] = a1 * kRawStride + o; po[nt][2] = a2 * kRawStride + o;
+        co[nt][0] = st == 2 ? a.rho : 1.0;
+        co[nt][1] = st == 0 ? a.rho : (st == 1 ? 1.0 : 0.0);
+        co[nt][2] = st == 0 ? a.lam : 0.0;
+      }
+      // A operand (U^T): columns n0 + mt*16 + gid (+8), entry j = k0 + tig -> staged U row R[cb + j]
+      const int c00 = n0 + gid, c01 = c00 + 8, c10 = c00 + 16, c11 = c00 + 24;
+      const bool v00 = c00 < r, v01 = c01 < r, v10 = c10 < r, v11 = c11 < r;
+      const int jmax = L - 1;
+      double acc[2][2][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.0;
+      const int L4 = (L + 3) & ~3;
+#pragma unroll 2
+      for (int k0 = 0; k0 < L4; k0 += 4) {
+        const double* u = su + R[cb + min(k0 + tig, jmax)] * ldu;
+        const double x0 = v00 ? u[c00] : 0.0, x1 = v01 ? u[c01] : 0.0;
+        const double x2 = v10 ? u[c10] : 0.0, x3 = v11 ? u[c11] : 0.0;
+        const bool jv = k0 + tig < L;
+        double bv[2];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          const double t0 = raw[po[nt][0] + k0], t1 = raw[po[nt][1] + k0], t2 = raw[po[nt][2] + k0];
+          const double v = fma(co[nt][2], t2, fma(co[nt][1], t1, co[nt][0] * t0));
+          bv[nt] = (jv && sv[nt]) ? v : 0.0;
+        }
+        dmma1684(acc[0][0], x0, x1, bv[0]);
+        dmma1684(acc[0][1], x0, x1, bv[1]);
+        dmma1684(acc[1][0], x2, x3, bv[0]);
+        dmma1684(acc[1][1], x2, x3, bv[1]);
+      }
+      // epilogue: frag (m, n) -> column n0 + mt*16 + gid (+8), slot nt*8 + 2 tig + e = 3 q + stream
+      const bool full_cols = n0 + 32 <= r;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int Rs = nt * 8 + 2 * tig + e;
+          if (Rs >= 3 * g) continue;
+          const int q = Rs / 3, st = Rs - q * 3;
+          const size_t row = (size_t)(row0 + q);
+          double* orow = a.out + st * sst + row * a.ldo + a.out_off + n0 + gid;
+          const bool s2 = (MODE == SPMM_S2STEP) && st == 0;
+          // the block's own U row (S2 epilogue) from the staged rows when present
+          const double* us_ = (lrow0 >= 0) ? su + (size_t)(lrow0 + q) * ldu + n0 + gid : a.U + row * ldu + n0 + gid;
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int hm = 0; hm < 2; ++hm) {
+              const int o = mt * 16 + hm * 8, c = n0 + gid + o;
+              if (full_cols || c < r) {
+                double v = acc[mt][nt][hm * 2 + e];
+                if (s2) v = fma(-a.gamma, v, us_[o]);
+                __stcs(orow + o, v);
+              } else if (c == r && (r & 1) && a.out_sstride) {
+                __stcs(orow + o, 0.0);        // zero pad column of the (even-padded) Ucat block
+              }
+            }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) { mbar_arrive(&empty[s]); mbar_arrive(&uempty[us]); }
+  }
+}
+
 // Config-5 dense application Y = sum_t c_t A_t S diag(e_t) (S dense M x ncols, ncols <= 256) on the
 // fp64 tensor pipe, shared-memory-U tiles.  Per tile the six value streams are combined once into
 // the three grouped streams; S is then processed in 64-column chunks: the chunk of the tile's
@@ -843,6 +1044,17 @@ size_t smem_for(int mode, int rmax) {
 }
 
 
+int sm_count() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
 template <int MODE>
 cudaError_t launch_m(const SpmmArgs& a0, int rmax, cudaStream_t s) {
   SpmmArgs a = a0;
@@ -853,6 +1065,21 @@ cudaError_t launch_m(const SpmmArgs& a0, int rmax, cudaStream_t s) {
     // slack: the predicate-free contraction reads up to 32*CT - 1 columns of the last staged U row
     const int ust = ust_for(rmax), slack = max(0, 32 * ((rmax + 31) / 32) - ust);
     const size_t sm_u = sizeof(double) * (kValCap + (size_t)kUCap * ust + slack);
+    // persistent TMA-fed kernel: 16-byte aligned value arrays and U rows, tile records available
+    bool al = a.trec != nullptr && a.trun != nullptr && rmax <= kTLdMax && a.ldu <= kTLdMax && (a.ldu % 2 == 0) &&
+              ((reinterpret_cast<uintptr_t>(a.U) & 15) == 0);
+    for (int v = 0; v < 6; ++v) al = al && ((reinterpret_cast<uintptr_t>(a.v[v]) & 15) == 0);
+    if (al && a.ntl_u > 0) {
+      const int grid = min(a.ntl_u, max(1, sm_count() - max(0, a.reserved_sms)));
+      spmm_tma_kernel<MODE><<<grid, (kTCons + 1) * 32, tma_smem(), s>>>(a);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      if (a.ntl_g > 0) {
+        a.tlist = a.tlist_g;
+        spmm_kernel<MODE, 5><<<a.ntl_g, kThreads, smem_for(MODE, rmax), s>>>(a, ust_for(rmax));
+      }
+      return cudaGetLastError();
+    }
     if (sm_u <= 75 * 1024) {                       // 3 CTAs / SM
       if (a.ntl_u > 0) {
         spmm_u_kernel<MODE><<<a.ntl_u, kThreads, sm_u, s>>>(a, ust);
@@ -897,6 +1124,8 @@ cudaError_t prep_m() {
   }
   if constexpr (MODE == SPMM_S2STEP || MODE == SPMM_PLAIN3) {
     e = cudaFuncSetAttribute(spmm_u_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 75 * 1024);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(spmm_tma_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem());
     if (e != cudaSuccess) return e;
   }
   return e;

@@ -188,62 +188,34 @@ __device__ __forceinline__ void issue_part(const TsArgs& a, const ChunkPlan& c, 
   }
 }
 
-// One k4 step of a warp's 8-row X slice against n-tiles [0, nact) of the staged T chunk.  nact < PT
-// (lower-trapezoidal T1, zero tail of the last chunk) jumps into a fall-through sequence, so the
-// skipped DMMAs are not issued at all (predicated-off DMMAs still occupy the tensor pipe).
-#define LRC_TS_MMA(n) if constexpr ((n) < PT) dmma884(x0[n], a0, bt[(n) * 8])
-template <int PT>
-__device__ __forceinline__ void mma_row(double (&x0)[PT][2], double a0, const double* bt, int nact) {
-  if (nact >= PT) {
+// One chunk (BK columns of the logical Ucat / rows of T) of a warp's 8-row X slice, with the set of
+// active n-tiles of every k4 step known at compile time: KIND 0 = all PT n-tiles (the bulk of the
+// K range), KIND 1 = chunk KC of a lower-trapezoidal T (T1 = R_V^T: n-tile n is zero for rows
+// < 8n), KIND 2 = chunk KC of an upper-triangular T (R1^{-1}: n-tile n is zero for rows >= 8n + 8).
+// Skipped DMMAs are not emitted at all (a predicated-off DMMA still occupies the tensor pipe), and
+// there is no per-k-step dispatch.  nka = active k4 steps of the chunk (the zero tail past w is
+// skipped); issue(kk) interleaves the next chunk's copy issue with the DMMA steps.
+template <int PT, int BK, int KIND, int KC, typename Issue>
+__device__ __forceinline__ void chunk_mma(double (&x0)[PT][2], const double* sa, const double* st, int nka,
+                                          Issue&& issue) {
+  constexpr int SX = PT * 8 + 4;
 #pragma unroll
-    for (int n = 0; n < PT; ++n) dmma884(x0[n], a0, bt[n * 8]);
-    return;
-  }
-  switch (nact) {
-    case 15: LRC_TS_MMA(14); [[fallthrough]];
-    case 14: LRC_TS_MMA(13); [[fallthrough]];
-    case 13: LRC_TS_MMA(12); [[fallthrough]];
-    case 12: LRC_TS_MMA(11); [[fallthrough]];
-    case 11: LRC_TS_MMA(10); [[fallthrough]];
-    case 10: LRC_TS_MMA(9); [[fallthrough]];
-    case 9: LRC_TS_MMA(8); [[fallthrough]];
-    case 8: LRC_TS_MMA(7); [[fallthrough]];
-    case 7: LRC_TS_MMA(6); [[fallthrough]];
-    case 6: LRC_TS_MMA(5); [[fallthrough]];
-    case 5: LRC_TS_MMA(4); [[fallthrough]];
-    case 4: LRC_TS_MMA(3); [[fallthrough]];
-    case 3: LRC_TS_MMA(2); [[fallthrough]];
-    case 2: LRC_TS_MMA(1); [[fallthrough]];
-    case 1: LRC_TS_MMA(0); [[fallthrough]];
-    default: break;
+  for (int kk = 0; kk < BK; kk += 4) {
+    if (kk / 4 < nka) {
+      const double a0 = sa[kk];
+      const double* bt = st + kk * SX;
+      constexpr int dummy = 0;
+      (void)dummy;
+#pragma unroll
+      for (int n = 0; n < PT; ++n) {
+        const int k = KC * BK + kk;                       // compile-time for KIND 1, 2
+        const bool on = KIND == 0 ? true : (KIND == 1 ? (8 * n <= k + 3) : (8 * n + 8 > k));
+        if (on) dmma884(x0[n], a0, bt[n * 8]);
+      }
+    }
+    issue(kk);
   }
 }
-#undef LRC_TS_MMA
-// Same for n-tiles [nstart, PT) (T upper triangular: tiles with all i < c are zero).
-#define LRC_TS_MMA(n) if constexpr ((n) < PT) dmma884(x0[n], a0, bt[(n) * 8])
-template <int PT>
-__device__ __forceinline__ void mma_row_from(double (&x0)[PT][2], double a0, const double* bt, int nstart) {
-  switch (nstart) {
-    case 0: LRC_TS_MMA(0); [[fallthrough]];
-    case 1: LRC_TS_MMA(1); [[fallthrough]];
-    case 2: LRC_TS_MMA(2); [[fallthrough]];
-    case 3: LRC_TS_MMA(3); [[fallthrough]];
-    case 4: LRC_TS_MMA(4); [[fallthrough]];
-    case 5: LRC_TS_MMA(5); [[fallthrough]];
-    case 6: LRC_TS_MMA(6); [[fallthrough]];
-    case 7: LRC_TS_MMA(7); [[fallthrough]];
-    case 8: LRC_TS_MMA(8); [[fallthrough]];
-    case 9: LRC_TS_MMA(9); [[fallthrough]];
-    case 10: LRC_TS_MMA(10); [[fallthrough]];
-    case 11: LRC_TS_MMA(11); [[fallthrough]];
-    case 12: LRC_TS_MMA(12); [[fallthrough]];
-    case 13: LRC_TS_MMA(13); [[fallthrough]];
-    case 14: LRC_TS_MMA(14); [[fallthrough]];
-    case 15: LRC_TS_MMA(15); [[fallthrough]];
-    default: break;
-  }
-}
-#undef LRC_TS_MMA
 
 // Gram contribution of the parked 128-row X tile to one 2x2 super tile (I0, J0) of G (8x8 tiles):
 // KIND 0 full, 1 diagonal (the lower tile is skipped), 2 last column of odd PT (J0+1 absent),
@@ -374,24 +346,38 @@ ts_kernel(TsArgs a) {
       const double* s_u = sm + (g % 3) * S::STAGE;
       const double* s_t = s_u + kBM * kSU;
       const int k0 = kc * kBK;
-#pragma unroll
-      for (int kk = 0; kk < kBK; kk += 4) {
-        // active n-tiles: none in the zero-filled tail of the last chunk; for T1 = R_V^T (lower
-        // trapezoidal) the tiles with all i > c are zero
-        int nact = (k0 + kk < w) ? PT : 0;
-        if (a.t_lower) nact = min(nact, (k0 + kk + 3) / 8 + 1);
-        const double a0 = s_u[(warp * 8 + gid) * kSU + kk + tig];
-        if (a.t_upper && nact > 0 && k0 + kk >= 8)   // T = R1^{-1}: tiles with all i < c are zero
-          mma_row_from<PT>(x0, a0, s_t + (kk + tig) * SX + gid, (k0 + kk) >> 3);
-        else
-          mma_row<PT>(x0, a0, s_t + (kk + tig) * SX + gid, nact);
-        // second half of the chunk: the stage of chunk g-1 is (almost surely) free by now
-        constexpr int kIssue0 = kBK - 16;   // the last four k4 steps issue two parts each
+      const double* sa = s_u + (warp * 8 + gid) * kSU + tig;
+      const double* st = s_t + tig * SX + gid;
+      const int nka = max(0, min(kBK / 4, (w - k0 + 3) / 4));
+      // second half of the chunk: issue chunk g+2 (the stage of chunk g-1 is (almost surely) free)
+      constexpr int kIssue0 = kBK - 16;   // the last four k4 steps issue two parts each
+      auto issue = [&](int kk) {
         if (pm0 >= 0 && kk >= kIssue0) {
           if (kk == kIssue0) produce_wait(g + 2);
           issue_part<PT, kBK>(a, c2, 2 * ((kk - kIssue0) / 4), w, tid);
           issue_part<PT, kBK>(a, c2, 2 * ((kk - kIssue0) / 4) + 1, w, tid);
         }
+      };
+      if constexpr (MODE == 0) {
+        if (a.t_lower && k0 + 3 < 8 * (PT - 1)) {
+          switch (kc) {
+            case 0: chunk_mma<PT, kBK, 1, 0>(x0, sa, st, nka, issue); break;
+            case 1: chunk_mma<PT, kBK, 1, 1>(x0, sa, st, nka, issue); break;
+            case 2: chunk_mma<PT, kBK, 1, 2>(x0, sa, st, nka, issue); break;
+            default: chunk_mma<PT, kBK, 1, 3>(x0, sa, st, nka, issue); break;
+          }
+        } else if (a.t_upper && kc < 4) {
+          switch (kc) {
+            case 0: chunk_mma<PT, kBK, 2, 0>(x0, sa, st, nka, issue); break;
+            case 1: chunk_mma<PT, kBK, 2, 1>(x0, sa, st, nka, issue); break;
+            case 2: chunk_mma<PT, kBK, 2, 2>(x0, sa, st, nka, issue); break;
+            default: chunk_mma<PT, kBK, 2, 3>(x0, sa, st, nka, issue); break;
+          }
+        } else {
+          chunk_mma<PT, kBK, 0, 0>(x0, sa, st, nka, issue);
+        }
+      } else {
+        chunk_mma<PT, kBK, 0, 0>(x0, sa, st, nka, issue);
       }
       if (pm0 >= 0) { mb_arrive_cp(&full[(g + 2) % 3]); issued = g + 2; }
       __syncwarp();
