@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--streams", type=int, default=3, help="concurrent subset solves per GPU")
     ap.add_argument("--no-dense", dest="dense", action="store_false", help="skip the config-5 measurement")
     ap.add_argument("--reserve-sms", type=int, default=3, help="SMs the persistent kernels leave free")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="f1: solve this many subsets in lockstep per call (one batched SpMM per iteration) "
+                         "instead of independent concurrent streams")
     return ap.parse_args()
 
 
@@ -247,8 +250,8 @@ class GpuLeg:
         self.dev = torch.device("cuda", local)
         self.prob = gen.make_problem(args.config)
         self.cfg, self.op = self.prob.cfg, self.prob.op
-        self.S = max(1, args.streams)
-        self.reserve = args.reserve_sms if self.S > 1 else 0
+        self.S = max(1, args.batch if args.batch > 1 else args.streams)
+        self.reserve = args.reserve_sms if (self.S > 1 and args.batch <= 1) else 0
         op, dev = self.op, self.dev
         self.rp_d, self.ci_d = torch.from_numpy(op.row_ptr).to(dev), torch.from_numpy(op.col_idx).to(dev)
         self.vals_d = [torch.from_numpy(v).to(dev) for v in op.vals]
@@ -287,8 +290,40 @@ class GpuLeg:
             return cx.solve(bu_h, bv_h, p.lam_min, p.lam_max, cfg.tol, cfg.rank_cap, cfg.n_iter, out=(Uh, Vh))[2]
         return cx.solve(bu, bv, p.lam_min, p.lam_max, cfg.tol, cfg.rank_cap, cfg.n_iter, out=(Uo, Vo))[2]
 
+    def run_batched(self, nsteps, host):
+        """nsteps subset solves in groups of S solved in lockstep by lrc_solve_batch.
+        host=True: each group's B factors are copied from pinned host memory and its outputs back
+        inside the call sequence (the e2e leg)."""
+        lrcheb, torch, p, cfg = self.lrcheb, self.torch, self.prob, self.cfg
+        infos = [None] * nsteps
+        for g0 in range(0, nsteps, self.S):
+            idx = list(range(g0, min(nsteps, g0 + self.S)))
+            cx = self.ctxs[:len(idx)]
+            bus, bvs = [], []
+            for c, i in zip(cx, idx):
+                d_mu, d_nu, bu, bv, bu_h, bv_h = self.inputs[i % len(self.inputs)]
+                c.set_params(d_mu, d_nu)
+                if host:
+                    bu = bu_h.to(self.dev, non_blocking=True)
+                    bv = bv_h.to(self.dev, non_blocking=True)
+                bus.append(bu)
+                bvs.append(bv)
+            outs = [(o[0], o[1]) for o in self.outs[:len(idx)]]
+            res = lrcheb.solve_batch(cx, bus, bvs, p.lam_min, p.lam_max, cfg.tol, cfg.rank_cap, cfg.n_iter,
+                                     outs=outs)
+            for j, i in enumerate(idx):
+                infos[i] = res[j][2]
+                if host:
+                    self.outs[j][2].copy_(res[j][0], non_blocking=True)
+                    self.outs[j][3].copy_(res[j][1], non_blocking=True)
+        if host:
+            torch.cuda.current_stream().synchronize()
+        return infos
+
     def run_steps(self, nsteps, host):
         """nsteps solves dealt round-robin to the S streams, one host thread per stream."""
+        if self.args.batch > 1:
+            return self.run_batched(nsteps, host)
         infos = [None] * nsteps
         errs = []
 
@@ -345,6 +380,9 @@ class GpuLeg:
         return {"workload": workload_str(self.cfg, self.op, self.n),
                 "step": "one full ChebyshevT solve of one parameter subset (N iterations + final residual)",
                 "concurrent_subsets_per_gpu": self.S, "reserved_sms": self.reserve,
+                "subset_schedule": (f"f1 batched lockstep: {self.S} subsets per lrc_solve_batch call (one fused SpMM "
+                                    f"pass per iteration for all of them)") if self.args.batch > 1 else
+                                   f"{self.S} independent solves on concurrent streams",
                 "l2": f"inputs larger than L2 (operator {operator_bytes(self.op) / 1e9:.2f} GB vs 126 MB)"
                       if operator_bytes(self.op) > L2_BYTES else "operator fits in L2 (latency-bound config)"}
 

@@ -133,6 +133,21 @@ lrc_status lrc_solve(lrc_ctx *ctx,
                      double *U_out, int64_t ld_u, double *V_out, int64_t ld_v,
                      lrc_mem where, lrc_solve_info *info);
 
+/* Batched lockstep solve of S (1..4) parameter subsets (Algorithm 1's loop
+ * over the subsets I_k, P:304-327 -- the subsets are independent given the operator).
+ * ctxs[q] holds subset q's parameters (lrc_set_params) and all contexts borrow the SAME operator
+ * arrays (lrc_set_operator with LRC_MEM_DEVICE_BORROW on identical device pointers; LRC_ERR_ARG
+ * otherwise).  Every iteration reads the operator once for all S subsets' U factors (one batched
+ * fused SpMM on ctxs[0]'s stream) and then runs the S truncations concurrently on the contexts'
+ * own streams.  Per subset q: B_U[q] (ld_bu[q]), B_V[q] (ld_bv[q]), outputs U_out[q] / V_out[q]
+ * (ld_u[q], ld_v[q]) and infos[q] (infos may be NULL) exactly as lrc_solve.  r_B >= 1 and the same
+ * opts for all; LRC_ASYNC / LRC_NO_GRAPH / LRC_RECORD_ITERATES are not supported here.  Returns the
+ * first error of any subset (outputs of a failing subset untouched, as lrc_solve). */
+lrc_status lrc_solve_batch(lrc_ctx *const *ctxs, int S, const double *const *B_U, const int64_t *ld_bu,
+                           const double *const *B_V, const int64_t *ld_bv, int64_t r_B,
+                           const lrc_solve_opts *opts, double *const *U_out, const int64_t *ld_u,
+                           double *const *V_out, const int64_t *ld_v, lrc_mem where, lrc_solve_info *infos);
+
 /* Completes a solve started with LRC_ASYNC: waits for ctx's stream, fills *info (may be NULL) and
  * returns the solve's status (LRC_ERR_STATE if no solve is pending).  The caller keeps B_U, B_V,
  * U_out and V_out alive until then.  A pending solve is also completed (info discarded) by the

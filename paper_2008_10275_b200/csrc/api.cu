@@ -9,6 +9,7 @@
 // with Ucat = [B_U | W0' | W1 | W2 | U_{k-1}] never copied (five strided blocks), ranks device-resident,
 // so the whole N-iteration loop is captured once into a CUDA graph and replayed.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <iterator>
 #include <cstdio>
@@ -29,6 +30,8 @@ cudaError_t small_prepare();
 using namespace lrc;
 
 static thread_local std::string g_create_err;   // lrc_last_error(NULL): lrc_create failures
+static std::atomic<int64_t> g_gen{0};           // workspace / operator generations, unique across contexts
+static int64_t next_gen() { return ++g_gen; }
 
 namespace {
 
@@ -100,7 +103,7 @@ struct lrc_ctx {
   int* tlist_u = nullptr; int ntl_u = 0; int* tlist_g = nullptr; int ntl_g = 0;
   int* tile_ev = nullptr;   // [ntiles][2] (first nnz, nnz count) of each tile (U tiles first)
   int* trec = nullptr;      // [ntl_u][kRecInts] tile records of the persistent TMA SpMM
-  int* trun = nullptr;      // [ntl_u][kRunInts] their U row runs
+  int* tmeta = nullptr;     // [ntl_u][kMetaInts] their first nnz, nnz and U row runs
   size_t meta_bytes = 0;
   double rho = 0, lam = 0;
   // params
@@ -117,6 +120,10 @@ struct lrc_ctx {
   // graph
   cudaGraphExec_t gexec = nullptr;
   GraphKey gkey;
+  cudaGraphExec_t bgexec = nullptr;       // lrc_solve_batch graph (this ctx first in the batch)
+  std::vector<int64_t> bkey;
+  int64_t bgraph_kernels = 0;
+  cudaEvent_t ev_k1 = nullptr;            // lrc_solve_batch: the batched SpMM of an iteration is done
   // last solve
   int64_t last_N = 0; bool last_record = false; int last_cap = 0;
   Pending pending;                                   // enqueued solve awaiting finish_solve
@@ -299,7 +306,7 @@ lrc_status ensure_ws(lrc_ctx* ctx, int rb, int cap, int N, int wmax, bool record
   cudaStreamSynchronize(ctx->stream);
   drop_graph(ctx);
   free_ws(w);
-  ++ctx->gen;
+  ctx->gen = next_gen();
   Workspace nw;
   ws_shape(ctx, nw, rb, cap, N, wmax, record);
   Carver c;
@@ -384,7 +391,7 @@ SpmmArgs spmm_base(lrc_ctx* ctx) {
   a.tlist_u = ctx->tlist_u; a.ntl_u = ctx->ntl_u;
   a.tile_ev = ctx->tile_ev;
   a.trec = ctx->trec;
-  a.trun = ctx->trun;
+  a.tmeta = ctx->tmeta;
   a.reserved_sms = ctx->reserved_sms;
   a.tlist_g = ctx->tlist_g; a.ntl_g = ctx->ntl_g;
   a.tlist = nullptr;
@@ -525,21 +532,12 @@ VBlock vblock(const double* ptr, int ld, int w_fixed, int w_idx, double scale, i
 }
 
 // One ChebyshevT iteration k: X_k -> X_{k+1}.
-lrc_status enqueue_iteration(lrc_ctx* ctx, int k, int rb, int cap, double gamma, double tol,
-                             bool record) {
+// K1 of iteration k (a1): W3 = [U_k - g W0 | W1 | W2] from U_k (rank rk[k+1]).
+SpmmArgs iteration_spmm_args(lrc_ctx* ctx, int k, double gamma) {
   Workspace& w = ctx->ws;
-  cudaStream_t s = ctx->stream;
   State st = make_state(w);
-  double* Ucur = w.Ubuf[(k + 1) % 3];
-  double* Uprev = w.Ubuf[k % 3];
-  double* Unext = w.Ubuf[(k + 2) % 3];
-  double* Vcur = w.Vbuf[(k + 1) % 3];
-  double* Vprev = w.Vbuf[k % 3];
-  double* Vnext = w.Vbuf[(k + 2) % 3];
-
-  CK(cudaEventRecord(ctx->ev_fork, s));
   SpmmArgs a = spmm_base(ctx);
-  a.U = Ucur;
+  a.U = w.Ubuf[(k + 1) % 3];
   a.ldu = w.LDU;
   a.d_r = st.rk + (k + 1);
   a.out = w.W3;
@@ -547,8 +545,19 @@ lrc_status enqueue_iteration(lrc_ctx* ctx, int k, int rb, int cap, double gamma,
   a.out_off = 0;
   a.out_sstride = (long long)ctx->M * w.LDU;
   a.gamma = gamma;
-  KL(P_SPMM, s, launch_spmm(SPMM_S2STEP, a, cap, s));
+  return a;
+}
 
+// The truncation of iteration k (a2-a6) once W3 holds K1's output; the V-side assembly forks from
+// ctx->ev_fork (recorded when U_k / V_k became final) onto the side stream.
+lrc_status enqueue_iteration_trunc(lrc_ctx* ctx, int k, int rb, int cap, double gamma, double tol, bool record) {
+  Workspace& w = ctx->ws;
+  cudaStream_t s = ctx->stream;
+  double* Uprev = w.Ubuf[k % 3];
+  double* Unext = w.Ubuf[(k + 2) % 3];
+  double* Vcur = w.Vbuf[(k + 1) % 3];
+  double* Vprev = w.Vbuf[k % 3];
+  double* Vnext = w.Vbuf[(k + 2) % 3];
   VDesc vd{};
   vd.nb = 5;
   vd.pad_even = 1;
@@ -568,6 +577,16 @@ lrc_status enqueue_iteration(lrc_ctx* ctx, int k, int rb, int cap, double gamma,
                        cudaMemcpyDeviceToDevice, s));
   }
   return LRC_OK;
+}
+
+// One ChebyshevT iteration k: X_k -> X_{k+1}.
+lrc_status enqueue_iteration(lrc_ctx* ctx, int k, int rb, int cap, double gamma, double tol,
+                             bool record) {
+  cudaStream_t s = ctx->stream;
+  CK(cudaEventRecord(ctx->ev_fork, s));
+  const SpmmArgs a = iteration_spmm_args(ctx, k, gamma);
+  KL(P_SPMM, s, launch_spmm(SPMM_S2STEP, a, cap, s));
+  return enqueue_iteration_trunc(ctx, k, rb, cap, gamma, tol, record);
 }
 
 std::vector<double> omega_schedule(double lmin, double lmax, int N, int restart) {
@@ -678,7 +697,8 @@ lrc_status lrc_create(lrc_ctx** out, int device, void* cuda_stream) {
   }
   if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_k1, cudaEventDisableTiming) != cudaSuccess) {
     lrc_destroy(ctx);
     return LRC_ERR_CUDA;
   }
@@ -707,10 +727,12 @@ void lrc_destroy(lrc_ctx* ctx) {
     for (int t = 0; t < 6; ++t) dfree(ctx->vals[t]);
   }
   dfree(ctx->tmpA); dfree(ctx->tmpB); dfree(ctx->tmpC);
-  dfree(ctx->group_ptr); dfree(ctx->tdesc); dfree(ctx->tlist_u); dfree(ctx->tlist_g); dfree(ctx->tile_ev); dfree(ctx->trec); dfree(ctx->trun); dfree(ctx->dmu); dfree(ctx->dnu);
+  dfree(ctx->group_ptr); dfree(ctx->tdesc); dfree(ctx->tlist_u); dfree(ctx->tlist_g); dfree(ctx->tile_ev); dfree(ctx->trec); dfree(ctx->tmeta); dfree(ctx->dmu); dfree(ctx->dnu);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->ev_k1) cudaEventDestroy(ctx->ev_k1);
+  if (ctx->bgexec) cudaGraphExecDestroy(ctx->bgexec);
   for (int i = 0; i < 4; ++i) if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
   for (cudaEvent_t e : ctx->evpool) cudaEventDestroy(e);
   if (ctx->h_ints) cudaFreeHost(ctx->h_ints);
@@ -757,7 +779,7 @@ lrc_status lrc_set_workspace(lrc_ctx* ctx, void* dev_ptr, size_t bytes) {
   cudaStreamSynchronize(ctx->stream);
   drop_graph(ctx);
   free_ws(ctx->ws);
-  ++ctx->gen;
+  ctx->gen = next_gen();
   ctx->user_ws = dev_ptr;
   ctx->user_ws_bytes = dev_ptr ? bytes : 0;
   ctx->last_record = false;
@@ -771,7 +793,7 @@ lrc_status lrc_set_reserved_sms(lrc_ctx* ctx, int n) {
     cudaStreamSynchronize(ctx->stream);
     drop_graph(ctx);
     free_ws(ctx->ws);      // the persistent grid (and its partial buffers) are sized from it
-    ++ctx->gen;
+    ctx->gen = next_gen();
     ctx->reserved_sms = n;
   }
   return LRC_OK;
@@ -928,13 +950,13 @@ lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t*
     for (int t = 0; t < 6; ++t) dfree(ctx->vals[t]);
   }
   dfree(ctx->group_ptr);
-  dfree(ctx->tdesc); dfree(ctx->tlist_u); dfree(ctx->tlist_g); dfree(ctx->tile_ev); dfree(ctx->trec); dfree(ctx->trun);
-  ctx->tlist_u = ctx->tlist_g = nullptr; ctx->tile_ev = nullptr; ctx->trec = nullptr; ctx->trun = nullptr;
+  dfree(ctx->tdesc); dfree(ctx->tlist_u); dfree(ctx->tlist_g); dfree(ctx->tile_ev); dfree(ctx->trec); dfree(ctx->tmeta);
+  ctx->tlist_u = ctx->tlist_g = nullptr; ctx->tile_ev = nullptr; ctx->trec = nullptr; ctx->tmeta = nullptr;
   ctx->row_ptr = nullptr; ctx->col_idx = nullptr; ctx->group_ptr = nullptr; ctx->tdesc = nullptr;
   for (int t = 0; t < 6; ++t) ctx->vals[t] = nullptr;
   ctx->op_set = false;
   ctx->par_set = false;   // params depend on nothing here, but workspaces do; keep semantics simple
-  ++ctx->gen;
+  ctx->gen = next_gen();
 
   if (where == LRC_MEM_DEVICE_BORROW) {
     ctx->borrowed = true;
@@ -984,8 +1006,8 @@ lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t*
     for (int t = 0; t < ctx->ntiles && ok; ++t) {
       const int32_t* d = tdesc.data() + (size_t)t * kDescInts;
       if (d[3] <= 0) break;
-      if (d[1] > 900 || d[3] > 90) { ok = false; break; }
-      std::vector<int32_t> R(kRecInts, 0), Q(kRunInts, 0);
+      if (d[1] > kTileNnz || d[3] > kTileUrows) { ok = false; break; }
+      std::vector<int32_t> R(kRecInts, 0), Q(kMetaInts, 0);
       R[0] = d[0]; R[1] = d[1]; R[2] = d[2]; R[3] = d[3];
       const uint16_t* lx = reinterpret_cast<const uint16_t*>(d + kDescLidx);
       int lo = 0, eb = 0;
@@ -1001,22 +1023,22 @@ lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t*
       for (int u = 0; u < d[3] && ok; ) {
         int v = u + 1;
         while (v < d[3] && d[kDescUrows + v] == d[kDescUrows + v - 1] + 1) ++v;
-        if (nr == kRunMax) { ok = false; break; }
-        Q[1 + 3 * nr] = d[kDescUrows + u]; Q[2 + 3 * nr] = v - u; Q[3 + 3 * nr] = u;
+        if (nr == kMetaRuns) { ok = false; break; }
+        Q[4 + 3 * nr] = d[kDescUrows + u]; Q[5 + 3 * nr] = v - u; Q[6 + 3 * nr] = u;
         ++nr;
         u = v;
       }
-      Q[0] = nr;
+      Q[0] = d[0]; Q[1] = d[1]; Q[2] = nr;
       rec.insert(rec.end(), R.begin(), R.end());
       runs.insert(runs.end(), Q.begin(), Q.end());
     }
-    dfree(ctx->trec); dfree(ctx->trun);
-    ctx->trec = nullptr; ctx->trun = nullptr;
+    dfree(ctx->trec); dfree(ctx->tmeta);
+    ctx->trec = nullptr; ctx->tmeta = nullptr;
     if (ok && !rec.empty()) {
       CK(dalloc(&ctx->trec, rec.size()));
       CK(cudaMemcpy(ctx->trec, rec.data(), sizeof(int32_t) * rec.size(), cudaMemcpyHostToDevice));
-      CK(dalloc(&ctx->trun, runs.size()));
-      CK(cudaMemcpy(ctx->trun, runs.data(), sizeof(int32_t) * runs.size(), cudaMemcpyHostToDevice));
+      CK(dalloc(&ctx->tmeta, runs.size()));
+      CK(cudaMemcpy(ctx->tmeta, runs.data(), sizeof(int32_t) * runs.size(), cudaMemcpyHostToDevice));
     }
   }
   {
@@ -1067,10 +1089,22 @@ lrc_status lrc_set_params(lrc_ctx* ctx, int64_t n, const double* d_mu, const dou
   return LRC_OK;
 }
 
-lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const double* B_V, int64_t ld_bv,
-                     int64_t r_B, const lrc_solve_opts* opts, double* U_out, int64_t ld_u,
-                     double* V_out, int64_t ld_v, lrc_mem where, lrc_solve_info* info) {
-  if (!ctx) return LRC_ERR_ARG;
+}  // extern "C"
+
+namespace {
+
+// ---- lrc_solve in phases (shared with lrc_solve_batch) ------------------------------------------
+struct SolveCall {
+  const double* B_U; int64_t ld_bu; const double* B_V; int64_t ld_bv;
+  double* U_out; int64_t ld_u; double* V_out; int64_t ld_v;
+  int rb, N, cap, wmax;
+  double gamma;
+  bool record;
+};
+
+lrc_status solve_validate(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const double* B_V, int64_t ld_bv,
+                          int64_t r_B, const lrc_solve_opts* opts, double* U_out, int64_t ld_u, double* V_out,
+                          int64_t ld_v, lrc_mem where, SolveCall& sc) {
   ctx->err.clear();
   if (!ctx->op_set || !ctx->par_set) return fail(ctx, LRC_ERR_STATE, "lrc_solve before lrc_set_operator + lrc_set_params");
   if (!opts) return fail(ctx, LRC_ERR_ARG, "null opts");
@@ -1104,77 +1138,57 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
     lrc_status ps = finish_solve(ctx, nullptr);
     if (ps != LRC_OK) return ps;
   }
-  const bool record = (opts->flags & LRC_RECORD_ITERATES) != 0;
-  const bool use_graph = (opts->flags & LRC_NO_GRAPH) == 0 && !ctx->profiling;
+  sc.B_U = B_U; sc.ld_bu = ld_bu; sc.B_V = B_V; sc.ld_bv = ld_bv;
+  sc.U_out = U_out; sc.ld_u = ld_u; sc.V_out = V_out; sc.ld_v = ld_v;
+  sc.rb = rb; sc.N = N; sc.cap = cap; sc.wmax = wmax;
+  sc.gamma = 2.0 / (lmax + lmin);
+  sc.record = (opts->flags & LRC_RECORD_ITERATES) != 0;
+  return LRC_OK;
+}
+
+// workspace, inputs, omega sequence, state reset and ||B||_F^2, on ctx's stream (ends with ev[1])
+lrc_status solve_prologue(lrc_ctx* ctx, const lrc_solve_opts* opts, lrc_mem where, const SolveCall& sc) {
   ctx->warm_start = (opts->flags & LRC_NO_WARM_START) == 0;
   CK(cudaSetDevice(ctx->device));
-  lrc_status st = ensure_ws_fit(ctx, std::max(rb, 1), cap, N, wmax, record);
+  lrc_status st = ensure_ws_fit(ctx, std::max(sc.rb, 1), sc.cap, sc.N, sc.wmax, sc.record);
   if (st != LRC_OK) return st;
   Workspace& w = ctx->ws;
   cudaStream_t s = ctx->stream;
-  State sd = make_state(w);
-  const double c_ = 0.5 * (lmax - lmin), d_ = 0.5 * (lmax + lmin);
-  (void)c_;
-  const double gamma = 1.0 / d_;
-
+  const int64_t M = ctx->M, n = ctx->n;
   CK(cudaEventRecord(ctx->ev[0], s));
-  // inputs: B_U into BUb, B_V into BV
-  if (rb > 0) {
-    CK(cudaMemcpy2DAsync(w.BUb, sizeof(double) * w.LDB, B_U, sizeof(double) * ld_bu,
-                         sizeof(double) * rb, M, kind_in(where), s));
-    CK(cudaMemcpy2DAsync(w.BV, sizeof(double) * rb, B_V, sizeof(double) * ld_bv,
-                         sizeof(double) * rb, n, kind_in(where), s));
+  if (sc.rb > 0) {
+    CK(cudaMemcpy2DAsync(w.BUb, sizeof(double) * w.LDB, sc.B_U, sizeof(double) * sc.ld_bu,
+                         sizeof(double) * sc.rb, M, kind_in(where), s));
+    CK(cudaMemcpy2DAsync(w.BV, sizeof(double) * sc.rb, sc.B_V, sizeof(double) * sc.ld_bv,
+                         sizeof(double) * sc.rb, n, kind_in(where), s));
   }
-  std::vector<double> om = omega_schedule(lmin, lmax, N, (int)opts->restart_every);
-  CK(cudaMemcpyAsync(w.omega, om.data(), sizeof(double) * N, cudaMemcpyHostToDevice, s));
+  std::vector<double> om = omega_schedule(opts->lambda_min, opts->lambda_max, sc.N, (int)opts->restart_every);
+  CK(cudaMemcpyAsync(w.omega, om.data(), sizeof(double) * sc.N, cudaMemcpyHostToDevice, s));
   CK(cudaMemsetAsync(w.ints, 0, sizeof(int) * (w.N + 16), s));
   CK(cudaMemsetAsync(w.scal, 0, sizeof(double) * 8, s));
-  CK(cudaMemsetAsync(w.sigma, 0, sizeof(double) * (size_t)(N + 4) * kSigmaStride, s));
-
-  if (rb > 0) {
-    // ||B||_F^2 -> scal[0]
-    const UDesc ub = ucat_desc(w, M, rb, -1, nullptr, -1);
+  CK(cudaMemsetAsync(w.sigma, 0, sizeof(double) * (size_t)(sc.N + 4) * kSigmaStride, s));
+  if (sc.rb > 0) {
+    const UDesc ub = ucat_desc(w, M, sc.rb, -1, nullptr, -1);
     VDesc vb{};
     vb.nb = 1;
     vb.pad_even = 1;
-    vb.b[0] = vblock(w.BV, rb, rb, -1, 1.0, 0, 0);
+    vb.b[0] = vblock(w.BV, sc.rb, sc.rb, -1, 1.0, 0, 0);
     st = enqueue_norm2(ctx, ub, vb, 0, s);
     if (st != LRC_OK) return st;
+  }
+  CK(cudaEventRecord(ctx->ev[1], s));
+  return LRC_OK;
+}
 
-    CK(cudaEventRecord(ctx->ev[1], s));
-    const uint32_t gflags = opts->flags & (LRC_RECORD_ITERATES | LRC_NO_WARM_START);
-    GraphKey key;
-    key.gen = ctx->gen; key.N = N; key.rb = rb; key.cap = cap; key.gamma = gamma; key.tol = opts->tol;
-    key.flags = gflags;
-    if (use_graph) {
-      if (!(ctx->gexec && ctx->gkey == key)) {
-        drop_graph(ctx);
-        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        ctx->capturing = true;
-        ctx->capture_count = 0;
-        lrc_status es = LRC_OK;
-        for (int k = 0; k < N && es == LRC_OK; ++k)
-          es = enqueue_iteration(ctx, k, rb, cap, gamma, opts->tol, record);
-        ctx->capturing = false;
-        cudaGraph_t g = nullptr;
-        cudaError_t ce = cudaStreamEndCapture(s, &g);
-        if (es != LRC_OK) { if (g) cudaGraphDestroy(g); return es; }
-        if (ce != cudaSuccess) return fail(ctx, LRC_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
-        ce = cudaGraphInstantiate(&ctx->gexec, g, 0);
-        cudaGraphDestroy(g);
-        if (ce != cudaSuccess) { ctx->gexec = nullptr; return fail(ctx, LRC_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce)); }
-        ctx->gkey = key;
-        ctx->graph_kernels = ctx->capture_count;
-      }
-      CK(cudaGraphLaunch(ctx->gexec, s));
-      ctx->launches += ctx->graph_kernels;
-    } else {
-      for (int k = 0; k < N; ++k) {
-        st = enqueue_iteration(ctx, k, rb, cap, gamma, opts->tol, record);
-        if (st != LRC_OK) return st;
-      }
-    }
-    CK(cudaEventRecord(ctx->ev[2], s));
+// after the iterations (ctx's stream): ev[2], final residual, outputs, ev[3], result mirrors, pending
+lrc_status solve_epilogue(lrc_ctx* ctx, const lrc_solve_opts* opts, lrc_mem where, const SolveCall& sc) {
+  Workspace& w = ctx->ws;
+  cudaStream_t s = ctx->stream;
+  State sd = make_state(w);
+  const int64_t M = ctx->M, n = ctx->n;
+  const int N = sc.N, cap = sc.cap, rb = sc.rb;
+  CK(cudaEventRecord(ctx->ev[2], s));
+  if (rb > 0) {
     const int slotN = N + 1;   // rk index of X_N
     double* UN = w.Ubuf[(N + 1) % 3];
     double* VN = w.Vbuf[(N + 1) % 3];
@@ -1192,29 +1206,25 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
       vr.b[1] = vblock(VN, cap, 0, slotN, -1.0, 0, 0);
       vr.b[2] = vblock(VN, cap, 0, slotN, -1.0, 1, 0);
       vr.b[3] = vblock(VN, cap, 0, slotN, -1.0, 2, 0);
-      st = enqueue_norm2(ctx, ur, vr, 1, s);
+      lrc_status st = enqueue_norm2(ctx, ur, vr, 1, s);
       if (st != LRC_OK) return st;
     }
     // outputs: DEVICE outputs by a guarded copy kernel (columns >= rank zeroed; nothing is written
     // when the device flags an error, so the outputs stay untouched on LRC_ERR_NUMERIC); HOST
     // outputs are copied in finish_solve after the flags were checked
     if (where == LRC_MEM_DEVICE) {
-      KL(P_MISC, s, launch_copy_out(UN, w.LDU, U_out, (int)ld_u, (int)M, cap, sd.rk + slotN, sd.flags, s));
-      KL(P_MISC, s, launch_copy_out(VN, cap, V_out, (int)ld_v, (int)n, cap, sd.rk + slotN, sd.flags, s));
+      KL(P_MISC, s, launch_copy_out(UN, w.LDU, sc.U_out, (int)sc.ld_u, (int)M, cap, sd.rk + slotN, sd.flags, s));
+      KL(P_MISC, s, launch_copy_out(VN, cap, sc.V_out, (int)sc.ld_v, (int)n, cap, sd.rk + slotN, sd.flags, s));
     } else {
       KL(P_MISC, s, launch_zero_cols(UN, (int)M, w.LDU, sd.rk + slotN, 0, cap, s));
       KL(P_MISC, s, launch_zero_cols(VN, (int)n, cap, sd.rk + slotN, 0, cap, s));
     }
+  } else if (where == LRC_MEM_HOST) {
+    for (int64_t i = 0; i < M; ++i) std::memset(sc.U_out + i * sc.ld_u, 0, sizeof(double) * cap);
+    for (int64_t i = 0; i < n; ++i) std::memset(sc.V_out + i * sc.ld_v, 0, sizeof(double) * cap);
   } else {
-    CK(cudaEventRecord(ctx->ev[1], s));
-    CK(cudaEventRecord(ctx->ev[2], s));
-    if (where == LRC_MEM_HOST) {
-      for (int64_t i = 0; i < M; ++i) std::memset(U_out + i * ld_u, 0, sizeof(double) * cap);
-      for (int64_t i = 0; i < n; ++i) std::memset(V_out + i * ld_v, 0, sizeof(double) * cap);
-    } else {
-      CK(cudaMemset2DAsync(U_out, sizeof(double) * ld_u, 0, sizeof(double) * cap, M, s));
-      CK(cudaMemset2DAsync(V_out, sizeof(double) * ld_v, 0, sizeof(double) * cap, n, s));
-    }
+    CK(cudaMemset2DAsync(sc.U_out, sizeof(double) * sc.ld_u, 0, sizeof(double) * cap, M, s));
+    CK(cudaMemset2DAsync(sc.V_out, sizeof(double) * sc.ld_v, 0, sizeof(double) * cap, n, s));
   }
   CK(cudaEventRecord(ctx->ev[3], s));
   // results -> pinned host mirrors (read by finish_solve after the stream synchronises)
@@ -1224,11 +1234,180 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
   CK(cudaMemcpyAsync(ctx->h_sigma, w.sigma, sizeof(double) * (size_t)N * kSigmaStride, cudaMemcpyDeviceToHost, s));
   Pending& pd = ctx->pending;
   pd.active = true;
-  pd.N = N; pd.rb = rb; pd.cap = cap; pd.M = M; pd.n = n; pd.opt_flags = opts->flags; pd.record = record;
-  pd.where = where; pd.U_out = U_out; pd.V_out = V_out; pd.ld_u = ld_u; pd.ld_v = ld_v;
+  pd.N = N; pd.rb = rb; pd.cap = cap; pd.M = M; pd.n = n; pd.opt_flags = opts->flags; pd.record = sc.record;
+  pd.where = where; pd.U_out = sc.U_out; pd.V_out = sc.V_out; pd.ld_u = sc.ld_u; pd.ld_v = sc.ld_v;
   pd.UN = w.Ubuf[(N + 1) % 3]; pd.VN = w.Vbuf[(N + 1) % 3];
+  return LRC_OK;
+}
+
+// capture (or reuse) a graph of `body` on stream s; body() enqueues the work, ctx counts its kernels
+template <typename F>
+lrc_status run_graph(lrc_ctx* ctx, cudaStream_t s, cudaGraphExec_t& gexec, bool reuse, int64_t& gkernels, F&& body) {
+  if (!reuse) {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    gexec = nullptr;
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    ctx->capturing = true;
+    ctx->capture_count = 0;
+    lrc_status es = body();
+    ctx->capturing = false;
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(s, &g);
+    if (es != LRC_OK) { if (g) cudaGraphDestroy(g); return es; }
+    if (ce != cudaSuccess) return fail(ctx, LRC_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    ce = cudaGraphInstantiate(&gexec, g, 0);
+    cudaGraphDestroy(g);
+    if (ce != cudaSuccess) { gexec = nullptr; return fail(ctx, LRC_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce)); }
+    gkernels = ctx->capture_count;
+  }
+  CK(cudaGraphLaunch(gexec, s));
+  ctx->launches += gkernels;
+  return LRC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const double* B_V, int64_t ld_bv,
+                     int64_t r_B, const lrc_solve_opts* opts, double* U_out, int64_t ld_u,
+                     double* V_out, int64_t ld_v, lrc_mem where, lrc_solve_info* info) {
+  if (!ctx) return LRC_ERR_ARG;
+  SolveCall sc;
+  lrc_status st = solve_validate(ctx, B_U, ld_bu, B_V, ld_bv, r_B, opts, U_out, ld_u, V_out, ld_v, where, sc);
+  if (st != LRC_OK) return st;
+  st = solve_prologue(ctx, opts, where, sc);
+  if (st != LRC_OK) return st;
+  cudaStream_t s = ctx->stream;
+  if (sc.rb > 0) {
+    const bool use_graph = (opts->flags & LRC_NO_GRAPH) == 0 && !ctx->profiling;
+    GraphKey key;
+    key.gen = ctx->gen; key.N = sc.N; key.rb = sc.rb; key.cap = sc.cap; key.gamma = sc.gamma; key.tol = opts->tol;
+    key.flags = opts->flags & (LRC_RECORD_ITERATES | LRC_NO_WARM_START);
+    auto body = [&]() -> lrc_status {
+      for (int k = 0; k < sc.N; ++k) {
+        lrc_status e = enqueue_iteration(ctx, k, sc.rb, sc.cap, sc.gamma, opts->tol, sc.record);
+        if (e != LRC_OK) return e;
+      }
+      return LRC_OK;
+    };
+    if (use_graph) {
+      const bool reuse = ctx->gexec && ctx->gkey == key;
+      st = run_graph(ctx, s, ctx->gexec, reuse, ctx->graph_kernels, body);
+      if (st != LRC_OK) { drop_graph(ctx); return st; }
+      ctx->gkey = key;
+    } else {
+      st = body();
+      if (st != LRC_OK) return st;
+    }
+  }
+  st = solve_epilogue(ctx, opts, where, sc);
+  if (st != LRC_OK) return st;
   if (opts->flags & LRC_ASYNC) return LRC_OK;     // lrc_solve_wait completes the call
   return finish_solve(ctx, info);
+}
+
+// Batched lockstep solve of S subsets sharing one operator (Algorithm 1's loop
+// over the subsets): per iteration one batched fused SpMM on ctxs[0]'s stream reads the
+// operator once for all S U factors, then every subset's truncation runs on its own context's
+// stream (V-side assembly forked to the side streams, overlapping the SpMM).  Captured once into a
+// CUDA graph over the S streams.
+lrc_status lrc_solve_batch(lrc_ctx* const* ctxs, int S, const double* const* B_U, const int64_t* ld_bu,
+                           const double* const* B_V, const int64_t* ld_bv, int64_t r_B,
+                           const lrc_solve_opts* opts, double* const* U_out, const int64_t* ld_u,
+                           double* const* V_out, const int64_t* ld_v, lrc_mem where, lrc_solve_info* infos) {
+  if (!ctxs || S < 1 || S > kMaxSub || !ctxs[0] || !B_U || !B_V || !ld_bu || !ld_bv || !U_out || !V_out || !ld_u || !ld_v)
+    return LRC_ERR_ARG;
+  lrc_ctx* c0 = ctxs[0];
+  lrc_ctx* const ctx = c0;   // errors are reported on the first context
+  if (!opts) return fail(c0, LRC_ERR_ARG, "null opts");
+  if (opts->flags & (LRC_ASYNC | LRC_NO_GRAPH | LRC_RECORD_ITERATES))
+    return fail(c0, LRC_ERR_ARG, "lrc_solve_batch: LRC_ASYNC / LRC_NO_GRAPH / LRC_RECORD_ITERATES not supported");
+  if (r_B < 1) return fail(c0, LRC_ERR_ARG, "lrc_solve_batch: r_B must be >= 1");
+  for (int q = 0; q < S; ++q) {
+    lrc_ctx* c = ctxs[q];
+    if (!c) return fail(c0, LRC_ERR_ARG, "null context");
+    for (int p = 0; p < q; ++p) if (ctxs[p] == c) return fail(c0, LRC_ERR_ARG, "contexts must be distinct");
+    if (!c->op_set || !c0->op_set) return fail(c0, LRC_ERR_STATE, "lrc_solve_batch before lrc_set_operator");
+    bool same = c->device == c0->device && c->M == c0->M && c->nnz == c0->nnz && c->row_ptr == c0->row_ptr &&
+                c->col_idx == c0->col_idx && c->rho == c0->rho && c->lam == c0->lam;
+    for (int t = 0; t < 6; ++t) same = same && c->vals[t] == c0->vals[t];
+    if (!same) return fail(c0, LRC_ERR_ARG, "lrc_solve_batch: contexts must borrow the same operator arrays");
+  }
+  std::vector<SolveCall> sc(S);
+  for (int q = 0; q < S; ++q) {
+    lrc_status st = solve_validate(ctxs[q], B_U[q], ld_bu[q], B_V[q], ld_bv[q], r_B, opts, U_out[q], ld_u[q],
+                                   V_out[q], ld_v[q], where, sc[q]);
+    if (st != LRC_OK) return st;
+  }
+  for (int q = 0; q < S; ++q) {
+    lrc_status st = solve_prologue(ctxs[q], opts, where, sc[q]);
+    if (st != LRC_OK) return st;
+  }
+  const int N = sc[0].N, rb = sc[0].rb, cap = sc[0].cap;
+  const double gamma = sc[0].gamma, tol = opts->tol;
+  cudaStream_t s0 = c0->stream;
+  // the capture stream waits for every subset's prologue
+  for (int q = 1; q < S; ++q) {
+    CK(cudaEventRecord(ctxs[q]->ev_join, ctxs[q]->stream));
+    CK(cudaStreamWaitEvent(s0, ctxs[q]->ev_join, 0));
+  }
+  auto body = [&]() -> lrc_status {
+    for (int q = 1; q < S; ++q) {                        // bring the subset streams into the capture
+      CK(cudaEventRecord(c0->ev_fork, s0));
+      CK(cudaStreamWaitEvent(ctxs[q]->stream, c0->ev_fork, 0));
+    }
+    for (int k = 0; k < N; ++k) {
+      // U_k / V_k of every subset final: record each subset's fork point, join into the SpMM stream
+      for (int q = 0; q < S; ++q) {
+        CK(cudaEventRecord(ctxs[q]->ev_fork, ctxs[q]->stream));
+        if (q > 0) CK(cudaStreamWaitEvent(s0, ctxs[q]->ev_fork, 0));
+      }
+      SpmmArgs a = iteration_spmm_args(c0, k, gamma);
+      a.nsub = S;
+      for (int q = 0; q < S; ++q) {
+        const SpmmArgs aq = iteration_spmm_args(ctxs[q], k, gamma);
+        a.Us[q] = aq.U; a.outs[q] = aq.out; a.d_rs[q] = aq.d_r;
+      }
+      KL(P_SPMM, s0, launch_spmm(SPMM_S2STEP, a, cap, s0));
+      CK(cudaEventRecord(c0->ev_k1, s0));
+      for (int q = 0; q < S; ++q) {
+        if (q > 0) CK(cudaStreamWaitEvent(ctxs[q]->stream, c0->ev_k1, 0));
+        lrc_status e = enqueue_iteration_trunc(ctxs[q], k, rb, cap, gamma, tol, false);
+        if (e != LRC_OK) return e;
+      }
+    }
+    for (int q = 1; q < S; ++q) {                        // join the subset streams
+      CK(cudaEventRecord(ctxs[q]->ev_join, ctxs[q]->stream));
+      CK(cudaStreamWaitEvent(s0, ctxs[q]->ev_join, 0));
+    }
+    return LRC_OK;
+  };
+  // graph cache (on ctxs[0]): the contexts, their generations and the solve shape
+  std::vector<int64_t> key;
+  key.push_back(S); key.push_back(N); key.push_back(rb); key.push_back(cap);
+  key.push_back((int64_t)(opts->flags & LRC_NO_WARM_START));
+  int64_t gb, tb;
+  std::memcpy(&gb, &gamma, 8); std::memcpy(&tb, &tol, 8);
+  key.push_back(gb); key.push_back(tb);
+  for (int q = 0; q < S; ++q) { key.push_back((int64_t)(uintptr_t)ctxs[q]); key.push_back(ctxs[q]->gen); }
+  const bool reuse = c0->bgexec && c0->bkey == key;
+  lrc_status st = run_graph(c0, s0, c0->bgexec, reuse, c0->bgraph_kernels, body);
+  if (st != LRC_OK) { if (c0->bgexec) cudaGraphExecDestroy(c0->bgexec); c0->bgexec = nullptr; c0->bkey.clear(); return st; }
+  c0->bkey = key;
+  // every subset stream waits for the batched iterations, then runs its own epilogue
+  CK(cudaEventRecord(c0->ev_join, s0));
+  for (int q = 1; q < S; ++q) CK(cudaStreamWaitEvent(ctxs[q]->stream, c0->ev_join, 0));
+  for (int q = 0; q < S; ++q) {
+    st = solve_epilogue(ctxs[q], opts, where, sc[q]);
+    if (st != LRC_OK) return st;
+  }
+  lrc_status worst = LRC_OK;
+  for (int q = 0; q < S; ++q) {
+    st = finish_solve(ctxs[q], infos ? infos + q : nullptr);
+    if (st != LRC_OK && worst == LRC_OK) worst = st;
+  }
+  return worst;
 }
 
 // Wait for the solve enqueued last on ctx, fill info, copy HOST outputs (only when no error was

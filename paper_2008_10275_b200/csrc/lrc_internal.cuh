@@ -28,18 +28,20 @@ constexpr int kSigmaStride = 128;
 // [0] e0 [1] tot [2] nb [3] staged U rows, [4+b] row0, [8+b] g, [12+b] L, [16+b] offset of block b's
 // column list in [kRecHdr ..), [20+b] first nnz of block b relative to e0, [24+b] local row of the
 // block's first row among the staged U rows (-1: not staged) (b < 4); [kRecHdr ..) the blocks' column
-// lists as local (staged) U row indices.  U-row runs (kRunInts words per tile): [0] count, then
-// (global first row, rows, local first row) per run of consecutive staged rows.
+// lists as local (staged) U row indices.
 constexpr int kRecInts = 256;
 constexpr int kRecHdr = 32;
 constexpr int kRecCols = kRecInts - kRecHdr;
-constexpr int kRunInts = 64;
-constexpr int kRunMax = (kRunInts - 1) / 3;
+constexpr int kTileNnz = 900;      // nnz per tile of the TMA kernel (4 interior FE node blocks)
+constexpr int kTileUrows = 90;     // staged U rows per tile of the TMA kernel
+constexpr int kMetaInts = 16;      // per-tile metadata of the TMA kernel: e0, nnz, runs, 0, 4 x (first row,
+constexpr int kMetaRuns = 4;       //   rows, local first row) of the staged U row runs
 
 // ------------------------------------------------------------------------------------------
 // a1: fused six-array CSR SpMM
 // ------------------------------------------------------------------------------------------
 enum SpmmMode { SPMM_S2STEP = 0, SPMM_PLAIN3 = 1, SPMM_SINGLE = 2, SPMM_DENSE = 3 };
+constexpr int kMaxSub = 4;        // subsets per batched SpMM pass
 
 struct SpmmArgs {
   int M;
@@ -51,7 +53,7 @@ struct SpmmArgs {
   int ntl_u;
   const int* tile_ev;       // [ntiles][2] first nnz and nnz count of each tile
   const int* trec;          // [ntl_u][kRecInts] tile records of the TMA kernel (null: not available)
-  const int* trun;          // [ntl_u][kRunInts] U row runs of the TMA kernel's tiles
+  const int* tmeta;         // [ntl_u][kMetaInts] first nnz, nnz and U row runs of the TMA kernel's tiles
   const int* tlist_g;       // L2-gather tiles (nu = 0)
   int ntl_g;
   const int* tlist;         // (set by the launcher) tile list, or null for all tiles
@@ -73,6 +75,12 @@ struct SpmmArgs {
   const double* dmu;        // DENSE: per-column scalings
   const double* dnu;
   int reserved_sms;         // persistent hot kernel: SMs left free (concurrent solves)
+  // f1 batched application: nsub > 1 subsets' U factors in one pass over the operator (TMA kernel
+  // only; same ldu / output layout for all); U / out / d_r above are then unused
+  int nsub;
+  const double* Us[kMaxSub];
+  double* outs[kMaxSub];
+  const int* d_rs[kMaxSub];
 };
 cudaError_t launch_spmm(int mode, const SpmmArgs& a, int rmax, cudaStream_t s);
 

@@ -18,6 +18,9 @@
 // tensor pipe (m16n8k4 DMMA, computed transposed so stores are full sectors).  Tiles whose rows do
 // not fit the U-path bounds take the general spmm_kernel (L2 gather).  spmm_dense_kernel is the
 // config-5 dense variant.
+#include <cstdio>
+#include <type_traits>
+
 #include "lrc_internal.cuh"
 
 namespace lrc {
@@ -196,6 +199,21 @@ __device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity)
                : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
   return ok != 0;
 }
+#ifdef LRC_WATCHDOG
+// developer build only: give up (with a message) on a barrier wait longer than ~2 s
+__device__ __forceinline__ void mbar_wait_dbg(unsigned long long* b, unsigned parity, int tag, int idx) {
+  const long long t0 = clock64();
+  while (!mbar_try(b, parity)) {
+    if (clock64() - t0 > 4000000000LL) {
+      printf("WATCHDOG blk %d warp %d tag %d idx %d parity %u\n", blockIdx.x, threadIdx.x >> 5, tag, idx, parity);
+      return;
+    }
+  }
+}
+#define MBAR_WAIT(b, p, tag, idx) mbar_wait_dbg(b, p, tag, idx)
+#else
+#define MBAR_WAIT(b, p, tag, idx) mbar_wait(b, p)
+#endif
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
   while (!mbar_try(b, parity)) {}
 }
@@ -203,6 +221,11 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+// warm L2 with a global range (no shared memory, no completion tracking): the producer of the TMA
+// kernel runs this a few tiles ahead of its shared-memory stages so more HBM traffic is in flight
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
@@ -684,10 +707,16 @@ spmm_u_kernel(SpmmArgs a, int ust) {
 constexpr int kTStages = 3;               // raw value / record stages
 constexpr int kUStages = 2;               // U row stages
 constexpr int kTCons = 12;                // consumer warps
-constexpr int kTileNnz = 900;             // nnz per tile of this kernel (4 interior FE node blocks)
 constexpr int kRawStride = 908;           // doubles per raw array per stage (>= kTileNnz + 3, == 12 mod 16)
-constexpr int kTUrowMax = 90;             // staged U rows per tile
+constexpr int kTUrowMax = kTileUrows;     // staged U rows per tile
 constexpr int kTLdMax = 64;               // U leading dimension supported (r <= 64)
+#ifndef LRC_EXP
+#define LRC_EXP 0
+#endif
+#ifndef LRC_TPREFETCH
+#define LRC_TPREFETCH 4
+#endif
+constexpr int kTPrefetch = LRC_TPREFETCH; // raw values warmed into L2 this many tiles ahead (0: off)
 
 size_t tma_smem() {
   return sizeof(double) * ((size_t)kTStages * 6 * kRawStride + (size_t)kUStages * kTUrowMax * kTLdMax) +
@@ -697,93 +726,166 @@ size_t tma_smem() {
 template <int MODE>
 __global__ void __launch_bounds__((kTCons + 1) * 32, 1)
 spmm_tma_kernel(SpmmArgs a) {
-  const int r = a.d_r ? *a.d_r : a.r_fixed;
-  if (r <= 0) return;
+  // subsets batched in this pass (one read of the operator for several subsets' U)
+  const int S = a.nsub > 1 ? a.nsub : 1;
+  int rmax = 0;
+  for (int q = 0; q < S; ++q) {
+    const int* dr = S > 1 ? a.d_rs[q] : a.d_r;
+    rmax = max(rmax, dr ? *dr : a.r_fixed);
+  }
+  if (rmax <= 0) return;
   extern __shared__ __align__(16) double smem_dyn[];
   double* s_raw = smem_dyn;                                                   // [stage][6][kRawStride]
   double* s_ub = s_raw + (size_t)kTStages * 6 * kRawStride;                   // [ustage][kTUrowMax * ldu]
   int* s_rec = reinterpret_cast<int*>(s_ub + (size_t)kUStages * kTUrowMax * kTLdMax);   // [stage][kRecInts]
-  __shared__ __align__(8) unsigned long long full[kTStages], empty[kTStages], uempty[kUStages];
+  // raw/record stages per tile i (ring of kTStages), U stages per work item m = i * S + subset
+  // (ring of kUStages)
+  __shared__ __align__(8) unsigned long long full_r[kTStages], empty_r[kTStages], full_u[kUStages], empty_u[kUStages];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int NCW = kTCons;
   const int ldu = a.ldu;
-  const int CT = (r + 31) >> 5;
-  const int tpt = 4 * CT;                        // (virtual) tasks per tile: every one arrives once
+  int rsub[kMaxSub];                              // ranks of the subsets (read once)
+#pragma unroll
+  for (int q = 0; q < kMaxSub; ++q) {
+    const int* dr = S > 1 ? a.d_rs[q] : a.d_r;
+    rsub[q] = (q < S) ? (dr ? *dr : a.r_fixed) : 0;
+  }
+  const int CT = (rmax + 31) >> 5;
+  const int tpt = 4 * CT;                        // (virtual) tasks per work item: 4 blocks x CT column slices
   if (tid == 0) {
-    for (int s = 0; s < kTStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], tpt); }
-    for (int s = 0; s < kUStages; ++s) mbar_init(&uempty[s], tpt);
+    for (int q = 0; q < kTStages; ++q) { mbar_init(&full_r[q], 1); mbar_init(&empty_r[q], NCW); }
+    for (int q = 0; q < kUStages; ++q) { mbar_init(&full_u[q], 1); mbar_init(&empty_u[q], NCW); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
   const int G = gridDim.x, ntl = a.ntl_u;
   const int nmine = ((int)blockIdx.x < ntl) ? (ntl - (int)blockIdx.x + G - 1) / G : 0;
+  const int nwork = nmine * S;
 
   if (warp == NCW) {
     // ------------------------------------------------------------------------------- producer
-    const int2* ev = reinterpret_cast<const int2*>(a.tile_ev);
-    // (first nnz, nnz) and the U row runs (lane l: run l - 8) of the next tile, one tile ahead
-    auto fetch = [&](int t, int2& e, int3& run, int& nrun) {
-      e = __ldg(ev + t);
-      const int* R = a.trun + (size_t)t * kRunInts;
-      nrun = __ldg(R);
-      const int ri = lane - 8;
-      run = (ri >= 0 && ri < nrun) ? make_int3(__ldg(R + 1 + 3 * ri), __ldg(R + 2 + 3 * ri), __ldg(R + 3 + 3 * ri))
-                                   : make_int3(0, 0, 0);
-    };
-    int2 e = make_int2(0, 0);
-    int3 run = make_int3(0, 0, 0);
-    int nrun = 0;
-    if (nmine > 0) fetch(blockIdx.x, e, run, nrun);
-    for (int i = 0; i < nmine; ++i) {
-      const int t = blockIdx.x + i * G, s = i % kTStages, us = i % kUStages;
-      int2 ne = make_int2(0, 0);
-      int3 nrunv = make_int3(0, 0, 0);
-      int nnrun = 0;
-      if (i + 1 < nmine) fetch(t + G, ne, nrunv, nnrun);
-      if (i >= kTStages) mbar_wait(&empty[s], ((i / kTStages) - 1) & 1);
-      if (i >= kUStages) mbar_wait(&uempty[us], ((i / kUStages) - 1) & 1);
-      const int e0a = e.x & ~1, end = e.x + e.y, endc = end & ~1;
-      double* raw = s_raw + (size_t)s * 6 * kRawStride;
-      unsigned ub = (unsigned)run.y * (unsigned)ldu * 8u;
+    // work item m: first the U rows of m (stage m % kUStages, last used by item m - kUStages), then
+    // the record + raw values of every tile up to two ahead of m's tile (stage last used by tile - 3).
+    // The per-tile metadata (first nnz, nnz, U row runs; tmeta) of 32 consecutive tiles of this CTA
+    // sits in registers (lane l: tile 32 b + l), loaded one batch ahead: no global-load latency on
+    // the producer's per-tile path.
+    int4 cur[kMetaInts / 4], nxt[kMetaInts / 4];
+    auto load_batch = [&](int b, int4 (&dst)[kMetaInts / 4]) {
+      const int j = 32 * b + lane;
+      if (j < nmine) {
+        const int4* src = reinterpret_cast<const int4*>(a.tmeta + (size_t)(blockIdx.x + j * G) * kMetaInts);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) ub += __shfl_xor_sync(0xffffffffu, ub, o);
-      if (lane == 0) {
-        if (end & 1)   // odd tail element: plain load (a bulk copy never reads past the tile)
-          for (int v = 0; v < 6; ++v) raw[v * kRawStride + (end - 1 - e0a)] = __ldg(a.v[v] + end - 1);
-        mbar_expect_tx(&full[s], 6u * 8u * (unsigned)(endc - e0a) + 4u * kRecInts + ub);
+        for (int w = 0; w < kMetaInts / 4; ++w) dst[w] = __ldg(src + w);
+      } else {
+#pragma unroll
+        for (int w = 0; w < kMetaInts / 4; ++w) dst[w] = make_int4(0, 0, 0, 0);
       }
-      __syncwarp();
-      if (lane < 6) {
-        if (endc > e0a) bulk_g2s(raw + lane * kRawStride, a.v[lane] + e0a, 8u * (unsigned)(endc - e0a), &full[s]);
-      } else if (lane == 6) {
-        bulk_g2s(s_rec + s * kRecInts, a.trec + (size_t)t * kRecInts, 4u * kRecInts, &full[s]);
-      } else if (lane >= 8 && lane - 8 < nrun && run.y > 0) {
-        bulk_g2s(s_ub + (size_t)us * kTUrowMax * kTLdMax + (size_t)run.z * ldu, a.U + (size_t)run.x * ldu,
-                 (unsigned)run.y * (unsigned)ldu * 8u, &full[s]);
+    };
+    int bcur = 0;
+    load_batch(0, cur);
+    load_batch(1, nxt);
+    // word W of local tile j (j in the current or the next batch), broadcast from its lane
+    auto meta = [&](int j, auto wc) -> int {
+      constexpr int W = decltype(wc)::value;
+      const int4 vc = cur[W / 4], vn = nxt[W / 4];
+      const int xc = (W % 4 == 0) ? vc.x : (W % 4 == 1) ? vc.y : (W % 4 == 2) ? vc.z : vc.w;
+      const int xn = (W % 4 == 0) ? vn.x : (W % 4 == 1) ? vn.y : (W % 4 == 2) ? vn.z : vn.w;
+      return __shfl_sync(0xffffffffu, (j >> 5) == bcur ? xc : xn, j & 31);
+    };
+    using W0 = std::integral_constant<int, 0>;
+    using W1 = std::integral_constant<int, 1>;
+    using W2 = std::integral_constant<int, 2>;
+    int ri = 0;                                   // next tile whose record + raw values are issued
+    for (int m = 0; m < nwork; ++m) {
+      const int i = m / S, q = m - i * S;
+      if ((i >> 5) != bcur && q == 0) {           // next batch of metadata
+#pragma unroll
+        for (int w = 0; w < kMetaInts / 4; ++w) cur[w] = nxt[w];
+        ++bcur;
+        load_batch(bcur + 1, nxt);
       }
-      e = ne; run = nrunv; nrun = nnrun;
+      // this lane's U row run (lanes 8 .. 8 + nrun - 1)
+      const int nrun = meta(i, W2{});
+      int rv[3 * kMetaRuns];
+      rv[0] = meta(i, std::integral_constant<int, 4>{});  rv[1] = meta(i, std::integral_constant<int, 5>{});
+      rv[2] = meta(i, std::integral_constant<int, 6>{});  rv[3] = meta(i, std::integral_constant<int, 7>{});
+      rv[4] = meta(i, std::integral_constant<int, 8>{});  rv[5] = meta(i, std::integral_constant<int, 9>{});
+      rv[6] = meta(i, std::integral_constant<int, 10>{}); rv[7] = meta(i, std::integral_constant<int, 11>{});
+      rv[8] = meta(i, std::integral_constant<int, 12>{}); rv[9] = meta(i, std::integral_constant<int, 13>{});
+      rv[10] = meta(i, std::integral_constant<int, 14>{}); rv[11] = meta(i, std::integral_constant<int, 15>{});
+      const int myr = lane - 8;
+      int rg = 0, rl = 0, rs = 0;
+#pragma unroll
+      for (int k = 0; k < kMetaRuns; ++k)
+        if (myr == k && k < nrun) { rg = rv[3 * k]; rl = rv[3 * k + 1]; rs = rv[3 * k + 2]; }
+      const int us = m % kUStages;
+      if (m >= kUStages) MBAR_WAIT(&empty_u[us], ((m / kUStages) - 1) & 1, 1, m);
+      {
+        unsigned ub = (LRC_EXP & 1) ? 0u : (unsigned)rl * (unsigned)ldu * 8u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ub += __shfl_xor_sync(0xffffffffu, ub, o);
+        if (lane == 0) mbar_expect_tx(&full_u[us], ub);
+        __syncwarp();
+        const double* Usrc = S > 1 ? a.Us[q] : a.U;
+        if (!(LRC_EXP & 1) && rl > 0)
+          bulk_g2s(s_ub + (size_t)us * kTUrowMax * kTLdMax + (size_t)rs * ldu, Usrc + (size_t)rg * ldu,
+                   (unsigned)rl * (unsigned)ldu * 8u, &full_u[us]);
+      }
+      for (; ri < nmine && ri <= i + 2; ++ri) {
+        const int tr = blockIdx.x + ri * G, sr = ri % kTStages;
+        const int e0 = meta(ri, W0{}), tot = meta(ri, W1{});
+        int pe0 = 0, ptot = 0;
+        if (kTPrefetch > 0 && ri + kTPrefetch < nmine) { pe0 = meta(ri + kTPrefetch, W0{}); ptot = meta(ri + kTPrefetch, W1{}); }
+        if (ri >= kTStages) MBAR_WAIT(&empty_r[sr], ((ri / kTStages) - 1) & 1, 2, ri);
+        if (kTPrefetch > 0 && ptot > 0 && lane < 6) {   // warm L2 further ahead
+          const int p0 = pe0 & ~1, p1 = (pe0 + ptot) & ~1;
+          if (p1 > p0) bulk_prefetch_l2(a.v[lane] + p0, 8u * (unsigned)(p1 - p0));
+        }
+        const int e0a = e0 & ~1, end = e0 + tot, endc = end & ~1;
+        double* raw = s_raw + (size_t)sr * 6 * kRawStride;
+        if (lane == 0) {
+          if (end & 1)   // odd tail element: plain load (a bulk copy never reads past the tile)
+            for (int v = 0; v < 6; ++v) raw[v * kRawStride + (end - 1 - e0a)] = __ldg(a.v[v] + end - 1);
+          mbar_expect_tx(&full_r[sr], ((LRC_EXP & 2) ? 0u : 6u * 8u * (unsigned)(endc - e0a)) + 4u * kRecInts);
+        }
+        __syncwarp();
+        if (lane < 6) {
+          if (!(LRC_EXP & 2) && endc > e0a) bulk_g2s(raw + lane * kRawStride, a.v[lane] + e0a, 8u * (unsigned)(endc - e0a), &full_r[sr]);
+        } else if (lane == 6) {
+          bulk_g2s(s_rec + sr * kRecInts, a.trec + (size_t)tr * kRecInts, 4u * kRecInts, &full_r[sr]);
+        }
+      }
     }
     return;
   }
 
   // ------------------------------------------------------------------------------- consumers
-  // the CTA's tasks form one sequence (tile i, task) = i * tpt + task, dealt round-robin to the
-  // consumer warps; a task is one (node block, 32-column slice) of a tile; the virtual tasks of a
-  // tile with fewer than 4 blocks only arrive on the stage barriers
+  // the CTA's tasks form one sequence (work item m, task) = m * tpt + task, dealt round-robin to the
+  // consumer warps; a task is one (node block, 32-column slice) of a work item; the virtual tasks
+  // (fewer than 4 blocks, or columns past this subset's rank) only arrive on the stage barriers
   const int gid = lane >> 2, tig = lane & 3;
-  const long long sst = a.out_sstride ? a.out_sstride : r;
-  const int ntask = nmine * tpt;
-  for (int T = warp; T < ntask; T += NCW) {
-    const int i = T / tpt, task = T - i * tpt;
-    const int s = i % kTStages, us = i % kUStages;
-    mbar_wait(&full[s], (i / kTStages) & 1);
-    const int* R = s_rec + s * kRecInts;
-    const double* raw = s_raw + (size_t)s * 6 * kRawStride;
+  // Every warp walks all work items in order and waits on every stage phase (a warp that skipped an
+  // item could see a stage's barrier two phases behind and take the stale parity for a completed one);
+  // it arrives once per item on the U stage's empty barrier and once per tile on the raw stage's.
+  for (int m = 0; m < nwork; ++m) {
+    const int i = m / S, q = m - i * S;
+    const int sr = i % kTStages, us = m % kUStages;
+    MBAR_WAIT(&full_r[sr], (i / kTStages) & 1, 3, i);
+    MBAR_WAIT(&full_u[us], (m / kUStages) & 1, 4, m);
+    for (int task = (warp - (int)(((long long)m * tpt) % NCW) + NCW) % NCW; task < tpt; task += NCW) {
+    const int* R = s_rec + sr * kRecInts;
+    const double* raw = s_raw + (size_t)sr * 6 * kRawStride;
     const double* su = s_ub + (size_t)us * kTUrowMax * kTLdMax;
+    int r = rsub[0];
+#pragma unroll
+    for (int k = 1; k < kMaxSub; ++k) if (q == k) r = rsub[k];
+    const double* Uq = S > 1 ? a.Us[q] : a.U;
+    double* outq = S > 1 ? a.outs[q] : a.out;
+    const long long sst = a.out_sstride ? a.out_sstride : r;
     const int nb = R[2];
     const int off = R[0] & 1;                      // the stage starts at the even element before e0
     const int b = task / CT, n0 = (task - b * CT) * 32;
-    if (b < nb) {
+    if (b < nb && n0 < r) {
       const int row0 = R[4 + b], g = R[8 + b], L = R[12 + b], cb = kRecHdr + R[16 + b], nbase = R[20 + b];
       const int lrow0 = R[24 + b];
       // B operand (staged values, combined in the load): slot = nt*8 + gid -> (row q, stream st)
@@ -826,10 +928,12 @@ spmm_tma_kernel(SpmmArgs a) {
           const double v = fma(co[nt][2], t2, fma(co[nt][1], t1, co[nt][0] * t0));
           bv[nt] = (jv && sv[nt]) ? v : 0.0;
         }
+        if (!(LRC_EXP & 4)) {
         dmma1684(acc[0][0], x0, x1, bv[0]);
         dmma1684(acc[0][1], x0, x1, bv[1]);
         dmma1684(acc[1][0], x2, x3, bv[0]);
         dmma1684(acc[1][1], x2, x3, bv[1]);
+        } else { acc[0][0][0] += x0 + bv[0]; acc[1][1][1] += x3 * bv[1]; }
       }
       // epilogue: frag (m, n) -> column n0 + mt*16 + gid (+8), slot nt*8 + 2 tig + e = 3 q + stream
       const bool full_cols = n0 + 32 <= r;
@@ -841,10 +945,10 @@ spmm_tma_kernel(SpmmArgs a) {
           if (Rs >= 3 * g) continue;
           const int q = Rs / 3, st = Rs - q * 3;
           const size_t row = (size_t)(row0 + q);
-          double* orow = a.out + st * sst + row * a.ldo + a.out_off + n0 + gid;
+          double* orow = outq + st * sst + row * a.ldo + a.out_off + n0 + gid;
           const bool s2 = (MODE == SPMM_S2STEP) && st == 0;
           // the block's own U row (S2 epilogue) from the staged rows when present
-          const double* us_ = (lrow0 >= 0) ? su + (size_t)(lrow0 + q) * ldu + n0 + gid : a.U + row * ldu + n0 + gid;
+          const double* us_ = (lrow0 >= 0) ? su + (size_t)(lrow0 + q) * ldu + n0 + gid : Uq + row * ldu + n0 + gid;
 #pragma unroll
           for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -853,7 +957,7 @@ spmm_tma_kernel(SpmmArgs a) {
               if (full_cols || c < r) {
                 double v = acc[mt][nt][hm * 2 + e];
                 if (s2) v = fma(-a.gamma, v, us_[o]);
-                __stcs(orow + o, v);
+                if (!(LRC_EXP & 8) || v == 12345.678) __stcs(orow + o, v);
               } else if (c == r && (r & 1) && a.out_sstride) {
                 __stcs(orow + o, 0.0);        // zero pad column of the (even-padded) Ucat block
               }
@@ -861,8 +965,12 @@ spmm_tma_kernel(SpmmArgs a) {
         }
       }
     }
+    }
     __syncwarp();
-    if (lane == 0) { mbar_arrive(&empty[s]); mbar_arrive(&uempty[us]); }
+    if (lane == 0) {
+      mbar_arrive(&empty_u[us]);
+      if (q == S - 1) mbar_arrive(&empty_r[sr]);
+    }
   }
 }
 
@@ -1055,6 +1163,20 @@ int sm_count() {
   return sms;
 }
 
+bool tma_ok(const SpmmArgs& a, int rmax) {
+#ifdef LRC_NO_TMA
+  return false;
+#endif
+  bool al = a.trec != nullptr && a.tmeta != nullptr && rmax <= kTLdMax && a.ldu <= kTLdMax && (a.ldu % 2 == 0) &&
+            a.nsub <= kMaxSub;
+  for (int q = 0; q < max(1, a.nsub); ++q) {
+    const double* u = a.nsub > 1 ? a.Us[q] : a.U;
+    al = al && ((reinterpret_cast<uintptr_t>(u) & 15) == 0);
+  }
+  for (int v = 0; v < 6; ++v) al = al && ((reinterpret_cast<uintptr_t>(a.v[v]) & 15) == 0);
+  return al;
+}
+
 template <int MODE>
 cudaError_t launch_m(const SpmmArgs& a0, int rmax, cudaStream_t s) {
   SpmmArgs a = a0;
@@ -1066,19 +1188,29 @@ cudaError_t launch_m(const SpmmArgs& a0, int rmax, cudaStream_t s) {
     const int ust = ust_for(rmax), slack = max(0, 32 * ((rmax + 31) / 32) - ust);
     const size_t sm_u = sizeof(double) * (kValCap + (size_t)kUCap * ust + slack);
     // persistent TMA-fed kernel: 16-byte aligned value arrays and U rows, tile records available
-    bool al = a.trec != nullptr && a.trun != nullptr && rmax <= kTLdMax && a.ldu <= kTLdMax && (a.ldu % 2 == 0) &&
-              ((reinterpret_cast<uintptr_t>(a.U) & 15) == 0);
-    for (int v = 0; v < 6; ++v) al = al && ((reinterpret_cast<uintptr_t>(a.v[v]) & 15) == 0);
-    if (al && a.ntl_u > 0) {
+    if (tma_ok(a, rmax) && a.ntl_u > 0) {
       const int grid = min(a.ntl_u, max(1, sm_count() - max(0, a.reserved_sms)));
       spmm_tma_kernel<MODE><<<grid, (kTCons + 1) * 32, tma_smem(), s>>>(a);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       if (a.ntl_g > 0) {
         a.tlist = a.tlist_g;
-        spmm_kernel<MODE, 5><<<a.ntl_g, kThreads, smem_for(MODE, rmax), s>>>(a, ust_for(rmax));
+        for (int q = 0; q < max(1, a.nsub); ++q) {      // L2-gather tiles: one launch per subset
+          SpmmArgs aq = a;
+          if (a.nsub > 1) { aq.nsub = 1; aq.U = a.Us[q]; aq.out = a.outs[q]; aq.d_r = a.d_rs[q]; }
+          spmm_kernel<MODE, 5><<<a.ntl_g, kThreads, smem_for(MODE, rmax), s>>>(aq, ust_for(rmax));
+        }
       }
       return cudaGetLastError();
+    }
+    if (a.nsub > 1) {                              // no batched path: one pass per subset
+      for (int q = 0; q < a.nsub; ++q) {
+        SpmmArgs aq = a;
+        aq.nsub = 1; aq.U = a.Us[q]; aq.out = a.outs[q]; aq.d_r = a.d_rs[q];
+        cudaError_t e = launch_m<MODE>(aq, rmax, s);
+        if (e != cudaSuccess) return e;
+      }
+      return cudaSuccess;
     }
     if (sm_u <= 75 * 1024) {                       // 3 CTAs / SM
       if (a.ntl_u > 0) {

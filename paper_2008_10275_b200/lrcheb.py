@@ -31,7 +31,7 @@ EXPORTS = (
     "lrc_create", "lrc_destroy", "lrc_last_error", "lrc_version", "lrc_set_operator",
     "lrc_set_params", "lrc_solve", "lrc_apply_lowrank", "lrc_apply_dense", "lrc_truncate",
     "lrc_get_iterate", "lrc_last_kernel_ms", "lrc_kernel_launches", "lrc_set_profiling", "lrc_get_profile",
-    "lrc_set_reserved_sms", "lrc_solve_wait", "lrc_workspace_bytes", "lrc_set_workspace",
+    "lrc_set_reserved_sms", "lrc_solve_wait", "lrc_workspace_bytes", "lrc_set_workspace", "lrc_solve_batch",
 )
 
 
@@ -79,6 +79,10 @@ def load_library(path: str = None) -> ctypes.CDLL:
     lib.lrc_last_kernel_ms.argtypes = [P]
     lib.lrc_last_kernel_ms.restype = ctypes.c_float
     lib.lrc_solve_wait.argtypes = [P, ctypes.POINTER(SolveInfo)]
+    PP = ctypes.POINTER(P)
+    PI = ctypes.POINTER(I64)
+    lib.lrc_solve_batch.argtypes = [PP, I32, PP, PI, PP, PI, I64, ctypes.POINTER(SolveOpts), PP, PI, PP, PI, I32,
+                                    ctypes.POINTER(SolveInfo)]
     lib.lrc_workspace_bytes.argtypes = [P, I64, I64, I64, U32, ctypes.POINTER(ctypes.c_size_t)]
     lib.lrc_set_workspace.argtypes = [P, P, ctypes.c_size_t]
     lib.lrc_set_reserved_sms.argtypes = [P, I32]
@@ -91,7 +95,7 @@ def load_library(path: str = None) -> ctypes.CDLL:
     lib.lrc_get_profile.restype = I32
     for name in ("lrc_create", "lrc_set_operator", "lrc_set_params", "lrc_solve", "lrc_apply_lowrank",
                  "lrc_apply_dense", "lrc_truncate", "lrc_get_iterate", "lrc_solve_wait", "lrc_workspace_bytes",
-                 "lrc_set_workspace"):
+                 "lrc_set_workspace", "lrc_solve_batch"):
         getattr(lib, name).restype = I32
     return lib
 
@@ -384,6 +388,54 @@ class Context:
             self._lib.lrc_get_profile(self._h, c, ctypes.byref(name), ctypes.byref(ms), ctypes.byref(cnt))
             out[name.value.decode()] = (ms.value, cnt.value)
         return out
+
+
+def solve_batch(ctxs, B_Us, B_Vs, lambda_min: float, lambda_max: float, tol: float, rank_cap: int, n_iter: int,
+                outs=None, warm_start: bool = True, skip_residual: bool = False):
+    """lrc_solve_batch: S contexts (sharing one borrowed operator, each with its subset's params) solved
+    in lockstep with one batched SpMM per iteration.  Device tensors in and out; returns
+    [(U, V, info)] per subset."""
+    import torch
+    S = len(ctxs)
+    lib_ = ctxs[0]._lib
+    P = ctypes.c_void_p
+    mats_u = [_mat(b) for b in B_Us]
+    mats_v = [_mat(b) for b in B_Vs]
+    assert all(m[2] == LRC_MEM_DEVICE for m in mats_u + mats_v)
+    r_B = mats_u[0][3].shape[1]
+    for c, mu, mv in zip(ctxs, mats_u, mats_v):
+        c._order(mu[3], mv[3])
+    # every context stream must also see the operator / params of the first one
+    for c in ctxs[1:]:
+        c.stream.wait_stream(ctxs[0].stream)
+        ctxs[0].stream.wait_stream(c.stream)
+    if outs is None:
+        outs = [(torch.empty((c.M, rank_cap), dtype=torch.float64, device=mats_u[0][3].device),
+                 torch.empty((c.n, rank_cap), dtype=torch.float64, device=mats_u[0][3].device)) for c in ctxs]
+    mo_u = [_mat(o[0]) for o in outs]
+    mo_v = [_mat(o[1]) for o in outs]
+    flags = (0 if warm_start else LRC_NO_WARM_START) | (LRC_SKIP_FINAL_RESIDUAL if skip_residual else 0)
+    opts = SolveOpts(float(lambda_min), float(lambda_max), float(tol), int(rank_cap), int(n_iter), 0, flags)
+    hs = (P * S)(*[c._h for c in ctxs])
+    bu = (P * S)(*[m[0] for m in mats_u]); ldbu = (ctypes.c_int64 * S)(*[m[1] for m in mats_u])
+    bv = (P * S)(*[m[0] for m in mats_v]); ldbv = (ctypes.c_int64 * S)(*[m[1] for m in mats_v])
+    uo = (P * S)(*[m[0] for m in mo_u]); ldu = (ctypes.c_int64 * S)(*[m[1] for m in mo_u])
+    vo = (P * S)(*[m[0] for m in mo_v]); ldv = (ctypes.c_int64 * S)(*[m[1] for m in mo_v])
+    infos = (SolveInfo * S)()
+    hists = [(ctypes.c_int64 * n_iter)() for _ in range(S)]
+    for q in range(S):
+        infos[q].rank_history = ctypes.cast(hists[q], ctypes.POINTER(ctypes.c_int64))
+    st = lib_.lrc_solve_batch(hs, S, bu, ldbu, bv, ldbv, r_B, ctypes.byref(opts), uo, ldu, vo, ldv, LRC_MEM_DEVICE,
+                              infos)
+    if st != LRC_OK:
+        raise LrcError(st, lib_.lrc_last_error(ctxs[0]._h).decode())
+    res = []
+    for q in range(S):
+        inf = infos[q]
+        res.append((outs[q][0], outs[q][1], dict(rank=inf.rank, rel_residual=inf.rel_residual, b_norm=inf.b_norm,
+                                                 diverged=bool(inf.diverged), ms_iterations=inf.ms_iterations,
+                                                 ms_total=inf.ms_total, rank_history=list(hists[q]))))
+    return res
 
 
 def version() -> str:

@@ -1,5 +1,5 @@
 set -u
-OUT=gpurun_out/r02c; mkdir -p $OUT
+OUT=gpurun_out/${TAG:-r02e}; mkdir -p $OUT
 NCU=/usr/local/cuda/bin/ncu
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1; echo build=$?
 timeout 600 python tools/quick_bench.py large 20 > $OUT/plain.log 2>&1 && \
