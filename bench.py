@@ -248,8 +248,15 @@ class GpuLeg:
         from synth import generator as gen
         self.args, self.local, self.torch, self.lrcheb, self.gen = args, local, torch, lrcheb, gen
         self.dev = torch.device("cuda", local)
-        self.prob = gen.make_problem(args.config)
-        self.cfg, self.op = self.prob.cfg, self.prob.op
+        from synth import terms as st
+        self.terms = args.config in st.TERM_CONFIGS      # a general term list
+        if self.terms:
+            self.prob = st.make_term_problem(args.config)
+            self.cfg, self.op = self.prob.cfg, self.prob     # (M, row_ptr, col_idx, vals)
+            self.op.nnz = int(self.prob.col_idx.shape[0])
+        else:
+            self.prob = gen.make_problem(args.config)
+            self.cfg, self.op = self.prob.cfg, self.prob.op
         self.S = max(1, args.batch if args.batch > 1 else args.streams)
         self.reserve = args.reserve_sms if (self.S > 1 and args.batch <= 1) else 0
         op, dev = self.op, self.dev
@@ -259,7 +266,10 @@ class GpuLeg:
         for _ in range(self.S):
             c = lrcheb.Context(local)
             c.set_reserved_sms(self.reserve)
-            c.set_operator(self.rp_d, self.ci_d, self.vals_d, op.rho_f, op.lambda_s, borrow=True)
+            if self.terms:
+                c.set_operator_terms(self.rp_d, self.ci_d, self.vals_d, self.prob.coef, self.prob.id_group, borrow=True)
+            else:
+                c.set_operator(self.rp_d, self.ci_d, self.vals_d, op.rho_f, op.lambda_s, borrow=True)
             self.ctxs.append(c)
         self.main_s = torch.cuda.Stream(device=dev)
         self.clk = ClockSampler(local)
@@ -284,11 +294,18 @@ class GpuLeg:
         cx = self.ctxs[si]
         Uo, Vo, Uh, Vh = self.outs[si]
         d_mu, d_nu, bu, bv, bu_h, bv_h = self.inputs[i % len(self.inputs)]
-        cx.set_params(d_mu, d_nu)
+        self.set_subset(cx, d_mu, d_nu)
         p, cfg = self.prob, self.cfg
         if host:
             return cx.solve(bu_h, bv_h, p.lam_min, p.lam_max, cfg.tol, cfg.rank_cap, cfg.n_iter, out=(Uh, Vh))[2]
         return cx.solve(bu, bv, p.lam_min, p.lam_max, cfg.tol, cfg.rank_cap, cfg.n_iter, out=(Uo, Vo))[2]
+
+    def set_subset(self, cx, x, y):
+        """The subset's right diagonals: set_params(d_mu, d_nu), or set_diagonals(D) for a term list."""
+        if self.terms:
+            cx.set_diagonals(y)
+        else:
+            cx.set_params(x, y)
 
     def run_batched(self, nsteps, host):
         """nsteps subset solves in groups of S solved in lockstep by lrc_solve_batch.
@@ -302,7 +319,7 @@ class GpuLeg:
             bus, bvs = [], []
             for c, i in zip(cx, idx):
                 d_mu, d_nu, bu, bv, bu_h, bv_h = self.inputs[i % len(self.inputs)]
-                c.set_params(d_mu, d_nu)
+                self.set_subset(c, d_mu, d_nu)
                 if host:
                     bu = bu_h.to(self.dev, non_blocking=True)
                     bv = bv_h.to(self.dev, non_blocking=True)
@@ -403,9 +420,34 @@ class GpuLeg:
                 "ms_per_iteration": ms / (steps * self.cfg.n_iter), "steps": steps,
                 "note": "one subset at a time on one stream (latency view); reserved SMs as in the headline"}
 
+    def batched_f1(self, calls=2):
+        """SURVEY §8 f1 measured beside the headline: groups of S subsets solved in lockstep by
+        lrc_solve_batch (one batched SpMM pass per iteration), S = the headline's concurrent streams."""
+        torch = self.torch
+        S = min(len(self.ctxs), 4)
+        if S < 2 or self.args.batch > 1:
+            return None
+        saved = self.args.batch
+        self.args.batch = S
+        try:
+            self.run_batched(S, False)                       # capture the batch graph
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            self.run_batched(S * calls, False)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+        finally:
+            self.args.batch = saved
+        return {"value": S * calls * self.cfg.n_iter / (ms / 1e3), "unit": "iterations/s", "subsets_per_call": S,
+                "calls": calls, "note": "f1 lockstep: one fused SpMM pass per iteration for all S subsets' U, their "
+                                        "truncations on S streams; the headline's independent concurrent streams "
+                                        "measure faster (the lockstep aligns every subset's single-CTA core steps)"}
+
     def extras(self, value, rank, world):
         args, cfg, op = self.args, self.cfg, self.op
-        out = {"single_stream": self.single_stream()}
+        out = {"single_stream": self.single_stream(), "f1_batched": self.batched_f1()}
         ctx = self.ctxs[0]
         # ---- roofline pass: per-kernel CUDA events on the launching streams (same workload, no graph)
         ctx.set_profiling(True)
@@ -417,7 +459,8 @@ class GpuLeg:
         M, nnz, r, rB, n = op.M, op.nnz, cfg.rank_cap, cfg.r_B, self.n
         w = rB + 4 * r
         p = min(n, w)
-        flops, byts = algorithmic_work(M, nnz, r, rB, n)
+        T, G = (len(op.vals), self.prob.coef.shape[1]) if self.terms else (6, 3)
+        flops, byts = algorithmic_work(M, nnz, r, rB, n, T, G)
 
         def kernel_entry(name):
             ms_tot, cnt = prof[name]
@@ -456,7 +499,7 @@ class GpuLeg:
             "bound": "fp64 tensor (the Gram / basis passes); the SpMM alone is HBM-bound"}
         if args.dense and rank == 0 and args.config == "large":
             out["config5_dense_spmm"] = self.dense_config5()
-        if rank == 0 and not args.no_cpu_baseline:
+        if rank == 0 and not args.no_cpu_baseline and not self.terms:
             rows = cpu_calibrate(self.prob, args.cpu_seconds)
             t = cpu_sample(self.prob, rows)
             out["cpu_baseline"] = {"value": (rows / M) / t, "unit": "iterations/s", "cores": cpu_cores(),
@@ -496,23 +539,24 @@ class GpuLeg:
                 "traffic": ncu_traffic("dense", "large")}
 
 
-def algorithmic_work(M, nnz, r, rB, n):
-    """Structurally necessary flops / bytes per launch at steady state (DESIGN.md §2 table):
-    pass 1  Y = Ucat R_V^T (R_V^T lower trapezoidal) + G1 = Y^T Y (symmetric);
-    pass 2  Q1 = Y R1^{-1} (upper triangular) + G2 = Q1^T Q1;  basis  U' = Y W_r Sigma_r^{-1}."""
-    w = rB + 4 * r
+def algorithmic_work(M, nnz, r, rB, n, T=6, G=3):
+    """Structurally necessary flops / bytes per launch at steady state (DESIGN.md §2 table): the SpMM reads
+    T value arrays + the column indices, U once and writes G grouped outputs (2 G nnz r flops); pass 1
+    Y = Ucat R_V^T (R_V^T lower trapezoidal) + G1 = Y^T Y (symmetric); pass 2 Q1 = Y R1^{-1} (upper
+    triangular) + G2 = Q1^T Q1;  basis  U' = Y W_r Sigma_r^{-1}.  w = r_B + (G + 1) r."""
+    w = rB + (G + 1) * r
     p = min(n, w)
-    flops = {"spmm": 6.0 * nnz * r,
+    flops = {"spmm": 2.0 * G * nnz * r,
              "ts_gram": 2.0 * M * (w * p - p * (p - 1) / 2.0) + 1.0 * M * p * (p + 1),
              "ts_gram2": 1.0 * M * p * (p + 1) + 1.0 * M * p * (p + 1),
              "ts_store": 2.0 * M * p * r}
-    byts = {"spmm": 52.0 * nnz + 4.0 * (M + 1) + 32.0 * M * r,
+    byts = {"spmm": (8.0 * T + 4.0) * nnz + 4.0 * (M + 1) + 8.0 * (1 + G) * M * r,
             "ts_gram": 8.0 * M * w + 8.0 * M * p, "ts_gram2": 8.0 * M * p, "ts_store": 8.0 * M * p + 8.0 * M * r}
     return flops, byts
 
 
 def operator_bytes(op):
-    return 52 * op.nnz + 4 * (op.M + 1)
+    return (8 * len(op.vals) + 4) * op.nnz + 4 * (op.M + 1)
 
 
 def main():

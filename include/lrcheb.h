@@ -31,7 +31,8 @@
  *     synchronous) unless stated otherwise.  One ctx per host thread; no internal locking.
  *
  * Limits of this build (checked, LRC_ERR_ARG otherwise): M < 2^31, nnz < 2^31,
- *   rank_cap <= 128, r_B <= 64, min(n, r_B + 4 rank_cap) <= 112, n <= 1024,
+ *   rank_cap <= 128, r_B <= 64, min(n, r_B + (G + 1) rank_cap) <= 112 (G = 3 right-diagonal
+ *   groups for the operator of P:30-36), r_B + (G + 1) rank_cap <= 256, n <= 1024,
  *   lrc_apply_dense: ncols <= 256.
  */
 #ifndef LRCHEB_H
@@ -88,6 +89,25 @@ lrc_status lrc_set_operator(lrc_ctx *ctx, int64_t M, int64_t nnz,
                             const int32_t *row_ptr, const int32_t *col_idx,
                             const double *const vals[6], double rho_f, double lambda_s,
                             lrc_mem where);
+
+/* General term list: the four-parameter operator of P:478-482
+ * (A0 S + A1 S D_mu- + A2 S D_nurho- + A3 S D_lambda- + Jmu S Dmu + Jlam S Dlam + Jrho S Drho), the
+ * theta-scheme mass term of P:388-396, the Picard operators of P:647-651 -- any
+ *     L(S) = sum_{g < G} ( sum_{t < T} coef[t*G + g] A_t ) S diag(d_g)
+ * with T <= 8 value arrays on the shared CSR pattern (same rules as lrc_set_operator), G <= 6 right
+ * diagonals (set by lrc_set_diagonals), at most 6 nonzero coefficients per group, and one group
+ * id_group whose diagonal is the identity (it carries the Chebyshev step U - gamma W).  The solve
+ * then concatenates w = r_B + (G + 1) rank_cap columns (<= 256).  Runs on the persistent TMA SpMM
+ * only: LRC_ERR_ARG unless the pattern forms FE node-block tiles (<= 900 nnz, <= 90 U rows,
+ * <= 4 row runs) -- true for the synthetic FE operators of BASELINE.json.  lrc_apply_lowrank then
+ * writes G blocks (PLAIN3 / S2STEP, r <= 64) or T blocks A_t U (SIX); lrc_apply_dense is unavailable. */
+lrc_status lrc_set_operator_terms(lrc_ctx *ctx, int64_t M, int64_t nnz, const int32_t *row_ptr,
+                                  const int32_t *col_idx, int T, const double *const *vals, int G,
+                                  const double *coef, int id_group, lrc_mem where);
+
+/* The right diagonals of a general term list: diags is G x n row-major (row g = d_g, finite; row
+ * id_group all ones).  Replaces lrc_set_params for such an operator. */
+lrc_status lrc_set_diagonals(lrc_ctx *ctx, int64_t n, int G, const double *diags, lrc_mem where);
 
 /* The subset's parameters: d_mu, d_nu of length n (finite). where: HOST or DEVICE. */
 lrc_status lrc_set_params(lrc_ctx *ctx, int64_t n, const double *d_mu, const double *d_nu,

@@ -47,7 +47,8 @@ def csr_matrices(M: int, row_ptr, col_idx, vals: Sequence[np.ndarray]) -> List[s
 
 
 def term_list(mats, rho_f: float, lambda_s: float, d_mu, d_nu):
-    """[(c_t, A_t, e_t)] of P:30-36: A0 S, A1 S Dmu, rho_f A2 S Dnu, rho_f Jrho S, Jmu S Dmu, lambda_s Jlam S."""
+    """[(c_t, A_t, e_t)] of P:30-36: A0 S, A1 S Dmu, rho_f A2 S Dnu, rho_f Jrho S, Jmu S Dmu, lambda_s Jlam S.
+    (Other operators of the paper: term_list_fourparam, term_list_theta, term_list_picard below.)"""
     n = len(d_mu)
     one = np.ones(n)
     d_mu = np.asarray(d_mu, dtype=np.float64)
@@ -60,6 +61,46 @@ def term_list(mats, rho_f: float, lambda_s: float, d_mu, d_nu):
         (1.0, mats[4], d_mu),
         (lambda_s, mats[5], one),
     ]
+
+
+# --------------------------------------------------------------------------------------------
+# generalized term lists: every operator below is a list of terms (c_t, A_t, e_t)
+# with L(S) = sum_t c_t A_t S diag(e_t), so apply_*, kron_operator and chebyshevt take them as they are
+# --------------------------------------------------------------------------------------------
+def term_list_general(mats, coef, diags):
+    """L(S) = sum_g (sum_t C[t][g] A_t) S diag(d_g) (the library's general form): one term per array
+    with the combined diagonal e_t = sum_g C[t][g] d_g."""
+    coef = np.asarray(coef, dtype=np.float64)
+    diags = np.asarray(diags, dtype=np.float64)
+    return [(1.0, A, coef[t] @ diags) for t, A in enumerate(mats)]
+
+
+def term_list_fourparam(mats, mu, nurho, lam, rho, mu_ref, nurho_ref, lam_ref):
+    """The four-parameter Newton operator of P:478-482 (`equation_matrix_fourpars1`), term by term:
+    A0 S + A1 S D_mu- + A2 S D_nurho- + A3 S D_lambda- + Jmu S D_mu + Jlam S D_lambda + Jrho S D_rho,
+    D_x- = D_x - x_ref I; mats = [A0, A1, A2, A3, Jmu, Jlam, Jrho]."""
+    one = np.ones(len(mu))
+    mu, nurho, lam, rho = (np.asarray(x, dtype=np.float64) for x in (mu, nurho, lam, rho))
+    return [(1.0, mats[0], one), (1.0, mats[1], mu - mu_ref), (1.0, mats[2], nurho - nurho_ref),
+            (1.0, mats[3], lam - lam_ref), (1.0, mats[4], mu), (1.0, mats[5], lam), (1.0, mats[6], rho)]
+
+
+def term_list_theta(mats, rho_f, lambda_s, d_mu, d_nu, mass_f, mass_s, rho_s, dt, theta):
+    """The theta-scheme Newton operator of P:388-396 (`equation_timedep_matrix1`):
+    (1/dt)(rho_f A_t^f + rho_s A_t^s) S + theta F(S), F the operator of P:30-36."""
+    one = np.ones(len(d_mu))
+    return [(rho_f / dt, mass_f, one), (rho_s / dt, mass_s, one)] + \
+        [(theta * c, A, e) for (c, A, e) in term_list(mats, rho_f, lambda_s, d_mu, d_nu)]
+
+
+def term_list_picard(mats, rho_f, lambda_s, mu, nu, mu_ref, nu_ref):
+    """The fixed-point (Picard) operator of P:647-651 (`equation_picard_matrix1`), term by term:
+    A0 X + A1 X D_mu- + rho_f A2 X D_nu- + F_mu X D_mu + lambda_s F_lam X + rho_f F_rho X;
+    mats = [A0, A1, A2, F_mu, F_lam, F_rho]."""
+    one = np.ones(len(mu))
+    mu, nu = np.asarray(mu, dtype=np.float64), np.asarray(nu, dtype=np.float64)
+    return [(1.0, mats[0], one), (1.0, mats[1], mu - mu_ref), (rho_f, mats[2], nu - nu_ref),
+            (1.0, mats[3], mu), (lambda_s, mats[4], one), (rho_f, mats[5], one)]
 
 
 def apply_dense(terms, S: np.ndarray) -> np.ndarray:

@@ -39,7 +39,7 @@ constexpr size_t kSmemLimit = 232448;   // B200 opt-in dynamic shared memory per
 
 struct Workspace {
   int64_t M = 0, n = 0;
-  int rb = 0, cap = 0, N = 0, pmax = 0, wmax = 0, capp = 0, grid = 0;
+  int rb = 0, cap = 0, N = 0, pmax = 0, wmax = 0, capp = 0, grid = 0, ngrp = 3;
   bool record = false;
   int LDB = 0, LDU = 0;
   double* BUb = nullptr;      // B_U (M x r_B, ld LDB)
@@ -97,7 +97,7 @@ struct lrc_ctx {
   // operator
   bool op_set = false, borrowed = false;
   int64_t M = 0, nnz = 0;
-  int* row_ptr = nullptr; int* col_idx = nullptr; double* vals[6] = {};
+  int* row_ptr = nullptr; int* col_idx = nullptr; double* vals[kMaxT] = {};
   int* group_ptr = nullptr; int ngroups = 0;
   int* tdesc = nullptr; int ntiles = 0;
   int* tlist_u = nullptr; int ntl_u = 0; int* tlist_g = nullptr; int ntl_g = 0;
@@ -109,7 +109,14 @@ struct lrc_ctx {
   // params
   bool par_set = false;
   int64_t n = 0;
-  double* dmu = nullptr; double* dnu = nullptr;
+  double* dmu = nullptr; double* dnu = nullptr;   // legacy views into dtab (rows 1, 2)
+  double* dtab = nullptr;   // right-diagonal table, G x n (legacy: [1, d_mu, d_nu])
+  // term list (legacy: the six arrays / three groups of P:30-36; general)
+  bool general = false;
+  int T = 6, G = 3, id_group = 0;
+  int gl_n[kMaxG] = {};
+  int gl_t[kMaxG][kGroupTerms] = {};
+  double gl_c[kMaxG][kGroupTerms] = {};
   Workspace ws;
   void* user_ws = nullptr;  // caller-owned device arena for the workspace (lrc_set_workspace)
   size_t user_ws_bytes = 0;
@@ -255,6 +262,7 @@ void ws_shape(const lrc_ctx* ctx, Workspace& w, int rb, int cap, int N, int wmax
   w.LDB = rb + (rb & 1);
   w.LDU = cap + (cap & 1);
   w.grid = ts_grid_for((int)ctx->M, ctx->reserved_sms);
+  w.ngrp = ctx->G;
 }
 
 // Every device buffer of a workspace whose shape fields are set.
@@ -263,7 +271,7 @@ cudaError_t ws_carve(Workspace& w, Carver& c) {
   cudaError_t e = cudaSuccess;
 #define CV(ptr, count) do { if ((e = c.get(ptr, count)) != cudaSuccess) return e; } while (0)
   CV(&w.BUb, M * w.LDB);
-  CV(&w.W3, 3 * M * w.LDU);
+  CV(&w.W3, (size_t)w.ngrp * M * w.LDU);
   for (int i = 0; i < 3; ++i) {
     CV(&w.Ubuf[i], M * w.LDU);
     CV(&w.Vbuf[i], n * w.cap);
@@ -300,7 +308,7 @@ lrc_status ensure_ws(lrc_ctx* ctx, int rb, int cap, int N, int wmax, bool record
   const int p_need = (int)std::min<int64_t>(ctx->n, wmax);
   const int pmax = ts_pmax_for(p_need < 1 ? 1 : p_need);
   if (pmax < 0) return fail(ctx, LRC_ERR_ARG, "Gram width out of range");
-  if (w.W3 && w.M == ctx->M && w.n == ctx->n && w.rb >= rb && w.cap == cap && w.N >= N &&
+  if (w.W3 && w.M == ctx->M && w.n == ctx->n && w.ngrp == ctx->G && w.rb >= rb && w.cap == cap && w.N >= N &&
       w.wmax >= wmax && w.pmax == pmax && (!record || w.record))
     return LRC_OK;
   cudaStreamSynchronize(ctx->stream);
@@ -323,7 +331,7 @@ lrc_status ensure_ws(lrc_ctx* ctx, int rb, int cap, int N, int wmax, bool record
   w = nw;
   const size_t M = (size_t)ctx->M, n = (size_t)ctx->n;
   CK(cudaMemsetAsync(w.BUb, 0, sizeof(double) * M * w.LDB, ctx->stream));
-  CK(cudaMemsetAsync(w.W3, 0, sizeof(double) * 3 * M * w.LDU, ctx->stream));
+  CK(cudaMemsetAsync(w.W3, 0, sizeof(double) * w.ngrp * M * w.LDU, ctx->stream));
   for (int i = 0; i < 3; ++i) {
     CK(cudaMemsetAsync(w.Ubuf[i], 0, sizeof(double) * M * w.LDU, ctx->stream));
     CK(cudaMemsetAsync(w.Vbuf[i], 0, sizeof(double) * n * cap, ctx->stream));
@@ -397,7 +405,12 @@ SpmmArgs spmm_base(lrc_ctx* ctx) {
   a.tlist = nullptr;
   a.row_ptr = ctx->row_ptr;
   a.col_idx = ctx->col_idx;
-  for (int t = 0; t < 6; ++t) a.v[t] = ctx->vals[t];
+  for (int t = 0; t < kMaxT; ++t) a.v[t] = ctx->vals[t];
+  a.gen = ctx->general ? 1 : 0; a.T = ctx->T; a.G = ctx->G; a.id_group = ctx->id_group;
+  for (int g = 0; g < kMaxG; ++g) {
+    a.gl_n[g] = ctx->gl_n[g];
+    for (int k = 0; k < kGroupTerms; ++k) { a.gl_t[g][k] = ctx->gl_t[g][k]; a.gl_c[g][k] = ctx->gl_c[g][k]; }
+  }
   a.rho = ctx->rho;
   a.lam = ctx->lam;
   return a;
@@ -417,14 +430,14 @@ lrc_status enqueue_truncation(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, co
   if (use_warm) b.W0 = w.W0;
   if (fork_from_spmm && !ctx->profiling) {   // profiling: serial, so per-kernel times are isolated
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-    KL(P_VSIDE, ctx->side, launch_vside(vd, (int)ctx->n, ctx->dmu, ctx->dnu, omega, k, st, b, w.wmax, ctx->side));
+    KL(P_VSIDE, ctx->side, launch_vside(vd, (int)ctx->n, ctx->dtab, omega, k, st, b, w.wmax, ctx->side));
     if (use_warm)   // W0 = Q_V^T B_prev (p x p, p = n), overlapping the SpMM
       KL(P_TINY, ctx->side, launch_tiny_gemm(w.QV, w.pmax, w.Bprev, w.pmax, w.W0, w.pmax, w.pmax, st.p, 0,
                                              w.pmax, nullptr, (int)ctx->n, ctx->side, 1));
     CK(cudaEventRecord(ctx->ev_join, ctx->side));
     CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
   } else {
-    KL(P_VSIDE, s, launch_vside(vd, (int)ctx->n, ctx->dmu, ctx->dnu, omega, k, st, b, w.wmax, s));
+    KL(P_VSIDE, s, launch_vside(vd, (int)ctx->n, ctx->dtab, omega, k, st, b, w.wmax, s));
     if (use_warm)
       KL(P_TINY, s, launch_tiny_gemm(w.QV, w.pmax, w.Bprev, w.pmax, w.W0, w.pmax, w.pmax, st.p, 0,
                                      w.pmax, nullptr, (int)ctx->n, s, 1));
@@ -490,7 +503,7 @@ lrc_status enqueue_norm2(lrc_ctx* ctx, const UDesc& ud, const VDesc& vd, int slo
   Workspace& w = ctx->ws;
   State st = make_state(w);
   SmallBufs b = make_bufs(w);
-  KL(P_VSIDE, s, launch_vside(vd, (int)ctx->n, ctx->dmu, ctx->dnu, nullptr, 0, st, b, w.wmax, s));
+  KL(P_VSIDE, s, launch_vside(vd, (int)ctx->n, ctx->dtab, nullptr, 0, st, b, w.wmax, s));
   TsArgs ta{};
   ta.M = (int)ctx->M;
   ta.u = ud;
@@ -513,13 +526,13 @@ UBlock ublock(const double* p, int ld, int w_fixed, int w_idx) {
 }
 
 // Ucat = [B_U | W0' | W1 | W2 | extra]: the three W blocks have width rk[ridx]
-UDesc ucat_desc(const Workspace& w, int64_t M, int rb, int ridx, const double* extra, int extra_idx) {
+UDesc ucat_desc(const Workspace& w, int64_t M, int rb, int ridx, const double* extra, int extra_idx, int G) {
   UDesc u{};
   u.nb = 0;
   u.pad_even = 1;      // every block at an even column: 16-byte Ucat copies in the ts kernels
   u.b[u.nb++] = ublock(w.BUb, w.LDB, rb, -1);
   if (ridx >= 0)
-    for (int t = 0; t < 3; ++t) u.b[u.nb++] = ublock(w.W3 + (size_t)t * M * w.LDU, w.LDU, 0, ridx);
+    for (int t = 0; t < G; ++t) u.b[u.nb++] = ublock(w.W3 + (size_t)t * M * w.LDU, w.LDU, 0, ridx);
   if (extra) u.b[u.nb++] = ublock(extra, w.LDU, 0, extra_idx);
   return u;
 }
@@ -558,15 +571,17 @@ lrc_status enqueue_iteration_trunc(lrc_ctx* ctx, int k, int rb, int cap, double 
   double* Vcur = w.Vbuf[(k + 1) % 3];
   double* Vprev = w.Vbuf[k % 3];
   double* Vnext = w.Vbuf[(k + 2) % 3];
+  // Vcat = [w g B_V | per group g: w V_k (identity group, paired with W' = U_k - g W) or
+  //         -w g d_g * V_k | (1-w) V_{k-1}]   (legacy: d_1 = d_mu, d_2 = d_nu)
   VDesc vd{};
-  vd.nb = 5;
+  vd.nb = 0;
   vd.pad_even = 1;
-  vd.b[0] = vblock(w.BV, rb, rb, -1, gamma, 0, 1);             // w g B_V
-  vd.b[1] = vblock(Vcur, cap, 0, k + 1, 1.0, 0, 1);            // w V_k
-  vd.b[2] = vblock(Vcur, cap, 0, k + 1, -gamma, 1, 1);         // -w g d_mu * V_k
-  vd.b[3] = vblock(Vcur, cap, 0, k + 1, -gamma, 2, 1);         // -w g d_nu * V_k
-  vd.b[4] = vblock(Vprev, cap, 0, k, 1.0, 0, 2);               // (1-w) V_{k-1}
-  const UDesc ud = ucat_desc(w, ctx->M, rb, k + 1, Uprev, k);
+  vd.b[vd.nb++] = vblock(w.BV, rb, rb, -1, gamma, -1, 1);
+  for (int g = 0; g < ctx->G; ++g)
+    vd.b[vd.nb++] = (g == ctx->id_group) ? vblock(Vcur, cap, 0, k + 1, 1.0, -1, 1)
+                                          : vblock(Vcur, cap, 0, k + 1, -gamma, g, 1);
+  vd.b[vd.nb++] = vblock(Vprev, cap, 0, k, 1.0, -1, 2);
+  const UDesc ud = ucat_desc(w, ctx->M, rb, k + 1, Uprev, k, ctx->G);
   lrc_status r = enqueue_truncation(ctx, ud, vd, w.omega, k, tol, cap, k + 2, k, Unext, w.LDU,
                                     Vnext, cap, s, true, ctx->warm_start);
   if (r != LRC_OK) return r;
@@ -724,10 +739,10 @@ void lrc_destroy(lrc_ctx* ctx) {
   free_ws(ctx->ws);
   if (!ctx->borrowed) {
     dfree(ctx->row_ptr); dfree(ctx->col_idx);
-    for (int t = 0; t < 6; ++t) dfree(ctx->vals[t]);
+    for (int t = 0; t < kMaxT; ++t) dfree(ctx->vals[t]);
   }
   dfree(ctx->tmpA); dfree(ctx->tmpB); dfree(ctx->tmpC);
-  dfree(ctx->group_ptr); dfree(ctx->tdesc); dfree(ctx->tlist_u); dfree(ctx->tlist_g); dfree(ctx->tile_ev); dfree(ctx->trec); dfree(ctx->tmeta); dfree(ctx->dmu); dfree(ctx->dnu);
+  dfree(ctx->group_ptr); dfree(ctx->tdesc); dfree(ctx->tlist_u); dfree(ctx->tlist_g); dfree(ctx->tile_ev); dfree(ctx->trec); dfree(ctx->tmeta); dfree(ctx->dtab);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
@@ -756,7 +771,7 @@ lrc_status lrc_workspace_bytes(lrc_ctx* ctx, int64_t r_B, int64_t rank_cap, int6
   if (r_B < 0 || r_B > 64 || rank_cap < 1 || rank_cap > kMaxRank || n_iter < 1 || n_iter > 100000)
     return fail(ctx, LRC_ERR_ARG, "r_B / rank_cap / n_iter out of range");
   const int rb = std::max((int)r_B, 1), cap = (int)rank_cap;
-  const int wmax = (rb + (rb & 1)) + 4 * (cap + (cap & 1));
+  const int wmax = (rb + (rb & 1)) + (ctx->G + 1) * (cap + (cap & 1));
   if (ts_pmax_for((int)std::min<int64_t>(ctx->n, wmax)) < 0) return fail(ctx, LRC_ERR_ARG, "Gram width out of range");
   Workspace w;
   ws_shape(ctx, w, rb, cap, (int)n_iter, wmax, (flags & LRC_RECORD_ITERATES) != 0);
@@ -815,15 +830,19 @@ int lrc_get_profile(const lrc_ctx* ctx, int cls, const char** name, double* ms_t
   return P_NCLASS;
 }
 
-lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t* row_ptr,
-                            const int32_t* col_idx, const double* const vals[6], double rho_f,
-                            double lambda_s, lrc_mem where) {
-  if (!ctx) return LRC_ERR_ARG;
+}  // extern "C"
+
+namespace {
+
+// The shared pattern + T value arrays (validation, node blocks, SpMM tiles, copies); the term
+// structure (legacy or general) is set by the caller afterwards.
+lrc_status set_operator_impl(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t* row_ptr, const int32_t* col_idx,
+                             int T, const double* const* vals, double rho_f, double lambda_s, lrc_mem where) {
   ctx->err.clear();
   if (M < 1 || M >= (int64_t)1 << 31) return fail(ctx, LRC_ERR_ARG, "M must be in [1, 2^31)");
   if (nnz < 0 || nnz >= (int64_t)1 << 31) return fail(ctx, LRC_ERR_ARG, "nnz must be in [0, 2^31)");
   if (!row_ptr || (nnz > 0 && !col_idx) || !vals) return fail(ctx, LRC_ERR_ARG, "null pointer");
-  for (int t = 0; t < 6; ++t)
+  for (int t = 0; t < T; ++t)
     if (nnz > 0 && !vals[t]) return fail(ctx, LRC_ERR_ARG, "null value array");
   if (!std::isfinite(rho_f) || !std::isfinite(lambda_s)) return fail(ctx, LRC_ERR_ARG, "rho_f, lambda_s must be finite");
   if (where != LRC_MEM_HOST && where != LRC_MEM_DEVICE && where != LRC_MEM_DEVICE_BORROW)
@@ -947,13 +966,13 @@ lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t*
   free_ws(ctx->ws);
   if (!ctx->borrowed) {
     dfree(ctx->row_ptr); dfree(ctx->col_idx);
-    for (int t = 0; t < 6; ++t) dfree(ctx->vals[t]);
+    for (int t = 0; t < kMaxT; ++t) dfree(ctx->vals[t]);
   }
   dfree(ctx->group_ptr);
   dfree(ctx->tdesc); dfree(ctx->tlist_u); dfree(ctx->tlist_g); dfree(ctx->tile_ev); dfree(ctx->trec); dfree(ctx->tmeta);
   ctx->tlist_u = ctx->tlist_g = nullptr; ctx->tile_ev = nullptr; ctx->trec = nullptr; ctx->tmeta = nullptr;
   ctx->row_ptr = nullptr; ctx->col_idx = nullptr; ctx->group_ptr = nullptr; ctx->tdesc = nullptr;
-  for (int t = 0; t < 6; ++t) ctx->vals[t] = nullptr;
+  for (int t = 0; t < kMaxT; ++t) ctx->vals[t] = nullptr;
   ctx->op_set = false;
   ctx->par_set = false;   // params depend on nothing here, but workspaces do; keep semantics simple
   ctx->gen = next_gen();
@@ -962,14 +981,14 @@ lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t*
     ctx->borrowed = true;
     ctx->row_ptr = const_cast<int*>(row_ptr);
     ctx->col_idx = const_cast<int*>(col_idx);
-    for (int t = 0; t < 6; ++t) ctx->vals[t] = const_cast<double*>(vals[t]);
+    for (int t = 0; t < T; ++t) ctx->vals[t] = const_cast<double*>(vals[t]);
   } else {
     ctx->borrowed = false;
     CK(dalloc(&ctx->row_ptr, M + 1));
     CK(dalloc(&ctx->col_idx, nnz));
     CK(cudaMemcpy(ctx->row_ptr, hrp.data(), sizeof(int32_t) * (M + 1), cudaMemcpyHostToDevice));
     if (nnz) CK(cudaMemcpy(ctx->col_idx, hci.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
-    for (int t = 0; t < 6; ++t) {
+    for (int t = 0; t < T; ++t) {
       CK(dalloc(&ctx->vals[t], nnz));
       if (nnz) CK(cudaMemcpy(ctx->vals[t], vals[t], sizeof(double) * nnz, kind_in(where)));
     }
@@ -1060,10 +1079,93 @@ lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t*
   return LRC_OK;
 }
 
+void set_legacy_terms(lrc_ctx* ctx) {
+  ctx->general = false; ctx->T = 6; ctx->G = 3; ctx->id_group = 0;
+  for (int g = 0; g < kMaxG; ++g) ctx->gl_n[g] = 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+lrc_status lrc_set_operator(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t* row_ptr,
+                            const int32_t* col_idx, const double* const vals[6], double rho_f,
+                            double lambda_s, lrc_mem where) {
+  if (!ctx) return LRC_ERR_ARG;
+  if (!std::isfinite(rho_f) || !std::isfinite(lambda_s)) return fail(ctx, LRC_ERR_ARG, "rho_f, lambda_s must be finite");
+  lrc_status st = set_operator_impl(ctx, M, nnz, row_ptr, col_idx, 6, vals, rho_f, lambda_s, where);
+  if (st == LRC_OK) set_legacy_terms(ctx);
+  return st;
+}
+
+lrc_status lrc_set_operator_terms(lrc_ctx* ctx, int64_t M, int64_t nnz, const int32_t* row_ptr,
+                                  const int32_t* col_idx, int T, const double* const* vals, int G,
+                                  const double* coef, int id_group, lrc_mem where) {
+  if (!ctx) return LRC_ERR_ARG;
+  ctx->err.clear();
+  if (T < 1 || T > kMaxT) return fail(ctx, LRC_ERR_ARG, "T must be in [1, 8]");
+  if (G < 1 || G > kMaxG) return fail(ctx, LRC_ERR_ARG, "G must be in [1, 6]");
+  if (!coef) return fail(ctx, LRC_ERR_ARG, "null coef");
+  if (id_group < 0 || id_group >= G) return fail(ctx, LRC_ERR_ARG, "id_group must name one of the G groups");
+  int gl_n[kMaxG] = {}, gl_t[kMaxG][kGroupTerms] = {};
+  double gl_c[kMaxG][kGroupTerms] = {};
+  for (int t = 0; t < T; ++t)
+    for (int g = 0; g < G; ++g) {
+      const double c = coef[t * G + g];
+      if (!std::isfinite(c)) return fail(ctx, LRC_ERR_ARG, "coefficients must be finite");
+      if (c == 0.0) continue;
+      if (gl_n[g] == kGroupTerms) return fail(ctx, LRC_ERR_ARG, "at most 6 arrays per right-diagonal group");
+      gl_t[g][gl_n[g]] = t; gl_c[g][gl_n[g]] = c; ++gl_n[g];
+    }
+  lrc_status st = set_operator_impl(ctx, M, nnz, row_ptr, col_idx, T, vals, 0.0, 0.0, where);
+  if (st != LRC_OK) return st;
+  if (!ctx->trec) {     // general term lists run on the persistent TMA kernel only
+    ctx->op_set = false;
+    return fail(ctx, LRC_ERR_ARG, "general term lists need an FE-like pattern (node-block tiles <= 900 nnz, <= 90 "
+                                  "U rows, <= 4 row runs)");
+  }
+  ctx->general = true; ctx->T = T; ctx->G = G; ctx->id_group = id_group;
+  for (int g = 0; g < kMaxG; ++g) {
+    ctx->gl_n[g] = gl_n[g];
+    for (int k = 0; k < kGroupTerms; ++k) { ctx->gl_t[g][k] = gl_t[g][k]; ctx->gl_c[g][k] = gl_c[g][k]; }
+  }
+  return LRC_OK;
+}
+
+lrc_status lrc_set_diagonals(lrc_ctx* ctx, int64_t n, int G, const double* diags, lrc_mem where) {
+  if (!ctx) return LRC_ERR_ARG;
+  ctx->err.clear();
+  if (!ctx->op_set || !ctx->general) return fail(ctx, LRC_ERR_STATE, "lrc_set_diagonals needs lrc_set_operator_terms first");
+  if (G != ctx->G) return fail(ctx, LRC_ERR_SHAPE, "G differs from the operator's term list");
+  if (n < 1 || n > 1024) return fail(ctx, LRC_ERR_ARG, "n must be in [1, 1024]");
+  if (!diags) return fail(ctx, LRC_ERR_ARG, "null pointer");
+  if (!valid_mem(where)) return fail(ctx, LRC_ERR_ARG, "bad lrc_mem");
+  CK(cudaSetDevice(ctx->device));
+  std::vector<double> h((size_t)G * n);
+  CK(cudaMemcpy(h.data(), diags, sizeof(double) * h.size(), where == LRC_MEM_HOST ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost));
+  for (double x : h) if (!std::isfinite(x)) return fail(ctx, LRC_ERR_ARG, "diagonals must be finite");
+  for (int64_t i = 0; i < n; ++i)
+    if (h[(size_t)ctx->id_group * n + i] != 1.0) return fail(ctx, LRC_ERR_ARG, "the id_group diagonal must be all ones");
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (n != ctx->n || !ctx->dtab) {
+    drop_graph(ctx);
+    free_ws(ctx->ws);
+    dfree(ctx->dtab);
+    ctx->dtab = nullptr;
+    CK(dalloc(&ctx->dtab, (size_t)kMaxG * n));
+  }
+  CK(cudaMemcpy(ctx->dtab, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+  ctx->dmu = ctx->dnu = nullptr;
+  ctx->n = n;
+  ctx->par_set = true;
+  return LRC_OK;
+}
+
 lrc_status lrc_set_params(lrc_ctx* ctx, int64_t n, const double* d_mu, const double* d_nu, lrc_mem where) {
   if (!ctx) return LRC_ERR_ARG;
   ctx->err.clear();
   if (!ctx->op_set) return fail(ctx, LRC_ERR_STATE, "lrc_set_params before lrc_set_operator");
+  if (ctx->general) return fail(ctx, LRC_ERR_STATE, "a general term list takes lrc_set_diagonals");
   if (n < 1 || n > 1024) return fail(ctx, LRC_ERR_ARG, "n must be in [1, 1024]");
   if (!d_mu || !d_nu) return fail(ctx, LRC_ERR_ARG, "null pointer");
   if (!valid_mem(where)) return fail(ctx, LRC_ERR_ARG, "bad lrc_mem");
@@ -1074,16 +1176,20 @@ lrc_status lrc_set_params(lrc_ctx* ctx, int64_t n, const double* d_mu, const dou
   for (int64_t i = 0; i < n; ++i)
     if (!std::isfinite(hm[i]) || !std::isfinite(hn[i])) return fail(ctx, LRC_ERR_ARG, "d_mu / d_nu must be finite");
   CK(cudaStreamSynchronize(ctx->stream));
-  if (n != ctx->n) {
+  if (n != ctx->n || !ctx->dtab) {
     drop_graph(ctx);
     free_ws(ctx->ws);
-    dfree(ctx->dmu); dfree(ctx->dnu);
-    ctx->dmu = ctx->dnu = nullptr;
-    CK(dalloc(&ctx->dmu, n));
-    CK(dalloc(&ctx->dnu, n));
+    dfree(ctx->dtab);
+    ctx->dtab = nullptr;
+    CK(dalloc(&ctx->dtab, (size_t)kMaxG * n));
   }
-  CK(cudaMemcpy(ctx->dmu, hm.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(ctx->dnu, hn.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+  // right-diagonal table of the three groups: [1, d_mu, d_nu]
+  std::vector<double> h(3 * (size_t)n, 1.0);
+  std::copy(hm.begin(), hm.end(), h.begin() + n);
+  std::copy(hn.begin(), hn.end(), h.begin() + 2 * n);
+  CK(cudaMemcpy(ctx->dtab, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+  ctx->dmu = ctx->dtab + n;
+  ctx->dnu = ctx->dtab + 2 * n;
   ctx->n = n;
   ctx->par_set = true;
   return LRC_OK;
@@ -1126,8 +1232,8 @@ lrc_status solve_validate(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const 
   if (ld_u < cap || ld_v < cap) return fail(ctx, LRC_ERR_SHAPE, "ld_u / ld_v < rank_cap");
   const int rb = (int)r_B, N = (int)opts->n_iter;
   // widest concatenation: every block padded to an even width (UDesc::pad_even)
-  const int wmax = (rb + (rb & 1)) + 4 * (cap + (cap & 1));
-  if (wmax > kMaxW) return fail(ctx, LRC_ERR_ARG, "r_B + 4 rank_cap must be <= 256");
+  const int wmax = (rb + (rb & 1)) + (ctx->G + 1) * (cap + (cap & 1));
+  if (wmax > kMaxW) return fail(ctx, LRC_ERR_ARG, "r_B + (G + 1) rank_cap must be <= 256");
   const int p_need = (int)std::min<int64_t>(n, wmax);
   if (p_need > 112) return fail(ctx, LRC_ERR_ARG, "min(n, r_B + 4 rank_cap) must be <= 112 in this build");
   if (lrc::vside_smem_bytes((int)n, wmax, ts_pmax_for(p_need)) > kSmemLimit)
@@ -1168,11 +1274,11 @@ lrc_status solve_prologue(lrc_ctx* ctx, const lrc_solve_opts* opts, lrc_mem wher
   CK(cudaMemsetAsync(w.scal, 0, sizeof(double) * 8, s));
   CK(cudaMemsetAsync(w.sigma, 0, sizeof(double) * (size_t)(sc.N + 4) * kSigmaStride, s));
   if (sc.rb > 0) {
-    const UDesc ub = ucat_desc(w, M, sc.rb, -1, nullptr, -1);
+    const UDesc ub = ucat_desc(w, M, sc.rb, -1, nullptr, -1, ctx->G);
     VDesc vb{};
     vb.nb = 1;
     vb.pad_even = 1;
-    vb.b[0] = vblock(w.BV, sc.rb, sc.rb, -1, 1.0, 0, 0);
+    vb.b[0] = vblock(w.BV, sc.rb, sc.rb, -1, 1.0, -1, 0);
     st = enqueue_norm2(ctx, ub, vb, 0, s);
     if (st != LRC_OK) return st;
   }
@@ -1198,14 +1304,13 @@ lrc_status solve_epilogue(lrc_ctx* ctx, const lrc_solve_opts* opts, lrc_mem wher
       a.U = UN; a.ldu = w.LDU; a.d_r = sd.rk + slotN; a.out = w.W3; a.ldo = w.LDU; a.out_off = 0;
       a.out_sstride = (long long)M * w.LDU;
       KL(P_SPMM, s, launch_spmm(SPMM_PLAIN3, a, cap, s));
-      const UDesc ur = ucat_desc(w, M, rb, slotN, nullptr, -1);
+      const UDesc ur = ucat_desc(w, M, rb, slotN, nullptr, -1, ctx->G);
       VDesc vr{};
-      vr.nb = 4;
+      vr.nb = 0;
       vr.pad_even = 1;
-      vr.b[0] = vblock(w.BV, rb, rb, -1, 1.0, 0, 0);
-      vr.b[1] = vblock(VN, cap, 0, slotN, -1.0, 0, 0);
-      vr.b[2] = vblock(VN, cap, 0, slotN, -1.0, 1, 0);
-      vr.b[3] = vblock(VN, cap, 0, slotN, -1.0, 2, 0);
+      vr.b[vr.nb++] = vblock(w.BV, rb, rb, -1, 1.0, -1, 0);
+      for (int g = 0; g < ctx->G; ++g)
+        vr.b[vr.nb++] = vblock(VN, cap, 0, slotN, -1.0, g == ctx->id_group ? -1 : g, 0);
       lrc_status st = enqueue_norm2(ctx, ur, vr, 1, s);
       if (st != LRC_OK) return st;
     }
@@ -1331,7 +1436,8 @@ lrc_status lrc_solve_batch(lrc_ctx* const* ctxs, int S, const double* const* B_U
     if (!c->op_set || !c0->op_set) return fail(c0, LRC_ERR_STATE, "lrc_solve_batch before lrc_set_operator");
     bool same = c->device == c0->device && c->M == c0->M && c->nnz == c0->nnz && c->row_ptr == c0->row_ptr &&
                 c->col_idx == c0->col_idx && c->rho == c0->rho && c->lam == c0->lam;
-    for (int t = 0; t < 6; ++t) same = same && c->vals[t] == c0->vals[t];
+    for (int t = 0; t < kMaxT; ++t) same = same && c->vals[t] == c0->vals[t];
+    same = same && c->general == c0->general && c->T == c0->T && c->G == c0->G;
     if (!same) return fail(c0, LRC_ERR_ARG, "lrc_solve_batch: contexts must borrow the same operator arrays");
   }
   std::vector<SolveCall> sc(S);
@@ -1428,8 +1534,10 @@ lrc_status lrc_apply_lowrank(lrc_ctx* ctx, const double* U, int64_t ld_u, int64_
   if (r < 1 || r > kMaxRank) return fail(ctx, LRC_ERR_ARG, "r must be in [1, 128]");
   if (!U || !W) return fail(ctx, LRC_ERR_ARG, "null pointer");
   if (mode > LRC_APPLY_S2STEP) return fail(ctx, LRC_ERR_ARG, "bad mode");
-  const int nout = (mode == LRC_APPLY_SIX) ? 6 : 3;
+  const int nout = (mode == LRC_APPLY_SIX) ? ctx->T : ctx->G;   // per array / per right-diagonal group
   if (ld_u < r || ld_w < nout * r) return fail(ctx, LRC_ERR_SHAPE, "leading dimension too small");
+  if (ctx->general && mode != LRC_APPLY_SIX && (r > 64 || (where == LRC_MEM_DEVICE && ((ld_u & 1) || (reinterpret_cast<uintptr_t>(U) & 15)))))
+    return fail(ctx, LRC_ERR_ARG, "general term lists: r <= 64 and 16-byte aligned U rows (even ld)");
   CK(cudaSetDevice(ctx->device));
   const int64_t M = ctx->M;
   cudaStream_t s = ctx->stream;
@@ -1437,12 +1545,13 @@ lrc_status lrc_apply_lowrank(lrc_ctx* ctx, const double* U, int64_t ld_u, int64_
   double* Wd = W;
   int ldu = (int)ld_u, ldw = (int)ld_w;
   if (where == LRC_MEM_HOST) {
-    lrc_status st = ensure_tmp(ctx, &ctx->tmpA, &ctx->tmpA_sz, (size_t)M * r);
+    const int lde = (int)(r + (r & 1));            // even: 16-byte rows for the TMA path
+    lrc_status st = ensure_tmp(ctx, &ctx->tmpA, &ctx->tmpA_sz, (size_t)M * lde);
     if (st != LRC_OK) return st;
     st = ensure_tmp(ctx, &ctx->tmpB, &ctx->tmpB_sz, (size_t)M * nout * r);
     if (st != LRC_OK) return st;
-    CK(cudaMemcpy2DAsync(ctx->tmpA, sizeof(double) * r, U, sizeof(double) * ld_u, sizeof(double) * r, M, cudaMemcpyHostToDevice, s));
-    Ud = ctx->tmpA; ldu = (int)r;
+    CK(cudaMemcpy2DAsync(ctx->tmpA, sizeof(double) * lde, U, sizeof(double) * ld_u, sizeof(double) * r, M, cudaMemcpyHostToDevice, s));
+    Ud = ctx->tmpA; ldu = lde;
     Wd = ctx->tmpB; ldw = nout * (int)r;
   }
   SpmmArgs a = spmm_base(ctx);
@@ -1450,7 +1559,7 @@ lrc_status lrc_apply_lowrank(lrc_ctx* ctx, const double* U, int64_t ld_u, int64_
   a.gamma = gamma;
   CK(cudaEventRecord(ctx->ev[0], s));
   if (mode == LRC_APPLY_SIX) {
-    for (int t = 0; t < 6; ++t) {
+    for (int t = 0; t < ctx->T; ++t) {
       a.single_t = t;
       a.out_off = t * (int)r;
       KL(P_SPMM, s, launch_spmm(SPMM_SINGLE, a, (int)r, s));
@@ -1472,6 +1581,7 @@ lrc_status lrc_apply_dense(lrc_ctx* ctx, const double* S, int64_t ld_s, int64_t 
   if (!ctx) return LRC_ERR_ARG;
   ctx->err.clear();
   if (!ctx->op_set || !ctx->par_set) return fail(ctx, LRC_ERR_STATE, "lrc_apply_dense before set_operator + set_params");
+  if (ctx->general) return fail(ctx, LRC_ERR_STATE, "lrc_apply_dense: the operator of P:30-36 only");
   if (!valid_mem(where)) return fail(ctx, LRC_ERR_ARG, "bad lrc_mem");
   if (ncols != ctx->n) return fail(ctx, LRC_ERR_SHAPE, "ncols must equal n of lrc_set_params");
   if (ncols < 1 || ncols > 256) return fail(ctx, LRC_ERR_ARG, "ncols must be in [1, 256]");
@@ -1548,7 +1658,7 @@ lrc_status lrc_truncate(lrc_ctx* ctx, const double* U, int64_t ld_u, const doubl
   ud.b[0] = ublock(ctx->tmpA, w, w, -1);
   VDesc vd{};
   vd.nb = 1;
-  vd.b[0] = vblock(ctx->tmpB, w, w, -1, 1.0, 0, 0);
+  vd.b[0] = vblock(ctx->tmpB, w, w, -1, 1.0, -1, 0);
   double* Vnew = ctx->tmpB + (size_t)n * w;
   st = enqueue_truncation(ctx, ud, vd, nullptr, 0, tol, capi, slot, ws.N, ctx->tmpC, capi, Vnew, capi, s, false);
   if (st != LRC_OK) return st;

@@ -42,6 +42,9 @@ constexpr int kMetaRuns = 4;       //   rows, local first row) of the staged U r
 // ------------------------------------------------------------------------------------------
 enum SpmmMode { SPMM_S2STEP = 0, SPMM_PLAIN3 = 1, SPMM_SINGLE = 2, SPMM_DENSE = 3 };
 constexpr int kMaxSub = 4;        // subsets per batched SpMM pass
+constexpr int kMaxT = 8;          // value arrays of a general term list
+constexpr int kMaxG = 6;          // right-diagonal groups of a general term list
+constexpr int kGroupTerms = 6;    // arrays per group
 
 struct SpmmArgs {
   int M;
@@ -60,7 +63,13 @@ struct SpmmArgs {
   int u_aligned16;          // (set by the launcher) U rows may be copied in 16-byte chunks
   const int* row_ptr;
   const int* col_idx;
-  const double* v[6];       // A0, A1, A2, Jrho, Jmu, Jlam
+  const double* v[kMaxT];   // value arrays: A0, A1, A2, Jrho, Jmu, Jlam (legacy) or the T arrays of a term list
+  // general term list (gen != 0): T arrays, G output groups, group g = sum over
+  // k < gl_n[g] of gl_c[g][k] * array gl_t[g][k]; id_group = the group with the identity diagonal
+  int gen, T, G, id_group;
+  int gl_n[kMaxG];
+  int gl_t[kMaxG][kGroupTerms];
+  double gl_c[kMaxG][kGroupTerms];
   double rho, lam;
   const double* U;          // M x r input (row-major, ld ldu)
   int ldu;
@@ -90,7 +99,7 @@ cudaError_t launch_spmm(int mode, const SpmmArgs& a, int rmax, cudaStream_t s);
 // Logical concatenation Ucat = [block 0 | ... | block nb-1] of row-major M-row blocks; block width =
 // w_fixed + (w_idx >= 0 ? rk[w_idx] : 0) (device-resident ranks).
 struct UBlock { const double* p; int ld; int w_fixed; int w_idx; };
-constexpr int kMaxUBlocks = 5;
+constexpr int kMaxUBlocks = 8;    // B_U | G <= 6 groups | U_{k-1}
 struct UDesc { UBlock b[kMaxUBlocks]; int nb; int pad_even; };   // pad_even: every block's logical
                                                                    // width rounded up to even (the pad
                                                                    // column holds zeros / finite data
@@ -129,10 +138,10 @@ struct VBlock {
   const double* ptr; int ld;
   int w_fixed; int w_idx; int w_mul;   // width = w_idx>=0 ? w_mul*rk[w_idx] : w_fixed ... (see kernel)
   double scale;                        // block multiplier
-  int diag;                            // 0: none, 1: d_mu, 2: d_nu
+  int diag;                            // -1: none, else the row of the right-diagonal table (G x n)
   int use_omega;                       // 0: scale, 1: scale*omega, 2: scale*(1-omega)
 };
-struct VDesc { VBlock b[5]; int nb; int pad_even; };   // pad_even: as UDesc (zero pad columns)
+struct VDesc { VBlock b[kMaxUBlocks]; int nb; int pad_even; };   // pad_even: as UDesc (zero pad columns)
 
 struct State {          // device-resident per-solve state
   int* rk;              // rank array, rk[j] = rank of X_{j-1} (j = 0..N+1)
@@ -163,7 +172,7 @@ struct SmallBufs {
 };
 
 // vside: build Vcat (n x w) from the descriptor, Householder QR, write T1 = R_V^T and Q_V.
-cudaError_t launch_vside(const VDesc& d, int n, const double* dmu, const double* dnu,
+cudaError_t launch_vside(const VDesc& d, int n, const double* dtab,
                          const double* omega, int k, State st, SmallBufs b, int wmax,
                          cudaStream_t s);
 // chol1: R1 = chol(G + s1 I) (escalating), R1^{-1}

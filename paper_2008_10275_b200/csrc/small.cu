@@ -102,15 +102,14 @@ __device__ void tri_inv_upper(const double* R, int ld, double* X, int p) {
 // ------------------------------------------------------------------------------------------
 // vside: build Vcat, Householder QR, write T1 = R_V^T and Q_V
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kT) vside_kernel(VDesc d, int n, const double* __restrict__ dmu,
-                                                   const double* __restrict__ dnu,
+__global__ void __launch_bounds__(kT) vside_kernel(VDesc d, int n, const double* __restrict__ dtab,
                                                    const double* __restrict__ omega, int k,
                                                    State st, SmallBufs b, int ncols_alloc) {
   extern __shared__ double sm[];
   const int NL = n | 1;                     // odd column stride: conflict-free column walks
   double* s_v = sm;                         // column-major [ncols_alloc][NL]
   __shared__ double s_tau[kMaxP];
-  __shared__ int s_off[6];
+  __shared__ int s_off[kMaxUBlocks + 1];
   const int tid = threadIdx.x;
 
   if (tid == 0) {
@@ -140,8 +139,7 @@ __global__ void __launch_bounds__(kT) vside_kernel(VDesc d, int n, const double*
       double v = 0.0;                                   // pad column: exactly zero
       if (c < wdt) {
         v = sc * B.ptr[(size_t)i * B.ld + c];
-        if (B.diag == 1) v *= dmu[i];
-        else if (B.diag == 2) v *= dnu[i];
+        if (B.diag >= 0) v *= dtab[(size_t)B.diag * n + i];   // right diagonal d_g (general: f4)
       }
       s_v[(o + c) * NL + i] = v;
     }
@@ -665,12 +663,12 @@ size_t vside_smem_bytes(int n, int wmax, int pmax) {
   return sizeof(double) * (size_t)NL * cols;
 }
 
-cudaError_t launch_vside(const VDesc& d, int n, const double* dmu, const double* dnu,
+cudaError_t launch_vside(const VDesc& d, int n, const double* dtab,
                          const double* omega, int k, State st, SmallBufs b, int wmax,
                          cudaStream_t s) {
   const int pmax = b.ldT;
   const size_t smem = vside_smem_bytes(n, wmax, pmax);
-  vside_kernel<<<1, kT, smem, s>>>(d, n, dmu, dnu, omega, k, st, b, 0);
+  vside_kernel<<<1, kT, smem, s>>>(d, n, dtab, omega, k, st, b, 0);
   return cudaGetLastError();
 }
 

@@ -18,6 +18,7 @@
 // tensor pipe (m16n8k4 DMMA, computed transposed so stores are full sectors).  Tiles whose rows do
 // not fit the U-path bounds take the general spmm_kernel (L2 gather).  spmm_dense_kernel is the
 // config-5 dense variant.
+#include <algorithm>
 #include <cstdio>
 #include <type_traits>
 
@@ -443,7 +444,7 @@ spmm_kernel(SpmmArgs a, int ust) {
 
   double cs = 1.0;
   if constexpr (MODE == SPMM_SINGLE)
-    cs = (a.single_t == 2 || a.single_t == 3) ? a.rho : (a.single_t == 5 ? a.lam : 1.0);
+    cs = a.gen ? 1.0 : ((a.single_t == 2 || a.single_t == 3) ? a.rho : (a.single_t == 5 ? a.lam : 1.0));
 
   // one coalesced load of the tile's packed descriptor
   const int t = a.tlist ? a.tlist[blockIdx.x] : blockIdx.x;
@@ -706,7 +707,8 @@ spmm_u_kernel(SpmmArgs a, int ust) {
 // ---------------------------------------------------------------------------------------------
 constexpr int kTStages = 3;               // raw value / record stages
 constexpr int kUStages = 2;               // U row stages
-constexpr int kTCons = 12;                // consumer warps
+constexpr int kTCons = 12;                // consumer warps (the operator of P:30-36)
+constexpr int kTConsGen = 8;              // consumer warps for general term lists (more registers)
 constexpr int kRawStride = 908;           // doubles per raw array per stage (>= kTileNnz + 3, == 12 mod 16)
 constexpr int kTUrowMax = kTileUrows;     // staged U rows per tile
 constexpr int kTLdMax = 64;               // U leading dimension supported (r <= 64)
@@ -718,13 +720,20 @@ constexpr int kTLdMax = 64;               // U leading dimension supported (r <=
 #endif
 constexpr int kTPrefetch = LRC_TPREFETCH; // raw values warmed into L2 this many tiles ahead (0: off)
 
-size_t tma_smem() {
-  return sizeof(double) * ((size_t)kTStages * 6 * kRawStride + (size_t)kUStages * kTUrowMax * kTLdMax) +
-         sizeof(int) * (size_t)kTStages * kRecInts;
+// raw value stages for nT value arrays (3 up to six arrays, 2 beyond: shared memory)
+__host__ __device__ __forceinline__ int tma_raw_stages(int nT) { return nT <= 6 ? 3 : 2; }
+
+size_t tma_smem(int nT) {
+  const int nsr = tma_raw_stages(nT);
+  return sizeof(double) * ((size_t)nsr * nT * kRawStride + (size_t)kUStages * kTUrowMax * kTLdMax) +
+         sizeof(int) * (size_t)nsr * kRecInts;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__((kTCons + 1) * 32, 1)
+// GEN = false: the operator of P:30-36 (six arrays, the three groups of DESIGN.md K1, fixed combination);
+// GEN = true: a general term list: nT arrays, G groups, group g = sum of up to
+// kGroupTerms arrays with coefficients, slots (row q, group g) = q G + g in NT n-tiles of 8.
+template <int MODE, bool GEN, int NT, int NCW_, int KCG = 4>
+__global__ void __launch_bounds__((NCW_ + 1) * 32, 1)
 spmm_tma_kernel(SpmmArgs a) {
   // subsets batched in this pass (one read of the operator for several subsets' U)
   const int S = a.nsub > 1 ? a.nsub : 1;
@@ -735,14 +744,17 @@ spmm_tma_kernel(SpmmArgs a) {
   }
   if (rmax <= 0) return;
   extern __shared__ __align__(16) double smem_dyn[];
-  double* s_raw = smem_dyn;                                                   // [stage][6][kRawStride]
-  double* s_ub = s_raw + (size_t)kTStages * 6 * kRawStride;                   // [ustage][kTUrowMax * ldu]
+  const int nT = GEN ? a.T : 6;                   // value arrays
+  const int nsr = tma_raw_stages(nT);             // raw value stages
+  const int G = GEN ? a.G : 3;                    // output groups
+  double* s_raw = smem_dyn;                                                   // [stage][nT][kRawStride]
+  double* s_ub = s_raw + (size_t)nsr * nT * kRawStride;                       // [ustage][kTUrowMax * ldu]
   int* s_rec = reinterpret_cast<int*>(s_ub + (size_t)kUStages * kTUrowMax * kTLdMax);   // [stage][kRecInts]
   // raw/record stages per tile i (ring of kTStages), U stages per work item m = i * S + subset
   // (ring of kUStages)
   __shared__ __align__(8) unsigned long long full_r[kTStages], empty_r[kTStages], full_u[kUStages], empty_u[kUStages];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int NCW = kTCons;
+  constexpr int NCW = NCW_;
   const int ldu = a.ldu;
   int rsub[kMaxSub];                              // ranks of the subsets (read once)
 #pragma unroll
@@ -753,13 +765,13 @@ spmm_tma_kernel(SpmmArgs a) {
   const int CT = (rmax + 31) >> 5;
   const int tpt = 4 * CT;                        // (virtual) tasks per work item: 4 blocks x CT column slices
   if (tid == 0) {
-    for (int q = 0; q < kTStages; ++q) { mbar_init(&full_r[q], 1); mbar_init(&empty_r[q], NCW); }
+    for (int q = 0; q < nsr; ++q) { mbar_init(&full_r[q], 1); mbar_init(&empty_r[q], NCW); }
     for (int q = 0; q < kUStages; ++q) { mbar_init(&full_u[q], 1); mbar_init(&empty_u[q], NCW); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  const int G = gridDim.x, ntl = a.ntl_u;
-  const int nmine = ((int)blockIdx.x < ntl) ? (ntl - (int)blockIdx.x + G - 1) / G : 0;
+  const int Gd = gridDim.x, ntl = a.ntl_u;
+  const int nmine = ((int)blockIdx.x < ntl) ? (ntl - (int)blockIdx.x + Gd - 1) / Gd : 0;
   const int nwork = nmine * S;
 
   if (warp == NCW) {
@@ -773,7 +785,7 @@ spmm_tma_kernel(SpmmArgs a) {
     auto load_batch = [&](int b, int4 (&dst)[kMetaInts / 4]) {
       const int j = 32 * b + lane;
       if (j < nmine) {
-        const int4* src = reinterpret_cast<const int4*>(a.tmeta + (size_t)(blockIdx.x + j * G) * kMetaInts);
+        const int4* src = reinterpret_cast<const int4*>(a.tmeta + (size_t)(blockIdx.x + j * Gd) * kMetaInts);
 #pragma unroll
         for (int w = 0; w < kMetaInts / 4; ++w) dst[w] = __ldg(src + w);
       } else {
@@ -813,7 +825,7 @@ spmm_tma_kernel(SpmmArgs a) {
       rv[6] = meta(i, std::integral_constant<int, 10>{}); rv[7] = meta(i, std::integral_constant<int, 11>{});
       rv[8] = meta(i, std::integral_constant<int, 12>{}); rv[9] = meta(i, std::integral_constant<int, 13>{});
       rv[10] = meta(i, std::integral_constant<int, 14>{}); rv[11] = meta(i, std::integral_constant<int, 15>{});
-      const int myr = lane - 8;
+      const int myr = lane - 16;
       int rg = 0, rl = 0, rs = 0;
 #pragma unroll
       for (int k = 0; k < kMetaRuns; ++k)
@@ -831,27 +843,27 @@ spmm_tma_kernel(SpmmArgs a) {
           bulk_g2s(s_ub + (size_t)us * kTUrowMax * kTLdMax + (size_t)rs * ldu, Usrc + (size_t)rg * ldu,
                    (unsigned)rl * (unsigned)ldu * 8u, &full_u[us]);
       }
-      for (; ri < nmine && ri <= i + 2; ++ri) {
-        const int tr = blockIdx.x + ri * G, sr = ri % kTStages;
+      for (; ri < nmine && ri <= i + nsr - 1; ++ri) {
+        const int tr = blockIdx.x + ri * Gd, sr = ri % nsr;
         const int e0 = meta(ri, W0{}), tot = meta(ri, W1{});
         int pe0 = 0, ptot = 0;
         if (kTPrefetch > 0 && ri + kTPrefetch < nmine) { pe0 = meta(ri + kTPrefetch, W0{}); ptot = meta(ri + kTPrefetch, W1{}); }
-        if (ri >= kTStages) MBAR_WAIT(&empty_r[sr], ((ri / kTStages) - 1) & 1, 2, ri);
-        if (kTPrefetch > 0 && ptot > 0 && lane < 6) {   // warm L2 further ahead
+        if (ri >= nsr) MBAR_WAIT(&empty_r[sr], ((ri / nsr) - 1) & 1, 2, ri);
+        if (kTPrefetch > 0 && ptot > 0 && lane < nT) {   // warm L2 further ahead
           const int p0 = pe0 & ~1, p1 = (pe0 + ptot) & ~1;
           if (p1 > p0) bulk_prefetch_l2(a.v[lane] + p0, 8u * (unsigned)(p1 - p0));
         }
         const int e0a = e0 & ~1, end = e0 + tot, endc = end & ~1;
-        double* raw = s_raw + (size_t)sr * 6 * kRawStride;
+        double* raw = s_raw + (size_t)sr * nT * kRawStride;
         if (lane == 0) {
           if (end & 1)   // odd tail element: plain load (a bulk copy never reads past the tile)
-            for (int v = 0; v < 6; ++v) raw[v * kRawStride + (end - 1 - e0a)] = __ldg(a.v[v] + end - 1);
-          mbar_expect_tx(&full_r[sr], ((LRC_EXP & 2) ? 0u : 6u * 8u * (unsigned)(endc - e0a)) + 4u * kRecInts);
+            for (int v = 0; v < nT; ++v) raw[v * kRawStride + (end - 1 - e0a)] = __ldg(a.v[v] + end - 1);
+          mbar_expect_tx(&full_r[sr], ((LRC_EXP & 2) ? 0u : (unsigned)nT * 8u * (unsigned)(endc - e0a)) + 4u * kRecInts);
         }
         __syncwarp();
-        if (lane < 6) {
+        if (lane < nT) {
           if (!(LRC_EXP & 2) && endc > e0a) bulk_g2s(raw + lane * kRawStride, a.v[lane] + e0a, 8u * (unsigned)(endc - e0a), &full_r[sr]);
-        } else if (lane == 6) {
+        } else if (lane == 8) {
           bulk_g2s(s_rec + sr * kRecInts, a.trec + (size_t)tr * kRecInts, 4u * kRecInts, &full_r[sr]);
         }
       }
@@ -869,12 +881,12 @@ spmm_tma_kernel(SpmmArgs a) {
   // it arrives once per item on the U stage's empty barrier and once per tile on the raw stage's.
   for (int m = 0; m < nwork; ++m) {
     const int i = m / S, q = m - i * S;
-    const int sr = i % kTStages, us = m % kUStages;
-    MBAR_WAIT(&full_r[sr], (i / kTStages) & 1, 3, i);
+    const int sr = i % nsr, us = m % kUStages;
+    MBAR_WAIT(&full_r[sr], (i / nsr) & 1, 3, i);
     MBAR_WAIT(&full_u[us], (m / kUStages) & 1, 4, m);
     for (int task = (warp - (int)(((long long)m * tpt) % NCW) + NCW) % NCW; task < tpt; task += NCW) {
     const int* R = s_rec + sr * kRecInts;
-    const double* raw = s_raw + (size_t)sr * 6 * kRawStride;
+    const double* raw = s_raw + (size_t)sr * nT * kRawStride;
     const double* su = s_ub + (size_t)us * kTUrowMax * kTLdMax;
     int r = rsub[0];
 #pragma unroll
@@ -888,32 +900,44 @@ spmm_tma_kernel(SpmmArgs a) {
     if (b < nb && n0 < r) {
       const int row0 = R[4 + b], g = R[8 + b], L = R[12 + b], cb = kRecHdr + R[16 + b], nbase = R[20 + b];
       const int lrow0 = R[24 + b];
-      // B operand (staged values, combined in the load): slot = nt*8 + gid -> (row q, stream st)
-      int po[2][3];
-      double co[2][3];
-      bool sv[2];
+      // B operand (staged values, combined in the load): slot = nt*8 + gid -> (row q, group st);
+      // KC arrays per group with coefficients (legacy: the fixed combination of P:30-36)
+      constexpr int KC = GEN ? KCG : 3;
+      int po[NT][KC];
+      double co[NT][KC];
+      bool sv[NT];
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        const int slot = nt * 8 + gid, q = slot / 3, st = slot - q * 3;
+      for (int nt = 0; nt < NT; ++nt) {
+        const int slot = nt * 8 + gid, q = slot / G, st = slot - q * G;
         sv[nt] = q < g;
         const int o = off + nbase + (sv[nt] ? q * L : 0) + tig;
-        const int a0 = st == 0 ? 0 : (st == 1 ? 1 : 2);
-        const int a1 = st == 0 ? 3 : (st == 1 ? 4 : 2);
-        const int a2 = st == 0 ? 5 : (st == 1 ? 4 : 2);
-        po[nt][0] = a0 * kRawStride + o; po[nt][1] = a1 * kRawStride + o; po[nt][2] = a2 * kRawStride + o;
-        co[nt][0] = st == 2 ? a.rho : 1.0;
-        co[nt][1] = st == 0 ? a.rho : (st == 1 ? 1.0 : 0.0);
-        co[nt][2] = st == 0 ? a.lam : 0.0;
+        if constexpr (GEN) {
+          const int gs = sv[nt] ? st : 0;
+#pragma unroll
+          for (int k = 0; k < KC; ++k) {
+            const bool on = k < a.gl_n[gs];
+            po[nt][k] = (on ? a.gl_t[gs][k] : 0) * kRawStride + o;
+            co[nt][k] = on ? a.gl_c[gs][k] : 0.0;
+          }
+        } else {
+          const int a0 = st == 0 ? 0 : (st == 1 ? 1 : 2);
+          const int a1 = st == 0 ? 3 : (st == 1 ? 4 : 2);
+          const int a2 = st == 0 ? 5 : (st == 1 ? 4 : 2);
+          po[nt][0] = a0 * kRawStride + o; po[nt][1] = a1 * kRawStride + o; po[nt][2] = a2 * kRawStride + o;
+          co[nt][0] = st == 2 ? a.rho : 1.0;
+          co[nt][1] = st == 0 ? a.rho : (st == 1 ? 1.0 : 0.0);
+          co[nt][2] = st == 0 ? a.lam : 0.0;
+        }
       }
       // A operand (U^T): columns n0 + mt*16 + gid (+8), entry j = k0 + tig -> staged U row R[cb + j]
       const int c00 = n0 + gid, c01 = c00 + 8, c10 = c00 + 16, c11 = c00 + 24;
       const bool v00 = c00 < r, v01 = c01 < r, v10 = c10 < r, v11 = c11 < r;
       const int jmax = L - 1;
-      double acc[2][2][4];
+      double acc[2][NT][4];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.0;
+        for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.0;
       const int L4 = (L + 3) & ~3;
 #pragma unroll 2
       for (int k0 = 0; k0 < L4; k0 += 4) {
@@ -921,32 +945,35 @@ spmm_tma_kernel(SpmmArgs a) {
         const double x0 = v00 ? u[c00] : 0.0, x1 = v01 ? u[c01] : 0.0;
         const double x2 = v10 ? u[c10] : 0.0, x3 = v11 ? u[c11] : 0.0;
         const bool jv = k0 + tig < L;
-        double bv[2];
+        double bv[NT];
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          const double t0 = raw[po[nt][0] + k0], t1 = raw[po[nt][1] + k0], t2 = raw[po[nt][2] + k0];
-          const double v = fma(co[nt][2], t2, fma(co[nt][1], t1, co[nt][0] * t0));
+        for (int nt = 0; nt < NT; ++nt) {
+          double v = co[nt][0] * raw[po[nt][0] + k0];
+#pragma unroll
+          for (int k = 1; k < KC; ++k) v = fma(co[nt][k], raw[po[nt][k] + k0], v);
           bv[nt] = (jv && sv[nt]) ? v : 0.0;
         }
         if (!(LRC_EXP & 4)) {
-        dmma1684(acc[0][0], x0, x1, bv[0]);
-        dmma1684(acc[0][1], x0, x1, bv[1]);
-        dmma1684(acc[1][0], x2, x3, bv[0]);
-        dmma1684(acc[1][1], x2, x3, bv[1]);
-        } else { acc[0][0][0] += x0 + bv[0]; acc[1][1][1] += x3 * bv[1]; }
-      }
-      // epilogue: frag (m, n) -> column n0 + mt*16 + gid (+8), slot nt*8 + 2 tig + e = 3 q + stream
-      const bool full_cols = n0 + 32 <= r;
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
+          for (int nt = 0; nt < NT; ++nt) {
+            dmma1684(acc[0][nt], x0, x1, bv[nt]);
+            dmma1684(acc[1][nt], x2, x3, bv[nt]);
+          }
+        } else { acc[0][0][0] += x0 + bv[0]; acc[1][0][1] += x3 * bv[NT - 1]; }
+      }
+      // epilogue: frag (m, n) -> column n0 + mt*16 + gid (+8), slot nt*8 + 2 tig + e = G q + group
+      const bool full_cols = n0 + 32 <= r;
+      const int s2g = GEN ? a.id_group : 0;       // the identity-diagonal group carries U - g W
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int Rs = nt * 8 + 2 * tig + e;
-          if (Rs >= 3 * g) continue;
-          const int q = Rs / 3, st = Rs - q * 3;
+          if (Rs >= G * g) continue;
+          const int q = Rs / G, st = Rs - q * G;
           const size_t row = (size_t)(row0 + q);
           double* orow = outq + st * sst + row * a.ldo + a.out_off + n0 + gid;
-          const bool s2 = (MODE == SPMM_S2STEP) && st == 0;
+          const bool s2 = (MODE == SPMM_S2STEP) && st == s2g;
           // the block's own U row (S2 epilogue) from the staged rows when present
           const double* us_ = (lrow0 >= 0) ? su + (size_t)(lrow0 + q) * ldu + n0 + gid : Uq + row * ldu + n0 + gid;
 #pragma unroll
@@ -1173,7 +1200,7 @@ bool tma_ok(const SpmmArgs& a, int rmax) {
     const double* u = a.nsub > 1 ? a.Us[q] : a.U;
     al = al && ((reinterpret_cast<uintptr_t>(u) & 15) == 0);
   }
-  for (int v = 0; v < 6; ++v) al = al && ((reinterpret_cast<uintptr_t>(a.v[v]) & 15) == 0);
+  for (int v = 0; v < (a.gen ? a.T : 6); ++v) al = al && ((reinterpret_cast<uintptr_t>(a.v[v]) & 15) == 0);
   return al;
 }
 
@@ -1190,9 +1217,27 @@ cudaError_t launch_m(const SpmmArgs& a0, int rmax, cudaStream_t s) {
     // persistent TMA-fed kernel: 16-byte aligned value arrays and U rows, tile records available
     if (tma_ok(a, rmax) && a.ntl_u > 0) {
       const int grid = min(a.ntl_u, max(1, sm_count() - max(0, a.reserved_sms)));
-      spmm_tma_kernel<MODE><<<grid, (kTCons + 1) * 32, tma_smem(), s>>>(a);
+      if (!a.gen) {
+        spmm_tma_kernel<MODE, false, 2, kTCons><<<grid, (kTCons + 1) * 32, tma_smem(6), s>>>(a);
+      } else {
+        const int nt = (5 * a.G + 7) / 8;          // slots (row, group) of a node block in n-tiles of 8
+        int kmax = 0;
+        for (int g = 0; g < a.G; ++g) kmax = max(kmax, a.gl_n[g]);
+        const int th = (kTConsGen + 1) * 32;
+        const size_t sm = tma_smem(a.T);
+        if (kmax <= 4) {
+          if (nt <= 2) spmm_tma_kernel<MODE, true, 2, kTConsGen, 4><<<grid, th, sm, s>>>(a);
+          else if (nt == 3) spmm_tma_kernel<MODE, true, 3, kTConsGen, 4><<<grid, th, sm, s>>>(a);
+          else spmm_tma_kernel<MODE, true, 4, kTConsGen, 4><<<grid, th, sm, s>>>(a);
+        } else {
+          if (nt <= 2) spmm_tma_kernel<MODE, true, 2, kTConsGen, 6><<<grid, th, sm, s>>>(a);
+          else if (nt == 3) spmm_tma_kernel<MODE, true, 3, kTConsGen, 6><<<grid, th, sm, s>>>(a);
+          else spmm_tma_kernel<MODE, true, 4, kTConsGen, 6><<<grid, th, sm, s>>>(a);
+        }
+      }
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
+      if (a.gen) return cudaSuccess;               // general term lists: TMA path only (host checks)
       if (a.ntl_g > 0) {
         a.tlist = a.tlist_g;
         for (int q = 0; q < max(1, a.nsub); ++q) {      // L2-gather tiles: one launch per subset
@@ -1257,7 +1302,15 @@ cudaError_t prep_m() {
   if constexpr (MODE == SPMM_S2STEP || MODE == SPMM_PLAIN3) {
     e = cudaFuncSetAttribute(spmm_u_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 75 * 1024);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(spmm_tma_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem());
+    const int mx = (int)std::max(tma_smem(6), tma_smem(kMaxT));
+    e = cudaFuncSetAttribute(spmm_tma_kernel<MODE, false, 2, kTCons>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    if (e != cudaSuccess) return e;
+#define LRC_TMA_ATTR(NT_, KC_)                                                                          \
+    e = cudaFuncSetAttribute(spmm_tma_kernel<MODE, true, NT_, kTConsGen, KC_>,                          \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, mx);                           \
+    if (e != cudaSuccess) return e;
+    LRC_TMA_ATTR(2, 4) LRC_TMA_ATTR(3, 4) LRC_TMA_ATTR(4, 4) LRC_TMA_ATTR(2, 6) LRC_TMA_ATTR(3, 6) LRC_TMA_ATTR(4, 6)
+#undef LRC_TMA_ATTR
     if (e != cudaSuccess) return e;
   }
   return e;

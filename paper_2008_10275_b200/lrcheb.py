@@ -32,6 +32,7 @@ EXPORTS = (
     "lrc_set_params", "lrc_solve", "lrc_apply_lowrank", "lrc_apply_dense", "lrc_truncate",
     "lrc_get_iterate", "lrc_last_kernel_ms", "lrc_kernel_launches", "lrc_set_profiling", "lrc_get_profile",
     "lrc_set_reserved_sms", "lrc_solve_wait", "lrc_workspace_bytes", "lrc_set_workspace", "lrc_solve_batch",
+    "lrc_set_operator_terms", "lrc_set_diagonals",
 )
 
 
@@ -70,6 +71,8 @@ def load_library(path: str = None) -> ctypes.CDLL:
     lib.lrc_version.restype = ctypes.c_char_p
     lib.lrc_set_operator.argtypes = [P, I64, I64, P, P, ctypes.POINTER(P), D, D, I32]
     lib.lrc_set_params.argtypes = [P, I64, P, P, I32]
+    lib.lrc_set_operator_terms.argtypes = [P, I64, I64, P, P, I32, ctypes.POINTER(P), I32, P, I32, I32]
+    lib.lrc_set_diagonals.argtypes = [P, I64, I32, P, I32]
     lib.lrc_solve.argtypes = [P, P, I64, P, I64, I64, ctypes.POINTER(SolveOpts), P, I64, P, I64, I32,
                               ctypes.POINTER(SolveInfo)]
     lib.lrc_apply_lowrank.argtypes = [P, P, I64, I64, P, I64, U32, D, I32]
@@ -95,7 +98,7 @@ def load_library(path: str = None) -> ctypes.CDLL:
     lib.lrc_get_profile.restype = I32
     for name in ("lrc_create", "lrc_set_operator", "lrc_set_params", "lrc_solve", "lrc_apply_lowrank",
                  "lrc_apply_dense", "lrc_truncate", "lrc_get_iterate", "lrc_solve_wait", "lrc_workspace_bytes",
-                 "lrc_set_workspace", "lrc_solve_batch"):
+                 "lrc_set_workspace", "lrc_solve_batch", "lrc_set_operator_terms", "lrc_set_diagonals"):
         getattr(lib, name).restype = I32
     return lib
 
@@ -208,6 +211,37 @@ class Context:
         self._check(self._lib.lrc_set_operator(self._h, M, nnz, rp, ci, arr, float(rho_f), float(lambda_s), where))
         self._keep = [k1, k2] + [v[2] for v in vs] if borrow else []
         self.M = M
+        self.G, self.T = 3, 6
+
+    def set_operator_terms(self, row_ptr, col_idx, vals: Sequence, coef, id_group: int, borrow: bool = False):
+        """General term list: L(S) = sum_g (sum_t coef[t, g] A_t) S diag(d_g); coef is T x G."""
+        rp, w1, k1 = _vec(row_ptr, np.int32)
+        ci, w2, k2 = _vec(col_idx, np.int32)
+        vs = [_vec(v, np.float64) for v in vals]
+        wheres = {w1, w2} | {v[1] for v in vs}
+        assert len(wheres) == 1, "all operator arrays must live in the same memory space"
+        where = wheres.pop()
+        if borrow:
+            assert where == LRC_MEM_DEVICE
+            where = LRC_MEM_DEVICE_BORROW
+        self._settle(*([k1, k2] + [v[2] for v in vs]))
+        C = np.ascontiguousarray(coef, dtype=np.float64)
+        T, G = C.shape
+        assert T == len(vs)
+        M = (k1.shape[0] if hasattr(k1, "shape") else len(k1)) - 1
+        arr = (ctypes.c_void_p * T)(*[v[0] for v in vs])
+        self._check(self._lib.lrc_set_operator_terms(self._h, M, k2.shape[0], rp, ci, T, arr, G, C.ctypes.data,
+                                                     int(id_group), where))
+        self._keep = [k1, k2] + [v[2] for v in vs] if borrow else []
+        self.M = M
+        self.G, self.T = G, T
+
+    def set_diagonals(self, diags):
+        """The G right diagonals (G x n) of a general term list."""
+        D = np.ascontiguousarray(diags, dtype=np.float64)
+        G, n = D.shape
+        self._check(self._lib.lrc_set_diagonals(self._h, n, G, D.ctypes.data, LRC_MEM_HOST))
+        self.n = n
 
     def set_params(self, d_mu, d_nu):
         pm, w1, k1 = _vec(d_mu, np.float64)
@@ -308,7 +342,7 @@ class Context:
     def apply_lowrank(self, U, mode: int = LRC_APPLY_PLAIN3, gamma: float = 0.0):
         pu, ldu, w, ku = _mat(U)
         r = ku.shape[1]
-        nout = 6 if mode == LRC_APPLY_SIX else 3
+        nout = getattr(self, "T", 6) if mode == LRC_APPLY_SIX else getattr(self, "G", 3)
         self._order(ku)
         if w == LRC_MEM_DEVICE:
             import torch

@@ -396,3 +396,113 @@ def test_counter_rng_is_pure_function():
     b = gen.counter_normal(0, 7, np.arange(500, 1000, dtype=np.uint64))
     assert np.array_equal(a[500:], b)
     assert abs(a.mean()) < 0.15 and abs(a.std() - 1.0) < 0.1
+
+
+# ------------------------------------------------------------------------------------------
+# restart (reading S8, "restarted once after 6 iterations"): after a restart at k0 the error
+# of an untruncated solve on a diagonal operator is p_j(Lambda) p_k0(Lambda) e_0 (Chebyshev error
+# polynomials composed), entry by entry
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("k0,N", [(3, 7), (6, 12), (1, 4)])
+def test_P1_restart_composes_error_polynomials(k0, N):
+    terms, Lam, BU, BV = diagonal_problem(seed=9)
+    lmin, lmax = Lam.min(), Lam.max()
+    res = orc.chebyshevt(terms, BU, BV, lmin, lmax, tau=0.0, R=BV.shape[0], N=N, restart_every=k0)
+    c, d = 0.5 * (lmax - lmin), 0.5 * (lmax + lmin)
+    S_star = (BU @ BV.T) / Lam
+    p = lambda j: cheb_T(j, (d - Lam) / c) / cheb_T(j, d / c)
+    for k in range(1, N + 1):
+        # k = q k0 + j updates: q completed cycles of k0 steps then j steps of a fresh cycle
+        q, j = divmod(k, k0)
+        err = p(k0) ** q * (p(j) if j else 1.0) * S_star
+        X = orc.dense_product(*res.iterates[k - 1])
+        assert np.linalg.norm(X - (S_star - err)) <= 1e-12 * np.linalg.norm(S_star), k
+
+
+# ------------------------------------------------------------------------------------------
+# generalized term lists -- the four-parameter operator, the
+# theta-scheme operator and the Picard operator
+# ------------------------------------------------------------------------------------------
+def _literal_terms(prob, P):
+    from synth import terms as st
+    mats = orc.csr_matrices(prob.M, prob.row_ptr, prob.col_idx, prob.vals)
+    cfg = prob.cfg
+    if cfg.kind == "fourparam":
+        return orc.term_list_fourparam(mats, P[:, 0], P[:, 1] * P[:, 3], P[:, 2], P[:, 3], *prob.refs)
+    if cfg.kind == "theta":
+        zero = sp.csr_matrix(mats[0].shape)
+        return orc.term_list_theta(mats[1:], prob.rho_f, prob.lambda_s, P[:, 0], P[:, 1], mats[0], zero,
+                                   st.RHO_S, st.DT, st.THETA)
+    return orc.term_list_picard(mats, prob.rho_f, prob.lambda_s, P[:, 0], P[:, 1], *prob.refs)
+
+
+@pytest.mark.parametrize("name", ["tiny4", "tinytheta", "tinypicard"])
+def test_f4_general_form_equals_the_papers_operator(name):
+    """The library's grouped form sum_g (sum_t C[t][g] A_t) S diag(d_g) (synth.terms) applies exactly the
+    operator of the paper written term by term (oracle term lists), on a dense S and in Kronecker form."""
+    from synth import terms as st
+    prob = st.make_term_problem(name)
+    P, D, BU, BV = prob.subset(0)
+    lit = _literal_terms(prob, P)
+    mats = orc.csr_matrices(prob.M, prob.row_ptr, prob.col_idx, prob.vals)
+    if prob.cfg.kind == "theta":     # the grouped form's first array is the assembled mass matrix
+        pass
+    grp = orc.term_list_general(mats, prob.coef, D)
+    rng = np.random.default_rng(4)
+    S = rng.standard_normal((prob.M, P.shape[0]))
+    a, b = orc.apply_dense(lit, S), orc.apply_dense(grp, S)
+    assert np.linalg.norm(a - b) <= 1e-13 * np.linalg.norm(a)
+    Ka, Kb = orc.kron_operator(lit), orc.kron_operator(grp)
+    assert abs(Ka - Kb).max() <= 1e-13 * abs(Ka).max()
+    assert np.all(D[prob.id_group] == 1.0)
+
+
+def test_f4_fourparam_diagonal_closed_form():
+    """Chebyshev error polynomial on a diagonal four-parameter operator: the eigenvalue of column j, entry
+    i, written out from P:478-482 (A0 + A1 (mu - mu_r) + A2 (nu rho - nurho_r) + A3 (lam - lam_r) + Jmu mu +
+    Jlam lam + Jrho rho, diagonal entries)."""
+    rng = np.random.default_rng(21)
+    M, n = 40, 6
+    a = [1.0 + 3.0 * rng.random(M)] + [rng.random(M) for _ in range(6)]
+    mats = [sp.diags(x).tocsr() for x in a]
+    mu, nu, lam, rho = (0.5 + 1.5 * rng.random(n) for _ in range(4))
+    refs = (0.5, 0.25, 0.5)
+    terms = orc.term_list_fourparam(mats, mu, nu * rho, lam, rho, *refs)
+    Lam = (a[0][:, None] + a[1][:, None] * (mu - refs[0])[None, :] + a[2][:, None] * (nu * rho - refs[1])[None, :]
+           + a[3][:, None] * (lam - refs[2])[None, :] + a[4][:, None] * mu[None, :] + a[5][:, None] * lam[None, :]
+           + a[6][:, None] * rho[None, :])
+    BU, BV = rng.standard_normal((M, 2)), rng.standard_normal((n, 2))
+    lmin, lmax = Lam.min(), Lam.max()
+    for N in (1, 3, 8):
+        res = orc.chebyshevt(terms, BU, BV, lmin, lmax, tau=0.0, R=n, N=N)
+        c, d = 0.5 * (lmax - lmin), 0.5 * (lmax + lmin)
+        S_star = (BU @ BV.T) / Lam
+        pN = cheb_T(N, (d - Lam) / c) / cheb_T(N, d / c)
+        X = orc.dense_product(res.U, res.V)
+        assert np.linalg.norm(X - (1.0 - pN) * S_star) <= 1e-13 * np.linalg.norm(S_star)
+
+
+def test_f4_theta_scheme_kronecker():
+    """theta-scheme operator = (1/dt) I (x) A_t + theta (Kronecker form of P:30-36), assembled independently."""
+    rng = np.random.default_rng(8)
+    M, n = 30, 4
+    mats = [sp.random(M, M, density=0.2, random_state=np.random.RandomState(i), format="csr") for i in range(6)]
+    mass_f, mass_s = sp.diags(rng.random(M)).tocsr(), sp.diags(rng.random(M)).tocsr()
+    d_mu, d_nu = rng.random(n), rng.random(n)
+    rho, lam, rho_s, dt, th = 1.3, 2.0, 0.7, 0.05, 0.6
+    terms = orc.term_list_theta(mats, rho, lam, d_mu, d_nu, mass_f, mass_s, rho_s, dt, th)
+    K = orc.kron_operator(terms).toarray()
+    I = np.eye(n)
+    ref = np.kron(I, (rho * mass_f + rho_s * mass_s).toarray() / dt)
+    F = (np.kron(I, mats[0].toarray()) + np.kron(np.diag(d_mu), mats[1].toarray()) + rho * np.kron(np.diag(d_nu), mats[2].toarray())
+         + rho * np.kron(I, mats[3].toarray()) + np.kron(np.diag(d_mu), mats[4].toarray()) + lam * np.kron(I, mats[5].toarray()))
+    assert np.abs(K - (ref + th * F)).max() <= 1e-13 * np.abs(ref + th * F).max()
+
+
+def test_f4_term_problems_generate():
+    from synth import terms as st
+    for name in ("tiny4", "tinytheta", "tinypicard"):
+        prob = st.make_term_problem(name)
+        assert len(prob.vals) == prob.coef.shape[0] and prob.coef.shape[1] == prob.diagonals(prob.params[:1]).shape[0]
+        assert 0 < prob.lam_min < prob.lam_max
+        assert max(int(np.count_nonzero(prob.coef[:, g])) for g in range(prob.coef.shape[1])) <= 6
