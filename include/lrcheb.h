@@ -185,6 +185,35 @@ lrc_status lrc_workspace_bytes(lrc_ctx *ctx, int64_t r_B, int64_t rank_cap, int6
                                size_t *bytes);
 lrc_status lrc_set_workspace(lrc_ctx *ctx, void *dev_ptr, size_t bytes);
 
+/* GMREST -- truncated restarted GMRES (named P:41, run P:513, "restarted
+ * once after 6 iterations" P:546; reading R14): GMRES(restart) on L(S) = B with every Krylov
+ * basis element and the iterate held as U V^T, T_{trunc_tol, rank_cap} applied after every
+ * operator application and every modified Gram-Schmidt / update step; the (restart+1) x restart
+ * Hessenberg least-squares problem is solved on the host.  Stops when the honest relative residual
+ * ||B - L(X)||_F / ||B||_F <= tol or after max_cycles restart cycles.  Outputs as lrc_solve (U_out
+ * M x rank_cap, V_out n x rank_cap, columns >= rank zero).  Host-synchronous (no graph): each Arnoldi
+ * step reads its coefficients back.  rank_cap <= 64, 1 <= restart <= 32, r_B >= 1. */
+typedef struct {
+  double trunc_tol;      /* tau of the truncation operator */
+  double tol;            /* stopping tolerance on the honest relative residual */
+  int64_t rank_cap;      /* R */
+  int64_t restart;       /* Arnoldi steps per cycle m */
+  int64_t max_cycles;    /* restart cycles */
+} lrc_gmres_opts;
+
+typedef struct {
+  int64_t cycles;              /* restart cycles run */
+  int64_t rank;                /* rank of X */
+  double rel_residual;         /* honest relative residual of X */
+  double b_norm;               /* ||B||_F */
+  int64_t *inner_steps;        /* caller array[max_cycles] or NULL: Arnoldi steps per cycle */
+  double *cycle_residuals;     /* caller array[max_cycles] or NULL: honest residual after each cycle */
+} lrc_gmres_info;
+
+lrc_status lrc_solve_gmres(lrc_ctx *ctx, const double *B_U, int64_t ld_bu, const double *B_V, int64_t ld_bv,
+                           int64_t r_B, const lrc_gmres_opts *opts, double *U_out, int64_t ld_u,
+                           double *V_out, int64_t ld_v, lrc_mem where, lrc_gmres_info *info);
+
 /* Test / bench hooks (same ctx state; where = HOST or DEVICE for all pointers of the call). */
 
 /* W = L-pieces of U (M x r, ld_u): mode LRC_APPLY_PLAIN3 / LRC_APPLY_S2STEP write M x 3r,

@@ -267,5 +267,89 @@ def chebyshevt(terms, BU, BV, lam_min: float, lam_max: float, tau: float, R: int
     return Result(Uk, Vk, ranks, sigmas, iterates, rho)
 
 
+# --------------------------------------------------------------------------------------------
+# GMREST: truncated restarted GMRES (named P:41, run P:513, restarted
+# once after 6 iterations P:546; algorithm text absent from the paper -- DESIGN.md reading R14:
+# Arnoldi with modified Gram-Schmidt on the low-rank iterates, every operator application and every
+# linear combination truncated by T, the small Hessenberg least-squares problem solved densely)
+# --------------------------------------------------------------------------------------------
+GMRES_BREAKDOWN = 1e-14     # h_{j+1,j} <= 1e-14 max_i |h_ij| counts as a breakdown (reading R14)
+
+
+def inner(U1: np.ndarray, V1: np.ndarray, U2: np.ndarray, V2: np.ndarray) -> float:
+    """Frobenius inner product <U1 V1^T, U2 V2^T> = tr((U1^T U2)(V2^T V1))."""
+    if U1.shape[1] == 0 or U2.shape[1] == 0:
+        return 0.0
+    return float(np.sum((U1.T @ U2) * (V1.T @ V2)))
+
+
+@dataclasses.dataclass
+class GmresResult:
+    U: np.ndarray
+    V: np.ndarray
+    cycles: int
+    inner_steps: List[int]              # Arnoldi steps per cycle
+    cycle_residuals: List[float]        # honest relative residual after every cycle
+    rel_residual: float
+    hessenbergs: List[np.ndarray]
+
+
+def gmrest(terms, BU, BV, tau: float, R: int, m: int, max_cycles: int, tol: float) -> GmresResult:
+    """Restarted GMRES(m) on L(X) = B with low-rank iterates (reading R14).  Per cycle:
+    R0 = T(B - L(X)), beta = ||R0||, V_1 = R0 / beta; for j = 1..m: W = T(L(V_j)); for i = 1..j:
+    h_ij = <W, V_i>, W = T(W - h_ij V_i); h_{j+1,j} = ||W||; V_{j+1} = W / h_{j+1,j} (stop at a
+    breakdown h_{j+1,j} <= 1e-14 max_i |h_ij|); y = argmin ||beta e_1 - H y||; X = T(... T(T(X + y_1 V_1) + y_2 V_2) ...).
+    Stops when the honest relative residual ||B - L(X)||_F / ||B||_F <= tol or after max_cycles."""
+    M, n = BU.shape[0], BV.shape[0]
+    XU, XV = np.zeros((M, 0)), np.zeros((n, 0))
+    steps, res, Hs = [], [], []
+    bnorm = frobenius_lowrank(BU, BV)
+    if bnorm == 0.0:
+        return GmresResult(XU, XV, 0, [], [], 0.0, [])
+    rho = 1.0
+    cyc = 0
+    for cyc in range(1, max_cycles + 1):
+        if XU.shape[1] == 0:
+            RU, RV, _ = truncate(BU, BV, tau, R)
+        else:
+            UL, VL = apply_lowrank(terms, XU, XV)
+            RU, RV, _ = truncate(np.hstack([BU, UL]), np.hstack([BV, -VL]), tau, R)
+        beta = frobenius_lowrank(RU, RV)
+        if beta == 0.0:
+            break
+        basis = [(RU, RV / beta)]
+        H = np.zeros((m + 1, m))
+        k = 0
+        for j in range(m):
+            Uj, Vj = basis[j]
+            UL, VL = apply_lowrank(terms, Uj, Vj)
+            WU, WV, _ = truncate(UL, VL, tau, R)
+            for i in range(j + 1):
+                Ui, Vi = basis[i]
+                h = inner(WU, WV, Ui, Vi)
+                H[i, j] = h
+                WU, WV, _ = truncate(np.hstack([WU, Ui]), np.hstack([WV, -h * Vi]), tau, R)
+            hn = frobenius_lowrank(WU, WV)
+            H[j + 1, j] = hn
+            k = j + 1
+            if hn <= GMRES_BREAKDOWN * np.max(np.abs(H[:j + 2, j])):   # (happy) breakdown
+                H[j + 1, j] = 0.0
+                break
+            basis.append((WU, WV / hn))
+        e1 = np.zeros(k + 1)
+        e1[0] = beta
+        y = np.linalg.lstsq(H[:k + 1, :k], e1, rcond=None)[0]
+        for j in range(k):
+            Uj, Vj = basis[j]
+            XU, XV, _ = truncate(np.hstack([XU, Uj]), np.hstack([XV, y[j] * Vj]), tau, R)
+        steps.append(k)
+        Hs.append(H[:k + 1, :k].copy())
+        rho = residual(terms, BU, BV, XU, XV)
+        res.append(rho)
+        if rho <= tol:
+            break
+    return GmresResult(XU, XV, cyc, steps, res, rho, Hs)
+
+
 def dense_product(U: np.ndarray, V: np.ndarray) -> np.ndarray:
     return U @ V.T

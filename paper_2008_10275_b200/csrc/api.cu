@@ -120,6 +120,8 @@ struct lrc_ctx {
   Workspace ws;
   void* user_ws = nullptr;  // caller-owned device arena for the workspace (lrc_set_workspace)
   size_t user_ws_bytes = 0;
+  double* gmU = nullptr; double* gmV = nullptr; size_t gm_cap = 0;   // GMREST Krylov basis (library-owned)
+  double* gmI = nullptr; double* gmP = nullptr; double* gmG = nullptr;   // identity T, Gram partials, Gram
   double* tmpA = nullptr; size_t tmpA_sz = 0;   // hook scratch (library-owned)
   double* tmpB = nullptr; size_t tmpB_sz = 0;
   double* tmpC = nullptr; size_t tmpC_sz = 0;
@@ -742,6 +744,7 @@ void lrc_destroy(lrc_ctx* ctx) {
     for (int t = 0; t < kMaxT; ++t) dfree(ctx->vals[t]);
   }
   dfree(ctx->tmpA); dfree(ctx->tmpB); dfree(ctx->tmpC);
+  dfree(ctx->gmU); dfree(ctx->gmV); dfree(ctx->gmI); dfree(ctx->gmP); dfree(ctx->gmG);
   dfree(ctx->group_ptr); dfree(ctx->tdesc); dfree(ctx->tlist_u); dfree(ctx->tlist_g); dfree(ctx->tile_ev); dfree(ctx->trec); dfree(ctx->tmeta); dfree(ctx->dtab);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
@@ -1702,6 +1705,352 @@ lrc_status lrc_get_iterate(lrc_ctx* ctx, int64_t k, double* U, double* V, int64_
   CK(cudaMemcpyAsync(V, Vk, sizeof(double) * n * cap, kind_out(where), s));
   CK(cudaStreamSynchronize(s));
   *rank = hr;
+  return LRC_OK;
+}
+
+}  // extern "C"
+
+// =============================================================================================
+// GMREST -- truncated restarted GMRES (restarted
+// once after 6 iterations P:546; reading R14).  The same building blocks as ChebyshevT: the
+// fused SpMM (PLAIN mode), the truncation operator T of P:544 (V-side QR, CholeskyQR2 + Jacobi), the
+// honest residual; plus Frobenius inner products of low-rank matrices, <U1 V1^T, U2 V2^T> =
+// tr((U1^T U2)(V2^T V1)), whose M-level part U1^T U2 is a Gram pass over [U1 | U2] with T = I.
+// Host-driven: the Arnoldi coefficients decide the next linear combination, so each step reads a few
+// scalars back (no graph).
+// =============================================================================================
+namespace {
+
+struct LR {                 // a low-rank matrix s * U V^T held in device buffers, rank in st.rk[slot]
+  double* U; double* V; int slot; double scale; int rank;
+};
+
+lrc_status gm_rank_sigma(lrc_ctx* ctx, int slot, int sigma_row, int& rank, double& fro) {
+  Workspace& w = ctx->ws;
+  State st = make_state(w);
+  int r = 0;
+  double sg[kSigmaStride];
+  CK(cudaMemcpyAsync(&r, st.rk + slot, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(sg, st.sigma + (size_t)sigma_row * kSigmaStride, sizeof(sg), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  double f = 0.0;
+  for (int i = 0; i < r; ++i) f += sg[i] * sg[i];
+  rank = r;
+  fro = std::sqrt(f);
+  return LRC_OK;
+}
+
+// out = T_{tau,cap}(sum_b scale_b * U_b V_b^T) over the given low-rank terms; out.scale = 1
+lrc_status gm_truncate(lrc_ctx* ctx, const std::vector<LR>& terms, double tau, int cap, LR& out, int sigma_row,
+                       double& fro) {
+  Workspace& w = ctx->ws;
+  UDesc ud{};
+  VDesc vd{};
+  ud.pad_even = 1; vd.pad_even = 1;
+  for (const LR& t : terms) {
+    ud.b[ud.nb++] = ublock(t.U, w.LDU, 0, t.slot);
+    vd.b[vd.nb++] = vblock(t.V, cap, 0, t.slot, t.scale, -1, 0);
+  }
+  lrc_status st = enqueue_truncation(ctx, ud, vd, nullptr, 0, tau, cap, out.slot, sigma_row, out.U, w.LDU, out.V, cap,
+                                     ctx->stream, false);
+  if (st != LRC_OK) return st;
+  out.scale = 1.0;
+  return gm_rank_sigma(ctx, out.slot, sigma_row, out.rank, fro);
+}
+
+// out = T(L(x)) (x.scale folded into the V side), through the grouped fused SpMM
+lrc_status gm_apply(lrc_ctx* ctx, const LR& x, double tau, int cap, LR& out, int sigma_row, double& fro) {
+  Workspace& w = ctx->ws;
+  State st = make_state(w);
+  cudaStream_t s = ctx->stream;
+  SpmmArgs a = spmm_base(ctx);
+  a.U = x.U; a.ldu = w.LDU; a.d_r = st.rk + x.slot; a.out = w.W3; a.ldo = w.LDU; a.out_off = 0;
+  a.out_sstride = (long long)ctx->M * w.LDU;
+  KL(P_SPMM, s, launch_spmm(SPMM_PLAIN3, a, cap, s));
+  UDesc ud{};
+  VDesc vd{};
+  ud.pad_even = 1; vd.pad_even = 1;
+  for (int g = 0; g < ctx->G; ++g) {
+    ud.b[ud.nb++] = ublock(w.W3 + (size_t)g * ctx->M * w.LDU, w.LDU, 0, x.slot);
+    vd.b[vd.nb++] = vblock(x.V, cap, 0, x.slot, x.scale, g == ctx->id_group ? -1 : g, 0);
+  }
+  lrc_status r = enqueue_truncation(ctx, ud, vd, nullptr, 0, tau, cap, out.slot, sigma_row, out.U, w.LDU, out.V, cap,
+                                    s, false);
+  if (r != LRC_OK) return r;
+  out.scale = 1.0;
+  return gm_rank_sigma(ctx, out.slot, sigma_row, out.rank, fro);
+}
+
+// <a, b>_F of two low-rank matrices (ranks known on the host)
+lrc_status gm_inner(lrc_ctx* ctx, const LR& a, const LR& b, int cap, double& out) {
+  out = 0.0;
+  if (a.rank == 0 || b.rank == 0) return LRC_OK;
+  Workspace& w = ctx->ws;
+  State st = make_state(w);
+  cudaStream_t s = ctx->stream;
+  const int ra = a.rank + (a.rank & 1), rbk = b.rank + (b.rank & 1);
+  const int wdt = ra + rbk, pmax = ts_pmax_for(wdt);
+  TsArgs ta{};
+  ta.M = (int)ctx->M;
+  ta.u.nb = 2; ta.u.pad_even = 1;
+  ta.u.b[0] = ublock(a.U, w.LDU, 0, a.slot);
+  ta.u.b[1] = ublock(b.U, w.LDU, 0, b.slot);
+  ta.rk = st.rk;
+  ta.T = ctx->gmI; ta.ldt = kMaxP;        // identity: X = [U_a | U_b], G = X^T X
+  ta.d_p = nullptr; ta.p_fixed = wdt;
+  ta.partials = ctx->gmP;
+  KL(P_TS_GRAM, s, launch_ts(0, ta, pmax, w.grid, s));
+  KL(P_REDUCE, s, launch_gram_reduce(ctx->gmP, w.grid, pmax, ctx->gmG, s));
+  std::vector<double> G((size_t)pmax * pmax), Va((size_t)ctx->n * cap), Vb((size_t)ctx->n * cap);
+  CK(cudaMemcpyAsync(G.data(), ctx->gmG, sizeof(double) * G.size(), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(Va.data(), a.V, sizeof(double) * Va.size(), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(Vb.data(), b.V, sizeof(double) * Vb.size(), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  // tr((U_a^T U_b)(V_b^T V_a)) = sum_{i,j} (U_a^T U_b)[i][j] (V_a^T V_b)[i][j]
+  double acc = 0.0;
+  for (int i = 0; i < a.rank; ++i)
+    for (int j = 0; j < b.rank; ++j) {
+      double vv = 0.0;
+      for (int64_t q = 0; q < ctx->n; ++q) vv += Va[(size_t)q * cap + i] * Vb[(size_t)q * cap + j];
+      acc += G[(size_t)i * pmax + ra + j] * vv;
+    }
+  out = acc * a.scale * b.scale;
+  return LRC_OK;
+}
+
+// y = argmin || beta e1 - H y ||  (H (k+1) x k upper Hessenberg, row-major ld m) by Givens rotations
+void gm_lsq(const std::vector<double>& Hin, int m, int k, double beta, std::vector<double>& y) {
+  std::vector<double> H(Hin), g(k + 1, 0.0);
+  g[0] = beta;
+  for (int j = 0; j < k; ++j) {
+    const double a = H[(size_t)j * m + j], b = H[(size_t)(j + 1) * m + j];
+    const double r = std::hypot(a, b);
+    const double c = r > 0 ? a / r : 1.0, sn = r > 0 ? b / r : 0.0;
+    for (int q = j; q < k; ++q) {
+      const double x = H[(size_t)j * m + q], z = H[(size_t)(j + 1) * m + q];
+      H[(size_t)j * m + q] = c * x + sn * z;
+      H[(size_t)(j + 1) * m + q] = -sn * x + c * z;
+    }
+    const double gx = g[j], gz = g[j + 1];
+    g[j] = c * gx + sn * gz;
+    g[j + 1] = -sn * gx + c * gz;
+  }
+  y.assign(k, 0.0);
+  for (int j = k - 1; j >= 0; --j) {
+    double acc = g[j];
+    for (int q = j + 1; q < k; ++q) acc -= H[(size_t)j * m + q] * y[q];
+    const double d = H[(size_t)j * m + j];
+    y[j] = d != 0.0 ? acc / d : 0.0;
+  }
+}
+
+// honest ||B - L(X)||_F^2 -> scal[1] (as the solve epilogue)
+lrc_status gm_residual2(lrc_ctx* ctx, const LR& x, int rb, int cap, double& r2) {
+  Workspace& w = ctx->ws;
+  State st = make_state(w);
+  cudaStream_t s = ctx->stream;
+  UDesc ud{};
+  VDesc vd{};
+  ud.pad_even = 1; vd.pad_even = 1;
+  ud.b[ud.nb++] = ublock(w.BUb, w.LDB, rb, -1);
+  vd.b[vd.nb++] = vblock(w.BV, rb, rb, -1, 1.0, -1, 0);
+  if (x.rank > 0) {
+    SpmmArgs a = spmm_base(ctx);
+    a.U = x.U; a.ldu = w.LDU; a.d_r = st.rk + x.slot; a.out = w.W3; a.ldo = w.LDU; a.out_off = 0;
+    a.out_sstride = (long long)ctx->M * w.LDU;
+    KL(P_SPMM, s, launch_spmm(SPMM_PLAIN3, a, cap, s));
+    for (int g = 0; g < ctx->G; ++g) {
+      ud.b[ud.nb++] = ublock(w.W3 + (size_t)g * ctx->M * w.LDU, w.LDU, 0, x.slot);
+      vd.b[vd.nb++] = vblock(x.V, cap, 0, x.slot, -x.scale, g == ctx->id_group ? -1 : g, 0);
+    }
+  }
+  lrc_status r = enqueue_norm2(ctx, ud, vd, 1, s);
+  if (r != LRC_OK) return r;
+  double sc[8];
+  CK(cudaMemcpyAsync(sc, w.scal, sizeof(sc), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  r2 = sc[1];
+  return LRC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+lrc_status lrc_solve_gmres(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const double* B_V, int64_t ld_bv,
+                           int64_t r_B, const lrc_gmres_opts* opts, double* U_out, int64_t ld_u, double* V_out,
+                           int64_t ld_v, lrc_mem where, lrc_gmres_info* info) {
+  if (!ctx) return LRC_ERR_ARG;
+  ctx->err.clear();
+  if (!ctx->op_set || !ctx->par_set) return fail(ctx, LRC_ERR_STATE, "lrc_solve_gmres before set_operator + params");
+  if (!opts) return fail(ctx, LRC_ERR_ARG, "null opts");
+  if (!valid_mem(where)) return fail(ctx, LRC_ERR_ARG, "bad lrc_mem");
+  const int64_t M = ctx->M, n = ctx->n;
+  const int cap = (int)opts->rank_cap, m = (int)opts->restart, maxc = (int)opts->max_cycles;
+  if (cap < 1 || cap > std::min<int64_t>(std::min(M, n), 64)) return fail(ctx, LRC_ERR_ARG, "rank_cap must be in [1, min(M, n, 64)]");
+  if (m < 1 || m > 32 || maxc < 1 || maxc > 1000) return fail(ctx, LRC_ERR_ARG, "restart in [1, 32], max_cycles in [1, 1000]");
+  if (!(opts->trunc_tol >= 0.0) || !(opts->tol >= 0.0)) return fail(ctx, LRC_ERR_ARG, "tolerances must be >= 0");
+  if (r_B < 1 || r_B > 64 || !B_U || !B_V || ld_bu < r_B || ld_bv < r_B) return fail(ctx, LRC_ERR_ARG, "bad B factors");
+  if (!U_out || !V_out || ld_u < cap || ld_v < cap) return fail(ctx, LRC_ERR_ARG, "bad outputs");
+  const int rb = (int)r_B;
+  const int wmax = std::max((rb + (rb & 1)) + ctx->G * (cap + (cap & 1)), (ctx->G) * (cap + (cap & 1)));
+  if (wmax > kMaxW || std::min<int64_t>(n, wmax) > 112) return fail(ctx, LRC_ERR_ARG, "r_B + G rank_cap too wide");
+  if (ctx->pending.active) {
+    lrc_status ps = finish_solve(ctx, nullptr);
+    if (ps != LRC_OK) return ps;
+  }
+  CK(cudaSetDevice(ctx->device));
+  // slots: 0 X, 1 W, 2 T (scratch), 3 .. 3 + m: the Krylov basis; sigma rows likewise
+  lrc_status st = ensure_ws_fit(ctx, rb, cap, m + 8, wmax, false);
+  if (st != LRC_OK) return st;
+  Workspace& w = ctx->ws;
+  cudaStream_t s = ctx->stream;
+  const size_t need = (size_t)(m + 1);
+  if (ctx->gm_cap < need || !ctx->gmU) {
+    dfree(ctx->gmU); dfree(ctx->gmV);
+    ctx->gmU = ctx->gmV = nullptr; ctx->gm_cap = 0;
+    CK(dalloc(&ctx->gmU, need * M * w.LDU));
+    CK(dalloc(&ctx->gmV, need * n * cap));
+    ctx->gm_cap = need;
+  }
+  if (!ctx->gmI) {
+    std::vector<double> I((size_t)kMaxP * kMaxP, 0.0);
+    for (int i = 0; i < kMaxP; ++i) I[(size_t)i * kMaxP + i] = 1.0;
+    CK(dalloc(&ctx->gmI, I.size()));
+    CK(cudaMemcpy(ctx->gmI, I.data(), sizeof(double) * I.size(), cudaMemcpyHostToDevice));
+    CK(dalloc(&ctx->gmP, (size_t)148 * kMaxP * kMaxP));
+    CK(dalloc(&ctx->gmG, (size_t)kMaxP * kMaxP));
+  }
+  State sd = make_state(w);
+  CK(cudaMemsetAsync(w.ints, 0, sizeof(int) * (w.N + 16), s));
+  CK(cudaMemsetAsync(w.scal, 0, sizeof(double) * 8, s));
+  CK(cudaMemsetAsync(w.sigma, 0, sizeof(double) * (size_t)(w.N + 4) * kSigmaStride, s));
+  CK(cudaMemcpy2DAsync(w.BUb, sizeof(double) * w.LDB, B_U, sizeof(double) * ld_bu, sizeof(double) * rb, M, kind_in(where), s));
+  CK(cudaMemcpy2DAsync(w.BV, sizeof(double) * rb, B_V, sizeof(double) * ld_bv, sizeof(double) * rb, n, kind_in(where), s));
+  CK(cudaMemcpyAsync(sd.rk + 0, &rb, sizeof(int), cudaMemcpyHostToDevice, s));     // slot 0 := r_B for B
+  // ||B||_F
+  double b2 = 0.0;
+  {
+    UDesc ub = ucat_desc(w, M, rb, -1, nullptr, -1, ctx->G);
+    VDesc vb{};
+    vb.nb = 1; vb.pad_even = 1;
+    vb.b[0] = vblock(w.BV, rb, rb, -1, 1.0, -1, 0);
+    st = enqueue_norm2(ctx, ub, vb, 0, s);
+    if (st != LRC_OK) return st;
+    double sc[8];
+    CK(cudaMemcpyAsync(sc, w.scal, sizeof(sc), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    b2 = sc[0];
+  }
+  const double bnorm = std::sqrt(b2);
+  const double tau = opts->trunc_tol;
+  LR X{w.Ubuf[0], w.Vbuf[0], 0, 1.0, 0};
+  CK(cudaMemsetAsync(sd.rk + 0, 0, sizeof(int), s));                               // X = 0
+  LR Wv{w.Ubuf[1], w.Vbuf[1], 1, 1.0, 0};
+  LR Tm{w.Ubuf[2], w.Vbuf[2], 2, 1.0, 0};
+  std::vector<LR> Vb(m + 1);
+  for (int j = 0; j <= m; ++j)
+    Vb[j] = LR{ctx->gmU + (size_t)j * M * w.LDU, ctx->gmV + (size_t)j * n * cap, 3 + j, 1.0, 0};
+  std::vector<int> steps;
+  std::vector<double> cres;
+  double rho = bnorm > 0 ? 1.0 : 0.0;
+  int cycles = 0;
+  const int srow = m + 6;           // sigma row for the scratch truncations
+  for (int c = 0; c < maxc && bnorm > 0; ++c) {
+    cycles = c + 1;
+    // R0 = T(B - L(X)) into the basis slot 0
+    double beta = 0.0;
+    {
+      UDesc ud{};
+      VDesc vd{};
+      ud.pad_even = 1; vd.pad_even = 1;
+      ud.b[ud.nb++] = ublock(w.BUb, w.LDB, rb, -1);
+      vd.b[vd.nb++] = vblock(w.BV, rb, rb, -1, 1.0, -1, 0);
+      if (X.rank > 0) {
+        SpmmArgs a = spmm_base(ctx);
+        a.U = X.U; a.ldu = w.LDU; a.d_r = sd.rk + X.slot; a.out = w.W3; a.ldo = w.LDU; a.out_off = 0;
+        a.out_sstride = (long long)M * w.LDU;
+        KL(P_SPMM, s, launch_spmm(SPMM_PLAIN3, a, cap, s));
+        for (int g = 0; g < ctx->G; ++g) {
+          ud.b[ud.nb++] = ublock(w.W3 + (size_t)g * M * w.LDU, w.LDU, 0, X.slot);
+          vd.b[vd.nb++] = vblock(X.V, cap, 0, X.slot, -X.scale, g == ctx->id_group ? -1 : g, 0);
+        }
+      }
+      st = enqueue_truncation(ctx, ud, vd, nullptr, 0, tau, cap, Vb[0].slot, srow, Vb[0].U, w.LDU, Vb[0].V, cap, s, false);
+      if (st != LRC_OK) return st;
+      st = gm_rank_sigma(ctx, Vb[0].slot, srow, Vb[0].rank, beta);
+      if (st != LRC_OK) return st;
+    }
+    if (beta == 0.0) { rho = 0.0; break; }
+    Vb[0].scale = 1.0 / beta;
+    std::vector<double> H((size_t)(m + 1) * m, 0.0);
+    int k = 0;
+    for (int j = 0; j < m; ++j) {
+      double fro = 0.0;
+      st = gm_apply(ctx, Vb[j], tau, cap, Wv, srow, fro);
+      if (st != LRC_OK) return st;
+      double hmax = 0.0;
+      for (int i = 0; i <= j; ++i) {
+        double h = 0.0;
+        st = gm_inner(ctx, Wv, Vb[i], cap, h);
+        if (st != LRC_OK) return st;
+        H[(size_t)i * m + j] = h;
+        hmax = std::max(hmax, std::fabs(h));
+        LR mi = Vb[i];
+        mi.scale = -h * Vb[i].scale;
+        st = gm_truncate(ctx, {Wv, mi}, tau, cap, Tm, srow, fro);
+        if (st != LRC_OK) return st;
+        std::swap(Wv.U, Tm.U); std::swap(Wv.V, Tm.V); std::swap(Wv.slot, Tm.slot);
+        Wv.rank = Tm.rank; Wv.scale = 1.0;
+      }
+      H[(size_t)(j + 1) * m + j] = fro;
+      k = j + 1;
+      if (fro <= 1e-14 * std::max(hmax, fro)) { H[(size_t)(j + 1) * m + j] = 0.0; break; }   // breakdown (R14)
+      // V_{j+1} = W / h_{j+1,j}: move W's factors into the basis slot
+      CK(cudaMemcpyAsync(Vb[j + 1].U, Wv.U, sizeof(double) * M * w.LDU, cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(Vb[j + 1].V, Wv.V, sizeof(double) * n * cap, cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(sd.rk + Vb[j + 1].slot, sd.rk + Wv.slot, sizeof(int), cudaMemcpyDeviceToDevice, s));
+      Vb[j + 1].rank = Wv.rank;
+      Vb[j + 1].scale = 1.0 / fro;
+    }
+    std::vector<double> y;
+    gm_lsq(H, m, k, beta, y);
+    for (int j = 0; j < k; ++j) {             // X = T(... T(X + y_1 V_1) ...)
+      LR vj = Vb[j];
+      vj.scale = y[j] * Vb[j].scale;
+      double fro = 0.0;
+      st = gm_truncate(ctx, {X, vj}, tau, cap, Tm, srow, fro);
+      if (st != LRC_OK) return st;
+      std::swap(X.U, Tm.U); std::swap(X.V, Tm.V); std::swap(X.slot, Tm.slot);
+      X.rank = Tm.rank; X.scale = 1.0;
+    }
+    steps.push_back(k);
+    double r2 = 0.0;
+    st = gm_residual2(ctx, X, rb, cap, r2);
+    if (st != LRC_OK) return st;
+    rho = std::sqrt(r2) / bnorm;
+    cres.push_back(rho);
+    if (rho <= opts->tol) break;
+  }
+  // outputs (columns >= rank zeroed)
+  KL(P_MISC, s, launch_zero_cols(X.U, (int)M, w.LDU, sd.rk + X.slot, 0, cap, s));
+  KL(P_MISC, s, launch_zero_cols(X.V, (int)n, cap, sd.rk + X.slot, 0, cap, s));
+  CK(cudaMemcpy2DAsync(U_out, sizeof(double) * ld_u, X.U, sizeof(double) * w.LDU, sizeof(double) * cap, M, kind_out(where), s));
+  CK(cudaMemcpy2DAsync(V_out, sizeof(double) * ld_v, X.V, sizeof(double) * cap, sizeof(double) * cap, n, kind_out(where), s));
+  int flags = 0;
+  CK(cudaMemcpyAsync(&flags, sd.flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  ctx->last_record = false;
+  if (info) {
+    info->cycles = cycles;
+    info->rank = X.rank;
+    info->rel_residual = rho;
+    info->b_norm = bnorm;
+    for (int c = 0; c < (int)steps.size() && info->inner_steps; ++c) info->inner_steps[c] = steps[c];
+    for (int c = 0; c < (int)cres.size() && info->cycle_residuals; ++c) info->cycle_residuals[c] = cres[c];
+  }
+  if (flags & 1) return fail(ctx, LRC_ERR_NUMERIC, "shifted Cholesky failed after all escalations");
+  if (flags & 2) return fail(ctx, LRC_ERR_NUMERIC, "non-finite singular value in the core SVD");
   return LRC_OK;
 }
 

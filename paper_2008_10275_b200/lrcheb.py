@@ -32,7 +32,7 @@ EXPORTS = (
     "lrc_set_params", "lrc_solve", "lrc_apply_lowrank", "lrc_apply_dense", "lrc_truncate",
     "lrc_get_iterate", "lrc_last_kernel_ms", "lrc_kernel_launches", "lrc_set_profiling", "lrc_get_profile",
     "lrc_set_reserved_sms", "lrc_solve_wait", "lrc_workspace_bytes", "lrc_set_workspace", "lrc_solve_batch",
-    "lrc_set_operator_terms", "lrc_set_diagonals",
+    "lrc_set_operator_terms", "lrc_set_diagonals", "lrc_solve_gmres",
 )
 
 
@@ -46,6 +46,17 @@ class SolveOpts(ctypes.Structure):
     _fields_ = [("lambda_min", ctypes.c_double), ("lambda_max", ctypes.c_double),
                 ("tol", ctypes.c_double), ("rank_cap", ctypes.c_int64), ("n_iter", ctypes.c_int64),
                 ("restart_every", ctypes.c_int64), ("flags", ctypes.c_uint32)]
+
+
+class GmresOpts(ctypes.Structure):
+    _fields_ = [("trunc_tol", ctypes.c_double), ("tol", ctypes.c_double), ("rank_cap", ctypes.c_int64),
+                ("restart", ctypes.c_int64), ("max_cycles", ctypes.c_int64)]
+
+
+class GmresInfo(ctypes.Structure):
+    _fields_ = [("cycles", ctypes.c_int64), ("rank", ctypes.c_int64), ("rel_residual", ctypes.c_double),
+                ("b_norm", ctypes.c_double), ("inner_steps", ctypes.POINTER(ctypes.c_int64)),
+                ("cycle_residuals", ctypes.POINTER(ctypes.c_double))]
 
 
 class SolveInfo(ctypes.Structure):
@@ -73,6 +84,8 @@ def load_library(path: str = None) -> ctypes.CDLL:
     lib.lrc_set_params.argtypes = [P, I64, P, P, I32]
     lib.lrc_set_operator_terms.argtypes = [P, I64, I64, P, P, I32, ctypes.POINTER(P), I32, P, I32, I32]
     lib.lrc_set_diagonals.argtypes = [P, I64, I32, P, I32]
+    lib.lrc_solve_gmres.argtypes = [P, P, I64, P, I64, I64, ctypes.POINTER(GmresOpts), P, I64, P, I64, I32,
+                                    ctypes.POINTER(GmresInfo)]
     lib.lrc_solve.argtypes = [P, P, I64, P, I64, I64, ctypes.POINTER(SolveOpts), P, I64, P, I64, I32,
                               ctypes.POINTER(SolveInfo)]
     lib.lrc_apply_lowrank.argtypes = [P, P, I64, I64, P, I64, U32, D, I32]
@@ -98,7 +111,8 @@ def load_library(path: str = None) -> ctypes.CDLL:
     lib.lrc_get_profile.restype = I32
     for name in ("lrc_create", "lrc_set_operator", "lrc_set_params", "lrc_solve", "lrc_apply_lowrank",
                  "lrc_apply_dense", "lrc_truncate", "lrc_get_iterate", "lrc_solve_wait", "lrc_workspace_bytes",
-                 "lrc_set_workspace", "lrc_solve_batch", "lrc_set_operator_terms", "lrc_set_diagonals"):
+                 "lrc_set_workspace", "lrc_solve_batch", "lrc_set_operator_terms", "lrc_set_diagonals",
+                 "lrc_solve_gmres"):
         getattr(lib, name).restype = I32
     return lib
 
@@ -292,6 +306,36 @@ class Context:
                    ms_total=info.ms_total, rank_history=list(rh), jacobi_sweeps=info.jacobi_sweeps, chol2_cycles=list(info.chol2_cycles),
                    sigma_history=np.frombuffer(sh, dtype=np.float64).reshape(n_iter, SIGMA_STRIDE).copy())
         return Uo, Vo, res
+
+    def solve_gmres(self, B_U, B_V, trunc_tol: float, tol: float, rank_cap: int, restart: int = 6,
+                    max_cycles: int = 10, out=None):
+        """GMREST (lrc_solve_gmres): truncated restarted GMRES.  Returns (U, V, info)."""
+        pu, ldbu, w1, ku = _mat(B_U)
+        pv, ldbv, w2, kv = _mat(B_V)
+        assert w1 == w2
+        self._order(ku, kv)
+        if out is None:
+            if w1 == LRC_MEM_DEVICE:
+                import torch
+                Uo = torch.empty((self.M, rank_cap), dtype=torch.float64, device=ku.device)
+                Vo = torch.empty((self.n, rank_cap), dtype=torch.float64, device=ku.device)
+            else:
+                Uo, Vo = np.empty((self.M, rank_cap)), np.empty((self.n, rank_cap))
+        else:
+            Uo, Vo = out
+        pUo, lduo, _, _ = _mat(Uo)
+        pVo, ldvo, _, _ = _mat(Vo)
+        opts = GmresOpts(float(trunc_tol), float(tol), int(rank_cap), int(restart), int(max_cycles))
+        steps = (ctypes.c_int64 * max_cycles)()
+        cres = (ctypes.c_double * max_cycles)()
+        info = GmresInfo()
+        info.inner_steps = ctypes.cast(steps, ctypes.POINTER(ctypes.c_int64))
+        info.cycle_residuals = ctypes.cast(cres, ctypes.POINTER(ctypes.c_double))
+        self._check(self._lib.lrc_solve_gmres(self._h, pu, ldbu, pv, ldbv, ku.shape[1], ctypes.byref(opts), pUo, lduo,
+                                              pVo, ldvo, w1, ctypes.byref(info)))
+        c = int(info.cycles)
+        return Uo, Vo, dict(cycles=c, rank=info.rank, rel_residual=info.rel_residual, b_norm=info.b_norm,
+                            inner_steps=list(steps)[:c], cycle_residuals=list(cres)[:c])
 
     def solve_async(self, B_U, B_V, lambda_min: float, lambda_max: float, tol: float, rank_cap: int,
                     n_iter: int, out, restart_every: int = 0, warm_start: bool = True):

@@ -506,3 +506,79 @@ def test_f4_term_problems_generate():
         assert len(prob.vals) == prob.coef.shape[0] and prob.coef.shape[1] == prob.diagonals(prob.params[:1]).shape[0]
         assert 0 < prob.lam_min < prob.lam_max
         assert max(int(np.count_nonzero(prob.coef[:, g])) for g in range(prob.coef.shape[1])) <= 6
+
+
+# ------------------------------------------------------------------------------------------
+# GMREST (reading R14) against things other than itself
+# ------------------------------------------------------------------------------------------
+def _small_operator(seed=3, M=24, n=4):
+    rng = np.random.default_rng(seed)
+    base = sp.random(M, M, density=0.25, random_state=np.random.RandomState(seed), format="csr")
+    mats = [(base + base.T) * 0.2 + sp.identity(M, format="csr") * 3.0]
+    mats += [sp.random(M, M, density=0.2, random_state=np.random.RandomState(seed + i), format="csr") * 0.3
+             for i in range(1, 6)]
+    d_mu, d_nu = 0.5 + rng.random(n), 0.5 + rng.random(n)
+    terms = orc.term_list(mats, 1.0, 2.0, d_mu, d_nu)
+    BU, BV = rng.standard_normal((M, 2)), rng.standard_normal((n, 2))
+    return terms, BU, BV
+
+
+def test_f3_gmrest_untruncated_is_restarted_gmres():
+    """tau = 0, R = n (no effective truncation): every cycle equals textbook restarted GMRES(m) on the
+    vectorized system vec(L(S)) = vec(B), written here as a plain Arnoldi/least squares."""
+    terms, BU, BV = _small_operator()
+    M, n = BU.shape[0], BV.shape[0]
+    K = orc.kron_operator(terms).toarray()
+    b = orc.vec(BU @ BV.T)
+    m, cycles = 5, 3
+    res = orc.gmrest(terms, BU, BV, 0.0, n, m, cycles, 0.0)
+    x = np.zeros(M * n)
+    for c in range(cycles):
+        r = b - K @ x
+        beta = np.linalg.norm(r)
+        Q = [r / beta]
+        H = np.zeros((m + 1, m))
+        for j in range(m):
+            w = K @ Q[j]
+            for i in range(j + 1):
+                H[i, j] = w @ Q[i]
+                w = w - H[i, j] * Q[i]
+            H[j + 1, j] = np.linalg.norm(w)
+            Q.append(w / H[j + 1, j])
+        e1 = np.zeros(m + 1)
+        e1[0] = beta
+        y = np.linalg.lstsq(H, e1, rcond=None)[0]
+        x = x + np.array(Q[:m]).T @ y
+        rel = np.linalg.norm(b - K @ x) / np.linalg.norm(b)
+        assert abs(res.cycle_residuals[c] - rel) <= 1e-9 * max(rel, 1e-12) + 1e-13, (c, res.cycle_residuals[c], rel)
+    X = orc.dense_product(res.U, res.V)
+    assert np.linalg.norm(orc.vec(X) - x) <= 1e-10 * np.linalg.norm(x)
+
+
+def test_f3_gmrest_first_cycle_is_krylov_minimal():
+    """The first cycle minimises the residual over the Krylov space span{b, Kb, ..., K^{m-1} b}
+    (brute force: least squares over the explicit Krylov matrix)."""
+    terms, BU, BV = _small_operator(seed=5)
+    n = BV.shape[0]
+    K = orc.kron_operator(terms).toarray()
+    b = orc.vec(BU @ BV.T)
+    for m in (1, 2, 4):
+        res = orc.gmrest(terms, BU, BV, 0.0, n, m, 1, 0.0)
+        Kr = np.array([np.linalg.matrix_power(K, i) @ b for i in range(m)]).T
+        y = np.linalg.lstsq(K @ Kr, b, rcond=None)[0]
+        best = np.linalg.norm(b - K @ Kr @ y) / np.linalg.norm(b)
+        assert abs(res.cycle_residuals[0] - best) <= 1e-9 * best + 1e-14, (m, res.cycle_residuals[0], best)
+
+
+def test_f3_gmrest_identity_and_zero_rhs():
+    rng = np.random.default_rng(1)
+    M, n = 20, 3
+    I = sp.identity(M, format="csr")
+    Z = sp.csr_matrix((M, M))
+    terms = orc.term_list([2.0 * I, Z, Z, Z, Z, Z], 1.0, 2.0, rng.random(n), rng.random(n))
+    BU, BV = rng.standard_normal((M, 2)), rng.standard_normal((n, 2))
+    res = orc.gmrest(terms, BU, BV, 0.0, n, 6, 2, 1e-14)
+    assert res.cycles == 1 and res.inner_steps == [1]            # breakdown after one step: exact
+    assert np.linalg.norm(orc.dense_product(res.U, res.V) - 0.5 * BU @ BV.T) <= 1e-14 * np.linalg.norm(BU @ BV.T)
+    res0 = orc.gmrest(terms, np.zeros((M, 1)), np.zeros((n, 1)), 0.0, n, 6, 2, 1e-12)
+    assert res0.cycles == 0 and res0.U.shape[1] == 0
