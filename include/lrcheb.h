@@ -67,6 +67,8 @@ typedef enum { LRC_MEM_HOST = 0, LRC_MEM_DEVICE = 1, LRC_MEM_DEVICE_BORROW = 2 }
                                         previous iteration's right singular basis when p == n) */
 #define LRC_ASYNC               16u  /* DEVICE inputs/outputs only: lrc_solve returns once the work is
                                         enqueued on ctx's stream; lrc_solve_wait completes the call */
+#define LRC_PRECONDITIONED      32u  /* iterate on P^{-1} L with the mean-based preconditioner of
+                                        lrc_set_preconditioner (lambda_min/max then bound P^{-1} L) */
 
 /* lrc_apply_lowrank modes */
 #define LRC_APPLY_PLAIN3  0u  /* W = [W0 | W1 | W2], W0 = (A0+rho Jrho+lam Jlam)U, W1 = (A1+Jmu)U, W2 = rho A2 U */
@@ -112,6 +114,21 @@ lrc_status lrc_set_diagonals(lrc_ctx *ctx, int64_t n, int G, const double *diags
 /* The subset's parameters: d_mu, d_nu of length n (finite). where: HOST or DEVICE. */
 lrc_status lrc_set_params(lrc_ctx *ctx, int64_t n, const double *d_mu, const double *d_nu,
                           lrc_mem where);
+
+/* Mean-based preconditioner ("Preconditioner"): P_T = the operator's
+ * block at the midpoint of the subset's parameter range, P_T = sum_t c_t A_t * (min e_t + max e_t) / 2
+ * over the current parameters (lrc_set_params / lrc_set_diagonals; setting them again discards the
+ * preconditioner).  A solve with LRC_PRECONDITIONED runs
+ *     X_{k+1} = T( w [X_k + gamma P_T^{-1}(B - L(X_k))] + (1 - w) X_{k-1} ),
+ * the factor concatenation [P^{-1}B_U | U_k - gamma P^{-1}W0 | P^{-1}W1 | ... | U_{k-1}], with
+ * lambda_min/lambda_max bounding the spectrum of P_T^{-1} L; info->rel_residual stays the
+ * unpreconditioned ||B - L(X_N)||_F / ||B||_F.  The paper applies P_T^{-1} by a permuted LU;
+ * here every P_T^{-1} R is inner_steps steps of a Chebyshev semi-iteration on P_T with its spectrum in
+ * [p_min, p_max] (reading R15: error <= 2 q^inner_steps with
+ * q = (sqrt(p_max) - sqrt(p_min)) / (sqrt(p_max) + sqrt(p_min)) relative to ||P_T^{-1} R||, for P_T
+ * symmetric positive definite).  0 < p_min <= p_max, 1 <= inner_steps <= 1000; LRC_ERR_STATE before
+ * the operator and parameters are set. */
+lrc_status lrc_set_preconditioner(lrc_ctx *ctx, double p_min, double p_max, int64_t inner_steps);
 
 typedef struct {
   double lambda_min, lambda_max;  /* spectrum bounds [d-c, d+c] (reading S2); 0 < min <= max */

@@ -208,14 +208,40 @@ class Result:
     rel_residual: float
 
 
-def chebyshevt_step(terms, BU, BV, Uk, Vk, Ukm1, Vkm1, omega: float, gamma: float, tau: float, R: int):
-    """One update X_{k+1} = T( w [X_k + gamma (B - L(X_k))] + (1 - w) X_{k-1} ) via the literal
-    six-term concatenation  U = [B_U | U_k | A_0U_k ... A_5U_k | U_{k-1}],
-    V = [w gamma B_V | w V_k | -w gamma c_t e_t*V_k ... | (1-w) V_{k-1}]  (empty blocks dropped)."""
+# --------------------------------------------------------------------------------------------
+# mean-based preconditioner (PAPER.md P:332-343 section "Preconditioner", LU-applied
+# P:544 "the preconditioners were decomposed into a permuted LU decomposition")
+# --------------------------------------------------------------------------------------------
+def mean_preconditioner(terms) -> sp.csr_matrix:
+    """P_T = A(x, mu_bar, nu_bar): the operator's block at the midpoint of the subset's
+    parameter range, mu_bar = (min mu + max mu) / 2 (likewise nu); every right diagonal e_t of the
+    term list is a parameter (or 1), so its midpoint is e_t at the mean parameters."""
+    P = None
+    for c, A, e in terms:
+        eb = 0.5 * (float(np.min(e)) + float(np.max(e)))
+        P = c * eb * A if P is None else P + c * eb * A
+    return P.tocsc()
+
+
+def lu_solver(P):
+    """Z = P^{-1} R by a sparse permuted LU decomposition (SuperLU)."""
+    import scipy.sparse.linalg as spla
+    lu = spla.splu(sp.csc_matrix(P))
+    return lambda R: lu.solve(np.asarray(R, dtype=np.float64)) if R.shape[1] > 0 else R
+
+
+def chebyshevt_step(terms, BU, BV, Uk, Vk, Ukm1, Vkm1, omega: float, gamma: float, tau: float, R: int,
+                    pinv=None):
+    """One update X_{k+1} = T( w [X_k + gamma P^{-1}(B - L(X_k))] + (1 - w) X_{k-1} ) via the literal
+    six-term concatenation  U = [P^{-1}B_U | U_k | P^{-1}A_0U_k ... P^{-1}A_5U_k | U_{k-1}],
+    V = [w gamma B_V | w V_k | -w gamma c_t e_t*V_k ... | (1-w) V_{k-1}]  (empty blocks dropped;
+    pinv = None: unpreconditioned, P = I).  (P^{-1}B_U may be passed in already applied.)"""
     Ublocks = [BU]
     Vblocks = [omega * gamma * BV]
     if Uk.shape[1] > 0:
         UL, VL = apply_lowrank(terms, Uk, Vk)
+        if pinv is not None:
+            UL = pinv(UL)
         Ublocks += [Uk, UL]
         Vblocks += [omega * Vk, -omega * gamma * VL]
     if Ukm1.shape[1] > 0:
@@ -237,12 +263,17 @@ def residual(terms, BU, BV, U, V) -> float:
 
 def chebyshevt(terms, BU, BV, lam_min: float, lam_max: float, tau: float, R: int, N: int,
                record_iterates: bool = True, final_residual: bool = True,
-               restart_every: Optional[int] = None, on_iterate=None) -> Result:
+               restart_every: Optional[int] = None, on_iterate=None, precond=None) -> Result:
     """N updates X_1..X_N from X_0 = X_{-1} = 0 (readings S6, S7).  Optional restart (S8,
     P:546 'restarted once after 6 iterations'): the w sequence restarts with X_{-1} := X_k.
     on_iterate(k, U_k, V_k, sigma) (optional, no arithmetic) sees every X_k as it is produced,
-    so a caller can keep selected iterates of a long solve without recording all of them."""
+    so a caller can keep selected iterates of a long solve without recording all of them.
+    precond = P_T: the preconditioned iteration on P^{-1} L with the
+    spectrum bounds [lam_min, lam_max] of P^{-1} L, P^{-1} by LU (lu_solver); the reported residual
+    stays the honest unpreconditioned ||B - L(X_N)|| / ||B||."""
     M, n = BU.shape[0], BV.shape[0]
+    pinv = lu_solver(precond) if precond is not None else None
+    BU_step = pinv(BU) if pinv is not None else BU
     c, d = chebyshev_cd(lam_min, lam_max)
     gamma = 1.0 / d
     w_all = omegas(lam_min, lam_max, N)
@@ -254,7 +285,7 @@ def chebyshevt(terms, BU, BV, lam_min: float, lam_max: float, tau: float, R: int
         if restart_every and k > 0 and k % restart_every == 0:
             j = 0
             Ukm1, Vkm1 = Uk, Vk
-        Un, Vn, s = chebyshevt_step(terms, BU, BV, Uk, Vk, Ukm1, Vkm1, w_all[j], gamma, tau, R)
+        Un, Vn, s = chebyshevt_step(terms, BU_step, BV, Uk, Vk, Ukm1, Vkm1, w_all[j], gamma, tau, R, pinv)
         j += 1
         Ukm1, Vkm1, Uk, Vk = Uk, Vk, Un, Vn
         ranks.append(Un.shape[1])

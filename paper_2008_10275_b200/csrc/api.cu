@@ -61,9 +61,10 @@ struct Workspace {
 };
 
 enum ProfClass { P_SPMM = 0, P_VSIDE, P_TS_GRAM, P_REDUCE, P_CHOL1, P_CHOL2, P_TS_STORE, P_TRACE,
-                 P_MISC, P_TINY, P_TS_GRAM2, P_NCLASS };
+                 P_MISC, P_TINY, P_TS_GRAM2, P_PREC, P_NCLASS };
 const char* const kProfNames[P_NCLASS] = {"spmm", "vside_qr", "ts_gram", "gram_reduce", "chol1",
-                                          "chol2_svd", "ts_store", "trace", "misc", "tiny_gemm", "ts_gram2"};
+                                          "chol2_svd", "ts_store", "trace", "misc", "tiny_gemm", "ts_gram2",
+                                          "precond"};
 
 struct Pending {             // a solve enqueued by lrc_solve (completed by finish_solve)
   bool active = false;
@@ -79,9 +80,10 @@ struct Pending {             // a solve enqueued by lrc_solve (completed by fini
 
 struct GraphKey {
   int64_t gen = -1, N = 0; int rb = 0, cap = 0; double gamma = 0, tol = 0; uint32_t flags = 0;
+  int64_t pc_gen = 0;
   bool operator==(const GraphKey& o) const {
     return gen == o.gen && N == o.N && rb == o.rb && cap == o.cap && gamma == o.gamma &&
-           tol == o.tol && flags == o.flags;
+           tol == o.tol && flags == o.flags && pc_gen == o.pc_gen;
   }
 };
 
@@ -120,6 +122,15 @@ struct lrc_ctx {
   Workspace ws;
   void* user_ws = nullptr;  // caller-owned device arena for the workspace (lrc_set_workspace)
   size_t user_ws_bytes = 0;
+  // mean-based preconditioner: P_T values, its spectrum bounds, inner Chebyshev steps
+  bool pc_set = false, pc_active = false;
+  double pc_min = 0, pc_max = 0;
+  int pc_q = 0;
+  int64_t pc_gen = 0;
+  double* pvals = nullptr;
+  double* pcbuf = nullptr; size_t pcbuf_sz = 0;     // Z (3 rotating) + Y: 4 x (3 M LDU) + P^-1 B_U
+  double* pc_zero = nullptr;                        // zero diagonals for the dense P application
+  std::vector<double> hdtab;                        // host copy of the right-diagonal table (G x n)
   double* gmU = nullptr; double* gmV = nullptr; size_t gm_cap = 0;   // GMREST Krylov basis (library-owned)
   double* gmI = nullptr; double* gmP = nullptr; double* gmG = nullptr;   // identity T, Gram partials, Gram
   double* tmpA = nullptr; size_t tmpA_sz = 0;   // hook scratch (library-owned)
@@ -528,11 +539,12 @@ UBlock ublock(const double* p, int ld, int w_fixed, int w_idx) {
 }
 
 // Ucat = [B_U | W0' | W1 | W2 | extra]: the three W blocks have width rk[ridx]
-UDesc ucat_desc(const Workspace& w, int64_t M, int rb, int ridx, const double* extra, int extra_idx, int G) {
+UDesc ucat_desc(const Workspace& w, int64_t M, int rb, int ridx, const double* extra, int extra_idx, int G,
+                const double* bu = nullptr) {
   UDesc u{};
   u.nb = 0;
   u.pad_even = 1;      // every block at an even column: 16-byte Ucat copies in the ts kernels
-  u.b[u.nb++] = ublock(w.BUb, w.LDB, rb, -1);
+  u.b[u.nb++] = ublock(bu ? bu : w.BUb, w.LDB, rb, -1);
   if (ridx >= 0)
     for (int t = 0; t < G; ++t) u.b[u.nb++] = ublock(w.W3 + (size_t)t * M * w.LDU, w.LDU, 0, ridx);
   if (extra) u.b[u.nb++] = ublock(extra, w.LDU, 0, extra_idx);
@@ -565,6 +577,8 @@ SpmmArgs iteration_spmm_args(lrc_ctx* ctx, int k, double gamma) {
 
 // The truncation of iteration k (a2-a6) once W3 holds K1's output; the V-side assembly forks from
 // ctx->ev_fork (recorded when U_k / V_k became final) onto the side stream.
+const double* pc_pbu(lrc_ctx* ctx);
+
 lrc_status enqueue_iteration_trunc(lrc_ctx* ctx, int k, int rb, int cap, double gamma, double tol, bool record) {
   Workspace& w = ctx->ws;
   cudaStream_t s = ctx->stream;
@@ -583,7 +597,7 @@ lrc_status enqueue_iteration_trunc(lrc_ctx* ctx, int k, int rb, int cap, double 
     vd.b[vd.nb++] = (g == ctx->id_group) ? vblock(Vcur, cap, 0, k + 1, 1.0, -1, 1)
                                           : vblock(Vcur, cap, 0, k + 1, -gamma, g, 1);
   vd.b[vd.nb++] = vblock(Vprev, cap, 0, k, 1.0, -1, 2);
-  const UDesc ud = ucat_desc(w, ctx->M, rb, k + 1, Uprev, k, ctx->G);
+  const UDesc ud = ucat_desc(w, ctx->M, rb, k + 1, Uprev, k, ctx->G, ctx->pc_active ? pc_pbu(ctx) : nullptr);
   lrc_status r = enqueue_truncation(ctx, ud, vd, w.omega, k, tol, cap, k + 2, k, Unext, w.LDU,
                                     Vnext, cap, s, true, ctx->warm_start);
   if (r != LRC_OK) return r;
@@ -596,13 +610,86 @@ lrc_status enqueue_iteration_trunc(lrc_ctx* ctx, int k, int rb, int cap, double 
   return LRC_OK;
 }
 
+std::vector<double> omega_schedule(double lmin, double lmax, int N, int restart);
+
+// Z / Y buffer size of the inner solve: three U-sized blocks (the G <= 6 W blocks go through in
+// slices of <= 3) or one B_U block
+size_t pc_block(lrc_ctx* ctx) {
+  return (size_t)ctx->M * std::max(3 * ctx->ws.LDU, ctx->ws.LDB);
+}
+
+// ---- Z = P_T^{-1} R by an inner Chebyshev semi-iteration on P_T (q steps, spectrum
+//      bounds [pc_min, pc_max]; reading R15): nb blocks of rows x ncols (ld, block stride bs)
+//      of R; the result goes to out (may alias R: the last step reads R before writing the element).
+lrc_status enqueue_pinv(lrc_ctx* ctx, const double* R, double* out, int nb, int rows, int ncols, int ld,
+                        long long bs, int r_fixed, const int* d_r, cudaStream_t s) {
+  const size_t blk = pc_block(ctx);                          // one rotating buffer (<= 3 blocks)
+  double* Z[3] = {ctx->pcbuf, ctx->pcbuf + blk, ctx->pcbuf + 2 * blk};
+  double* Y = ctx->pcbuf + 3 * blk;
+  const std::vector<double> om = omega_schedule(ctx->pc_min, ctx->pc_max, ctx->pc_q, 0);
+  const double g = 2.0 / (ctx->pc_min + ctx->pc_max);
+  int zc = 0, zp = 1, zn = 2;
+  for (int j = 0; j < ctx->pc_q; ++j) {
+    double* dst = (j == ctx->pc_q - 1) ? out : Z[zn];
+    if (j > 0) {                                             // Y = P Z_c, one dense application per block
+      for (int b = 0; b < nb; ++b) {
+        SpmmArgs a = spmm_base(ctx);
+        a.gen = 0;
+        for (int t = 0; t < 6; ++t) a.v[t] = ctx->pvals;
+        a.rho = 0.0; a.lam = 0.0; a.dmu = ctx->pc_zero; a.dnu = ctx->pc_zero;
+        a.U = Z[zc] + (size_t)b * bs; a.ldu = ld; a.d_r = d_r; a.r_fixed = r_fixed;
+        a.out = Y + (size_t)b * bs; a.ldo = ld; a.out_off = 0;
+        KL(P_PREC, s, launch_spmm(SPMM_DENSE, a, ncols, s));
+      }
+    }
+    KL(P_PREC, s, launch_cheb_inner(nb, rows, ncols, ld, bs, R, Y, Z[zc], j == 1 ? nullptr : Z[zp], dst, om[j], g,
+                                    j == 0 ? 1 : 0, d_r, r_fixed, s));
+    const int t = zp; zp = zc; zc = zn; zn = t;
+  }
+  return LRC_OK;
+}
+
+const double* pc_pbu(lrc_ctx* ctx) {                         // P^{-1} B_U (M x LDB) after the buffers
+  return ctx->pcbuf + 4 * pc_block(ctx);
+}
+
+// the preconditioner's buffers for the current workspace shape
+lrc_status ensure_pc_buffers(lrc_ctx* ctx) {
+  const size_t need = 4 * pc_block(ctx) + (size_t)ctx->M * ctx->ws.LDB;
+  if (ctx->pcbuf_sz < need || !ctx->pcbuf) {
+    cudaStreamSynchronize(ctx->stream);
+    dfree(ctx->pcbuf);
+    ctx->pcbuf = nullptr; ctx->pcbuf_sz = 0;
+    CK(dalloc(&ctx->pcbuf, need));
+    CK(cudaMemset(ctx->pcbuf, 0, sizeof(double) * need));
+    ctx->pcbuf_sz = need;
+    drop_graph(ctx);
+  }
+  return LRC_OK;
+}
+
 // One ChebyshevT iteration k: X_k -> X_{k+1}.
 lrc_status enqueue_iteration(lrc_ctx* ctx, int k, int rb, int cap, double gamma, double tol,
                              bool record) {
   cudaStream_t s = ctx->stream;
   CK(cudaEventRecord(ctx->ev_fork, s));
-  const SpmmArgs a = iteration_spmm_args(ctx, k, gamma);
-  KL(P_SPMM, s, launch_spmm(SPMM_S2STEP, a, cap, s));
+  if (!ctx->pc_active) {
+    const SpmmArgs a = iteration_spmm_args(ctx, k, gamma);
+    KL(P_SPMM, s, launch_spmm(SPMM_S2STEP, a, cap, s));
+  } else {
+    // preconditioned step (f2): W = L-pieces of U_k (plain), W <- P^{-1} W, W0 <- U_k - gamma W0
+    Workspace& w = ctx->ws;
+    const SpmmArgs a = iteration_spmm_args(ctx, k, gamma);
+    KL(P_SPMM, s, launch_spmm(SPMM_PLAIN3, a, cap, s));
+    const long long bs = (long long)ctx->M * w.LDU;
+    for (int g0 = 0; g0 < ctx->G; g0 += 3) {
+      const int nb = std::min(3, ctx->G - g0);
+      lrc_status r = enqueue_pinv(ctx, w.W3 + g0 * bs, w.W3 + g0 * bs, nb, (int)ctx->M, w.LDU, w.LDU, bs, cap, a.d_r, s);
+      if (r != LRC_OK) return r;
+    }
+    const size_t g0 = (size_t)ctx->id_group * ctx->M * w.LDU;
+    KL(P_PREC, s, launch_s2_update((int)ctx->M, w.LDU, w.LDU, w.Ubuf[(k + 1) % 3], w.LDU, w.W3 + g0, gamma, s));
+  }
   return enqueue_iteration_trunc(ctx, k, rb, cap, gamma, tol, record);
 }
 
@@ -745,6 +832,7 @@ void lrc_destroy(lrc_ctx* ctx) {
   }
   dfree(ctx->tmpA); dfree(ctx->tmpB); dfree(ctx->tmpC);
   dfree(ctx->gmU); dfree(ctx->gmV); dfree(ctx->gmI); dfree(ctx->gmP); dfree(ctx->gmG);
+  dfree(ctx->pvals); dfree(ctx->pcbuf); dfree(ctx->pc_zero);
   dfree(ctx->group_ptr); dfree(ctx->tdesc); dfree(ctx->tlist_u); dfree(ctx->tlist_g); dfree(ctx->tile_ev); dfree(ctx->trec); dfree(ctx->tmeta); dfree(ctx->dtab);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
@@ -1158,6 +1246,8 @@ lrc_status lrc_set_diagonals(lrc_ctx* ctx, int64_t n, int G, const double* diags
     CK(dalloc(&ctx->dtab, (size_t)kMaxG * n));
   }
   CK(cudaMemcpy(ctx->dtab, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+  ctx->hdtab = h;
+  ctx->pc_set = false;
   ctx->dmu = ctx->dnu = nullptr;
   ctx->n = n;
   ctx->par_set = true;
@@ -1191,10 +1281,60 @@ lrc_status lrc_set_params(lrc_ctx* ctx, int64_t n, const double* d_mu, const dou
   std::copy(hm.begin(), hm.end(), h.begin() + n);
   std::copy(hn.begin(), hn.end(), h.begin() + 2 * n);
   CK(cudaMemcpy(ctx->dtab, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+  ctx->hdtab = h;
+  ctx->pc_set = false;                             // the preconditioner follows the parameters
   ctx->dmu = ctx->dtab + n;
   ctx->dnu = ctx->dtab + 2 * n;
   ctx->n = n;
   ctx->par_set = true;
+  return LRC_OK;
+}
+
+// P_T = sum_t c_t A_t * mean(e_t) on the device, applied inside
+// the iteration by q steps of an inner Chebyshev semi-iteration on [p_min, p_max].
+lrc_status lrc_set_preconditioner(lrc_ctx* ctx, double p_min, double p_max, int64_t inner_steps) {
+  if (!ctx) return LRC_ERR_ARG;
+  ctx->err.clear();
+  if (!ctx->op_set || !ctx->par_set) return fail(ctx, LRC_ERR_STATE, "lrc_set_preconditioner before set_operator + parameters");
+  if (!(p_min > 0.0) || !(p_max >= p_min) || !std::isfinite(p_max))
+    return fail(ctx, LRC_ERR_ARG, "need 0 < p_min <= p_max");
+  if (inner_steps < 1 || inner_steps > 1000) return fail(ctx, LRC_ERR_ARG, "inner_steps must be in [1, 1000]");
+  CK(cudaSetDevice(ctx->device));
+  const int64_t n = ctx->n;
+  const int G = ctx->general ? ctx->G : 3;
+  if ((int64_t)ctx->hdtab.size() < (int64_t)G * n) return fail(ctx, LRC_ERR_STATE, "parameters not set");
+  double mid[kMaxG];
+  for (int g = 0; g < G; ++g) {                    // midpoint of each right diagonal's range
+    double lo = ctx->hdtab[(size_t)g * n], hi = lo;
+    for (int64_t i = 1; i < n; ++i) {
+      lo = std::min(lo, ctx->hdtab[(size_t)g * n + i]);
+      hi = std::max(hi, ctx->hdtab[(size_t)g * n + i]);
+    }
+    mid[g] = 0.5 * (lo + hi);
+  }
+  PvalArgs pa{};
+  int T;
+  if (!ctx->general) {                             // arrays [A0, A1, A2, Jrho, Jmu, Jlam], e_t means
+    T = 6;
+    const double e[6] = {1.0, mid[1], ctx->rho * mid[2], ctx->rho, mid[1], ctx->lam};
+    for (int t = 0; t < 6; ++t) { pa.v[t] = ctx->vals[t]; pa.e[t] = e[t]; }
+  } else {                                         // e_t = sum_g C[t][g] mean(d_g)
+    T = ctx->T;
+    for (int t = 0; t < T; ++t) { pa.v[t] = ctx->vals[t]; pa.e[t] = 0.0; }
+    for (int g = 0; g < ctx->G; ++g)
+      for (int k = 0; k < ctx->gl_n[g]; ++k) pa.e[ctx->gl_t[g][k]] += ctx->gl_c[g][k] * mid[g];
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (!ctx->pvals) CK(dalloc(&ctx->pvals, (size_t)std::max<int64_t>(ctx->nnz, 1)));
+  if (!ctx->pc_zero) {
+    CK(dalloc(&ctx->pc_zero, 256));
+    CK(cudaMemset(ctx->pc_zero, 0, sizeof(double) * 256));
+  }
+  CK(launch_form_pvals(pa, T, (long long)ctx->nnz, ctx->pvals, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->pc_min = p_min; ctx->pc_max = p_max; ctx->pc_q = (int)inner_steps;
+  ctx->pc_gen = next_gen();
+  ctx->pc_set = true;
   return LRC_OK;
 }
 
@@ -1243,6 +1383,8 @@ lrc_status solve_validate(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const 
     return fail(ctx, LRC_ERR_ARG, "n x (r_B + 4 rank_cap) too large for the single-CTA V-side QR");
   if ((opts->flags & LRC_ASYNC) && where != LRC_MEM_DEVICE)
     return fail(ctx, LRC_ERR_ARG, "LRC_ASYNC needs DEVICE inputs and outputs");
+  if ((opts->flags & LRC_PRECONDITIONED) && !ctx->pc_set)
+    return fail(ctx, LRC_ERR_STATE, "LRC_PRECONDITIONED before lrc_set_preconditioner (or the parameters changed)");
   if (ctx->pending.active) {                         // an LRC_ASYNC solve never waited for
     lrc_status ps = finish_solve(ctx, nullptr);
     if (ps != LRC_OK) return ps;
@@ -1261,6 +1403,11 @@ lrc_status solve_prologue(lrc_ctx* ctx, const lrc_solve_opts* opts, lrc_mem wher
   CK(cudaSetDevice(ctx->device));
   lrc_status st = ensure_ws_fit(ctx, std::max(sc.rb, 1), sc.cap, sc.N, sc.wmax, sc.record);
   if (st != LRC_OK) return st;
+  ctx->pc_active = (opts->flags & LRC_PRECONDITIONED) != 0;
+  if (ctx->pc_active) {
+    st = ensure_pc_buffers(ctx);
+    if (st != LRC_OK) return st;
+  }
   Workspace& w = ctx->ws;
   cudaStream_t s = ctx->stream;
   const int64_t M = ctx->M, n = ctx->n;
@@ -1284,6 +1431,10 @@ lrc_status solve_prologue(lrc_ctx* ctx, const lrc_solve_opts* opts, lrc_mem wher
     vb.b[0] = vblock(w.BV, sc.rb, sc.rb, -1, 1.0, -1, 0);
     st = enqueue_norm2(ctx, ub, vb, 0, s);
     if (st != LRC_OK) return st;
+    if (ctx->pc_active) {                          // P^{-1} B_U once per solve (f2)
+      st = enqueue_pinv(ctx, w.BUb, const_cast<double*>(pc_pbu(ctx)), 1, (int)M, w.LDB, w.LDB, 0, sc.rb, nullptr, s);
+      if (st != LRC_OK) return st;
+    }
   }
   CK(cudaEventRecord(ctx->ev[1], s));
   return LRC_OK;
@@ -1391,7 +1542,8 @@ lrc_status lrc_solve(lrc_ctx* ctx, const double* B_U, int64_t ld_bu, const doubl
     const bool use_graph = (opts->flags & LRC_NO_GRAPH) == 0 && !ctx->profiling;
     GraphKey key;
     key.gen = ctx->gen; key.N = sc.N; key.rb = sc.rb; key.cap = sc.cap; key.gamma = sc.gamma; key.tol = opts->tol;
-    key.flags = opts->flags & (LRC_RECORD_ITERATES | LRC_NO_WARM_START);
+    key.flags = opts->flags & (LRC_RECORD_ITERATES | LRC_NO_WARM_START | LRC_PRECONDITIONED);
+    key.pc_gen = ctx->pc_active ? ctx->pc_gen : 0;
     auto body = [&]() -> lrc_status {
       for (int k = 0; k < sc.N; ++k) {
         lrc_status e = enqueue_iteration(ctx, k, sc.rb, sc.cap, sc.gamma, opts->tol, sc.record);
@@ -1429,8 +1581,9 @@ lrc_status lrc_solve_batch(lrc_ctx* const* ctxs, int S, const double* const* B_U
   lrc_ctx* c0 = ctxs[0];
   lrc_ctx* const ctx = c0;   // errors are reported on the first context
   if (!opts) return fail(c0, LRC_ERR_ARG, "null opts");
-  if (opts->flags & (LRC_ASYNC | LRC_NO_GRAPH | LRC_RECORD_ITERATES))
-    return fail(c0, LRC_ERR_ARG, "lrc_solve_batch: LRC_ASYNC / LRC_NO_GRAPH / LRC_RECORD_ITERATES not supported");
+  if (opts->flags & (LRC_ASYNC | LRC_NO_GRAPH | LRC_RECORD_ITERATES | LRC_PRECONDITIONED))
+    return fail(c0, LRC_ERR_ARG, "lrc_solve_batch: LRC_ASYNC / LRC_NO_GRAPH / LRC_RECORD_ITERATES / "
+                                 "LRC_PRECONDITIONED not supported");
   if (r_B < 1) return fail(c0, LRC_ERR_ARG, "lrc_solve_batch: r_B must be >= 1");
   for (int q = 0; q < S; ++q) {
     lrc_ctx* c = ctxs[q];

@@ -190,6 +190,13 @@ cudaError_t launch_trace(State st, const double* G, int pmax, int slot, cudaStre
 
 // misc
 cudaError_t launch_fill_int(int* p, int v, int n, cudaStream_t s);
+struct PvalArgs { const double* v[kMaxT]; double e[kMaxT]; };
+cudaError_t launch_form_pvals(const PvalArgs& pa, int T, long long nnz, double* p, cudaStream_t s);
+cudaError_t launch_cheb_inner(int nb, int rows, int ncols, int ld, long long bs, const double* R, const double* Y,
+                              const double* Zc, const double* Zp, double* Zout, double w, double g, int first,
+                              const int* d_r, int r_fixed, cudaStream_t s);
+cudaError_t launch_s2_update(int rows, int ncols, int ld, const double* U, int ldu, double* W, double g,
+                             cudaStream_t s);
 cudaError_t launch_copy_out(const double* src, int ld_src, double* dst, int ld_dst, int rows, int cols,
                             const int* d_rank, const int* flags, cudaStream_t s);
 cudaError_t launch_zero_cols(double* X, int rows, int ld, const int* d_r, int r_fixed, int cols,

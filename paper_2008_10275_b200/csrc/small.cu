@@ -629,6 +629,42 @@ __global__ void copy_out_kernel(const double* __restrict__ src, int ld_src, doub
   dst[(size_t)i * ld_dst + c] = (c < r) ? src[(size_t)i * ld_src + c] : 0.0;
 }
 
+// the mean-based preconditioner P_T: its values on the shared pattern,
+// p = sum_t e_t v_t (e_t = the term's coefficient times its right diagonal at the mean parameters)
+__global__ void form_pvals_kernel(PvalArgs pa, int T, long long nnz, double* __restrict__ p) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nnz) return;
+  double acc = 0.0;
+  for (int t = 0; t < T; ++t) acc = fma(pa.e[t], pa.v[t][i], acc);
+  p[i] = acc;
+}
+
+// one step of the inner Chebyshev semi-iteration for P Z = R on nb blocks (rows x ncols, ld, block
+// stride bs): Zout = w (Zc + g (R - Y)) + (1 - w) Zp with Y = P Zc (Zp null: Z_0 = 0); first: Zout = g R
+__global__ void cheb_inner_kernel(int nb, int rows, int ncols, int ld, long long bs, const double* __restrict__ R,
+                                  const double* __restrict__ Y, const double* __restrict__ Zc,
+                                  const double* __restrict__ Zp, double* __restrict__ Zout, double w, double g,
+                                  int first, const int* __restrict__ d_r, int r_fixed) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long per = (long long)rows * ncols;
+  if (e >= per * nb) return;
+  const int b = (int)(e / per);
+  const long long q = e - (long long)b * per;
+  const int i = (int)(q / ncols), c = (int)(q - (long long)(q / ncols) * ncols);
+  if (c >= (d_r ? *d_r : r_fixed)) return;        // columns past the rank (and the zero pad) untouched
+  const long long o = (long long)b * bs + (long long)i * ld + c;
+  Zout[o] = first ? g * R[o] : fma(w, fma(g, R[o] - Y[o], Zc[o]), (1.0 - w) * (Zp ? Zp[o] : 0.0));
+}
+
+// W = U - g W (the Chebyshev-step block of the preconditioned iteration), rows x ncols, ld
+__global__ void s2_update_kernel(int rows, int ncols, int ld, const double* __restrict__ U, int ldu,
+                                 double* __restrict__ W, double g) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)rows * ncols) return;
+  const int i = (int)(e / ncols), c = (int)(e - (e / ncols) * ncols);
+  W[(size_t)i * ld + c] = fma(-g, W[(size_t)i * ld + c], U[(size_t)i * ldu + c]);
+}
+
 template <typename K>
 cudaError_t set_smem(K kern, size_t bytes) {
   cudaFuncAttributes fa;
@@ -704,6 +740,30 @@ cudaError_t launch_copy_out(const double* src, int ld_src, double* dst, int ld_d
   const size_t tot = (size_t)rows * cols;
   if (tot == 0) return cudaSuccess;
   copy_out_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(src, ld_src, dst, ld_dst, rows, cols, d_rank, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_form_pvals(const PvalArgs& pa, int T, long long nnz, double* p, cudaStream_t s) {
+  if (nnz <= 0) return cudaSuccess;
+  form_pvals_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, s>>>(pa, T, nnz, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cheb_inner(int nb, int rows, int ncols, int ld, long long bs, const double* R, const double* Y,
+                              const double* Zc, const double* Zp, double* Zout, double w, double g, int first,
+                              const int* d_r, int r_fixed, cudaStream_t s) {
+  const long long tot = (long long)nb * rows * ncols;
+  if (tot == 0) return cudaSuccess;
+  cheb_inner_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(nb, rows, ncols, ld, bs, R, Y, Zc, Zp, Zout, w, g,
+                                                                   first, d_r, r_fixed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_s2_update(int rows, int ncols, int ld, const double* U, int ldu, double* W, double g,
+                             cudaStream_t s) {
+  const long long tot = (long long)rows * ncols;
+  if (tot == 0) return cudaSuccess;
+  s2_update_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(rows, ncols, ld, U, ldu, W, g);
   return cudaGetLastError();
 }
 

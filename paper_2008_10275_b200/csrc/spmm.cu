@@ -19,7 +19,6 @@
 // not fit the U-path bounds take the general spmm_kernel (L2 gather).  spmm_dense_kernel is the
 // config-5 dense variant.
 #include <algorithm>
-#include <cstdio>
 #include <type_traits>
 
 #include "lrc_internal.cuh"
@@ -200,21 +199,6 @@ __device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity)
                : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
   return ok != 0;
 }
-#ifdef LRC_WATCHDOG
-// developer build only: give up (with a message) on a barrier wait longer than ~2 s
-__device__ __forceinline__ void mbar_wait_dbg(unsigned long long* b, unsigned parity, int tag, int idx) {
-  const long long t0 = clock64();
-  while (!mbar_try(b, parity)) {
-    if (clock64() - t0 > 4000000000LL) {
-      printf("WATCHDOG blk %d warp %d tag %d idx %d parity %u\n", blockIdx.x, threadIdx.x >> 5, tag, idx, parity);
-      return;
-    }
-  }
-}
-#define MBAR_WAIT(b, p, tag, idx) mbar_wait_dbg(b, p, tag, idx)
-#else
-#define MBAR_WAIT(b, p, tag, idx) mbar_wait(b, p)
-#endif
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
   while (!mbar_try(b, parity)) {}
 }
@@ -712,13 +696,7 @@ constexpr int kTConsGen = 8;              // consumer warps for general term lis
 constexpr int kRawStride = 908;           // doubles per raw array per stage (>= kTileNnz + 3, == 12 mod 16)
 constexpr int kTUrowMax = kTileUrows;     // staged U rows per tile
 constexpr int kTLdMax = 64;               // U leading dimension supported (r <= 64)
-#ifndef LRC_EXP
-#define LRC_EXP 0
-#endif
-#ifndef LRC_TPREFETCH
-#define LRC_TPREFETCH 4
-#endif
-constexpr int kTPrefetch = LRC_TPREFETCH; // raw values warmed into L2 this many tiles ahead (0: off)
+constexpr int kTPrefetch = 4;             // raw values warmed into L2 this many tiles ahead (0: off)
 
 // raw value stages for nT value arrays (3 up to six arrays, 2 beyond: shared memory)
 __host__ __device__ __forceinline__ int tma_raw_stages(int nT) { return nT <= 6 ? 3 : 2; }
@@ -831,15 +809,15 @@ spmm_tma_kernel(SpmmArgs a) {
       for (int k = 0; k < kMetaRuns; ++k)
         if (myr == k && k < nrun) { rg = rv[3 * k]; rl = rv[3 * k + 1]; rs = rv[3 * k + 2]; }
       const int us = m % kUStages;
-      if (m >= kUStages) MBAR_WAIT(&empty_u[us], ((m / kUStages) - 1) & 1, 1, m);
+      if (m >= kUStages) mbar_wait(&empty_u[us], ((m / kUStages) - 1) & 1);
       {
-        unsigned ub = (LRC_EXP & 1) ? 0u : (unsigned)rl * (unsigned)ldu * 8u;
+        unsigned ub = (unsigned)rl * (unsigned)ldu * 8u;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) ub += __shfl_xor_sync(0xffffffffu, ub, o);
         if (lane == 0) mbar_expect_tx(&full_u[us], ub);
         __syncwarp();
         const double* Usrc = S > 1 ? a.Us[q] : a.U;
-        if (!(LRC_EXP & 1) && rl > 0)
+        if (rl > 0)
           bulk_g2s(s_ub + (size_t)us * kTUrowMax * kTLdMax + (size_t)rs * ldu, Usrc + (size_t)rg * ldu,
                    (unsigned)rl * (unsigned)ldu * 8u, &full_u[us]);
       }
@@ -848,7 +826,7 @@ spmm_tma_kernel(SpmmArgs a) {
         const int e0 = meta(ri, W0{}), tot = meta(ri, W1{});
         int pe0 = 0, ptot = 0;
         if (kTPrefetch > 0 && ri + kTPrefetch < nmine) { pe0 = meta(ri + kTPrefetch, W0{}); ptot = meta(ri + kTPrefetch, W1{}); }
-        if (ri >= nsr) MBAR_WAIT(&empty_r[sr], ((ri / nsr) - 1) & 1, 2, ri);
+        if (ri >= nsr) mbar_wait(&empty_r[sr], ((ri / nsr) - 1) & 1);
         if (kTPrefetch > 0 && ptot > 0 && lane < nT) {   // warm L2 further ahead
           const int p0 = pe0 & ~1, p1 = (pe0 + ptot) & ~1;
           if (p1 > p0) bulk_prefetch_l2(a.v[lane] + p0, 8u * (unsigned)(p1 - p0));
@@ -858,11 +836,11 @@ spmm_tma_kernel(SpmmArgs a) {
         if (lane == 0) {
           if (end & 1)   // odd tail element: plain load (a bulk copy never reads past the tile)
             for (int v = 0; v < nT; ++v) raw[v * kRawStride + (end - 1 - e0a)] = __ldg(a.v[v] + end - 1);
-          mbar_expect_tx(&full_r[sr], ((LRC_EXP & 2) ? 0u : (unsigned)nT * 8u * (unsigned)(endc - e0a)) + 4u * kRecInts);
+          mbar_expect_tx(&full_r[sr], (unsigned)nT * 8u * (unsigned)(endc - e0a) + 4u * kRecInts);
         }
         __syncwarp();
         if (lane < nT) {
-          if (!(LRC_EXP & 2) && endc > e0a) bulk_g2s(raw + lane * kRawStride, a.v[lane] + e0a, 8u * (unsigned)(endc - e0a), &full_r[sr]);
+          if (endc > e0a) bulk_g2s(raw + lane * kRawStride, a.v[lane] + e0a, 8u * (unsigned)(endc - e0a), &full_r[sr]);
         } else if (lane == 8) {
           bulk_g2s(s_rec + sr * kRecInts, a.trec + (size_t)tr * kRecInts, 4u * kRecInts, &full_r[sr]);
         }
@@ -882,8 +860,8 @@ spmm_tma_kernel(SpmmArgs a) {
   for (int m = 0; m < nwork; ++m) {
     const int i = m / S, q = m - i * S;
     const int sr = i % nsr, us = m % kUStages;
-    MBAR_WAIT(&full_r[sr], (i / nsr) & 1, 3, i);
-    MBAR_WAIT(&full_u[us], (m / kUStages) & 1, 4, m);
+    mbar_wait(&full_r[sr], (i / nsr) & 1);
+    mbar_wait(&full_u[us], (m / kUStages) & 1);
     for (int task = (warp - (int)(((long long)m * tpt) % NCW) + NCW) % NCW; task < tpt; task += NCW) {
     const int* R = s_rec + sr * kRecInts;
     const double* raw = s_raw + (size_t)sr * nT * kRawStride;
@@ -953,13 +931,11 @@ spmm_tma_kernel(SpmmArgs a) {
           for (int k = 1; k < KC; ++k) v = fma(co[nt][k], raw[po[nt][k] + k0], v);
           bv[nt] = (jv && sv[nt]) ? v : 0.0;
         }
-        if (!(LRC_EXP & 4)) {
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            dmma1684(acc[0][nt], x0, x1, bv[nt]);
-            dmma1684(acc[1][nt], x2, x3, bv[nt]);
-          }
-        } else { acc[0][0][0] += x0 + bv[0]; acc[1][0][1] += x3 * bv[NT - 1]; }
+        for (int nt = 0; nt < NT; ++nt) {
+          dmma1684(acc[0][nt], x0, x1, bv[nt]);
+          dmma1684(acc[1][nt], x2, x3, bv[nt]);
+        }
       }
       // epilogue: frag (m, n) -> column n0 + mt*16 + gid (+8), slot nt*8 + 2 tig + e = G q + group
       const bool full_cols = n0 + 32 <= r;
@@ -984,7 +960,7 @@ spmm_tma_kernel(SpmmArgs a) {
               if (full_cols || c < r) {
                 double v = acc[mt][nt][hm * 2 + e];
                 if (s2) v = fma(-a.gamma, v, us_[o]);
-                if (!(LRC_EXP & 8) || v == 12345.678) __stcs(orow + o, v);
+                __stcs(orow + o, v);
               } else if (c == r && (r & 1) && a.out_sstride) {
                 __stcs(orow + o, 0.0);        // zero pad column of the (even-padded) Ucat block
               }
@@ -1191,9 +1167,6 @@ int sm_count() {
 }
 
 bool tma_ok(const SpmmArgs& a, int rmax) {
-#ifdef LRC_NO_TMA
-  return false;
-#endif
   bool al = a.trec != nullptr && a.tmeta != nullptr && rmax <= kTLdMax && a.ldu <= kTLdMax && (a.ldu % 2 == 0) &&
             a.nsub <= kMaxSub;
   for (int q = 0; q < max(1, a.nsub); ++q) {

@@ -23,6 +23,7 @@ LIB_PATH = os.path.join(_HERE, "liblrcheb.so")
 LRC_OK, LRC_ERR_ARG, LRC_ERR_SHAPE, LRC_ERR_STATE, LRC_ERR_NOMEM, LRC_ERR_CUDA, LRC_ERR_NUMERIC = range(7)
 LRC_MEM_HOST, LRC_MEM_DEVICE, LRC_MEM_DEVICE_BORROW = 0, 1, 2
 LRC_RECORD_ITERATES, LRC_SKIP_FINAL_RESIDUAL, LRC_NO_GRAPH, LRC_NO_WARM_START, LRC_ASYNC = 1, 2, 4, 8, 16
+LRC_PRECONDITIONED = 32
 LRC_APPLY_PLAIN3, LRC_APPLY_SIX, LRC_APPLY_S2STEP = 0, 1, 2
 SIGMA_STRIDE = 128
 
@@ -32,7 +33,7 @@ EXPORTS = (
     "lrc_set_params", "lrc_solve", "lrc_apply_lowrank", "lrc_apply_dense", "lrc_truncate",
     "lrc_get_iterate", "lrc_last_kernel_ms", "lrc_kernel_launches", "lrc_set_profiling", "lrc_get_profile",
     "lrc_set_reserved_sms", "lrc_solve_wait", "lrc_workspace_bytes", "lrc_set_workspace", "lrc_solve_batch",
-    "lrc_set_operator_terms", "lrc_set_diagonals", "lrc_solve_gmres",
+    "lrc_set_operator_terms", "lrc_set_diagonals", "lrc_solve_gmres", "lrc_set_preconditioner",
 )
 
 
@@ -84,6 +85,7 @@ def load_library(path: str = None) -> ctypes.CDLL:
     lib.lrc_set_params.argtypes = [P, I64, P, P, I32]
     lib.lrc_set_operator_terms.argtypes = [P, I64, I64, P, P, I32, ctypes.POINTER(P), I32, P, I32, I32]
     lib.lrc_set_diagonals.argtypes = [P, I64, I32, P, I32]
+    lib.lrc_set_preconditioner.argtypes = [P, D, D, I64]
     lib.lrc_solve_gmres.argtypes = [P, P, I64, P, I64, I64, ctypes.POINTER(GmresOpts), P, I64, P, I64, I32,
                                     ctypes.POINTER(GmresInfo)]
     lib.lrc_solve.argtypes = [P, P, I64, P, I64, I64, ctypes.POINTER(SolveOpts), P, I64, P, I64, I32,
@@ -112,7 +114,7 @@ def load_library(path: str = None) -> ctypes.CDLL:
     for name in ("lrc_create", "lrc_set_operator", "lrc_set_params", "lrc_solve", "lrc_apply_lowrank",
                  "lrc_apply_dense", "lrc_truncate", "lrc_get_iterate", "lrc_solve_wait", "lrc_workspace_bytes",
                  "lrc_set_workspace", "lrc_solve_batch", "lrc_set_operator_terms", "lrc_set_diagonals",
-                 "lrc_solve_gmres"):
+                 "lrc_solve_gmres", "lrc_set_preconditioner"):
         getattr(lib, name).restype = I32
     return lib
 
@@ -257,6 +259,11 @@ class Context:
         self._check(self._lib.lrc_set_diagonals(self._h, n, G, D.ctypes.data, LRC_MEM_HOST))
         self.n = n
 
+    def set_preconditioner(self, p_min: float, p_max: float, inner_steps: int):
+        """Mean-based preconditioner P_T (SURVEY §8 f2) for solves with ``preconditioned=True``;
+        [p_min, p_max] bounds the spectrum of P_T, inner_steps Chebyshev steps apply P_T^{-1}."""
+        self._check(self._lib.lrc_set_preconditioner(self._h, float(p_min), float(p_max), int(inner_steps)))
+
     def set_params(self, d_mu, d_nu):
         pm, w1, k1 = _vec(d_mu, np.float64)
         pn, w2, k2 = _vec(d_nu, np.float64)
@@ -269,7 +276,8 @@ class Context:
     # ------------------------------------------------------------------------------------
     def solve(self, B_U, B_V, lambda_min: float, lambda_max: float, tol: float, rank_cap: int,
               n_iter: int, restart_every: int = 0, record_iterates: bool = False,
-              skip_residual: bool = False, no_graph: bool = False, warm_start: bool = True, out=None):
+              skip_residual: bool = False, no_graph: bool = False, warm_start: bool = True, out=None,
+              preconditioned: bool = False):
         """Returns (U, V, info).  Outputs live where the inputs live (torch CUDA tensors for device
         inputs, numpy for host inputs) unless ``out=(U_out, V_out)`` is given."""
         pu, ldbu, w1, ku = _mat(B_U)
@@ -291,7 +299,8 @@ class Context:
         pVo, ldvo, w4, _ = _mat(Vo)
         assert w3 == w1 and w4 == w1
         flags = ((LRC_RECORD_ITERATES if record_iterates else 0) | (LRC_SKIP_FINAL_RESIDUAL if skip_residual else 0)
-                 | (LRC_NO_GRAPH if no_graph else 0) | (0 if warm_start else LRC_NO_WARM_START))
+                 | (LRC_NO_GRAPH if no_graph else 0) | (0 if warm_start else LRC_NO_WARM_START)
+                 | (LRC_PRECONDITIONED if preconditioned else 0))
         opts = SolveOpts(float(lambda_min), float(lambda_max), float(tol), int(rank_cap), int(n_iter),
                          int(restart_every), flags)
         rh = (ctypes.c_int64 * n_iter)()

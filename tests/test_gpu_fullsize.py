@@ -8,7 +8,8 @@ PAPER.md P:30-36, truncation P:544).
   and the final residual (|d rho| <= 1e-9).
 * Large in the exact bench launch configuration: 3 contexts on 3 streams / host threads, borrowed
   operator, 3 reserved SMs, subsets 0, 1, 2 concurrently -> X_N rows and rho of each subset.
-* Medium (configs[2]) subset 0: all 80 iterations compared with the live oracle, every iteration.
+* Medium (configs[2]) subset 0: all 80 iterations, every X_k on 256 sampled rows against the golden
+  (tests/golden/medium_s0.npz; the live oracle when the file is absent).
 * Config 5 (configs[4]): the dense M x 256 application on the Large operator, compared with the
   oracle's apply_dense on a seeded block of rows (the oracle restricted to rows R computes
   sum_t c_t A_t[R, :] S diag(e_t) -- the same formula, fewer rows).
@@ -27,7 +28,7 @@ pytestmark = pytest.mark.gpu
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 sys.path.insert(0, GOLDEN)
-import make_goldens  # noqa: E402  (fingerprint / row sampling of the golden files)
+import make_goldens  # noqa: E402  (input signature / row sampling of the golden files)
 
 
 def _golden(name, subset):
@@ -36,8 +37,8 @@ def _golden(name, subset):
     g = np.load(path)
     prob = problem(name)
     d_mu, d_nu, BU, BV = prob.subset(subset)
-    fp = make_goldens.fingerprint(prob.op, d_mu, d_nu, BU, BV, prob.lam_min, prob.lam_max)
-    assert str(g["fingerprint"]) == fp, "golden was written for different inputs (synth/ changed?)"
+    sig = make_goldens.signature(prob.op, d_mu, d_nu, BU, BV, prob.lam_min, prob.lam_max)
+    assert make_goldens.same_inputs(g["signature"], sig), "golden was written for different inputs (synth/ changed?)"
     return g
 
 
@@ -161,8 +162,10 @@ def test_large_bench_configuration_concurrent(large_dev):
         c.close()
 
 
-def test_medium_every_iteration_live_oracle():
-    """Medium subset 0, all N = 80 iterations, every X_k against the live oracle."""
+def test_medium_every_iteration():
+    """Medium subset 0, all N = 80 iterations: every X_k on the golden's 256 sampled rows, every rank and
+    core singular-value vector (tests/golden/medium_s0.npz, written by the oracle); without the golden
+    file the same comparison runs against the live oracle (~11 min)."""
     require_gpu()
     prob = problem("medium")
     cfg, op = prob.cfg, prob.op
@@ -171,6 +174,24 @@ def test_medium_every_iteration_live_oracle():
     N, cap, tol = cfg.n_iter, cfg.rank_cap, cfg.tol
     _, _, info = ctx.solve(torch.from_numpy(BU).cuda(), torch.from_numpy(BV).cuda(), prob.lam_min, prob.lam_max,
                            tol, cap, N, record_iterates=True)
+    if os.path.exists(os.path.join(GOLDEN, "medium_s0.npz")):
+        g = _golden("medium", 0)
+        assert list(g["ck"]) == list(range(1, N + 1))
+        _check_ranks(info["rank_history"], g, tol, cap)
+        S = info["sigma_history"]
+        worst = 0.0
+        for k in range(1, N + 1):
+            so = g["sigmas"][k - 1]
+            m = int(min(np.count_nonzero(so), np.count_nonzero(S[k - 1]), 100))
+            assert np.max(np.abs(S[k - 1][:m] - so[:m])) <= 1e-10 * so[0], k
+            Uk, Vk, rk = ctx.get_iterate(k, cap)
+            err = _rows_rel(Uk, Vk, rk, g["U_ck"][k - 1], g["V_ck"][k - 1], int(g["ranks"][k - 1]), g["rows"])
+            worst = max(worst, err)
+            assert err <= 1e-8, (k, err)
+        assert abs(info["rel_residual"] - float(g["rel_residual"])) <= 1e-9
+        print(f"medium s0 (golden): worst iterate rel err on sampled rows {worst:.2e}")
+        ctx.close()
+        return
     terms = oracle_terms(op, d_mu, d_nu)
     Uk_prev = {}
 

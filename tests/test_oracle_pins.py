@@ -582,3 +582,70 @@ def test_f3_gmrest_identity_and_zero_rhs():
     assert np.linalg.norm(orc.dense_product(res.U, res.V) - 0.5 * BU @ BV.T) <= 1e-14 * np.linalg.norm(BU @ BV.T)
     res0 = orc.gmrest(terms, np.zeros((M, 1)), np.zeros((n, 1)), 0.0, n, 6, 2, 1e-12)
     assert res0.cycles == 0 and res0.U.shape[1] == 0
+
+
+# ------------------------------------------------------------------------------------------
+# the mean-based preconditioner, LU-applied
+# ------------------------------------------------------------------------------------------
+def test_f2_preconditioned_diagonal_closed_form():
+    """Diagonal operator, diagonal P_T: the preconditioned operator has eigenvalues Lambda_ij / pi_i, so
+    X_N = (1 - p_N(Lambda / Pi)) * S* with p_N the Chebyshev error polynomial of the preconditioned
+    interval (P1 on P^{-1} L)."""
+    terms, Lam, BU, BV = diagonal_problem(seed=13)
+    P = orc.mean_preconditioner(terms)
+    pi = P.diagonal()
+    # P_T entries written out from P:334-341: every term at the midpoint of its diagonal
+    ref = sum(c * 0.5 * (e.min() + e.max()) * A.diagonal() for c, A, e in terms)
+    assert np.allclose(pi, ref, rtol=1e-15, atol=0)
+    Q = Lam / pi[:, None]
+    lmin, lmax = Q.min(), Q.max()
+    S_star = (BU @ BV.T) / Lam
+    c, d = 0.5 * (lmax - lmin), 0.5 * (lmax + lmin)
+    for N in (1, 2, 5):
+        res = orc.chebyshevt(terms, BU, BV, lmin, lmax, tau=0.0, R=BV.shape[0], N=N, precond=P)
+        pN = cheb_T(N, (d - Q) / c) / cheb_T(N, d / c)
+        X = orc.dense_product(res.U, res.V)
+        assert np.linalg.norm(X - (1.0 - pN) * S_star) <= 1e-12 * np.linalg.norm(S_star), N
+
+
+def test_f2_exact_preconditioner_converges_in_one_step():
+    """One parameter at the mean: P_T equals the operator, P^{-1} L = I, bounds [1, 1] -> X_1 = S*."""
+    prob = gen.make_problem("tiny")
+    op = prob.op
+    mats = orc.csr_matrices(op.M, op.row_ptr, op.col_idx, op.vals)
+    terms = orc.term_list(mats, op.rho_f, op.lambda_s, np.array([1.3]), np.array([0.7]))
+    rng = np.random.default_rng(2)
+    BU, BV = rng.standard_normal((op.M, 1)), rng.standard_normal((1, 1))
+    P = orc.mean_preconditioner(terms)
+    res = orc.chebyshevt(terms, BU, BV, 1.0, 1.0, tau=0.0, R=1, N=1, precond=P)
+    S = block_solve(terms, BU @ BV.T)
+    assert np.linalg.norm(orc.dense_product(res.U, res.V) - S) <= 1e-12 * np.linalg.norm(S)
+    assert res.rel_residual <= 1e-12
+
+
+def test_f2_harness_bounds_enclose_the_spectra():
+    """synth.precond (the bounds the f2 tests and bench pass in): its midpoint multipliers rebuild the
+    oracle's P_T from the raw arrays, and the closed-form intervals contain the exact spectra of P_T
+    and of P_T^{-1} A_j (dense generalized eigenvalues) for the Tiny subset."""
+    import scipy.linalg as sla
+    from synth import precond as spc
+    prob = gen.make_problem("tiny")
+    op, cfg = prob.op, prob.cfg
+    d_mu, d_nu, _, _ = prob.subset(0)
+    mats = orc.csr_matrices(op.M, op.row_ptr, op.col_idx, op.vals)
+    terms = orc.term_list(mats, op.rho_f, op.lambda_s, d_mu, d_nu)
+    E = spc.legacy_multipliers(op.rho_f, op.lambda_s, d_mu, d_nu)
+    P_h = sum(m * A for m, A in zip(spc.midpoint(E), mats)).toarray()
+    P_o = orc.mean_preconditioner(terms).toarray()
+    assert np.max(np.abs(P_h - P_o)) <= 1e-14 * np.max(np.abs(P_o))
+    p_min, p_max, lo, hi = spc.closed_form_bounds(cfg.g, op.rho_f, op.lambda_s, d_mu, d_nu)
+    ev = np.linalg.eigvalsh(P_o)
+    assert p_min <= ev[0] and ev[-1] <= p_max
+    for j in (0, 5, 15):
+        A = sum(m * M_ for m, M_ in zip(E[j], mats)).toarray()
+        g = sla.eigh(A, P_o, eigvals_only=True)
+        assert lo <= g[0] and g[-1] <= hi, (j, g[0], g[-1], lo, hi)
+    assert spc.inner_steps(1.0, 1.0) == 1
+    r = (np.sqrt(9.0) - 1) / (np.sqrt(9.0) + 1)
+    q = spc.inner_steps(1.0, 9.0, 1e-10)
+    assert 2 * r ** q <= 1e-10 < 2 * r ** (q - 1)
