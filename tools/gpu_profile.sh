@@ -8,7 +8,7 @@ OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
 NCU=/usr/local/cuda/bin/ncu
 if [ "${2:-}" != "skip-tests" ]; then
-  timeout 900 python -m pytest tests -m gpu -x -q > "$OUT/pytest_gpu.log" 2>&1
+  timeout 2400 python -m pytest tests -m gpu -x -q --durations=0 > "$OUT/pytest_gpu.log" 2>&1
   echo "pytest_exit=$?"; tail -2 "$OUT/pytest_gpu.log"
 fi
 timeout 900 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"
@@ -21,7 +21,7 @@ timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none -c 800 --
   --log-file "$OUT/launches.csv" python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-dense --streams 1 \
   > "$OUT/ncu_launches.log" 2>&1
 echo "ncu_launches_exit=$?"
-timeout 900 $NCU --set full --clock-control none --import-source on -k regex:spmm_u_kernel -s 3 -c 1 \
+timeout 900 $NCU --set full --clock-control none --import-source on -k regex:spmm_tma_kernel -s 3 -c 1 \
   -o "$OUT/spmm_full" -f python tools/quick_bench.py large 4 > "$OUT/ncu_spmm.log" 2>&1
 echo "ncu_spmm_exit=$?"
 # steady state (rank = cap): the 46th..48th tall-skinny launches of the first N = 20 solve

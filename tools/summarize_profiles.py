@@ -112,7 +112,7 @@ def main():
                       f"{r['dram_bytes'] / r['ms'] / 1e6:.0f} | {r['tensor_pct']:.1f} | {r['issue_pct']:.1f} | "
                       f"{r['dram_pct']:.1f} | {r['regs']:.0f} | {r['grid']:.0f} |")
             k = r["kernel"]
-            if k.startswith("spmm_u_kernel"):
+            if k.startswith(("spmm_u_kernel", "spmm_tma_kernel")):
                 traffic["spmm"] = r["dram_bytes"]
             elif k.startswith("ts_kernel") and k.endswith("0>"):
                 # captures run pass 1 (over Ucat) before pass 2 (over Y) within an iteration
