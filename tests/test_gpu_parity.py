@@ -189,11 +189,6 @@ def test_solve_small_subsets():
         _solve_parity("small", k, 50)
 
 
-def test_solve_medium_first_iterations():
-    require_gpu()
-    _solve_parity("medium", 0, 8)
-
-
 def test_solve_restart_and_tau0():
     require_gpu()
     _solve_parity("tiny", 0, 14, restart_every=6, tau=0.0, cap=16)
