@@ -689,21 +689,35 @@ spmm_u_kernel(SpmmArgs a, int ust) {
 //                   pipe (m16n8k4, transposed so the stores are full sectors).  A warp signals the
 //                   stages' empty barriers when it is done with the tile; no CTA-wide barrier.
 // ---------------------------------------------------------------------------------------------
-constexpr int kTStages = 3;               // raw value / record stages
-constexpr int kUStages = 2;               // U row stages
-constexpr int kTCons = 12;                // consumer warps (the operator of P:30-36)
+#ifndef LRC_SPMM_RAW_STAGES
+#define LRC_SPMM_RAW_STAGES 3
+#endif
+#ifndef LRC_SPMM_U_STAGES
+#define LRC_SPMM_U_STAGES 2
+#endif
+constexpr int kTStages = LRC_SPMM_RAW_STAGES;   // raw value / record stages
+constexpr int kUStages = LRC_SPMM_U_STAGES;     // U row stages
+#ifndef LRC_SPMM_CONS
+#define LRC_SPMM_CONS 12
+#endif
+#ifndef LRC_SPMM_PREFETCH
+#define LRC_SPMM_PREFETCH 4
+#endif
+constexpr int kTCons = LRC_SPMM_CONS;     // consumer warps (the operator of P:30-36)
 constexpr int kTConsGen = 8;              // consumer warps for general term lists (more registers)
 constexpr int kRawStride = 908;           // doubles per raw array per stage (>= kTileNnz + 3, == 12 mod 16)
 constexpr int kTUrowMax = kTileUrows;     // staged U rows per tile
 constexpr int kTLdMax = 64;               // U leading dimension supported (r <= 64)
-constexpr int kTPrefetch = 4;             // raw values warmed into L2 this many tiles ahead (0: off)
+constexpr int kTPrefetch = LRC_SPMM_PREFETCH;   // raw values warmed into L2 this many tiles ahead (0: off)
 
 // raw value stages for nT value arrays (3 up to six arrays, 2 beyond: shared memory)
-__host__ __device__ __forceinline__ int tma_raw_stages(int nT) { return nT <= 6 ? 3 : 2; }
+__host__ __device__ __forceinline__ int tma_raw_stages(int nT) { return nT <= 6 ? kTStages : 2; }
 
-size_t tma_smem(int nT) {
+constexpr int kTmaSmemMax = 232448 - 2048;      // opt-in dynamic shared memory granted to the TMA kernel
+// dynamic shared memory of the TMA kernel for nT value arrays and U rows of leading dimension ldu
+size_t tma_smem(int nT, int ldu = kTLdMax) {
   const int nsr = tma_raw_stages(nT);
-  return sizeof(double) * ((size_t)nsr * nT * kRawStride + (size_t)kUStages * kTUrowMax * kTLdMax) +
+  return sizeof(double) * ((size_t)nsr * nT * kRawStride + (size_t)kUStages * kTUrowMax * ldu) +
          sizeof(int) * (size_t)nsr * kRecInts;
 }
 
@@ -727,7 +741,8 @@ spmm_tma_kernel(SpmmArgs a) {
   const int G = GEN ? a.G : 3;                    // output groups
   double* s_raw = smem_dyn;                                                   // [stage][nT][kRawStride]
   double* s_ub = s_raw + (size_t)nsr * nT * kRawStride;                       // [ustage][kTUrowMax * ldu]
-  int* s_rec = reinterpret_cast<int*>(s_ub + (size_t)kUStages * kTUrowMax * kTLdMax);   // [stage][kRecInts]
+  const int ldu_s = a.ldu;                        // U stage row stride (even, <= kTLdMax)
+  int* s_rec = reinterpret_cast<int*>(s_ub + (size_t)kUStages * kTUrowMax * ldu_s);   // [stage][kRecInts]
   // raw/record stages per tile i (ring of kTStages), U stages per work item m = i * S + subset
   // (ring of kUStages)
   __shared__ __align__(8) unsigned long long full_r[kTStages], empty_r[kTStages], full_u[kUStages], empty_u[kUStages];
@@ -818,7 +833,7 @@ spmm_tma_kernel(SpmmArgs a) {
         __syncwarp();
         const double* Usrc = S > 1 ? a.Us[q] : a.U;
         if (rl > 0)
-          bulk_g2s(s_ub + (size_t)us * kTUrowMax * kTLdMax + (size_t)rs * ldu, Usrc + (size_t)rg * ldu,
+          bulk_g2s(s_ub + (size_t)us * kTUrowMax * ldu_s + (size_t)rs * ldu, Usrc + (size_t)rg * ldu,
                    (unsigned)rl * (unsigned)ldu * 8u, &full_u[us]);
       }
       for (; ri < nmine && ri <= i + nsr - 1; ++ri) {
@@ -865,7 +880,7 @@ spmm_tma_kernel(SpmmArgs a) {
     for (int task = (warp - (int)(((long long)m * tpt) % NCW) + NCW) % NCW; task < tpt; task += NCW) {
     const int* R = s_rec + sr * kRecInts;
     const double* raw = s_raw + (size_t)sr * nT * kRawStride;
-    const double* su = s_ub + (size_t)us * kTUrowMax * kTLdMax;
+    const double* su = s_ub + (size_t)us * kTUrowMax * ldu_s;
     int r = rsub[0];
 #pragma unroll
     for (int k = 1; k < kMaxSub; ++k) if (q == k) r = rsub[k];
@@ -917,26 +932,43 @@ spmm_tma_kernel(SpmmArgs a) {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.0;
       const int L4 = (L + 3) & ~3;
+#define LRC_TMA_STEP(U_OFF, K0)                                                           \
+  {                                                                                  \
+    const int k0 = (K0);                                                             \
+    const double* u = su + (U_OFF);                                                  \
+        const double x0 = v00 ? u[c00] : 0.0, x1 = v01 ? u[c01] : 0.0;              \
+        const double x2 = v10 ? u[c10] : 0.0, x3 = v11 ? u[c11] : 0.0;              \
+        const bool jv = k0 + tig < L;                                               \
+        double bv[NT];                                                              \
+_Pragma("unroll")                                                                   \
+        for (int nt = 0; nt < NT; ++nt) {                                           \
+          double v = co[nt][0] * raw[po[nt][0] + k0];                               \
+_Pragma("unroll")                                                                   \
+          for (int k = 1; k < KC; ++k) v = fma(co[nt][k], raw[po[nt][k] + k0], v);  \
+          bv[nt] = (jv && sv[nt]) ? v : 0.0;                                        \
+        }                                                                           \
+_Pragma("unroll")                                                                   \
+        for (int nt = 0; nt < NT; ++nt) {                                           \
+          dmma1684(acc[0][nt], x0, x1, bv[nt]);                                     \
+          dmma1684(acc[1][nt], x2, x3, bv[nt]);                                     \
+        }                                                                           \
+  }
+      if (L4 <= 48) {
+        // node blocks of <= 12 k4 steps (interior FE nodes: L = 45): this lane's staged U row offset of
+        // every step first, so no step waits on an index load before its U fragment loads
+        int uo[12];
+#pragma unroll
+        for (int t = 0; t < 12; ++t) uo[t] = R[cb + min(4 * t + tig, jmax)] * ldu;
+#pragma unroll
+        for (int t = 0; t < 12; ++t) {
+          if (4 * t >= L4) break;
+          LRC_TMA_STEP(uo[t], 4 * t)
+        }
+      } else {
 #pragma unroll 2
-      for (int k0 = 0; k0 < L4; k0 += 4) {
-        const double* u = su + R[cb + min(k0 + tig, jmax)] * ldu;
-        const double x0 = v00 ? u[c00] : 0.0, x1 = v01 ? u[c01] : 0.0;
-        const double x2 = v10 ? u[c10] : 0.0, x3 = v11 ? u[c11] : 0.0;
-        const bool jv = k0 + tig < L;
-        double bv[NT];
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          double v = co[nt][0] * raw[po[nt][0] + k0];
-#pragma unroll
-          for (int k = 1; k < KC; ++k) v = fma(co[nt][k], raw[po[nt][k] + k0], v);
-          bv[nt] = (jv && sv[nt]) ? v : 0.0;
-        }
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          dmma1684(acc[0][nt], x0, x1, bv[nt]);
-          dmma1684(acc[1][nt], x2, x3, bv[nt]);
-        }
+        for (int kk = 0; kk < L4; kk += 4) LRC_TMA_STEP(R[cb + min(kk + tig, jmax)] * ldu, kk)
       }
+#undef LRC_TMA_STEP
       // epilogue: frag (m, n) -> column n0 + mt*16 + gid (+8), slot nt*8 + 2 tig + e = G q + group
       const bool full_cols = n0 + 32 <= r;
       const int s2g = GEN ? a.id_group : 0;       // the identity-diagonal group carries U - g W
@@ -1168,7 +1200,7 @@ int sm_count() {
 
 bool tma_ok(const SpmmArgs& a, int rmax) {
   bool al = a.trec != nullptr && a.tmeta != nullptr && rmax <= kTLdMax && a.ldu <= kTLdMax && (a.ldu % 2 == 0) &&
-            a.nsub <= kMaxSub;
+            a.nsub <= kMaxSub && tma_smem(a.gen ? a.T : 6, a.ldu) <= (size_t)kTmaSmemMax;
   for (int q = 0; q < max(1, a.nsub); ++q) {
     const double* u = a.nsub > 1 ? a.Us[q] : a.U;
     al = al && ((reinterpret_cast<uintptr_t>(u) & 15) == 0);
@@ -1191,13 +1223,13 @@ cudaError_t launch_m(const SpmmArgs& a0, int rmax, cudaStream_t s) {
     if (tma_ok(a, rmax) && a.ntl_u > 0) {
       const int grid = min(a.ntl_u, max(1, sm_count() - max(0, a.reserved_sms)));
       if (!a.gen) {
-        spmm_tma_kernel<MODE, false, 2, kTCons><<<grid, (kTCons + 1) * 32, tma_smem(6), s>>>(a);
+        spmm_tma_kernel<MODE, false, 2, kTCons><<<grid, (kTCons + 1) * 32, tma_smem(6, a.ldu), s>>>(a);
       } else {
         const int nt = (5 * a.G + 7) / 8;          // slots (row, group) of a node block in n-tiles of 8
         int kmax = 0;
         for (int g = 0; g < a.G; ++g) kmax = max(kmax, a.gl_n[g]);
         const int th = (kTConsGen + 1) * 32;
-        const size_t sm = tma_smem(a.T);
+        const size_t sm = tma_smem(a.T, a.ldu);
         if (kmax <= 4) {
           if (nt <= 2) spmm_tma_kernel<MODE, true, 2, kTConsGen, 4><<<grid, th, sm, s>>>(a);
           else if (nt == 3) spmm_tma_kernel<MODE, true, 3, kTConsGen, 4><<<grid, th, sm, s>>>(a);
@@ -1275,7 +1307,7 @@ cudaError_t prep_m() {
   if constexpr (MODE == SPMM_S2STEP || MODE == SPMM_PLAIN3) {
     e = cudaFuncSetAttribute(spmm_u_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 75 * 1024);
     if (e != cudaSuccess) return e;
-    const int mx = (int)std::max(tma_smem(6), tma_smem(kMaxT));
+    const int mx = (int)std::min(std::max(tma_smem(6), tma_smem(kMaxT)), (size_t)kTmaSmemMax);
     e = cudaFuncSetAttribute(spmm_tma_kernel<MODE, false, 2, kTCons>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     if (e != cudaSuccess) return e;
 #define LRC_TMA_ATTR(NT_, KC_)                                                                          \
