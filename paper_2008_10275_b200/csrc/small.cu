@@ -26,6 +26,7 @@ constexpr int kMaxEsc = 3;            // escalations x100
 constexpr double kJacobiTol = 1e-14;  // rotate while |a_i.a_j| > tol ||a_i|| ||a_j||
 constexpr double kJacobiFloor = 1e-30;   // (1e-15)^2: column-norm^2 floor relative to ||R||_F^2
 constexpr int kMaxSweeps = 40;
+constexpr int kJacE = 7;              // Jacobi elements per lane of a pair (16 lanes, p <= 112)
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -462,12 +463,18 @@ __global__ void __launch_bounds__(kT) chol2_svd_kernel(State st, SmallBufs b, in
         }
         double* ai = A + i * LD;
         double* aj = A + j * LD;
+        // the pair's two columns in registers (p <= 112, the host-checked limit: <= 7 elements per lane),
+        // read once per round
+        double xa[kJacE], ya[kJacE];
         double al = 0.0, be = 0.0, ga = 0.0;
-        if (act)
-          for (int e = hl; e < p; e += 16) {
-            const double x = ai[e], y = aj[e];
-            al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
-          }
+#pragma unroll
+        for (int t = 0; t < kJacE; ++t) {
+          const int e = hl + 16 * t;
+          const bool in = act && e < p;
+          xa[t] = in ? ai[e] : 0.0;
+          ya[t] = in ? aj[e] : 0.0;
+          al = fma(xa[t], xa[t], al); be = fma(ya[t], ya[t], be); ga = fma(xa[t], ya[t], ga);
+        }
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) {
           al += __shfl_xor_sync(0xffffffffu, al, o);
@@ -479,10 +486,13 @@ __global__ void __launch_bounds__(kT) chol2_svd_kernel(State st, SmallBufs b, in
           const double dd = be - al;
           const double t = ((dd >= 0.0) ? 2.0 * ga : -2.0 * ga) / (fabs(dd) + sqrt(fma(dd, dd, 4.0 * ga * ga)));
           const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
-          for (int e = hl; e < p; e += 16) {
-            const double x = ai[e], y = aj[e];
-            ai[e] = c * x - sn * y;
-            aj[e] = sn * x + c * y;
+#pragma unroll
+          for (int t = 0; t < kJacE; ++t) {
+            const int e = hl + 16 * t;
+            if (e < p) {
+              ai[e] = c * xa[t] - sn * ya[t];
+              aj[e] = sn * xa[t] + c * ya[t];
+            }
           }
           double* wi = Wm + i * LD;
           double* wj = Wm + j * LD;

@@ -67,7 +67,33 @@ def profile(name="large", N=20, warm=True):
             print(f"   {k:12s} {ms:9.2f} ms total  {cnt:5d} launches  {ms / cnt:8.4f} ms avg", flush=True)
 
 
+def dense(reps=10):
+    """Config 5: the dense M x 256 application on the Large operator (CUDA-event kernel time)."""
+    prob = gen.make_problem("large")
+    op = prob.op
+    dev = torch.device("cuda:0")
+    cfg5 = gen.config_by_name("fullrank")
+    mu5, nu5 = gen.parameter_grid(cfg5)
+    ctx = lrcheb.Context(0)
+    ctx.set_operator(torch.from_numpy(op.row_ptr).to(dev), torch.from_numpy(op.col_idx).to(dev),
+                     [torch.from_numpy(v).to(dev) for v in op.vals], op.rho_f, op.lambda_s)
+    ctx.set_params(mu5, nu5)
+    S5 = torch.randn((op.M, cfg5.dense_cols), dtype=torch.float64, device=dev)
+    for _ in range(3):
+        ctx.apply_dense(S5)
+    ms = []
+    for _ in range(reps):
+        ctx.apply_dense(S5)
+        ms.append(ctx.last_kernel_ms())
+    t = float(np.median(ms))
+    fl = 6.0 * op.nnz * cfg5.dense_cols
+    print(f"config5 dense: {t:.3f} ms  {fl / t / 1e9:.2f} TFLOP/s", flush=True)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "dense":
+        dense()
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "profile":
         for nm in sys.argv[2:] or ["large"]:
             for warm in (True, False):
