@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--streams", type=int, default=3, help="concurrent subset solves per GPU")
     ap.add_argument("--no-dense", dest="dense", action="store_false", help="skip the config-5 measurement")
     ap.add_argument("--reserve-sms", type=int, default=3, help="SMs the persistent kernels leave free")
+    ap.add_argument("--groups", type=int, default=1,
+                    help="with --batch S: this many lockstep groups of S subsets run concurrently (own host "
+                         "threads, contexts and streams; SMs reserved as for --streams)")
     ap.add_argument("--batch", type=int, default=0,
                     help="f1: solve this many subsets in lockstep per call (one batched SpMM per iteration) "
                          "instead of independent concurrent streams")
@@ -257,8 +260,10 @@ class GpuLeg:
         else:
             self.prob = gen.make_problem(args.config)
             self.cfg, self.op = self.prob.cfg, self.prob.op
-        self.S = max(1, args.batch if args.batch > 1 else args.streams)
-        self.reserve = args.reserve_sms if (self.S > 1 and args.batch <= 1) else 0
+        self.G = max(1, args.groups) if args.batch > 1 else 1     # concurrent lockstep groups (f1)
+        self.B = args.batch if args.batch > 1 else 1                # subsets per lockstep group
+        self.S = max(1, self.B * self.G if args.batch > 1 else args.streams)
+        self.reserve = args.reserve_sms if (self.S > 1 and (args.batch <= 1 or self.G > 1)) else 0
         op, dev = self.op, self.dev
         self.rp_d, self.ci_d = torch.from_numpy(op.row_ptr).to(dev), torch.from_numpy(op.col_idx).to(dev)
         self.vals_d = [torch.from_numpy(v).to(dev) for v in op.vals]
@@ -308,14 +313,50 @@ class GpuLeg:
             cx.set_params(x, y)
 
     def run_batched(self, nsteps, host):
-        """nsteps subset solves in groups of S solved in lockstep by lrc_solve_batch.
-        host=True: each group's B factors are copied from pinned host memory and its outputs back
-        inside the call sequence (the e2e leg)."""
-        lrcheb, torch, p, cfg = self.lrcheb, self.torch, self.prob, self.cfg
+        """nsteps subset solves in lockstep groups of B subsets (lrc_solve_batch); with G > 1
+        groups, G host threads each run their share of the groups on their own B contexts concurrently."""
+        if self.G > 1:
+            infos = [None] * nsteps
+            errs = []
+            per = self.B * self.G
+
+            def worker(gi):
+                try:
+                    for g0 in range(gi * self.B, nsteps, per):
+                        n = min(self.B, nsteps - g0)
+                        res = self._run_group(g0, n, gi * self.B, host)
+                        for j in range(n):
+                            infos[g0 + j] = res[j]
+                except Exception as e:  # surfaced below
+                    errs.append(e)
+            ths = [threading.Thread(target=worker, args=(gi,)) for gi in range(self.G)]
+            for t in ths:
+                t.start()
+            for t in ths:
+                t.join()
+            if errs:
+                raise errs[0]
+            if host:
+                self.torch.cuda.synchronize()
+            return infos
         infos = [None] * nsteps
-        for g0 in range(0, nsteps, self.S):
-            idx = list(range(g0, min(nsteps, g0 + self.S)))
-            cx = self.ctxs[:len(idx)]
+        for g0 in range(0, nsteps, self.B):
+            n = min(self.B, nsteps - g0)
+            res = self._run_group(g0, n, 0, host)
+            for j in range(n):
+                infos[g0 + j] = res[j]
+        if host:
+            self.torch.cuda.current_stream().synchronize()
+        return infos
+
+    def _run_group(self, g0, n, c0, host):
+        """Subsets g0 .. g0+n-1 in lockstep on contexts c0 .. c0+n-1 (one lrc_solve_batch call).
+        host=True: the B factors are copied from pinned host memory and the outputs back (e2e leg)."""
+        lrcheb, torch, p, cfg = self.lrcheb, self.torch, self.prob, self.cfg
+        infos = [None] * n
+        if True:
+            idx = list(range(g0, g0 + n))
+            cx = self.ctxs[c0:c0 + n]
             bus, bvs = [], []
             for c, i in zip(cx, idx):
                 d_mu, d_nu, bu, bv, bu_h, bv_h = self.inputs[i % len(self.inputs)]
@@ -325,16 +366,14 @@ class GpuLeg:
                     bv = bv_h.to(self.dev, non_blocking=True)
                 bus.append(bu)
                 bvs.append(bv)
-            outs = [(o[0], o[1]) for o in self.outs[:len(idx)]]
+            outs = [(o[0], o[1]) for o in self.outs[c0:c0 + n]]
             res = lrcheb.solve_batch(cx, bus, bvs, p.lam_min, p.lam_max, cfg.tol, cfg.rank_cap, cfg.n_iter,
                                      outs=outs)
-            for j, i in enumerate(idx):
-                infos[i] = res[j][2]
+            for j in range(n):
+                infos[j] = res[j][2]
                 if host:
-                    self.outs[j][2].copy_(res[j][0], non_blocking=True)
-                    self.outs[j][3].copy_(res[j][1], non_blocking=True)
-        if host:
-            torch.cuda.current_stream().synchronize()
+                    self.outs[c0 + j][2].copy_(res[j][0], non_blocking=True)
+                    self.outs[c0 + j][3].copy_(res[j][1], non_blocking=True)
         return infos
 
     def run_steps(self, nsteps, host):
@@ -397,8 +436,9 @@ class GpuLeg:
         return {"workload": workload_str(self.cfg, self.op, self.n),
                 "step": "one full ChebyshevT solve of one parameter subset (N iterations + final residual)",
                 "concurrent_subsets_per_gpu": self.S, "reserved_sms": self.reserve,
-                "subset_schedule": (f"f1 batched lockstep: {self.S} subsets per lrc_solve_batch call (one fused SpMM "
-                                    f"pass per iteration for all of them)") if self.args.batch > 1 else
+                "subset_schedule": (f"f1 batched lockstep: {self.B} subsets per lrc_solve_batch call (one fused SpMM "
+                                    f"pass per iteration for all of them), {self.G} such group(s) concurrently")
+                                   if self.args.batch > 1 else
                                    f"{self.S} independent solves on concurrent streams",
                 "l2": f"inputs larger than L2 (operator {operator_bytes(self.op) / 1e9:.2f} GB vs 126 MB)"
                       if operator_bytes(self.op) > L2_BYTES else "operator fits in L2 (latency-bound config)"}
@@ -427,8 +467,8 @@ class GpuLeg:
         S = min(len(self.ctxs), 4)
         if S < 2 or self.args.batch > 1:
             return None
-        saved = self.args.batch
-        self.args.batch = S
+        saved = self.args.batch, self.B, self.G
+        self.args.batch, self.B, self.G = S, S, 1
         try:
             self.run_batched(S, False)                       # capture the batch graph
             torch.cuda.synchronize()
@@ -439,7 +479,7 @@ class GpuLeg:
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1)
         finally:
-            self.args.batch = saved
+            self.args.batch, self.B, self.G = saved
         return {"value": S * calls * self.cfg.n_iter / (ms / 1e3), "unit": "iterations/s", "subsets_per_call": S,
                 "calls": calls, "note": "f1 lockstep: one fused SpMM pass per iteration for all S subsets' U, their "
                                         "truncations on S streams; the headline's independent concurrent streams "

@@ -703,7 +703,11 @@ constexpr int kUStages = LRC_SPMM_U_STAGES;     // U row stages
 #ifndef LRC_SPMM_PREFETCH
 #define LRC_SPMM_PREFETCH 4
 #endif
+#ifndef LRC_SPMM_MT
+#define LRC_SPMM_MT 2
+#endif
 constexpr int kTCons = LRC_SPMM_CONS;     // consumer warps (the operator of P:30-36)
+constexpr int kTMt = LRC_SPMM_MT;         // 16-column m-tiles per consumer task (columns per task = 16 kTMt)
 constexpr int kTConsGen = 8;              // consumer warps for general term lists (more registers)
 constexpr int kRawStride = 908;           // doubles per raw array per stage (>= kTileNnz + 3, == 12 mod 16)
 constexpr int kTUrowMax = kTileUrows;     // staged U rows per tile
@@ -755,7 +759,7 @@ spmm_tma_kernel(SpmmArgs a) {
     const int* dr = S > 1 ? a.d_rs[q] : a.d_r;
     rsub[q] = (q < S) ? (dr ? *dr : a.r_fixed) : 0;
   }
-  const int CT = (rmax + 31) >> 5;
+  const int CT = (rmax + 16 * kTMt - 1) / (16 * kTMt);
   const int tpt = 4 * CT;                        // (virtual) tasks per work item: 4 blocks x CT column slices
   if (tid == 0) {
     for (int q = 0; q < nsr; ++q) { mbar_init(&full_r[q], 1); mbar_init(&empty_r[q], NCW); }
@@ -889,7 +893,7 @@ spmm_tma_kernel(SpmmArgs a) {
     const long long sst = a.out_sstride ? a.out_sstride : r;
     const int nb = R[2];
     const int off = R[0] & 1;                      // the stage starts at the even element before e0
-    const int b = task / CT, n0 = (task - b * CT) * 32;
+    const int b = task / CT, n0 = (task - b * CT) * (16 * kTMt);
     if (b < nb && n0 < r) {
       const int row0 = R[4 + b], g = R[8 + b], L = R[12 + b], cb = kRecHdr + R[16 + b], nbase = R[20 + b];
       const int lrow0 = R[24 + b];
@@ -923,12 +927,16 @@ spmm_tma_kernel(SpmmArgs a) {
         }
       }
       // A operand (U^T): columns n0 + mt*16 + gid (+8), entry j = k0 + tig -> staged U row R[cb + j]
-      const int c00 = n0 + gid, c01 = c00 + 8, c10 = c00 + 16, c11 = c00 + 24;
-      const bool v00 = c00 < r, v01 = c01 < r, v10 = c10 < r, v11 = c11 < r;
-      const int jmax = L - 1;
-      double acc[2][NT][4];
+      int cc[kTMt][2];
+      bool vv[kTMt][2];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+      for (int mt = 0; mt < kTMt; ++mt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) { cc[mt][h] = n0 + gid + 16 * mt + 8 * h; vv[mt][h] = cc[mt][h] < r; }
+      const int jmax = L - 1;
+      double acc[kTMt][NT][4];
+#pragma unroll
+      for (int mt = 0; mt < kTMt; ++mt)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.0;
       const int L4 = (L + 3) & ~3;
@@ -936,8 +944,12 @@ spmm_tma_kernel(SpmmArgs a) {
   {                                                                                  \
     const int k0 = (K0);                                                             \
     const double* u = su + (U_OFF);                                                  \
-        const double x0 = v00 ? u[c00] : 0.0, x1 = v01 ? u[c01] : 0.0;              \
-        const double x2 = v10 ? u[c10] : 0.0, x3 = v11 ? u[c11] : 0.0;              \
+        double xf[kTMt][2];                                                         \
+_Pragma("unroll")                                                                   \
+        for (int mt = 0; mt < kTMt; ++mt) {                                         \
+          xf[mt][0] = vv[mt][0] ? u[cc[mt][0]] : 0.0;                               \
+          xf[mt][1] = vv[mt][1] ? u[cc[mt][1]] : 0.0;                               \
+        }                                                                           \
         const bool jv = k0 + tig < L;                                               \
         double bv[NT];                                                              \
 _Pragma("unroll")                                                                   \
@@ -949,8 +961,8 @@ _Pragma("unroll")                                                               
         }                                                                           \
 _Pragma("unroll")                                                                   \
         for (int nt = 0; nt < NT; ++nt) {                                           \
-          dmma1684(acc[0][nt], x0, x1, bv[nt]);                                     \
-          dmma1684(acc[1][nt], x2, x3, bv[nt]);                                     \
+_Pragma("unroll")                                                                   \
+          for (int mt = 0; mt < kTMt; ++mt) dmma1684(acc[mt][nt], xf[mt][0], xf[mt][1], bv[nt]); \
         }                                                                           \
   }
       if (L4 <= 48) {
@@ -970,7 +982,7 @@ _Pragma("unroll")                                                               
       }
 #undef LRC_TMA_STEP
       // epilogue: frag (m, n) -> column n0 + mt*16 + gid (+8), slot nt*8 + 2 tig + e = G q + group
-      const bool full_cols = n0 + 32 <= r;
+      const bool full_cols = n0 + 16 * kTMt <= r;
       const int s2g = GEN ? a.id_group : 0;       // the identity-diagonal group carries U - g W
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
@@ -985,7 +997,7 @@ _Pragma("unroll")                                                               
           // the block's own U row (S2 epilogue) from the staged rows when present
           const double* us_ = (lrow0 >= 0) ? su + (size_t)(lrow0 + q) * ldu + n0 + gid : Uq + row * ldu + n0 + gid;
 #pragma unroll
-          for (int mt = 0; mt < 2; ++mt)
+          for (int mt = 0; mt < kTMt; ++mt)
 #pragma unroll
             for (int hm = 0; hm < 2; ++hm) {
               const int o = mt * 16 + hm * 8, c = n0 + gid + o;

@@ -236,3 +236,64 @@ def test_config5_dense_on_large_operator(large_dev):
     err = np.linalg.norm(Y[rows] - ref) / np.linalg.norm(ref)
     assert err <= 1e-12, err
     ctx.close()
+
+
+def test_large_lockstep_groups_concurrent(large_dev):
+    """f1 in the bench's group form (bench.py --batch 3 --groups 2): two lockstep groups of three
+    subsets (lrc_solve_batch, one batched SpMM per iteration each) on their own host threads, contexts
+    and streams, 3 SMs reserved -> every subset's X_N rows and rho against the oracle goldens."""
+    require_gpu()
+    from paper_2008_10275_b200 import lrcheb
+    prob, rp, ci, vals = large_dev
+    cfg, op = prob.cfg, prob.op
+    groups = [(0, 1, 2), (2, 1, 0)]
+    ctxs, ins, outs = [], [], []
+    for grp in groups:
+        cg, ig, og = [], [], []
+        for k in grp:
+            c = lrcheb.Context(0)
+            c.set_reserved_sms(3)
+            c.set_operator(rp, ci, vals, op.rho_f, op.lambda_s, borrow=True)
+            d_mu, d_nu, BU, BV = prob.subset(k)
+            c.set_params(d_mu, d_nu)
+            cg.append(c)
+            ig.append((k, torch.from_numpy(BU).cuda(), torch.from_numpy(BV).cuda()))
+            og.append((torch.empty((op.M, cfg.rank_cap), dtype=torch.float64, device="cuda"),
+                       torch.empty((len(d_mu), cfg.rank_cap), dtype=torch.float64, device="cuda")))
+        ctxs.append(cg); ins.append(ig); outs.append(og)
+    results = [None, None]
+    errs = []
+
+    def worker(gi):
+        try:
+            for _ in range(2):      # the second call replays the captured batch graph
+                results[gi] = lrcheb.solve_batch(ctxs[gi], [x[1] for x in ins[gi]], [x[2] for x in ins[gi]],
+                                                 prob.lam_min, prob.lam_max, cfg.tol, cfg.rank_cap, cfg.n_iter,
+                                                 outs=outs[gi])
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    ths = [threading.Thread(target=worker, args=(gi,)) for gi in range(2)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errs, errs
+    torch.cuda.synchronize()
+    checked = 0
+    for gi in range(2):
+        for j, (k, _, _) in enumerate(ins[gi]):
+            if not os.path.exists(os.path.join(GOLDEN, f"large_s{k}.npz")):
+                continue
+            g = _golden("large", k)
+            U, V, info = results[gi][j]
+            _check_ranks(info["rank_history"], g, cfg.tol, cfg.rank_cap)
+            err = _rows_rel(U.cpu().numpy(), V.cpu().numpy(), info["rank"], g["U_ck"][-1], g["V_ck"][-1],
+                            int(g["ranks"][-1]), g["rows"])
+            assert err <= 1e-8, (gi, k, err)
+            assert abs(info["rel_residual"] - float(g["rel_residual"])) <= 1e-9, (gi, k, info["rel_residual"])
+            checked += 1
+    assert checked >= 2
+    for cg in ctxs:
+        for c in cg:
+            c.close()
