@@ -445,11 +445,15 @@ __global__ void __launch_bounds__(kT) chol2_svd_kernel(State st, SmallBufs b, in
   const double tol2 = kJacobiTol * kJacobiTol;
   const int half = lane >> 4, hl = lane & 15;
   const int P = p + (p & 1), NP = P / 2;
+  // only the warps that own pairs (two per warp) take part; they synchronise on a named barrier
+  const int nwj = (NP + 1) / 2;
+  const unsigned jbar = 32u * (unsigned)nwj;
   int sweeps_done = 0;
+  if (warp < nwj) {
   for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
     ++sweeps_done;
     if (tid == 0) s_rot = 0;
-    __syncthreads();
+    asm volatile("bar.sync 1, %0;\n" ::"r"(jbar) : "memory");
     for (int r = 0; r < P - 1; ++r) {
       for (int qb = warp * 2; qb < NP; qb += kT / 16) {
         const int q = qb + half;
@@ -504,12 +508,14 @@ __global__ void __launch_bounds__(kT) chol2_svd_kernel(State st, SmallBufs b, in
           if (hl == 0) s_rot = 1;
         }
       }
-      __syncthreads();
+      asm volatile("bar.sync 1, %0;\n" ::"r"(jbar) : "memory");
     }
     const int rot = s_rot;
-    __syncthreads();
+    asm volatile("bar.sync 1, %0;\n" ::"r"(jbar) : "memory");
     if (rot == 0) break;
   }
+  }
+  __syncthreads();   // the idle warps rejoin here
   if (tid == 0) atomicAdd(st.sweeps, sweeps_done);
   long long tclk2 = clock64();
   // singular values of R, then of X:  R^T R = (1 + s2) X^T X + s1 s2 I  (exact for the shifted
