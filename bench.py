@@ -354,26 +354,25 @@ class GpuLeg:
         host=True: the B factors are copied from pinned host memory and the outputs back (e2e leg)."""
         lrcheb, torch, p, cfg = self.lrcheb, self.torch, self.prob, self.cfg
         infos = [None] * n
-        if True:
-            idx = list(range(g0, g0 + n))
-            cx = self.ctxs[c0:c0 + n]
-            bus, bvs = [], []
-            for c, i in zip(cx, idx):
-                d_mu, d_nu, bu, bv, bu_h, bv_h = self.inputs[i % len(self.inputs)]
-                self.set_subset(c, d_mu, d_nu)
-                if host:
-                    bu = bu_h.to(self.dev, non_blocking=True)
-                    bv = bv_h.to(self.dev, non_blocking=True)
-                bus.append(bu)
-                bvs.append(bv)
-            outs = [(o[0], o[1]) for o in self.outs[c0:c0 + n]]
-            res = lrcheb.solve_batch(cx, bus, bvs, p.lam_min, p.lam_max, cfg.tol, cfg.rank_cap, cfg.n_iter,
-                                     outs=outs)
-            for j in range(n):
-                infos[j] = res[j][2]
-                if host:
-                    self.outs[c0 + j][2].copy_(res[j][0], non_blocking=True)
-                    self.outs[c0 + j][3].copy_(res[j][1], non_blocking=True)
+        idx = list(range(g0, g0 + n))
+        cx = self.ctxs[c0:c0 + n]
+        bus, bvs = [], []
+        for c, i in zip(cx, idx):
+            d_mu, d_nu, bu, bv, bu_h, bv_h = self.inputs[i % len(self.inputs)]
+            self.set_subset(c, d_mu, d_nu)
+            if host:
+                bu = bu_h.to(self.dev, non_blocking=True)
+                bv = bv_h.to(self.dev, non_blocking=True)
+            bus.append(bu)
+            bvs.append(bv)
+        outs = [(o[0], o[1]) for o in self.outs[c0:c0 + n]]
+        res = lrcheb.solve_batch(cx, bus, bvs, p.lam_min, p.lam_max, cfg.tol, cfg.rank_cap, cfg.n_iter,
+                                 outs=outs)
+        for j in range(n):
+            infos[j] = res[j][2]
+            if host:
+                self.outs[c0 + j][2].copy_(res[j][0], non_blocking=True)
+                self.outs[c0 + j][3].copy_(res[j][1], non_blocking=True)
         return infos
 
     def run_steps(self, nsteps, host):
