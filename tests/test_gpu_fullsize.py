@@ -2,7 +2,7 @@
 ChebyshevT results match the oracle within the stated tolerances on all five configs"; operator
 PAPER.md P:30-36, truncation P:544).
 
-* Large (configs[3]), subset 0, all N = 100 iterations through the C ABI, against goldens written by
+* Large (configs[3]), subsets 0 and 1, all N = 100 iterations through the C ABI, against goldens written by
   tests/golden/make_goldens.py (oracle/ + synth/ only): every rank (near-tie exemption S13), every
   core singular-value vector, X_k on 512 seeded rows at k = 10, 20, ..., 100 (rel. Frobenius <= 1e-8),
   and the final residual (|d rho| <= 1e-9).
@@ -66,13 +66,14 @@ def large_dev():
     torch.cuda.empty_cache()
 
 
-def test_large_all_iterations_vs_golden(large_dev):
+@pytest.mark.parametrize("subset", [0, 1])
+def test_large_all_iterations_vs_golden(large_dev, subset):
     require_gpu()
     from paper_2008_10275_b200 import lrcheb
     prob, rp, ci, vals = large_dev
     cfg, op = prob.cfg, prob.op
-    g = _golden("large", 0)
-    d_mu, d_nu, BU, BV = prob.subset(0)
+    g = _golden("large", subset)
+    d_mu, d_nu, BU, BV = prob.subset(subset)
     ctx = lrcheb.Context(0)
     ctx.set_operator(rp, ci, vals, op.rho_f, op.lambda_s, borrow=True)
     ctx.set_params(d_mu, d_nu)
@@ -98,7 +99,7 @@ def test_large_all_iterations_vs_golden(large_dev):
     assert abs(info["rel_residual"] - float(g["rel_residual"])) <= 1e-9, (info["rel_residual"], float(g["rel_residual"]))
     Uh, Vh = U.cpu().numpy(), V.cpu().numpy()
     assert _rows_rel(Uh, Vh, info["rank"], g["U_ck"][-1], g["V_ck"][-1], int(g["ranks"][-1]), rows) <= 1e-8
-    print(f"large s0: worst checkpoint rel err {worst:.2e}, rho {info['rel_residual']:.6e} "
+    print(f"large s{subset}: worst checkpoint rel err {worst:.2e}, rho {info['rel_residual']:.6e} "
           f"(oracle {float(g['rel_residual']):.6e})")
     ctx.close()
 
