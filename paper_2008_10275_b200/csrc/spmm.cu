@@ -728,7 +728,10 @@ size_t tma_smem(int nT, int ldu = kTLdMax) {
 // GEN = false: the operator of P:30-36 (six arrays, the three groups of DESIGN.md K1, fixed combination);
 // GEN = true: a general term list: nT arrays, G groups, group g = sum of up to
 // kGroupTerms arrays with coefficients, slots (row q, group g) = q G + g in NT n-tiles of 8.
-template <int MODE, bool GEN, int NT, int NCW_, int KCG = 4>
+// PAIR: the m index of an m-tile maps to U columns (2 gid, 2 gid + 1) instead of (gid, gid + 8), so a
+// lane's two A-fragment elements, its S2 operand and its two outputs of a slot are one 16-byte access
+// each (needs 16-byte aligned output rows; the host decides).
+template <int MODE, bool GEN, int NT, int NCW_, int KCG = 4, bool PAIR = false>
 __global__ void __launch_bounds__((NCW_ + 1) * 32, 1)
 spmm_tma_kernel(SpmmArgs a) {
   // subsets batched in this pass (one read of the operator for several subsets' U)
@@ -932,7 +935,10 @@ spmm_tma_kernel(SpmmArgs a) {
 #pragma unroll
       for (int mt = 0; mt < kTMt; ++mt)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) { cc[mt][h] = n0 + gid + 16 * mt + 8 * h; vv[mt][h] = cc[mt][h] < r; }
+        for (int h = 0; h < 2; ++h) {
+          cc[mt][h] = PAIR ? n0 + 16 * mt + 2 * gid + h : n0 + gid + 16 * mt + 8 * h;
+          vv[mt][h] = cc[mt][h] < r;
+        }
       const int jmax = L - 1;
       double acc[kTMt][NT][4];
 #pragma unroll
@@ -947,8 +953,15 @@ spmm_tma_kernel(SpmmArgs a) {
         double xf[kTMt][2];                                                         \
 _Pragma("unroll")                                                                   \
         for (int mt = 0; mt < kTMt; ++mt) {                                         \
-          xf[mt][0] = vv[mt][0] ? u[cc[mt][0]] : 0.0;                               \
-          xf[mt][1] = vv[mt][1] ? u[cc[mt][1]] : 0.0;                               \
+          if constexpr (PAIR) {                                                     \
+            const double2 t2 = vv[mt][0] ? *reinterpret_cast<const double2*>(u + cc[mt][0]) \
+                                         : make_double2(0.0, 0.0);                  \
+            xf[mt][0] = t2.x;                                                       \
+            xf[mt][1] = vv[mt][1] ? t2.y : 0.0;                                     \
+          } else {                                                                  \
+            xf[mt][0] = vv[mt][0] ? u[cc[mt][0]] : 0.0;                             \
+            xf[mt][1] = vv[mt][1] ? u[cc[mt][1]] : 0.0;                             \
+          }                                                                         \
         }                                                                           \
         const bool jv = k0 + tig < L;                                               \
         double bv[NT];                                                              \
@@ -992,8 +1005,29 @@ _Pragma("unroll")                                                               
           if (Rs >= G * g) continue;
           const int q = Rs / G, st = Rs - q * G;
           const size_t row = (size_t)(row0 + q);
-          double* orow = outq + st * sst + row * a.ldo + a.out_off + n0 + gid;
           const bool s2 = (MODE == SPMM_S2STEP) && st == s2g;
+          if constexpr (PAIR) {
+            double* orow = outq + st * sst + row * a.ldo + a.out_off + n0 + 2 * gid;
+            const double* us_ = (lrow0 >= 0) ? su + (size_t)(lrow0 + q) * ldu + n0 + 2 * gid
+                                             : Uq + row * ldu + n0 + 2 * gid;
+#pragma unroll
+            for (int mt = 0; mt < kTMt; ++mt) {
+              const int o = mt * 16, c = n0 + 2 * gid + o;
+              if (full_cols || c < r) {
+                double v0 = acc[mt][nt][e], v1 = acc[mt][nt][2 + e];
+                if (s2) {
+                  const double2 uu = *reinterpret_cast<const double2*>(us_ + o);
+                  v0 = fma(-a.gamma, v0, uu.x);
+                  v1 = fma(-a.gamma, v1, uu.y);
+                }
+                if (full_cols || c + 1 < r) __stcs(reinterpret_cast<double2*>(orow + o), make_double2(v0, v1));
+                else if (a.out_sstride) __stcs(reinterpret_cast<double2*>(orow + o), make_double2(v0, 0.0));   // zero pad column
+                else __stcs(orow + o, v0);
+              }
+            }
+            continue;
+          }
+          double* orow = outq + st * sst + row * a.ldo + a.out_off + n0 + gid;
           // the block's own U row (S2 epilogue) from the staged rows when present
           const double* us_ = (lrow0 >= 0) ? su + (size_t)(lrow0 + q) * ldu + n0 + gid : Uq + row * ldu + n0 + gid;
 #pragma unroll
@@ -1221,6 +1255,22 @@ bool tma_ok(const SpmmArgs& a, int rmax) {
   return al;
 }
 
+// 16-byte output accesses of the PAIR column mapping: even row stride / offsets, aligned bases, and a
+// group stride known to be even on the host
+bool tma_pair_ok(const SpmmArgs& a) {
+#ifdef LRC_SPMM_NOPAIR
+  return false;
+#endif
+  bool ok = !a.gen && (a.ldo % 2 == 0) && (a.out_off % 2 == 0);
+  if (a.out_sstride) ok = ok && (a.out_sstride % 2 == 0);
+  else ok = ok && a.nsub <= 1 && a.d_r == nullptr && (a.r_fixed % 2 == 0);
+  for (int q = 0; q < max(1, a.nsub); ++q) {
+    const double* o = a.nsub > 1 ? a.outs[q] : a.out;
+    ok = ok && ((reinterpret_cast<uintptr_t>(o) & 15) == 0);
+  }
+  return ok;
+}
+
 template <int MODE>
 cudaError_t launch_m(const SpmmArgs& a0, int rmax, cudaStream_t s) {
   SpmmArgs a = a0;
@@ -1235,7 +1285,10 @@ cudaError_t launch_m(const SpmmArgs& a0, int rmax, cudaStream_t s) {
     if (tma_ok(a, rmax) && a.ntl_u > 0) {
       const int grid = min(a.ntl_u, max(1, sm_count() - max(0, a.reserved_sms)));
       if (!a.gen) {
-        spmm_tma_kernel<MODE, false, 2, kTCons><<<grid, (kTCons + 1) * 32, tma_smem(6, a.ldu), s>>>(a);
+        if (tma_pair_ok(a))
+          spmm_tma_kernel<MODE, false, 2, kTCons, 4, true><<<grid, (kTCons + 1) * 32, tma_smem(6, a.ldu), s>>>(a);
+        else
+          spmm_tma_kernel<MODE, false, 2, kTCons><<<grid, (kTCons + 1) * 32, tma_smem(6, a.ldu), s>>>(a);
       } else {
         const int nt = (5 * a.G + 7) / 8;          // slots (row, group) of a node block in n-tiles of 8
         int kmax = 0;
@@ -1321,6 +1374,8 @@ cudaError_t prep_m() {
     if (e != cudaSuccess) return e;
     const int mx = (int)std::min(std::max(tma_smem(6), tma_smem(kMaxT)), (size_t)kTmaSmemMax);
     e = cudaFuncSetAttribute(spmm_tma_kernel<MODE, false, 2, kTCons>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(spmm_tma_kernel<MODE, false, 2, kTCons, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     if (e != cudaSuccess) return e;
 #define LRC_TMA_ATTR(NT_, KC_)                                                                          \
     e = cudaFuncSetAttribute(spmm_tma_kernel<MODE, true, NT_, kTConsGen, KC_>,                          \
