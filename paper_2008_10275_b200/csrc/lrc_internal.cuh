@@ -12,7 +12,10 @@ constexpr int kMaxW = 256;       // max concatenation width w = r_B + 4 r
 constexpr int kGroupMax = 8;     // rows per node block in the fused SpMM
 constexpr int kSpmmCap = 1024;   // nnz staged per SpMM CTA tile
 constexpr int kValCap = 3200;    // staged (combined, row-padded) doubles per SpMM tile
-constexpr int kTileBlocks = 4;   // node blocks per SpMM tile
+#ifndef LRC_TILE_BLOCKS
+#define LRC_TILE_BLOCKS 4
+#endif
+constexpr int kTileBlocks = LRC_TILE_BLOCKS;   // node blocks per SpMM tile
 constexpr int kUCap = 90;        // deduplicated U rows staged in shared memory per SpMM tile
 // SpMM tile descriptor (int32 words): [0] e0 (first nnz) [1] tot (nnz) [2] nb (blocks) [3] nu (U rows
 // staged; 0 = L2-gather tile) [4] rbeg [5] rend [6] staged doubles (3 streams, padded rows) [7] pad, [8+b] row0, [12+b] g, [16+b] L, [20+b] local U row of the block's
@@ -32,8 +35,8 @@ constexpr int kSigmaStride = 128;
 constexpr int kRecInts = 256;
 constexpr int kRecHdr = 32;
 constexpr int kRecCols = kRecInts - kRecHdr;
-constexpr int kTileNnz = 900;      // nnz per tile of the TMA kernel (4 interior FE node blocks)
-constexpr int kTileUrows = 90;     // staged U rows per tile of the TMA kernel
+constexpr int kTileNnz = 225 * kTileBlocks;      // nnz per tile of the TMA kernel (interior FE node blocks: 5 rows x 45)
+constexpr int kTileUrows = 15 * (kTileBlocks + 2);     // staged U rows per tile of the TMA kernel (3 grid rows x (blocks + 2) nodes x 5)
 constexpr int kMetaInts = 16;      // per-tile metadata of the TMA kernel: e0, nnz, runs, 0, 4 x (first row,
 constexpr int kMetaRuns = 4;       //   rows, local first row) of the staged U row runs
 

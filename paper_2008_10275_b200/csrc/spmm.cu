@@ -709,10 +709,15 @@ constexpr int kUStages = LRC_SPMM_U_STAGES;     // U row stages
 constexpr int kTCons = LRC_SPMM_CONS;     // consumer warps (the operator of P:30-36)
 constexpr int kTMt = LRC_SPMM_MT;         // 16-column m-tiles per consumer task (columns per task = 16 kTMt)
 constexpr int kTConsGen = 8;              // consumer warps for general term lists (more registers)
-constexpr int kRawStride = 908;           // doubles per raw array per stage (>= kTileNnz + 3, == 12 mod 16)
+constexpr int kRawStride = ((kTileNnz + 3 + 3) / 16) * 16 + 12;   // doubles per raw array per stage (>= kTileNnz + 3, == 12 mod 16)
+static_assert(kRawStride >= kTileNnz + 3 && kRawStride % 16 == 12, "raw stage stride");
 constexpr int kTUrowMax = kTileUrows;     // staged U rows per tile
 constexpr int kTLdMax = 64;               // U leading dimension supported (r <= 64)
 constexpr int kTPrefetch = LRC_SPMM_PREFETCH;   // raw values warmed into L2 this many tiles ahead (0: off)
+#ifndef LRC_SPMM_UPREFETCH
+#define LRC_SPMM_UPREFETCH 2
+#endif
+constexpr int kTUPrefetch = LRC_SPMM_UPREFETCH;  // U row runs warmed into L2 this many tiles ahead (0: off)
 
 // raw value stages for nT value arrays (3 up to six arrays, 2 beyond: shared memory)
 __host__ __device__ __forceinline__ int tma_raw_stages(int nT) { return nT <= 6 ? kTStages : 2; }
@@ -763,7 +768,7 @@ spmm_tma_kernel(SpmmArgs a) {
     rsub[q] = (q < S) ? (dr ? *dr : a.r_fixed) : 0;
   }
   const int CT = (rmax + 16 * kTMt - 1) / (16 * kTMt);
-  const int tpt = 4 * CT;                        // (virtual) tasks per work item: 4 blocks x CT column slices
+  const int tpt = kTileBlocks * CT;              // (virtual) tasks per work item: blocks x CT column slices
   if (tid == 0) {
     for (int q = 0; q < nsr; ++q) { mbar_init(&full_r[q], 1); mbar_init(&empty_r[q], NCW); }
     for (int q = 0; q < kUStages; ++q) { mbar_init(&full_u[q], 1); mbar_init(&empty_u[q], NCW); }
@@ -842,8 +847,27 @@ spmm_tma_kernel(SpmmArgs a) {
         if (rl > 0)
           bulk_g2s(s_ub + (size_t)us * kTUrowMax * ldu_s + (size_t)rs * ldu, Usrc + (size_t)rg * ldu,
                    (unsigned)rl * (unsigned)ldu * 8u, &full_u[us]);
+        // warm the U row runs of a later tile into L2: the first touch of a U row (written evict-first
+        // by the basis pass) is a DRAM read, and the U copy is the tile's critical path
+        if (kTUPrefetch > 0 && i + kTUPrefetch < nmine) {
+          const int ip = i + kTUPrefetch;
+          const int nrp = meta(ip, W2{});
+          int pv[2 * kMetaRuns];
+          pv[0] = meta(ip, std::integral_constant<int, 4>{});  pv[1] = meta(ip, std::integral_constant<int, 5>{});
+          pv[2] = meta(ip, std::integral_constant<int, 7>{});  pv[3] = meta(ip, std::integral_constant<int, 8>{});
+          pv[4] = meta(ip, std::integral_constant<int, 10>{}); pv[5] = meta(ip, std::integral_constant<int, 11>{});
+          pv[6] = meta(ip, std::integral_constant<int, 13>{}); pv[7] = meta(ip, std::integral_constant<int, 14>{});
+          int pg = 0, pl = 0;
+#pragma unroll
+          for (int k = 0; k < kMetaRuns; ++k)
+            if (myr == k && k < nrp) { pg = pv[2 * k]; pl = pv[2 * k + 1]; }
+          if (pl > 0) bulk_prefetch_l2(Usrc + (size_t)pg * ldu, (unsigned)pl * (unsigned)ldu * 8u);
+        }
       }
-      for (; ri < nmine && ri <= i + nsr - 1; ++ri) {
+#ifndef LRC_SPMM_RAW_AHEAD
+#define LRC_SPMM_RAW_AHEAD 2
+#endif
+      for (; ri < nmine && ri <= i + nsr - LRC_SPMM_RAW_AHEAD; ++ri) {
         const int tr = blockIdx.x + ri * Gd, sr = ri % nsr;
         const int e0 = meta(ri, W0{}), tot = meta(ri, W1{});
         int pe0 = 0, ptot = 0;
