@@ -64,6 +64,7 @@ struct SpmmArgs {
   int ntl_g;
   const int* tlist;         // (set by the launcher) tile list, or null for all tiles
   int u_aligned16;          // (set by the launcher) U rows may be copied in 16-byte chunks
+  int o_pair;               // (set by the launcher) output rows admit 16-byte stores at even columns
   const int* row_ptr;
   const int* col_idx;
   const double* v[kMaxT];   // value arrays: A0, A1, A2, Jrho, Jmu, Jlam (legacy) or the T arrays of a term list

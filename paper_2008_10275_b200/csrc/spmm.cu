@@ -715,7 +715,7 @@ constexpr int kTUrowMax = kTileUrows;     // staged U rows per tile
 constexpr int kTLdMax = 64;               // U leading dimension supported (r <= 64)
 constexpr int kTPrefetch = LRC_SPMM_PREFETCH;   // raw values warmed into L2 this many tiles ahead (0: off)
 #ifndef LRC_SPMM_UPREFETCH
-#define LRC_SPMM_UPREFETCH 2
+#define LRC_SPMM_UPREFETCH 0
 #endif
 constexpr int kTUPrefetch = LRC_SPMM_UPREFETCH;  // U row runs warmed into L2 this many tiles ahead (0: off)
 
@@ -1085,7 +1085,9 @@ _Pragma("unroll")                                                               
 // deduplicated S rows is staged (16-byte cp.async), every warp contracts one (node block, 32-column
 // half) exactly like the hot kernel (transposed m16n8k4, D = S_chunk^T Vals^T) and combines the three
 // streams of D in registers (five quad shuffles) into Y[row][c] = D[c][3q] + d_mu[c] D[c][3q+1] +
-// d_nu[c] D[c][3q+2], stored as 64-byte row segments.  No D slab: ~75 KB of shared memory per CTA.
+// d_nu[c] D[c][3q+2].  The m rows (gid, gid + 8) of an m-tile map to the adjacent columns
+// (2 gid, 2 gid + 1): one 16-byte A-fragment load per m-tile and k4 step, one 16-byte store per
+// output row and m-tile (128-byte row segments per warp store).  No D slab: ~75 KB of shared memory per CTA.
 constexpr int kDenseChunk = 64;
 constexpr int kDenseUst = kDenseChunk + 4;          // == 4 mod 16 doubles
 
@@ -1193,28 +1195,35 @@ spmm_dense_kernel(SpmmArgs a) {
           for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.0;
         const int L4 = (L + 3) & ~3;
         const double* vb = s_v + s_vbase[b] + (qo * 3 + gid) * lp + tig;
-        const double* ub = s_u + n0 + gid;
+        const double* ub = s_u + n0 + 2 * gid;     // paired columns: m rows (gid, gid + 8) <-> columns (2 gid, 2 gid + 1)
         const unsigned short* lc = lx + cb + tig;
         const int lmax = L - 1 - tig;
 #pragma unroll 2
         for (int k0 = 0; k0 < L4; k0 += 4) {
           const double b0 = vb[k0], b1 = vb[8 * lp + k0];
           const double* urow = ub + (int)lc[min(k0, lmax)] * kDenseUst;
-          const double a00 = urow[0], a01 = urow[8], a10 = urow[16], a11 = urow[24];
-          dmma1684(acc[0][0], a00, a01, b0);
-          dmma1684(acc[0][1], a00, a01, b1);
-          dmma1684(acc[1][0], a10, a11, b0);
-          dmma1684(acc[1][1], a10, a11, b1);
+          const double2 p0 = *reinterpret_cast<const double2*>(urow), p1 = *reinterpret_cast<const double2*>(urow + 16);
+          dmma1684(acc[0][0], p0.x, p0.y, b0);
+          dmma1684(acc[0][1], p0.x, p0.y, b1);
+          dmma1684(acc[1][0], p1.x, p1.y, b0);
+          dmma1684(acc[1][1], p1.x, p1.y, b1);
         }
         // Y[row q][c] = D[c][3q] + d_mu[c] D[c][3q+1] + d_nu[c] D[c][3q+2].  Lane (gid, t) holds, per
-        // column c = n0 + mt*16 + gid + hm*8, slots v0 = 2t, v1 = 2t+1, v2 = 8+2t, v3 = 9+2t; each of the
+        // column c = n0 + mt*16 + 2 gid + hm, slots v0 = 2t, v1 = 2t+1, v2 = 8+2t, v3 = 9+2t; each of the
         // five outputs of a quad needs exactly one slot of another lane of the quad (five shuffles):
         //   q0 = t0 (0, 1 | 2 from t1)    q1 = t2 (3 from t1 | 4, 5)    q2 = t3 (6, 7 | 8 from t0)
         //   q3 = t1 (9 from t0 | 10, 11)  q4 = t2 (12, 13 | 14 from t3)
+        // The two columns (hm = 0, 1) of a lane are adjacent: one 16-byte store per output row.
         const int base = lane & ~3;
         const int rowq = s_desc[8 + b] + qo;
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int mt = 0; mt < 2; ++mt) {
+          double ya[2] = {0.0, 0.0}, yb[2] = {0.0, 0.0};   // row A (every lane), row B (tig == 2: q4)
+          const int cl = n0 + mt * 16 + 2 * gid;
+          const int c = c0 + cl;
+          double dmv[2] = {0.0, 0.0}, dnv[2] = {0.0, 0.0};
+          if (cl < cw) { dmv[0] = __ldg(a.dmu + c); dnv[0] = __ldg(a.dnu + c); }
+          if (cl + 1 < cw) { dmv[1] = __ldg(a.dmu + c + 1); dnv[1] = __ldg(a.dnu + c + 1); }
 #pragma unroll
           for (int hm = 0; hm < 2; ++hm) {
             const double v0 = acc[mt][0][hm * 2], v1 = acc[mt][0][hm * 2 + 1];
@@ -1224,27 +1233,31 @@ spmm_dense_kernel(SpmmArgs a) {
             const double x0v2 = __shfl_sync(0xffffffffu, v2, base + 0);
             const double x0v3 = __shfl_sync(0xffffffffu, v3, base + 0);
             const double x3v2 = __shfl_sync(0xffffffffu, v2, base + 3);
-            const int cl = n0 + mt * 16 + gid + hm * 8;
-            if (cl >= cw) continue;
-            const int c = c0 + cl;
-            const double dm = __ldg(a.dmu + c), dn = __ldg(a.dnu + c);
-            double* oc = a.out + a.out_off + c;
-            if (tig == 0) {
-              if (0 < gs) __stcs(oc + (size_t)(rowq + 0) * a.ldo, fma(dn, x1v0, fma(dm, v1, v0)));
-            } else if (tig == 1) {
-              if (3 < gs) __stcs(oc + (size_t)(rowq + 3) * a.ldo, fma(dn, v3, fma(dm, v2, x0v3)));
-            } else if (tig == 2) {
-              if (1 < gs) __stcs(oc + (size_t)(rowq + 1) * a.ldo, fma(dn, v1, fma(dm, v0, x1v1)));
-              if (4 < gs) __stcs(oc + (size_t)(rowq + 4) * a.ldo, fma(dn, x3v2, fma(dm, v3, v2)));
-            } else {
-              if (2 < gs) __stcs(oc + (size_t)(rowq + 2) * a.ldo, fma(dn, x0v2, fma(dm, v1, v0)));
-            }
+            const double dm = dmv[hm], dn = dnv[hm];
+            if (tig == 0) ya[hm] = fma(dn, x1v0, fma(dm, v1, v0));
+            else if (tig == 1) ya[hm] = fma(dn, v3, fma(dm, v2, x0v3));
+            else if (tig == 2) { ya[hm] = fma(dn, v1, fma(dm, v0, x1v1)); yb[hm] = fma(dn, x3v2, fma(dm, v3, v2)); }
+            else ya[hm] = fma(dn, x0v2, fma(dm, v1, v0));
           }
+          if (cl >= cw) continue;
+          const int qa = tig == 0 ? 0 : (tig == 1 ? 3 : (tig == 2 ? 1 : 2));
+          double* oc = a.out + a.out_off + c;
+          const bool two = cl + 1 < cw;
+          if (qa < gs) {
+            double* o = oc + (size_t)(rowq + qa) * a.ldo;
+            if (two && a.o_pair) __stcs(reinterpret_cast<double2*>(o), make_double2(ya[0], ya[1]));
+            else { __stcs(o, ya[0]); if (two) __stcs(o + 1, ya[1]); }
+          }
+          if (tig == 2 && 4 < gs) {
+            double* o = oc + (size_t)(rowq + 4) * a.ldo;
+            if (two && a.o_pair) __stcs(reinterpret_cast<double2*>(o), make_double2(yb[0], yb[1]));
+            else { __stcs(o, yb[0]); if (two) __stcs(o + 1, yb[1]); }
+          }
+        }
       }
     }
   }
 }
-
 int ust_for(int rmax) { return ((rmax + 11) / 16) * 16 + 4; }   // >= rmax + 1, == 4 mod 16 (even)
 
 size_t dense_smem() {
@@ -1300,6 +1313,7 @@ cudaError_t launch_m(const SpmmArgs& a0, int rmax, cudaStream_t s) {
   SpmmArgs a = a0;
   // 16-byte U row copies need 16-byte aligned rows and room for the padding element of an odd r
   a.u_aligned16 = ((reinterpret_cast<uintptr_t>(a.U) & 15) == 0) && (a.ldu % 2 == 0) && (rmax < a.ldu || rmax % 2 == 0);
+  a.o_pair = ((reinterpret_cast<uintptr_t>(a.out) & 15) == 0) && (a.ldo % 2 == 0) && (a.out_off % 2 == 0);
   constexpr bool HOT = (MODE == SPMM_S2STEP || MODE == SPMM_PLAIN3);
   if constexpr (HOT) {
     // slack: the predicate-free contraction reads up to 32*CT - 1 columns of the last staged U row
