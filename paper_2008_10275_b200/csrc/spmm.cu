@@ -714,6 +714,9 @@ static_assert(kRawStride >= kTileNnz + 3 && kRawStride % 16 == 12, "raw stage st
 constexpr int kTUrowMax = kTileUrows;     // staged U rows per tile
 constexpr int kTLdMax = 64;               // U leading dimension supported (r <= 64)
 constexpr int kTPrefetch = LRC_SPMM_PREFETCH;   // raw values warmed into L2 this many tiles ahead (0: off)
+#ifndef LRC_SPMM_NOPRED
+#define LRC_SPMM_NOPRED 1
+#endif
 #ifndef LRC_SPMM_UPREFETCH
 #define LRC_SPMM_UPREFETCH 0
 #endif
@@ -977,7 +980,13 @@ spmm_tma_kernel(SpmmArgs a) {
         double xf[kTMt][2];                                                         \
 _Pragma("unroll")                                                                   \
         for (int mt = 0; mt < kTMt; ++mt) {                                         \
-          if constexpr (PAIR) {                                                     \
+          if constexpr (PAIR && LRC_SPMM_NOPRED) {                                  \
+            /* no column predicate: an A element of a column >= r only reaches accumulator rows   \
+               that are never stored, and the read stays inside the dynamic shared memory */     \
+            const double2 t2 = *reinterpret_cast<const double2*>(u + cc[mt][0]);    \
+            xf[mt][0] = t2.x;                                                       \
+            xf[mt][1] = t2.y;                                                       \
+          } else if constexpr (PAIR) {                                              \
             const double2 t2 = vv[mt][0] ? *reinterpret_cast<const double2*>(u + cc[mt][0]) \
                                          : make_double2(0.0, 0.0);                  \
             xf[mt][0] = t2.x;                                                       \
@@ -994,7 +1003,8 @@ _Pragma("unroll")                                                               
           double v = co[nt][0] * raw[po[nt][0] + k0];                               \
 _Pragma("unroll")                                                                   \
           for (int k = 1; k < KC; ++k) v = fma(co[nt][k], raw[po[nt][k] + k0], v);  \
-          bv[nt] = (jv && sv[nt]) ? v : 0.0;                                        \
+          /* an absent slot (sv false) only feeds output columns that are never stored */        \
+          bv[nt] = (jv && (sv[nt] || (PAIR && LRC_SPMM_NOPRED))) ? v : 0.0;         \
         }                                                                           \
 _Pragma("unroll")                                                                   \
         for (int nt = 0; nt < NT; ++nt) {                                           \
