@@ -906,12 +906,14 @@ spmm_tma_kernel(SpmmArgs a) {
   // Every warp walks all work items in order and waits on every stage phase (a warp that skipped an
   // item could see a stage's barrier two phases behind and take the stale parity for a completed one);
   // it arrives once per item on the U stage's empty barrier and once per tile on the raw stage's.
+  // item counters kept incrementally (no per-item divisions): tile i, subset q, raw stage sr and its
+  // phase pr, U stage us and its phase pu, rot = (m * tpt) mod NCW
+  int i = 0, q = 0, sr = 0, us = 0, rot = 0;
+  unsigned pr = 0, pu = 0;
   for (int m = 0; m < nwork; ++m) {
-    const int i = m / S, q = m - i * S;
-    const int sr = i % nsr, us = m % kUStages;
-    mbar_wait(&full_r[sr], (i / nsr) & 1);
-    mbar_wait(&full_u[us], (m / kUStages) & 1);
-    for (int task = (warp - (int)(((long long)m * tpt) % NCW) + NCW) % NCW; task < tpt; task += NCW) {
+    mbar_wait(&full_r[sr], pr);
+    mbar_wait(&full_u[us], pu);
+    for (int task = warp - rot + (warp < rot ? NCW : 0); task < tpt; task += NCW) {
     const int* R = s_rec + sr * kRecInts;
     const double* raw = s_raw + (size_t)sr * nT * kRawStride;
     const double* su = s_ub + (size_t)us * kTUrowMax * ldu_s;
@@ -923,7 +925,9 @@ spmm_tma_kernel(SpmmArgs a) {
     const long long sst = a.out_sstride ? a.out_sstride : r;
     const int nb = R[2];
     const int off = R[0] & 1;                      // the stage starts at the even element before e0
-    const int b = task / CT, n0 = (task - b * CT) * (16 * kTMt);
+    // CT <= 2 for 32-column tasks (r <= 64): no integer division on the task path
+    const int b = (kTMt == 2) ? (CT == 2 ? task >> 1 : task) : task / CT;
+    const int n0 = (task - b * CT) * (16 * kTMt);
     if (b < nb && n0 < r) {
       const int row0 = R[4 + b], g = R[8 + b], L = R[12 + b], cb = kRecHdr + R[16 + b], nbase = R[20 + b];
       const int lrow0 = R[24 + b];
@@ -1085,6 +1089,13 @@ _Pragma("unroll")                                                               
     if (lane == 0) {
       mbar_arrive(&empty_u[us]);
       if (q == S - 1) mbar_arrive(&empty_r[sr]);
+    }
+    rot += tpt;
+    while (rot >= NCW) rot -= NCW;
+    if (++us == kUStages) { us = 0; pu ^= 1u; }
+    if (++q == S) {
+      q = 0; ++i;
+      if (++sr == nsr) { sr = 0; pr ^= 1u; }
     }
   }
 }
