@@ -1035,8 +1035,48 @@ _Pragma("unroll")                                                               
       // epilogue: frag (m, n) -> column n0 + mt*16 + gid (+8), slot nt*8 + 2 tig + e = G q + group
       const bool full_cols = n0 + 16 * kTMt <= r;
       const int s2g = GEN ? a.id_group : 0;       // the identity-diagonal group carries U - g W
+      if constexpr (PAIR) {
+        // paired mapping: the 64-bit bases and the per-m-tile column predicates are formed once per
+        // task; a slot (nt, e) then costs one select, one 32-bit offset and the 16-byte accesses
+        double* ob = outq + ((long long)row0 * a.ldo + a.out_off + n0 + 2 * gid);
+        const double* ubs = (lrow0 >= 0) ? su + lrow0 * ldu + n0 + 2 * gid
+                                         : Uq + ((size_t)row0 * ldu + n0 + 2 * gid);
+        bool ok[kTMt], two[kTMt];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
+        for (int mt = 0; mt < kTMt; ++mt) {
+          const int c = n0 + 2 * gid + 16 * mt;
+          ok[mt] = full_cols || c < r;
+          two[mt] = full_cols || c + 1 < r;
+        }
+        const bool padz = a.out_sstride != 0;     // (even-padded Ucat block) zero pad column of an odd r
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int Rs = nt * 8 + 2 * tig + e;
+            if (Rs >= G * g) continue;
+            const int q = Rs / G, st = Rs - q * G;
+            double* orow = ob + ((long long)st * sst + q * a.ldo);
+            const bool s2 = (MODE == SPMM_S2STEP) && st == s2g;
+            const double* us_ = ubs + q * ldu;
+#pragma unroll
+            for (int mt = 0; mt < kTMt; ++mt) {
+              if (ok[mt]) {
+                double v0 = acc[mt][nt][e], v1 = acc[mt][nt][2 + e];
+                if (s2) {
+                  const double2 uu = *reinterpret_cast<const double2*>(us_ + 16 * mt);
+                  v0 = fma(-a.gamma, v0, uu.x);
+                  v1 = fma(-a.gamma, v1, uu.y);
+                }
+                if (two[mt] || padz) __stcs(reinterpret_cast<double2*>(orow + 16 * mt), make_double2(v0, two[mt] ? v1 : 0.0));
+                else __stcs(orow + 16 * mt, v0);
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int nt = 0; nt < (PAIR ? 0 : NT); ++nt) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int Rs = nt * 8 + 2 * tig + e;
@@ -1044,27 +1084,6 @@ _Pragma("unroll")                                                               
           const int q = Rs / G, st = Rs - q * G;
           const size_t row = (size_t)(row0 + q);
           const bool s2 = (MODE == SPMM_S2STEP) && st == s2g;
-          if constexpr (PAIR) {
-            double* orow = outq + st * sst + row * a.ldo + a.out_off + n0 + 2 * gid;
-            const double* us_ = (lrow0 >= 0) ? su + (size_t)(lrow0 + q) * ldu + n0 + 2 * gid
-                                             : Uq + row * ldu + n0 + 2 * gid;
-#pragma unroll
-            for (int mt = 0; mt < kTMt; ++mt) {
-              const int o = mt * 16, c = n0 + 2 * gid + o;
-              if (full_cols || c < r) {
-                double v0 = acc[mt][nt][e], v1 = acc[mt][nt][2 + e];
-                if (s2) {
-                  const double2 uu = *reinterpret_cast<const double2*>(us_ + o);
-                  v0 = fma(-a.gamma, v0, uu.x);
-                  v1 = fma(-a.gamma, v1, uu.y);
-                }
-                if (full_cols || c + 1 < r) __stcs(reinterpret_cast<double2*>(orow + o), make_double2(v0, v1));
-                else if (a.out_sstride) __stcs(reinterpret_cast<double2*>(orow + o), make_double2(v0, 0.0));   // zero pad column
-                else __stcs(orow + o, v0);
-              }
-            }
-            continue;
-          }
           double* orow = outq + st * sst + row * a.ldo + a.out_off + n0 + gid;
           // the block's own U row (S2 epilogue) from the staged rows when present
           const double* us_ = (lrow0 >= 0) ? su + (size_t)(lrow0 + q) * ldu + n0 + gid : Uq + row * ldu + n0 + gid;
