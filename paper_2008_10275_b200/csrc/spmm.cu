@@ -906,6 +906,20 @@ spmm_tma_kernel(SpmmArgs a) {
   // Every warp walks all work items in order and waits on every stage phase (a warp that skipped an
   // item could see a stage's barrier two phases behind and take the stale parity for a completed one);
   // it arrives once per item on the U stage's empty barrier and once per tile on the raw stage's.
+  // lane constants of the operator of P:30-36: slot nt*8 + gid = 3 q + group st combines the arrays
+  // (A0, Jrho, Jlam) / (A1, Jmu) / (A2) with the coefficients (1, rho, lam) / (1, 1) / (rho)
+  int lc_ao[2][3];
+  double lc_co[2][3];
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) {
+    const int slot = nt * 8 + gid, st = slot - (slot / 3) * 3;
+    lc_ao[nt][0] = (st == 0 ? 0 : (st == 1 ? 1 : 2)) * kRawStride;
+    lc_ao[nt][1] = (st == 0 ? 3 : (st == 1 ? 4 : 2)) * kRawStride;
+    lc_ao[nt][2] = (st == 0 ? 5 : (st == 1 ? 4 : 2)) * kRawStride;
+    lc_co[nt][0] = st == 2 ? a.rho : 1.0;
+    lc_co[nt][1] = st == 0 ? a.rho : (st == 1 ? 1.0 : 0.0);
+    lc_co[nt][2] = st == 0 ? a.lam : 0.0;
+  }
   // item counters kept incrementally (no per-item divisions): tile i, subset q, raw stage sr and its
   // phase pr, U stage us and its phase pu, rot = (m * tpt) mod NCW
   int i = 0, q = 0, sr = 0, us = 0, rot = 0;
@@ -951,13 +965,9 @@ spmm_tma_kernel(SpmmArgs a) {
             co[nt][k] = on ? a.gl_c[gs][k] : 0.0;
           }
         } else {
-          const int a0 = st == 0 ? 0 : (st == 1 ? 1 : 2);
-          const int a1 = st == 0 ? 3 : (st == 1 ? 4 : 2);
-          const int a2 = st == 0 ? 5 : (st == 1 ? 4 : 2);
-          po[nt][0] = a0 * kRawStride + o; po[nt][1] = a1 * kRawStride + o; po[nt][2] = a2 * kRawStride + o;
-          co[nt][0] = st == 2 ? a.rho : 1.0;
-          co[nt][1] = st == 0 ? a.rho : (st == 1 ? 1.0 : 0.0);
-          co[nt][2] = st == 0 ? a.lam : 0.0;
+          // the lane's arrays and coefficients were fixed at kernel start (lc_ao, lc_co)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) { po[nt][k] = lc_ao[nt < 2 ? nt : 0][k] + o; co[nt][k] = lc_co[nt < 2 ? nt : 0][k]; }
         }
       }
       // A operand (U^T): columns n0 + mt*16 + gid (+8), entry j = k0 + tig -> staged U row R[cb + j]
