@@ -678,10 +678,12 @@ spmm_u_kernel(SpmmArgs a, int ust) {
 
 // ---------------------------------------------------------------------------------------------
 // Persistent TMA-fed hot kernel (S2STEP / PLAIN3), one CTA per SM, warp-specialised:
-//   producer warp : per tile, by cp.async.bulk (completion on the stage's mbarrier): the 1 KB tile
-//                   record (block geometry + local U-row index per column-list entry), the six raw
-//                   value segments (a 3-deep ring: up to two tiles ahead) and the tile's deduplicated
-//                   U rows as a few contiguous row runs (a 2-deep ring);
+//   producer warp : per tile, by cp.async.bulk (completion on the stage's mbarrier): the tile's
+//                   deduplicated U rows as a few contiguous row runs (a 2-deep ring) FIRST -- a U stage
+//                   frees only when the tile two back is done, so this copy is the tile's critical
+//                   path and must not queue behind value copies -- then the 1 KB tile record (block
+//                   geometry + local U-row index per column-list entry) and the six raw value
+//                   segments of the NEXT tile (a 3-deep ring used LRC_SPMM_RAW_AHEAD - 1 tiles ahead);
 //   consumer warps: NG groups of kTCons warps; group g takes every NG-th tile of the CTA.  A warp
 //                   owns (node block, 32-column slice) tasks; the 6 -> 3 value combination happens in
 //                   the B-fragment loads (three LDS + two FMA per element, branch-free), the U
@@ -870,7 +872,7 @@ spmm_tma_kernel(SpmmArgs a) {
 #ifndef LRC_SPMM_RAW_AHEAD
 #define LRC_SPMM_RAW_AHEAD 2
 #endif
-      for (; ri < nmine && ri <= i + nsr - LRC_SPMM_RAW_AHEAD; ++ri) {
+      for (; ri < nmine && ri <= i + nsr - (nsr >= 3 ? LRC_SPMM_RAW_AHEAD : 1); ++ri) {   // at least one tile ahead
         const int tr = blockIdx.x + ri * Gd, sr = ri % nsr;
         const int e0 = meta(ri, W0{}), tot = meta(ri, W1{});
         int pe0 = 0, ptot = 0;
