@@ -841,17 +841,19 @@ spmm_tma_kernel(SpmmArgs a) {
       for (int k = 0; k < kMetaRuns; ++k)
         if (myr == k && k < nrun) { rg = rv[3 * k]; rl = rv[3 * k + 1]; rs = rv[3 * k + 2]; }
       const int us = m % kUStages;
+      // everything the copy needs is ready before the wait: the issue follows the stage's release at once
+      unsigned ub = (unsigned)rl * (unsigned)ldu * 8u;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ub += __shfl_xor_sync(0xffffffffu, ub, o);
+      const double* Usrc0 = S > 1 ? a.Us[q] : a.U;
+      double* udst = s_ub + (size_t)us * kTUrowMax * ldu_s + (size_t)rs * ldu;
+      const double* usrc = Usrc0 + (size_t)rg * ldu;
       if (m >= kUStages) mbar_wait(&empty_u[us], ((m / kUStages) - 1) & 1);
       {
-        unsigned ub = (unsigned)rl * (unsigned)ldu * 8u;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) ub += __shfl_xor_sync(0xffffffffu, ub, o);
         if (lane == 0) mbar_expect_tx(&full_u[us], ub);
         __syncwarp();
-        const double* Usrc = S > 1 ? a.Us[q] : a.U;
-        if (rl > 0)
-          bulk_g2s(s_ub + (size_t)us * kTUrowMax * ldu_s + (size_t)rs * ldu, Usrc + (size_t)rg * ldu,
-                   (unsigned)rl * (unsigned)ldu * 8u, &full_u[us]);
+        const double* Usrc = Usrc0;
+        if (rl > 0) bulk_g2s(udst, usrc, (unsigned)rl * (unsigned)ldu * 8u, &full_u[us]);
         // warm the U row runs of a later tile into L2: the first touch of a U row (written evict-first
         // by the basis pass) is a DRAM read, and the U copy is the tile's critical path
         if (kTUPrefetch > 0 && i + kTUPrefetch < nmine) {
